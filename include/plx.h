@@ -1,0 +1,162 @@
+/*
+ * plx.h -- C ABI of the B200 (sm_100a) Plenoxels optimisation hot path.
+ *
+ * This is the drop-in boundary: every entry point replaces one L0 kernel call
+ * of the reference package `plenoxel` (pkg/src/plenoxel/_kernels.py, "K"),
+ * or one numpy structure op (grid.py, "G"), at the seam where the reference's
+ * L1 wrappers call into numba.  Conventions follow the
+ * reference's:
+ *   - the caller owns and allocates every buffer (outputs, gradients, scratch);
+ *     entry points never allocate persistent state;
+ *   - kernels never fail on data; argument validation returns PLX_EINVAL;
+ *   - all pointers are DEVICE pointers unless stated; work is enqueued on
+ *     `stream` (a cudaStream_t, NULL = legacy default stream) and is
+ *     asynchronous -- nothing here synchronises the host.
+ *
+ * Storage differs from the reference only in precision: the data table, the
+ * gradient buffer and the RMSProp state are float32 (rows x 28, 112 B / row,
+ * column 0 = sigma, 1..27 = SH channel-major), all arithmetic is float64.
+ * Rays are float64 (N x 3).  The touched-row set of GradientBuffer (G:25-68:
+ * touched_mask + insertion-ordered touched_ids + count) is kept as the byte
+ * mask alone; the count is produced by plx_opt_step / plx_count_touched.
+ */
+#ifndef PLX_H
+#define PLX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PLX_ROW 28
+
+enum {
+    PLX_OK = 0,
+    PLX_EINVAL = 1,   /* bad argument (reference: ValueError) */
+    PLX_ECUDA = 2,    /* launch / runtime error */
+};
+
+/* Sparse grid: replaces the (links, table, lo, hi, scale, dmax) argument
+ * group of render_forward / render_backward / max_weight_accum / tv_grid
+ * (K:174-177, K:242-248, K:415-416, K:457-459) and SparseGrid (G:71-92). */
+typedef struct {
+    const int32_t *links;  /* [Dx*Dy*Dz] C-order (z fastest), -1 = empty     */
+    float *table;          /* [rows*28]                                      */
+    int64_t dims[3];       /* Dx, Dy, Dz (each >= 2)                         */
+    int64_t rows;
+    double lo[3], hi[3];   /* aabb_min / aabb_max                            */
+    double scale[3];       /* lattice_scale = (D-1)/extent   (G:137-139)     */
+    double dmax[3];        /* D-1                            (R:132)         */
+    const uint32_t *cell_occ; /* optional: 1 bit per trilinear base cell,
+                                 set iff any of its 8 corners is occupied
+                                 (plx_build_cell_occ); NULL = test the links */
+} plx_grid;
+
+/* GradientBuffer (G:25-68): data + touched mask. */
+typedef struct {
+    float *grad;           /* [rows*28] */
+    uint8_t *tmask;        /* [rows]    */
+} plx_grad;
+
+/* RenderOptions (R:27-42) resolved to kernel scalars (R:63-64, R:132-139). */
+typedef struct {
+    double step;           /* step_frac * min(voxel_size)                    */
+    double stop_thresh;
+    double bg[3];
+    int32_t nearest;       /* interp == "nearest"                            */
+    int32_t absolute;      /* formula == "absolute"                          */
+} plx_render_opts;
+
+/* A ray batch.  If idx != NULL ray r of the batch is pool row idx[r] of
+ * origins/dirs/viewdirs/target (device-resident ray pool);
+ * outputs are always indexed by batch position r. */
+typedef struct {
+    const double *origins;   /* [*,3]                                        */
+    const double *dirs;      /* [*,3] march directions                       */
+    const double *viewdirs;  /* [*,3] SH directions (unit)                   */
+    const double *target;    /* [*,3] gt rgb (mse_mode) or dL/dC; may be NULL */
+    const double *jitter;    /* [n] start offsets in steps, or NULL (= 0)    */
+    const int64_t *idx;      /* [n] pool indices, or NULL                    */
+    int64_t n;
+} plx_rays;
+
+/* render_forward (K:173-238) via render_rays (R:114-140).
+ * out_trans / out_wsum may be NULL. */
+int plx_render_fwd(const plx_grid *g, const plx_rays *rays, const plx_render_opts *o,
+                   double *out_rgb, double *out_trans, double *out_wsum, void *stream);
+
+/* render_backward (K:241-411) via fused_mse_backward (R:253-279, mse_mode=1,
+ * up_scale = 2/n_total) and render_rays_backward (R:205-239, mse_mode=0,
+ * target = upstream dL/dC).  Gradients are ADDED into gb->grad with f32
+ * atomics; every occupied stencil row of every recorded sample is marked in
+ * gb->tmask.  out_sums (device double[2]) is ACCUMULATED with
+ * {mse_sum, cauchy_sum}; out_rgb may be NULL. */
+int plx_render_fused_bwd(const plx_grid *g, const plx_rays *rays,
+                         const plx_render_opts *o, int32_t mse_mode, double up_scale,
+                         double lam_cauchy, plx_grad *gb, double *out_rgb,
+                         double *out_sums, void *stream);
+
+/* max_weight_accum (K:414-453) via SparseGrid.max_weight_accumulate
+ * (G:287-302).  out_w [rows] float64 is max-updated in place (caller zeroes). */
+int plx_max_weight(const plx_grid *g, const plx_rays *rays, const plx_render_opts *o,
+                   double *out_w, void *stream);
+
+/* tv_grid (K:456-569) via tv_loss (L:50-77).  Cells are either the explicit
+ * list `cells` [count] (flat C-order ids) or, when cells == NULL, the wrapped
+ * contiguous run start, start+1, ... (mod ncell) of sample_tv_cells
+ * (L:41-47).  out_sums (device double[2]) is ACCUMULATED with the raw
+ * {sigma_sum, sh_sum}. */
+int plx_tv(const plx_grid *g, const int64_t *cells, int64_t start, int64_t count,
+           double fac_x, double fac_y, double fac_z, double eps, double f_sigma,
+           double f_sh, int32_t wrap_x, int32_t wrap_y, int32_t wrap_z,
+           int32_t with_grad, plx_grad *gb, double *out_sums, void *stream);
+
+/* opt_step (K:572-590) via optim.step (O:81-97), fused with clear_grad
+ * (K:593-600) when clear != 0.  Visits rows whose tmask is set; entries with
+ * g == 0 keep their stale state.  out_count (device int64, may be NULL)
+ * receives the number of touched rows (GradientBuffer.n_touched). */
+int plx_opt_step(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, double lr_sh,
+                 double beta, double eps, int32_t rmsprop, int32_t clear,
+                 int64_t *out_count, void *stream);
+
+/* clear_grad (K:593-600) alone (GradientBuffer.clear, G:62-64): zero the
+ * touched rows of gb->grad and reset gb->tmask.  out_count as above. */
+int plx_clear_grad(plx_grad *gb, int64_t rows, int64_t *out_count, void *stream);
+
+/* GradientBuffer.n_touched (G:42-44): out_count (device int64) = popcount. */
+int plx_count_touched(const uint8_t *tmask, int64_t rows, int64_t *out_count,
+                      void *stream);
+
+/* Structure ops (G:228-285).  Both are two-phase because the new row count
+ * must reach the host to size the new table (as numpy does):
+ *   1. *_mark   -> flags[ncell_new] (uint8)
+ *   2. plx_scan_ids(flags) -> new_links (int32, -1 where flag==0) + count
+ *   3. *_apply  -> new table (+ kept ids for prune)
+ * plx_scan_scratch_bytes(n) sizes the scan workspace. */
+int plx_prune_mark(const plx_grid *g, const double *weights, double threshold,
+                   uint8_t *deemed_scratch, uint8_t *flags, void *stream);
+int plx_prune_apply(const plx_grid *g, const int32_t *new_links, int64_t *kept_old,
+                    float *new_table, void *stream);
+int plx_upsample_mark(const plx_grid *g, const int64_t new_dims[3], uint8_t *flags,
+                      void *stream);
+int plx_upsample_apply(const plx_grid *g, const int64_t new_dims[3],
+                       const int32_t *new_links, float *new_table, void *stream);
+int64_t plx_scan_scratch_bytes(int64_t n);
+int plx_scan_ids(const uint8_t *flags, int64_t n, int32_t *ids, int64_t *count,
+                 void *scratch, void *stream);
+
+/* Empty-space skipping helper: cell_occ bit (i,j,k) for every trilinear base
+ * cell (i<Dx-1, j<Dy-1, k<Dz-1; stored over the full Dx*Dy*Dz index space)
+ * = any of the 8 corner links >= 0.  Must be rebuilt after prune/upsample. */
+int64_t plx_cell_occ_words(const int64_t dims[3]);
+int plx_build_cell_occ(const plx_grid *g, uint32_t *cell_occ, void *stream);
+
+/* Library identification / self-check. */
+const char *plx_version(void);
+int plx_device_check(void);   /* 0 iff a CUDA device with cc >= 10.0 is present */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PLX_H */

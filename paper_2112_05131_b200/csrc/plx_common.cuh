@@ -1,0 +1,222 @@
+// plx_common.cuh -- device-side helpers shared by the sm_100a kernels.
+//
+// Arithmetic follows the reference kernels (pkg/src/plenoxel/_kernels.py,
+// "K") operation by operation in float64; translation units that include this
+// header are compiled with -fmad=false so no a*b+c is contracted into an FMA
+// (numba compiles the reference without fast-math, i.e. without contraction).
+// With f32-representable table values this reproduces the reference's sample
+// positions, stencil rows/weights, opacities and pre-clamp colours bit-for-bit.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/plx.h"
+
+#define PLX_FULL_MASK 0xffffffffu
+
+namespace plx {
+
+// Kernel-side copy of plx_grid (passed by value).
+struct DGrid {
+    const int32_t *__restrict__ links;
+    const float *__restrict__ table;
+    const uint32_t *__restrict__ cell_occ;
+    int32_t Dx, Dy, Dz;
+    double lo[3], hi[3], scale[3], dmax[3];
+};
+
+inline DGrid make_dgrid(const plx_grid &g) {
+    DGrid d;
+    d.links = g.links;
+    d.table = g.table;
+    d.cell_occ = g.cell_occ;
+    d.Dx = (int32_t)g.dims[0];
+    d.Dy = (int32_t)g.dims[1];
+    d.Dz = (int32_t)g.dims[2];
+    for (int a = 0; a < 3; ++a) {
+        d.lo[a] = g.lo[a];
+        d.hi[a] = g.hi[a];
+        d.scale[a] = g.scale[a];
+        d.dmax[a] = g.dmax[a];
+    }
+    return d;
+}
+
+// sh.py:18-22
+constexpr double SH_C0 = 0.28209479177387814;
+constexpr double SH_C1 = 0.4886025119029199;
+constexpr double SH_C2_0 = 1.0925484305920792;
+constexpr double SH_C2_2 = 0.31539156525252005;
+constexpr double SH_C2_4 = 0.5462742152960396;
+
+// K:27-37
+__device__ __forceinline__ void sh_basis9(double x, double y, double z, double *b) {
+    b[0] = SH_C0;
+    b[1] = -SH_C1 * y;
+    b[2] = SH_C1 * z;
+    b[3] = -SH_C1 * x;
+    b[4] = SH_C2_0 * x * y;
+    b[5] = -SH_C2_0 * y * z;
+    b[6] = SH_C2_2 * (2.0 * z * z - x * x - y * y);
+    b[7] = -SH_C2_0 * x * z;
+    b[8] = SH_C2_4 * (x * x - y * y);
+}
+
+// K:40-81.  Returns (t0, t1); miss iff t1 <= t0.
+__device__ __forceinline__ void ray_aabb(const double *o, const double *d, const double *lo,
+                                         const double *hi, double &t0_out, double &t1_out) {
+    double t0 = 0.0, t1 = __longlong_as_double(0x7ff0000000000000ULL);  // +inf
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (fabs(d[a]) < 1e-15) {
+            if (o[a] < lo[a] || o[a] > hi[a]) {
+                t0_out = 1.0;
+                t1_out = 0.0;
+                return;
+            }
+        } else {
+            double ta = (lo[a] - o[a]) / d[a];
+            double tb = (hi[a] - o[a]) / d[a];
+            if (ta > tb) {
+                double tmp = ta;
+                ta = tb;
+                tb = tmp;
+            }
+            if (ta > t0) t0 = ta;
+            if (tb < t1) t1 = tb;
+        }
+    }
+    t0_out = t0;
+    t1_out = t1;
+}
+
+// K:163-170
+__device__ __forceinline__ double clamp_coord(double p, double lo, double scale, double dmax) {
+    double g = (p - lo) * scale;
+    if (g < 0.0) g = 0.0;
+    if (g > dmax) g = dmax;
+    return g;
+}
+
+__device__ __forceinline__ int64_t flat(const DGrid &G, int64_t i, int64_t j, int64_t k) {
+    return (i * G.Dy + j) * G.Dz + k;
+}
+
+// Per-ray march parameters (K:189-205).
+struct RayMarch {
+    double o[3], d[3];
+    double t0, L;
+    int64_t nsamp;   // 0 on a miss
+};
+
+__device__ __forceinline__ void ray_march_setup(RayMarch &rm, const DGrid &G, double step,
+                                                double jitter) {
+    double t1;
+    ray_aabb(rm.o, rm.d, G.lo, G.hi, rm.t0, t1);
+    rm.t0 = rm.t0 + jitter * step;
+    rm.L = t1 - rm.t0;
+    rm.nsamp = 0;
+    if (rm.L > 0.0) {
+        int64_t n = (int64_t)ceil(rm.L / step - 1e-9);
+        rm.nsamp = n < 1 ? 1 : n;
+    }
+}
+
+// Lattice coordinates of sample si (K:203-208): t, delta, g.
+__device__ __forceinline__ void sample_coords(const RayMarch &rm, const DGrid &G, double step,
+                                              int64_t si, double &t, double &dlt, double *g) {
+    t = rm.t0 + (double)si * step;
+    dlt = si < rm.nsamp - 1 ? step : rm.L - step * (double)(rm.nsamp - 1);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) g[a] = clamp_coord(rm.o[a] + t * rm.d[a], G.lo[a], G.scale[a], G.dmax[a]);
+}
+
+// Stencil (K:84-123): rows[8] (-1 = empty) and weights; returns 1 or 8.
+template <bool NEAREST>
+__device__ __forceinline__ int stencil(const DGrid &G, const double *g, int32_t *rows, double *ws,
+                                       bool &any_occ) {
+    if (NEAREST) {
+        int64_t i = (int64_t)(g[0] + 0.5), j = (int64_t)(g[1] + 0.5), k = (int64_t)(g[2] + 0.5);
+        if (i > G.Dx - 1) i = G.Dx - 1;
+        if (j > G.Dy - 1) j = G.Dy - 1;
+        if (k > G.Dz - 1) k = G.Dz - 1;
+        rows[0] = __ldg(G.links + flat(G, i, j, k));
+        ws[0] = 1.0;
+        any_occ = rows[0] >= 0;
+        return 1;
+    }
+    int64_t i0 = (int64_t)g[0], j0 = (int64_t)g[1], k0 = (int64_t)g[2];
+    if (i0 > G.Dx - 2) i0 = G.Dx - 2;
+    if (j0 > G.Dy - 2) j0 = G.Dy - 2;
+    if (k0 > G.Dz - 2) k0 = G.Dz - 2;
+    if (G.cell_occ) {
+        int64_t c = flat(G, i0, j0, k0);
+        if (!((__ldg(G.cell_occ + (c >> 5)) >> (c & 31)) & 1u)) {
+            any_occ = false;
+            return 8;
+        }
+    }
+    double fx = g[0] - (double)i0, fy = g[1] - (double)j0, fz = g[2] - (double)k0;
+    const int32_t *base = G.links + flat(G, i0, j0, k0);
+    const int64_t sy = G.Dz, sx = (int64_t)G.Dy * G.Dz;
+    bool occ = false;
+    int n = 0;
+#pragma unroll
+    for (int di = 0; di < 2; ++di) {
+        double wx = di == 1 ? fx : 1.0 - fx;
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj) {
+            double wy = dj == 1 ? fy : 1.0 - fy;
+#pragma unroll
+            for (int dk = 0; dk < 2; ++dk) {
+                double wz = dk == 1 ? fz : 1.0 - fz;
+                int32_t r = __ldg(base + di * sx + dj * sy + dk);
+                rows[n] = r;
+                ws[n] = wx * wy * wz;
+                occ |= r >= 0;
+                ++n;
+            }
+        }
+    }
+    any_occ = occ;
+    return 8;
+}
+
+// ---- warp collectives (f64) ----------------------------------------------
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(PLX_FULL_MASK, x, off);
+    return x;
+}
+
+__device__ __forceinline__ double warp_scan_add(double x, int lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        double y = __shfl_up_sync(PLX_FULL_MASK, x, off);
+        if (lane >= off) x = y + x;
+    }
+    return x;
+}
+
+__device__ __forceinline__ double warp_scan_mul(double x, int lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        double y = __shfl_up_sync(PLX_FULL_MASK, x, off);
+        if (lane >= off) x = y * x;
+    }
+    return x;
+}
+
+// Vectorised fire-and-forget f32 reduction (sm_90+ PTX; SASS REDG.E.ADD.F32x4).
+__device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
+                 "f"(d)
+                 : "memory");
+}
+
+__device__ __forceinline__ void red_add_f32(float *addr, float a) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(a) : "memory");
+}
+
+}  // namespace plx

@@ -1,0 +1,614 @@
+// plx_grid_ops.cu -- per-row / per-cell kernels for sm_100a: TV regulariser,
+// sparse RMSProp/SGD with fused gradient clear, touched-row count, prune,
+// upsample, id compaction scan and the empty-space cell bitmask.
+//
+// Reference: pkg/src/plenoxel/_kernels.py tv_grid (K:456-569), opt_step
+// (K:572-590), clear_grad (K:593-600); grid.py prune (G:228-258), upsample
+// (G:260-285).  All of these are HBM-streaming kernels: coalesced float4
+// row access, one pass, grids sized in multiples of the 148 SMs.
+#include <cub/block/block_reduce.cuh>
+
+#include "plx_common.cuh"
+
+namespace plx {
+
+// ---------------------------------------------------------------- TV ------
+struct TvArgs {
+    const int64_t *cells;
+    int64_t start, count, ncell;
+    double fac[3], eps, f_sigma, f_sh;
+    int wrap[3];
+    int with_grad;
+    float *grad;
+    uint8_t *tmask;
+    double *sums;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
+    using BR = cub::BlockReduce<double, NT>;
+    __shared__ typename BR::TempStorage tmp;
+    const int64_t ci = (int64_t)blockIdx.x * NT + threadIdx.x;
+    double sig_sum = 0.0, sh_sum = 0.0;
+    if (ci < a.count) {
+        int64_t cid = a.cells ? a.cells[ci] : (a.start + ci) % a.ncell;   // L:41-47
+        const int64_t Dyz = (int64_t)G.Dy * G.Dz;
+        const int64_t i = cid / Dyz, rem = cid % Dyz, j = rem / G.Dz, k = rem % G.Dz;
+        const int32_t r0 = __ldg(G.links + cid);
+        int64_t ii = i + 1, jj = j + 1, kk = k + 1;
+        bool hx = true, hy = true, hz = true;
+        if (ii >= G.Dx) { if (a.wrap[0]) ii = 0; else hx = false; }
+        if (jj >= G.Dy) { if (a.wrap[1]) jj = 0; else hy = false; }
+        if (kk >= G.Dz) { if (a.wrap[2]) kk = 0; else hz = false; }
+        const int32_t rx = hx ? __ldg(G.links + flat(G, ii, j, k)) : -1;
+        const int32_t ry = hy ? __ldg(G.links + flat(G, i, jj, k)) : -1;
+        const int32_t rz = hz ? __ldg(G.links + flat(G, i, j, kk)) : -1;
+        const double e2 = a.eps * a.eps;
+        const float *T = G.table;
+        // opacity term (K:505-532): missing neighbours read as 0
+        const double s0 = r0 >= 0 ? (double)__ldg(T + (int64_t)r0 * PLX_ROW) : 0.0;
+        const double sx = rx >= 0 ? (double)__ldg(T + (int64_t)rx * PLX_ROW) : 0.0;
+        const double sy = ry >= 0 ? (double)__ldg(T + (int64_t)ry * PLX_ROW) : 0.0;
+        const double sz = rz >= 0 ? (double)__ldg(T + (int64_t)rz * PLX_ROW) : 0.0;
+        const double dxv = (sx - s0) * a.fac[0], dyv = (sy - s0) * a.fac[1], dzv = (sz - s0) * a.fac[2];
+        const double val = sqrt(dxv * dxv + dyv * dyv + dzv * dzv + e2);
+        sig_sum = val;
+        // per-row gradient accumulators for the current 4-column group
+        float gx[4], gy[4], gz[4], g0v[4];
+        bool tx = false, ty = false, tz = false, t0 = false;
+        const bool okx = rx >= 0, oky = ry >= 0, okz = rz >= 0;
+        const bool sh_on = r0 >= 0 && (okx || oky || okz);
+        if (!sh_on) sh_sum = 27.0 * a.eps;
+#pragma unroll 1
+        for (int m = 0; m < 7; ++m) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) gx[e] = gy[e] = gz[e] = g0v[e] = 0.0f;
+            float4 v0 = make_float4(0, 0, 0, 0), vx = v0, vy = v0, vz = v0;
+            if (sh_on) {
+                v0 = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)r0 * PLX_ROW) + m);
+                if (okx) vx = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)rx * PLX_ROW) + m);
+                if (oky) vy = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)ry * PLX_ROW) + m);
+                if (okz) vz = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)rz * PLX_ROW) + m);
+            }
+            const float c0[4] = {v0.x, v0.y, v0.z, v0.w}, cx[4] = {vx.x, vx.y, vx.z, vx.w};
+            const float cy[4] = {vy.x, vy.y, vy.z, vy.w}, cz[4] = {vz.x, vz.y, vz.z, vz.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int d = 4 * m + e;
+                if (d == 0) {
+                    if (a.with_grad && val > 0.0) {
+                        const double inv = a.f_sigma / val;
+                        double g0 = 0.0;
+                        if (rx >= 0) { tx = true; gx[0] = (float)(dxv * a.fac[0] * inv); }
+                        g0 -= dxv * a.fac[0] * inv;
+                        if (ry >= 0) { ty = true; gy[0] = (float)(dyv * a.fac[1] * inv); }
+                        g0 -= dyv * a.fac[1] * inv;
+                        if (rz >= 0) { tz = true; gz[0] = (float)(dzv * a.fac[2] * inv); }
+                        g0 -= dzv * a.fac[2] * inv;
+                        if (r0 >= 0 && g0 != 0.0) { t0 = true; g0v[0] = (float)g0; }
+                    }
+                    continue;
+                }
+                if (!sh_on) continue;   // K:534-568
+                const double v0d = (double)c0[e];
+                const double ax = okx ? ((double)cx[e] - v0d) * a.fac[0] : 0.0;
+                const double ay = oky ? ((double)cy[e] - v0d) * a.fac[1] : 0.0;
+                const double az = okz ? ((double)cz[e] - v0d) * a.fac[2] : 0.0;
+                const double v = sqrt(ax * ax + ay * ay + az * az + e2);
+                sh_sum += v;
+                if (a.with_grad && v > 0.0) {
+                    const double inv = a.f_sh / v;
+                    double g0 = 0.0;
+                    if (okx) { tx = true; gx[e] = (float)(ax * a.fac[0] * inv); g0 -= ax * a.fac[0] * inv; }
+                    if (oky) { ty = true; gy[e] = (float)(ay * a.fac[1] * inv); g0 -= ay * a.fac[1] * inv; }
+                    if (okz) { tz = true; gz[e] = (float)(az * a.fac[2] * inv); g0 -= az * a.fac[2] * inv; }
+                    if (g0 != 0.0) { t0 = true; g0v[e] = (float)g0; }
+                }
+            }
+            if (a.with_grad) {
+                if (rx >= 0 && (gx[0] != 0.f || gx[1] != 0.f || gx[2] != 0.f || gx[3] != 0.f))
+                    red_add_v4(a.grad + (int64_t)rx * PLX_ROW + 4 * m, gx[0], gx[1], gx[2], gx[3]);
+                if (ry >= 0 && (gy[0] != 0.f || gy[1] != 0.f || gy[2] != 0.f || gy[3] != 0.f))
+                    red_add_v4(a.grad + (int64_t)ry * PLX_ROW + 4 * m, gy[0], gy[1], gy[2], gy[3]);
+                if (rz >= 0 && (gz[0] != 0.f || gz[1] != 0.f || gz[2] != 0.f || gz[3] != 0.f))
+                    red_add_v4(a.grad + (int64_t)rz * PLX_ROW + 4 * m, gz[0], gz[1], gz[2], gz[3]);
+                if (r0 >= 0 && (g0v[0] != 0.f || g0v[1] != 0.f || g0v[2] != 0.f || g0v[3] != 0.f))
+                    red_add_v4(a.grad + (int64_t)r0 * PLX_ROW + 4 * m, g0v[0], g0v[1], g0v[2], g0v[3]);
+            }
+        }
+        if (a.with_grad) {   // _touch (K:155-160) semantics, idempotent byte stores
+            if (tx) a.tmask[rx] = 1;
+            if (ty) a.tmask[ry] = 1;
+            if (tz) a.tmask[rz] = 1;
+            if (t0) a.tmask[r0] = 1;
+        }
+    }
+    double s1 = BR(tmp).Sum(sig_sum);
+    __syncthreads();
+    double s2 = BR(tmp).Sum(sh_sum);
+    if (threadIdx.x == 0) {
+        atomicAdd(a.sums + 0, s1);
+        atomicAdd(a.sums + 1, s2);
+    }
+}
+
+// ------------------------------------------------------- optimiser --------
+// One warp serves 4 rows x 7 float4 (lanes 28..31 idle), so the touched
+// byte of a row is read and cleared inside one warp.
+struct OptArgs {
+    float *table, *v, *grad;
+    uint8_t *tmask;
+    int64_t rows;
+    double lr_sigma, lr_sh, beta, eps;
+    int rmsprop, clear, update;
+    unsigned long long *count;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT) opt_kernel(OptArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * NT + threadIdx.x) >> 5;
+    const int64_t row = wid * 4 + lane / 7;
+    const int quad = lane % 7;
+    const bool active = lane < 28 && row < a.rows;
+    bool touched = false;
+    if (active) touched = a.tmask[row] != 0;
+    if (touched && !a.update) {
+        if (a.clear) reinterpret_cast<float4 *>(a.grad + row * PLX_ROW)[quad] = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else if (touched) {
+        float4 *gp = reinterpret_cast<float4 *>(a.grad + row * PLX_ROW) + quad;
+        float4 *tp = reinterpret_cast<float4 *>(a.table + row * PLX_ROW) + quad;
+        float4 *vp = reinterpret_cast<float4 *>(a.v + row * PLX_ROW) + quad;
+        const float4 g4 = *gp;
+        float4 t4 = *tp;
+        float g[4] = {g4.x, g4.y, g4.z, g4.w};
+        float t[4] = {t4.x, t4.y, t4.z, t4.w};
+        if (a.rmsprop) {
+            float4 v4 = *vp;
+            float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (g[e] == 0.0f) continue;   // K:581-583 stale state
+                const double gd = (double)g[e];
+                const double lr = (quad == 0 && e == 0) ? a.lr_sigma : a.lr_sh;
+                const double nv = a.beta * (double)v[e] + (1.0 - a.beta) * gd * gd;
+                v[e] = (float)nv;
+                t[e] = (float)((double)t[e] - lr * gd / (sqrt(nv) + a.eps));
+            }
+            *vp = make_float4(v[0], v[1], v[2], v[3]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (g[e] == 0.0f) continue;
+                const double lr = (quad == 0 && e == 0) ? a.lr_sigma : a.lr_sh;
+                t[e] = (float)((double)t[e] - lr * (double)g[e]);
+            }
+        }
+        *tp = make_float4(t[0], t[1], t[2], t[3]);
+        if (a.clear) *gp = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const unsigned rows_touched = __ballot_sync(PLX_FULL_MASK, touched && quad == 0);
+    __syncwarp();
+    if (a.clear && touched && quad == 0) a.tmask[row] = 0;
+    if (a.count && lane == 0 && rows_touched) atomicAdd(a.count, (unsigned long long)__popc(rows_touched));
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) count_kernel(const uint8_t *m, int64_t n,
+                                                   unsigned long long *count) {
+    using BR = cub::BlockReduce<int, NT>;
+    __shared__ typename BR::TempStorage tmp;
+    int c = 0;
+    const int64_t stride = (int64_t)gridDim.x * NT * 16;
+    for (int64_t base = ((int64_t)blockIdx.x * NT + threadIdx.x) * 16; base < n; base += stride) {
+        if (base + 16 <= n && ((reinterpret_cast<uintptr_t>(m) & 15) == 0)) {
+            const uint4 v = *reinterpret_cast<const uint4 *>(m + base);
+            const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                // count nonzero bytes
+                unsigned x = w[e];
+                x = (x | (x >> 4)) & 0x0f0f0f0fu;
+                x = (x | (x >> 2)) & 0x03030303u;
+                x = (x | (x >> 1)) & 0x01010101u;
+                c += __popc(x);
+            }
+        } else {
+            for (int64_t i = base; i < n && i < base + 16; ++i) c += m[i] != 0;
+        }
+    }
+    const int s = BR(tmp).Sum(c);
+    if (threadIdx.x == 0 && s) atomicAdd(count, (unsigned long long)s);
+}
+
+// ----------------------------------------------------------- prune --------
+__global__ void prune_deem_kernel(DGrid G, const double *weights, double thr, uint8_t *deemed,
+                                  int64_t ncell) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncell) return;
+    const int32_t r = G.links[c];
+    uint8_t d = 0;
+    if (r >= 0) {
+        const double v = weights ? weights[r] : (double)G.table[(int64_t)r * PLX_ROW];
+        d = v >= thr;
+    }
+    deemed[c] = d;
+}
+
+// One axis of the separable 3x3x3 box dilation (border_value = 0).
+__global__ void dilate_axis_kernel(const uint8_t *in, uint8_t *out, int64_t ncell, int64_t stride,
+                                   int64_t extent, const int32_t *links_and) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncell) return;
+    const int64_t pos = (c / stride) % extent;
+    uint8_t v = in[c];
+    if (pos > 0) v |= in[c - stride];
+    if (pos < extent - 1) v |= in[c + stride];
+    if (links_and) v = v && links_and[c] >= 0;   // survive = occ & dilated
+    out[c] = v;
+}
+
+__global__ void prune_apply_kernel(DGrid G, const int32_t *new_links, int64_t ncell,
+                                   int64_t *kept_old, float *new_table) {
+    // one warp-quarter (8 lanes) per cell: 7 lanes copy the row as float4
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t c = t >> 3;
+    const int part = t & 7;
+    if (c >= ncell) return;
+    const int32_t id = new_links[c];
+    if (id < 0) return;
+    const int32_t old = G.links[c];
+    if (part == 7) {
+        if (kept_old) kept_old[id] = old;
+        return;
+    }
+    reinterpret_cast<float4 *>(new_table + (int64_t)id * PLX_ROW)[part] =
+        reinterpret_cast<const float4 *>(G.table + (int64_t)old * PLX_ROW)[part];
+}
+
+// -------------------------------------------------------- upsample --------
+struct UpArgs {
+    int64_t N[3];
+    double spacing[3];
+};
+
+// New lattice point (i,j,k) -> stencil on the old grid (G:270-279), in the
+// numpy operation order, float64, no contraction.
+__device__ __forceinline__ bool up_stencil(const DGrid &G, const UpArgs &u, int64_t c,
+                                           int32_t *rows, double *ws) {
+    const int64_t NyNz = u.N[1] * u.N[2];
+    const int64_t ijk[3] = {c / NyNz, (c % NyNz) / u.N[2], c % u.N[2]};
+    const int64_t dm2[3] = {G.Dx - 2, G.Dy - 2, G.Dz - 2};
+    double f[3];
+    int64_t i0[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double p = G.lo[a] + (double)ijk[a] * u.spacing[a];
+        double g = (p - G.lo[a]) * G.scale[a];
+        if (g < 0.0) g = 0.0;
+        if (g > G.dmax[a]) g = G.dmax[a];
+        int64_t fl = (int64_t)floor(g);
+        i0[a] = fl < dm2[a] ? fl : dm2[a];
+        f[a] = g - (double)i0[a];
+    }
+    bool occ = false;
+    int q = 0;
+#pragma unroll
+    for (int di = 0; di < 2; ++di) {
+        const double wx = di ? f[0] : 1.0 - f[0];
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj) {
+            const double wy = dj ? f[1] : 1.0 - f[1];
+#pragma unroll
+            for (int dk = 0; dk < 2; ++dk) {
+                const double wz = dk ? f[2] : 1.0 - f[2];
+                const int32_t r = __ldg(G.links + flat(G, i0[0] + di, i0[1] + dj, i0[2] + dk));
+                rows[q] = r;
+                ws[q] = wx * wy * wz;
+                occ |= (r >= 0) && ws[q] > 0.0;   // G:275-276: sum w*[occ] > 0
+                ++q;
+            }
+        }
+    }
+    return occ;
+}
+
+__global__ void upsample_mark_kernel(DGrid G, UpArgs u, uint8_t *flags, int64_t ncell) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncell) return;
+    int32_t rows[8];
+    double ws[8];
+    flags[c] = up_stencil(G, u, c, rows, ws);
+}
+
+__global__ void upsample_apply_kernel(DGrid G, UpArgs u, const int32_t *new_links, int64_t ncell,
+                                      float *new_table) {
+    // 7 lanes per new cell, each producing one float4 of the row
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t c = t >> 3;
+    const int part = t & 7;
+    if (c >= ncell || part == 7) return;
+    const int32_t id = new_links[c];
+    if (id < 0) return;
+    int32_t rows[8];
+    double ws[8];
+    up_stencil(G, u, c, rows, ws);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        if (rows[q] < 0) continue;   // empty corners read 0, no renormalisation
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(G.table + (int64_t)rows[q] * PLX_ROW) + part);
+        acc[0] += ws[q] * (double)v.x;
+        acc[1] += ws[q] * (double)v.y;
+        acc[2] += ws[q] * (double)v.z;
+        acc[3] += ws[q] * (double)v.w;
+    }
+    reinterpret_cast<float4 *>(new_table + (int64_t)id * PLX_ROW)[part] =
+        make_float4((float)acc[0], (float)acc[1], (float)acc[2], (float)acc[3]);
+}
+
+// -------------------------------------------------- compaction scan -------
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int64_t kScanTile = (int64_t)kScanThreads * kScanItems;
+
+__global__ void __launch_bounds__(kScanThreads) scan_count_kernel(const uint8_t *flags, int64_t n,
+                                                                  int64_t *partial) {
+    using BR = cub::BlockReduce<int, kScanThreads>;
+    __shared__ typename BR::TempStorage tmp;
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    int c = 0;
+#pragma unroll
+    for (int e = 0; e < kScanItems; ++e) c += (base + e < n) && flags[base + e];
+    const int s = BR(tmp).Sum(c);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(1024) scan_partials_kernel(int64_t *partial, int64_t nb,
+                                                             int64_t *count) {
+    // single block: exclusive scan of nb partial counts
+    __shared__ int64_t sh[1024];
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < nb; base += 1024) {
+        const int64_t i = base + threadIdx.x;
+        const int64_t v = i < nb ? partial[i] : 0;
+        sh[threadIdx.x] = v;
+        __syncthreads();
+        for (int off = 1; off < 1024; off <<= 1) {
+            int64_t y = threadIdx.x >= (unsigned)off ? sh[threadIdx.x - off] : 0;
+            __syncthreads();
+            sh[threadIdx.x] += y;
+            __syncthreads();
+        }
+        if (i < nb) partial[i] = carry + sh[threadIdx.x] - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += sh[1023];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *count = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_write_kernel(const uint8_t *flags, int64_t n,
+                                                                  const int64_t *partial,
+                                                                  int32_t *ids) {
+    __shared__ int sh[kScanThreads];
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    uint8_t f[kScanItems];
+    int c = 0;
+#pragma unroll
+    for (int e = 0; e < kScanItems; ++e) {
+        f[e] = (base + e < n) ? flags[base + e] : 0;
+        c += f[e] != 0;
+    }
+    sh[threadIdx.x] = c;
+    __syncthreads();
+    for (int off = 1; off < kScanThreads; off <<= 1) {
+        int y = threadIdx.x >= (unsigned)off ? sh[threadIdx.x - off] : 0;
+        __syncthreads();
+        sh[threadIdx.x] += y;
+        __syncthreads();
+    }
+    int64_t id = partial[blockIdx.x] + sh[threadIdx.x] - c;
+#pragma unroll
+    for (int e = 0; e < kScanItems; ++e) {
+        if (base + e >= n) break;
+        ids[base + e] = f[e] ? (int32_t)(id++) : -1;
+    }
+}
+
+// ---------------------------------------------------- cell bitmask --------
+__global__ void cell_occ_kernel(DGrid G, uint32_t *words, int64_t nwords, int64_t ncell) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= nwords) return;
+    const int64_t Dyz = (int64_t)G.Dy * G.Dz;
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; ++b) {
+        const int64_t c = w * 32 + b;
+        if (c >= ncell) break;
+        const int64_t i = c / Dyz, j = (c % Dyz) / G.Dz, k = c % G.Dz;
+        if (i >= G.Dx - 1 || j >= G.Dy - 1 || k >= G.Dz - 1) continue;
+        const int32_t *p = G.links + c;
+        const bool any = p[0] >= 0 || p[1] >= 0 || p[G.Dz] >= 0 || p[G.Dz + 1] >= 0 ||
+                         p[Dyz] >= 0 || p[Dyz + 1] >= 0 || p[Dyz + G.Dz] >= 0 ||
+                         p[Dyz + G.Dz + 1] >= 0;
+        if (any) bits |= 1u << b;
+    }
+    words[w] = bits;
+}
+
+}  // namespace plx
+
+using namespace plx;
+
+namespace {
+bool grid_ok(const plx_grid *g) {
+    return g && g->links && g->dims[0] >= 2 && g->dims[1] >= 2 && g->dims[2] >= 2 &&
+           (g->rows == 0 || g->table) && g->dims[0] * g->dims[1] * g->dims[2] < (int64_t)1 << 31;
+}
+int status() { return cudaPeekAtLastError() == cudaSuccess ? PLX_OK : PLX_ECUDA; }
+unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+int64_t ncell(const plx_grid *g) { return g->dims[0] * g->dims[1] * g->dims[2]; }
+}  // namespace
+
+extern "C" int plx_tv(const plx_grid *g, const int64_t *cells, int64_t start, int64_t count,
+                      double fac_x, double fac_y, double fac_z, double eps, double f_sigma,
+                      double f_sh, int32_t wrap_x, int32_t wrap_y, int32_t wrap_z,
+                      int32_t with_grad, plx_grad *gb, double *out_sums, void *stream) {
+    if (!grid_ok(g) || !out_sums || count < 0 || (with_grad && (!gb || !gb->grad || !gb->tmask)))
+        return PLX_EINVAL;
+    if (count == 0) return PLX_OK;
+    TvArgs a;
+    a.cells = cells;
+    a.start = start;
+    a.count = count;
+    a.ncell = ncell(g);
+    a.fac[0] = fac_x;
+    a.fac[1] = fac_y;
+    a.fac[2] = fac_z;
+    a.eps = eps;
+    a.f_sigma = f_sigma;
+    a.f_sh = f_sh;
+    a.wrap[0] = wrap_x;
+    a.wrap[1] = wrap_y;
+    a.wrap[2] = wrap_z;
+    a.with_grad = with_grad;
+    a.grad = gb ? gb->grad : nullptr;
+    a.tmask = gb ? gb->tmask : nullptr;
+    a.sums = out_sums;
+    constexpr int NT = 256;
+    tv_kernel<NT><<<blocks(count, NT), NT, 0, (cudaStream_t)stream>>>(make_dgrid(*g), a);
+    return status();
+}
+
+extern "C" int plx_opt_step(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, double lr_sh,
+                            double beta, double eps, int32_t rmsprop, int32_t clear,
+                            int64_t *out_count, void *stream) {
+    if (!g || !gb || !gb->grad || !gb->tmask || (rmsprop && !v) || (g->rows > 0 && !g->table))
+        return PLX_EINVAL;
+    if (g->rows == 0) return PLX_OK;
+    OptArgs a{g->table, v, gb->grad, gb->tmask, g->rows, lr_sigma, lr_sh, beta, eps, rmsprop, clear,
+              1, reinterpret_cast<unsigned long long *>(out_count)};
+    constexpr int NT = 256;
+    const int64_t warps = (g->rows + 3) / 4;
+    opt_kernel<NT><<<blocks(warps * 32, NT), NT, 0, (cudaStream_t)stream>>>(a);
+    return status();
+}
+
+extern "C" int plx_clear_grad(plx_grad *gb, int64_t rows, int64_t *out_count, void *stream) {
+    if (!gb || !gb->grad || !gb->tmask || rows < 0) return PLX_EINVAL;
+    if (rows == 0) return PLX_OK;
+    OptArgs a{nullptr, nullptr, gb->grad, gb->tmask, rows, 0.0, 0.0, 0.0, 0.0, 0, 1, 0,
+              reinterpret_cast<unsigned long long *>(out_count)};
+    constexpr int NT = 256;
+    const int64_t warps = (rows + 3) / 4;
+    opt_kernel<NT><<<blocks(warps * 32, NT), NT, 0, (cudaStream_t)stream>>>(a);
+    return status();
+}
+
+extern "C" int plx_count_touched(const uint8_t *tmask, int64_t rows, int64_t *out_count,
+                                 void *stream) {
+    if (!tmask || !out_count || rows < 0) return PLX_EINVAL;
+    if (rows == 0) return PLX_OK;
+    constexpr int NT = 256;
+    unsigned nb = blocks((rows + 15) / 16, NT);
+    if (nb > 148 * 8) nb = 148 * 8;
+    count_kernel<NT><<<nb, NT, 0, (cudaStream_t)stream>>>(
+        tmask, rows, reinterpret_cast<unsigned long long *>(out_count));
+    return status();
+}
+
+extern "C" int plx_prune_mark(const plx_grid *g, const double *weights, double threshold,
+                              uint8_t *deemed_scratch, uint8_t *flags, void *stream) {
+    if (!grid_ok(g) || !deemed_scratch || !flags) return PLX_EINVAL;
+    const int64_t n = ncell(g);
+    cudaStream_t s = (cudaStream_t)stream;
+    DGrid G = make_dgrid(*g);
+    uint8_t *A = deemed_scratch, *B = deemed_scratch + n;
+    prune_deem_kernel<<<blocks(n, 256), 256, 0, s>>>(G, weights, threshold, A, n);
+    const int64_t Dz = g->dims[2], Dy = g->dims[1], Dx = g->dims[0];
+    dilate_axis_kernel<<<blocks(n, 256), 256, 0, s>>>(A, B, n, 1, Dz, nullptr);
+    dilate_axis_kernel<<<blocks(n, 256), 256, 0, s>>>(B, A, n, Dz, Dy, nullptr);
+    dilate_axis_kernel<<<blocks(n, 256), 256, 0, s>>>(A, flags, n, Dy * Dz, Dx, g->links);
+    return status();
+}
+
+extern "C" int plx_prune_apply(const plx_grid *g, const int32_t *new_links, int64_t *kept_old,
+                               float *new_table, void *stream) {
+    if (!grid_ok(g) || !new_links) return PLX_EINVAL;
+    const int64_t n = ncell(g);
+    prune_apply_kernel<<<blocks(n * 8, 256), 256, 0, (cudaStream_t)stream>>>(
+        make_dgrid(*g), new_links, n, kept_old, new_table);
+    return status();
+}
+
+static UpArgs make_up(const plx_grid *g, const int64_t nd[3]) {
+    UpArgs u;
+    for (int a = 0; a < 3; ++a) {
+        u.N[a] = nd[a];
+        // G:272 spacing = extent / (new_dims - 1.0)
+        u.spacing[a] = (g->hi[a] - g->lo[a]) / ((double)nd[a] - 1.0);
+    }
+    return u;
+}
+
+extern "C" int plx_upsample_mark(const plx_grid *g, const int64_t new_dims[3], uint8_t *flags,
+                                 void *stream) {
+    if (!grid_ok(g) || !new_dims || !flags || new_dims[0] < 2 || new_dims[1] < 2 || new_dims[2] < 2)
+        return PLX_EINVAL;
+    const int64_t n = new_dims[0] * new_dims[1] * new_dims[2];
+    if (n >= (int64_t)1 << 31) return PLX_EINVAL;
+    upsample_mark_kernel<<<blocks(n, 256), 256, 0, (cudaStream_t)stream>>>(make_dgrid(*g),
+                                                                          make_up(g, new_dims), flags, n);
+    return status();
+}
+
+extern "C" int plx_upsample_apply(const plx_grid *g, const int64_t new_dims[3],
+                                  const int32_t *new_links, float *new_table, void *stream) {
+    if (!grid_ok(g) || !new_dims || !new_links) return PLX_EINVAL;
+    const int64_t n = new_dims[0] * new_dims[1] * new_dims[2];
+    upsample_apply_kernel<<<blocks(n * 8, 256), 256, 0, (cudaStream_t)stream>>>(
+        make_dgrid(*g), make_up(g, new_dims), new_links, n, new_table);
+    return status();
+}
+
+extern "C" int64_t plx_scan_scratch_bytes(int64_t n) {
+    return (int64_t)sizeof(int64_t) * ((n + kScanTile - 1) / kScanTile + 1);
+}
+
+extern "C" int plx_scan_ids(const uint8_t *flags, int64_t n, int32_t *ids, int64_t *count,
+                            void *scratch, void *stream) {
+    if (!flags || !ids || !count || !scratch || n < 0) return PLX_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nb = (n + kScanTile - 1) / kScanTile;
+    int64_t *partial = reinterpret_cast<int64_t *>(scratch);
+    if (nb == 0) {
+        cudaMemsetAsync(count, 0, sizeof(int64_t), s);
+        return status();
+    }
+    scan_count_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(flags, n, partial);
+    scan_partials_kernel<<<1, 1024, 0, s>>>(partial, nb, count);
+    scan_write_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(flags, n, partial, ids);
+    return status();
+}
+
+extern "C" int64_t plx_cell_occ_words(const int64_t dims[3]) {
+    return (dims[0] * dims[1] * dims[2] + 31) / 32;
+}
+
+extern "C" int plx_build_cell_occ(const plx_grid *g, uint32_t *cell_occ, void *stream) {
+    if (!grid_ok(g) || !cell_occ) return PLX_EINVAL;
+    const int64_t n = ncell(g), nw = (n + 31) / 32;
+    cell_occ_kernel<<<blocks(nw, 256), 256, 0, (cudaStream_t)stream>>>(make_dgrid(*g), cell_occ, nw, n);
+    return status();
+}
+
+extern "C" const char *plx_version(void) { return "plx-b200 0.1.0 (sm_100a)"; }
+
+extern "C" int plx_device_check(void) {
+    int dev = 0, major = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return 1;
+    return major >= 10 ? 0 : 1;
+}

@@ -1,0 +1,327 @@
+"""Device-resident sparse voxel grid and gradient buffer.
+
+Mirrors pkg/src/plenoxel/grid.py (SparseGrid G:71-320, GradientBuffer
+G:25-68) with HBM-resident storage:
+
+  links   torch.int32  (Dx, Dy, Dz) C-order, -1 = empty      4 B / cell
+  table   torch.float32 (rows, 28): sigma, 27 SH (112 B, 7 x float4 / row)
+  grad    torch.float32 (rows, 28)  (GradientBuffer.data)
+  tmask   torch.uint8   (rows,)     (GradientBuffer.touched_mask)
+
+Structure ops (prune, upsample, max_weight_accumulate) run on the device
+through libplx.so; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import ROW
+from .sh import SH_C0
+
+EMPTY = -1
+ROW_SIZE = ROW
+
+# Empty-space skipping through the per-cell occupancy bitmask (an exact
+# shortcut: a cell whose 8 corners are all empty has occ == False, K:126-135).
+USE_CELL_OCC = True
+
+
+def _dev(device):
+    return torch.device(device if device is not None else "cuda")
+
+
+class GradientBuffer:
+    """Sparse accumulator of per-row gradients (G:25-68).
+
+    `touched_mask` marks rows that received any contribution; the reference's
+    insertion-ordered `touched_ids` list is not materialised (only its sorted
+    view `touched_rows()` and its length `n_touched` are observable)."""
+
+    def __init__(self, n_rows: int, device=None):
+        dev = _dev(device)
+        self.data = torch.zeros((int(n_rows), ROW), dtype=torch.float32, device=dev)
+        self.touched_mask = torch.zeros(int(n_rows), dtype=torch.uint8, device=dev)
+        self._count = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    @property
+    def n_rows(self) -> int:
+        return self.data.shape[0]
+
+    def _c(self) -> _lib.PlxGrad:
+        g = _lib.PlxGrad()
+        g.grad = self.data.data_ptr()
+        g.tmask = self.touched_mask.data_ptr()
+        return g
+
+    def count_touched_async(self) -> torch.Tensor:
+        """Device int64[1] holding n_touched (no host sync)."""
+        self._count.zero_()
+        if self.n_rows:
+            _lib.check(_lib.lib().plx_count_touched(
+                self.touched_mask.data_ptr(), self.n_rows, self._count.data_ptr(),
+                _lib.stream_ptr()), "count_touched")
+        return self._count
+
+    @property
+    def n_touched(self) -> int:
+        return int(self.count_touched_async().item())
+
+    def touched_rows(self) -> np.ndarray:
+        return torch.nonzero(self.touched_mask).flatten().cpu().numpy().astype(np.int64)
+
+    def nnz_fraction(self) -> float:
+        return self.n_touched / max(self.n_rows, 1)
+
+    def add(self, row: int, values) -> None:
+        values = torch.as_tensor(np.asarray(values, dtype=np.float64),
+                                 dtype=torch.float32, device=self.data.device)
+        if values.shape != (ROW,):
+            raise ValueError(f"expected {ROW} gradient values")
+        self.touched_mask[row] = 1
+        self.data[row] += values
+
+    def clear(self) -> None:
+        """clear_grad (K:593-600): zero touched rows, reset the mask."""
+        if self.n_rows:
+            _lib.check(_lib.lib().plx_clear_grad(ctypes.byref(self._c()), self.n_rows, None,
+                                                 _lib.stream_ptr()), "clear_grad")
+
+    def dense(self) -> np.ndarray:
+        return self.data.double().cpu().numpy()
+
+
+class SparseGrid:
+    """Dense int32 pointer lattice + f32 data table in HBM (G:71-320)."""
+
+    def __init__(self, links, table, aabb_min, aabb_max, device=None):
+        dev = _dev(device if device is not None else
+                   (links.device if isinstance(links, torch.Tensor) and links.is_cuda else None))
+        links = torch.as_tensor(links) if not isinstance(links, torch.Tensor) else links
+        table = torch.as_tensor(np.asarray(table)) if not isinstance(table, torch.Tensor) else table
+        if links.dim() != 3:
+            raise ValueError("links must be a 3-d lattice")
+        if any(int(d) < 2 for d in links.shape):
+            raise ValueError("grid needs at least 2 lattice points per axis")
+        if table.dim() != 2 or table.shape[1] != ROW:
+            raise ValueError(f"table must be (rows, {ROW})")
+        self._links = links.to(device=dev, dtype=torch.int32).contiguous()
+        self.table = table.to(device=dev, dtype=torch.float32).contiguous()
+        self.aabb_min = np.asarray(aabb_min, dtype=np.float64).reshape(3).copy()
+        self.aabb_max = np.asarray(aabb_max, dtype=np.float64).reshape(3).copy()
+        if np.any(self.aabb_max <= self.aabb_min):
+            raise ValueError("degenerate AABB")
+        if int(np.prod(self.dims)) >= 2 ** 31:
+            raise ValueError("lattice too large for int32 cell ids")
+        self._cell_occ = None
+
+    # -- constructors -------------------------------------------------------
+    @classmethod
+    def dense(cls, dims, aabb_min, aabb_max, sigma: float = 0.0, rgb: float | None = None,
+              device=None) -> "SparseGrid":
+        """G:96-109: fully occupied; DC coefficients = rgb / SH_C0."""
+        dims = tuple(int(d) for d in dims)
+        dev = _dev(device)
+        n = dims[0] * dims[1] * dims[2]
+        links = torch.arange(n, dtype=torch.int32, device=dev).reshape(dims)
+        table = torch.zeros((n, ROW), dtype=torch.float32, device=dev)
+        table[:, 0] = sigma
+        if rgb is not None:
+            for ch in range(3):
+                table[:, 1 + 9 * ch] = rgb / SH_C0
+        return cls(links, table, aabb_min, aabb_max, device=dev)
+
+    @classmethod
+    def empty(cls, dims, aabb_min, aabb_max, device=None) -> "SparseGrid":
+        dims = tuple(int(d) for d in dims)
+        dev = _dev(device)
+        return cls(torch.full(dims, EMPTY, dtype=torch.int32, device=dev),
+                   torch.zeros((0, ROW), dtype=torch.float32, device=dev),
+                   aabb_min, aabb_max, device=dev)
+
+    # -- storage ------------------------------------------------------------
+    @property
+    def links(self) -> torch.Tensor:
+        return self._links
+
+    @links.setter
+    def links(self, value) -> None:
+        self._links = torch.as_tensor(value).to(self._links.device, torch.int32).contiguous()
+        self._cell_occ = None
+
+    @property
+    def device(self):
+        return self.table.device
+
+    @property
+    def dims(self) -> tuple[int, int, int]:
+        return tuple(int(d) for d in self._links.shape)
+
+    @property
+    def n_rows(self) -> int:
+        return int(self.table.shape[0])
+
+    @property
+    def extent(self) -> np.ndarray:
+        return self.aabb_max - self.aabb_min
+
+    @property
+    def voxel_size(self) -> np.ndarray:
+        return self.extent / (np.array(self.dims, dtype=np.float64) - 1.0)
+
+    @property
+    def lattice_scale(self) -> np.ndarray:
+        return (np.array(self.dims, dtype=np.float64) - 1.0) / self.extent
+
+    def world_to_lattice(self, pts) -> np.ndarray:
+        return (np.asarray(pts, dtype=np.float64) - self.aabb_min) * self.lattice_scale
+
+    def lattice_to_world(self, ijk) -> np.ndarray:
+        return self.aabb_min + np.asarray(ijk, dtype=np.float64) * self.voxel_size
+
+    def invalidate(self) -> None:
+        """Call after editing `links` in place (drops the cell bitmask)."""
+        self._cell_occ = None
+
+    def cell_occ(self) -> torch.Tensor:
+        if self._cell_occ is None:
+            words = _lib.load().plx_cell_occ_words(_lib.dims_array(self.dims))
+            occ = torch.empty(int(words), dtype=torch.int32, device=self.device)
+            c = self._c(with_occ=False)
+            _lib.check(_lib.lib().plx_build_cell_occ(ctypes.byref(c), occ.data_ptr(),
+                                                     _lib.stream_ptr()), "build_cell_occ")
+            self._cell_occ = occ
+        return self._cell_occ
+
+    def _c(self, with_occ: bool = True) -> _lib.PlxGrid:
+        g = _lib.PlxGrid()
+        g.links = self._links.data_ptr()
+        g.table = self.table.data_ptr() if self.n_rows else None
+        g.dims = _lib.dims_array(self.dims)
+        g.rows = self.n_rows
+        g.lo = (ctypes.c_double * 3)(*self.aabb_min)
+        g.hi = (ctypes.c_double * 3)(*self.aabb_max)
+        g.scale = (ctypes.c_double * 3)(*self.lattice_scale)
+        g.dmax = (ctypes.c_double * 3)(*(np.array(self.dims, dtype=np.float64) - 1.0))
+        g.cell_occ = self.cell_occ().data_ptr() if (with_occ and USE_CELL_OCC) else None
+        return g
+
+    def to_numpy(self):
+        """(links int32 (Dx,Dy,Dz), table float32 (rows, 28)) host copies."""
+        return self._links.cpu().numpy(), self.table.cpu().numpy()
+
+    def copy(self) -> "SparseGrid":
+        return SparseGrid(self._links.clone(), self.table.clone(), self.aabb_min.copy(),
+                          self.aabb_max.copy(), device=self.device)
+
+    def occupancy(self) -> torch.Tensor:
+        return self._links >= 0
+
+    # -- structure ops ------------------------------------------------------
+    def _compact(self, flags: torch.Tensor):
+        """flags (ncell uint8) -> (new_links int32 (ncell), n) via plx_scan_ids."""
+        n = flags.numel()
+        L = _lib.lib()
+        scratch = torch.empty(int(L.plx_scan_scratch_bytes(n)), dtype=torch.uint8,
+                              device=self.device)
+        ids = torch.empty(n, dtype=torch.int32, device=self.device)
+        count = torch.zeros(1, dtype=torch.int64, device=self.device)
+        _lib.check(L.plx_scan_ids(flags.data_ptr(), n, ids.data_ptr(), count.data_ptr(),
+                                  scratch.data_ptr(), _lib.stream_ptr()), "scan_ids")
+        return ids, int(count.item())
+
+    def prune(self, criterion: str, threshold: float, weights=None):
+        """G:228-258 -> (new_grid, kept_old_rows torch.int64)."""
+        if criterion == "weight":
+            if weights is None:
+                raise ValueError("weight criterion needs per-row max weights")
+            w = torch.as_tensor(weights).to(self.device, torch.float64).contiguous()
+            if tuple(w.shape) != (self.n_rows,):
+                raise ValueError("weights must have one entry per data row")
+        elif criterion == "density":
+            w = None
+        else:
+            raise ValueError(f"unknown prune criterion {criterion!r}")
+        L = _lib.lib()
+        ncell = int(np.prod(self.dims))
+        scratch = torch.empty(2 * ncell, dtype=torch.uint8, device=self.device)
+        flags = torch.empty(ncell, dtype=torch.uint8, device=self.device)
+        c = self._c(with_occ=False)
+        s = _lib.stream_ptr()
+        _lib.check(L.plx_prune_mark(ctypes.byref(c), _lib.ptr(w), float(threshold),
+                                    scratch.data_ptr(), flags.data_ptr(), s), "prune_mark")
+        del scratch
+        ids, n_keep = self._compact(flags)
+        kept = torch.empty(max(n_keep, 1), dtype=torch.int64, device=self.device)
+        table = torch.empty((n_keep, ROW), dtype=torch.float32, device=self.device)
+        if n_keep:
+            _lib.check(L.plx_prune_apply(ctypes.byref(c), ids.data_ptr(), kept.data_ptr(),
+                                         table.data_ptr(), s), "prune_apply")
+        grid = SparseGrid(ids.reshape(self.dims), table, self.aabb_min, self.aabb_max,
+                          device=self.device)
+        return grid, kept[:n_keep]
+
+    def upsample(self, new_dims) -> "SparseGrid":
+        """G:260-285.  A 0-row grid upsamples to an empty grid (the reference
+        raises IndexError there, G:277-278)."""
+        new_dims = tuple(int(d) for d in new_dims)
+        if any(d < 2 for d in new_dims):
+            raise ValueError("upsample needs at least 2 points per axis")
+        if self.n_rows == 0:
+            return SparseGrid.empty(new_dims, self.aabb_min, self.aabb_max, device=self.device)
+        L = _lib.lib()
+        nd = _lib.dims_array(new_dims)
+        ncell = int(np.prod(new_dims))
+        flags = torch.empty(ncell, dtype=torch.uint8, device=self.device)
+        c = self._c(with_occ=False)
+        s = _lib.stream_ptr()
+        _lib.check(L.plx_upsample_mark(ctypes.byref(c), nd, flags.data_ptr(), s),
+                   "upsample_mark")
+        ids, n_new = self._compact(flags)
+        del flags
+        table = torch.empty((n_new, ROW), dtype=torch.float32, device=self.device)
+        if n_new:
+            _lib.check(L.plx_upsample_apply(ctypes.byref(c), nd, ids.data_ptr(),
+                                            table.data_ptr(), s), "upsample_apply")
+        return SparseGrid(ids.reshape(new_dims), table, self.aabb_min, self.aabb_max,
+                          device=self.device)
+
+    def max_weight_accumulate(self, origins, dirs, step_frac: float = 0.5,
+                              stop_thresh: float = 1e-4, interp: str = "trilinear",
+                              chunk: int = 1 << 22):
+        """G:287-302: per-row max of T*(1-exp(-sigma*delta)) over the rays.
+        Returns float64 weights (numpy if the inputs are numpy)."""
+        from .render import _ray_tensor
+        as_np = not isinstance(origins, torch.Tensor)
+        o = _ray_tensor(origins, self.device)
+        d = _ray_tensor(dirs, self.device)
+        out = torch.zeros(self.n_rows, dtype=torch.float64, device=self.device)
+        step = step_frac * float(np.min(self.voxel_size))
+        opts = _lib.make_opts(step, stop_thresh, (0, 0, 0), interp == "nearest", False)
+        c = self._c()
+        L = _lib.lib()
+        for s0 in range(0, o.shape[0], chunk):
+            r = _lib.PlxRays()
+            r.origins = o[s0:s0 + chunk].data_ptr()
+            r.dirs = d[s0:s0 + chunk].data_ptr()
+            r.n = min(chunk, o.shape[0] - s0)
+            _lib.check(L.plx_max_weight(ctypes.byref(c), ctypes.byref(r), ctypes.byref(opts),
+                                        out.data_ptr(), _lib.stream_ptr()), "max_weight")
+        return out.cpu().numpy() if as_np else out
+
+    # -- consistency --------------------------------------------------------
+    def validate(self) -> None:
+        """G:306-316: links/table bijection and finite values."""
+        rows = self._links[self._links >= 0].long()
+        if rows.numel() != self.n_rows:
+            raise AssertionError("row count does not match occupied cells")
+        if rows.numel():
+            counts = torch.bincount(rows, minlength=self.n_rows)
+            if int(rows.max()) >= self.n_rows or not bool(torch.all(counts == 1)):
+                raise AssertionError("links and table rows are not a bijection")
+        if not bool(torch.all(torch.isfinite(self.table))):
+            raise AssertionError("non-finite values in data table")

@@ -1,0 +1,255 @@
+"""Differentiable volume rendering on the B200 (drop-in for
+pkg/src/plenoxel/render.py).
+
+Same public surface and argument meaning as the reference: RenderOptions
+(R:27-42), march (R:72-95), render_rays (R:114-140), render_ray (R:143-155),
+render_rays_backward (R:205-239), render_ray_backward (R:242-250),
+fused_mse_backward (R:253-279), render_image (R:282-293).  Each call enqueues
+one sm_100a kernel through libplx.so.  Inputs may be numpy arrays (results
+come back as numpy, like the reference) or CUDA tensors (results stay on the
+device, no host synchronisation except for returned Python scalars).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .grid import GradientBuffer, SparseGrid
+from .sh import normalize_dirs
+
+
+@dataclass
+class RenderOptions:
+    step_frac: float = 0.5
+    stop_thresh: float = 1e-4
+    background: tuple = (1.0, 1.0, 1.0)
+    interp: str = "trilinear"
+    formula: str = "relative"
+    jitter: float = 0.0
+
+    def __post_init__(self):
+        if self.step_frac <= 0:
+            raise ValueError("step_frac must be positive")
+        if self.interp not in ("trilinear", "nearest"):
+            raise ValueError(f"unknown interpolation mode {self.interp!r}")
+        if self.formula not in ("relative", "absolute"):
+            raise ValueError(f"unknown rendering formula {self.formula!r}")
+
+
+@dataclass
+class RenderResult:
+    rgb: np.ndarray
+    trans: float
+    weight_sum: float
+    samples: list = field(default_factory=list)
+
+
+def _step_size(grid: SparseGrid, step_frac: float) -> float:
+    return step_frac * float(np.min(grid.voxel_size))          # R:63-64
+
+
+def _max_samples(grid: SparseGrid, step: float) -> int:
+    return int(math.ceil(float(np.linalg.norm(grid.extent)) / step)) + 4   # R:67-69
+
+
+def kernel_opts(grid: SparseGrid, opts: RenderOptions) -> _lib.PlxRenderOpts:
+    return _lib.make_opts(_step_size(grid, opts.step_frac), opts.stop_thresh, opts.background,
+                          opts.interp == "nearest", opts.formula == "absolute")
+
+
+def march(grid: SparseGrid, origin, direction, step_frac: float = 0.5):
+    """Uniform samples along the chord (R:72-95), host float64."""
+    o = np.asarray(origin, dtype=np.float64)
+    d = np.asarray(direction, dtype=np.float64)
+    t0, t1 = 0.0, math.inf
+    for a in range(3):
+        if abs(d[a]) < 1e-15:
+            if o[a] < grid.aabb_min[a] or o[a] > grid.aabb_max[a]:
+                return np.empty(0), np.empty(0)
+        else:
+            ta = (grid.aabb_min[a] - o[a]) / d[a]
+            tb = (grid.aabb_max[a] - o[a]) / d[a]
+            ta, tb = min(ta, tb), max(ta, tb)
+            t0, t1 = max(t0, ta), min(t1, tb)
+    length = t1 - t0
+    if length <= 0.0:
+        return np.empty(0), np.empty(0)
+    step = _step_size(grid, step_frac)
+    n = max(1, int(math.ceil(length / step - 1e-9)))
+    ts = t0 + np.arange(n) * step
+    deltas = np.full(n, step)
+    deltas[-1] = length - step * (n - 1)
+    return ts, deltas
+
+
+def _ray_tensor(x, device) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=device, dtype=torch.float64)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.atleast_2d(x), dtype=np.float64)).to(device)
+    t = t.reshape(-1, 3) if t.dim() == 1 else t
+    if t.dim() != 2 or t.shape[1] != 3:
+        raise ValueError("origins and directions must both be (N, 3)")
+    return t.contiguous()
+
+
+def _jitter_offsets(n: int, jitter: float, rng):
+    if jitter <= 0.0:
+        return None
+    if rng is None:
+        rng = np.random.default_rng()
+    return rng.random(n) * jitter                               # R:106-111
+
+
+def _batch(grid, origins, dirs, viewdirs, target=None, jitter=None):
+    dev = grid.device
+    o = _ray_tensor(origins, dev)
+    d = _ray_tensor(dirs, dev)
+    if o.shape != d.shape:
+        raise ValueError("origins and directions must both be (N, 3)")
+    if viewdirs is None:
+        if isinstance(dirs, torch.Tensor):
+            v = (d / torch.linalg.norm(d, dim=-1, keepdim=True)).contiguous()
+        else:
+            v = _ray_tensor(normalize_dirs(np.atleast_2d(dirs)), dev)
+    else:
+        v = _ray_tensor(viewdirs, dev)
+    tg = _ray_tensor(target, dev) if target is not None else None
+    jt = None
+    if jitter is not None:
+        jt = torch.from_numpy(np.ascontiguousarray(jitter, np.float64)).to(dev)
+    r = _lib.PlxRays()
+    r.origins, r.dirs, r.viewdirs = o.data_ptr(), d.data_ptr(), v.data_ptr()
+    r.target = _lib.ptr(tg)
+    r.jitter = _lib.ptr(jt)
+    r.idx = None
+    r.n = o.shape[0]
+    keep = (o, d, v, tg, jt)        # keep device buffers alive until launch
+    return r, keep
+
+
+def render_rays(grid: SparseGrid, origins, dirs, opts: RenderOptions | None = None,
+                viewdirs=None, rng=None):
+    """R:114-140 -> (rgb (N,3), trans (N,), weight_sum (N,)), float64."""
+    opts = opts or RenderOptions()
+    as_np = not isinstance(origins, torch.Tensor)
+    n = int(np.atleast_2d(origins).shape[0]) if as_np else int(origins.reshape(-1, 3).shape[0])
+    r, keep = _batch(grid, origins, dirs, viewdirs,
+                     jitter=_jitter_offsets(n, opts.jitter, rng))
+    dev = grid.device
+    rgb = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    trans = torch.empty(n, dtype=torch.float64, device=dev)
+    wsum = torch.empty(n, dtype=torch.float64, device=dev)
+    if grid.n_rows == 0:
+        rgb[:] = torch.as_tensor(np.asarray(opts.background, np.float64), device=dev)
+        trans.fill_(1.0)
+        wsum.zero_()
+    else:
+        c, ko = grid._c(with_occ=opts.interp == "trilinear"), kernel_opts(grid, opts)
+        _lib.check(_lib.lib().plx_render_fwd(ctypes.byref(c), ctypes.byref(r), ctypes.byref(ko),
+                                             rgb.data_ptr(), trans.data_ptr(), wsum.data_ptr(),
+                                             _lib.stream_ptr()), "render_fwd")
+    del keep
+    if as_np:
+        return rgb.cpu().numpy(), trans.cpu().numpy(), wsum.cpu().numpy()
+    return rgb, trans, wsum
+
+
+def render_ray(grid: SparseGrid, origin, direction, opts: RenderOptions | None = None,
+               viewdir=None, record: bool = False) -> RenderResult:
+    """R:143-155 (the record=True numpy twin is a reference-side test aid and
+    is not provided on the device path)."""
+    if record:
+        raise NotImplementedError("record=True is the reference's numpy twin (R:158-202)")
+    vd = None if viewdir is None else np.atleast_2d(viewdir)
+    rgb, trans, wsum = render_rays(grid, np.atleast_2d(origin), np.atleast_2d(direction),
+                                   opts, vd)
+    return RenderResult(rgb=rgb[0], trans=float(trans[0]), weight_sum=float(wsum[0]))
+
+
+def _launch_bwd(grid, r, opts, mse_mode, up_scale, lam_cauchy, grads, rgb, sums):
+    if grid.n_rows == 0:
+        raise ValueError("cannot backpropagate into an empty grid")
+    if grads.n_rows != grid.n_rows:
+        raise ValueError("gradient buffer rows do not match the grid table")
+    c, ko, gb = grid._c(with_occ=opts.interp == "trilinear"), kernel_opts(grid, opts), grads._c()
+    _lib.check(_lib.lib().plx_render_fused_bwd(
+        ctypes.byref(c), ctypes.byref(r), ctypes.byref(ko), int(mse_mode), float(up_scale),
+        float(lam_cauchy), ctypes.byref(gb), _lib.ptr(rgb), sums.data_ptr(),
+        _lib.stream_ptr()), "render_fused_bwd")
+
+
+def render_rays_backward(grid: SparseGrid, origins, dirs, upstream, grads: GradientBuffer,
+                         opts: RenderOptions | None = None, viewdirs=None,
+                         lam_cauchy: float = 0.0, rng=None):
+    """R:205-239: scatter dL/dC (N,3) -> grads.  Returns (rgb, cauchy_raw)."""
+    opts = opts or RenderOptions()
+    as_np = not isinstance(origins, torch.Tensor)
+    r, keep = _batch(grid, origins, dirs, viewdirs, target=upstream)
+    r.jitter = None
+    jt = _jitter_offsets(r.n, opts.jitter, rng)
+    if jt is not None:
+        jtt = torch.from_numpy(jt).to(grid.device)
+        r.jitter = jtt.data_ptr()
+    rgb = torch.empty((r.n, 3), dtype=torch.float64, device=grid.device)
+    sums = torch.zeros(2, dtype=torch.float64, device=grid.device)
+    _launch_bwd(grid, r, opts, False, 0.0, lam_cauchy, grads, rgb, sums)
+    del keep
+    cauchy = float(sums[1].item())
+    return (rgb.cpu().numpy() if as_np else rgb), cauchy
+
+
+def render_ray_backward(grid: SparseGrid, origin, direction, upstream,
+                        opts: RenderOptions | None = None, viewdir=None) -> GradientBuffer:
+    """R:242-250."""
+    grads = GradientBuffer(grid.n_rows, device=grid.device)
+    vd = None if viewdir is None else np.atleast_2d(viewdir)
+    render_rays_backward(grid, np.atleast_2d(origin), np.atleast_2d(direction),
+                         np.atleast_2d(upstream), grads, opts, vd)
+    return grads
+
+
+def fused_mse_backward(grid: SparseGrid, origins, dirs, viewdirs, gt_rgb,
+                       grads: GradientBuffer, opts: RenderOptions, n_total: int,
+                       lam_cauchy: float = 0.0, rng=None, sums: torch.Tensor | None = None):
+    """R:253-279: forward render + MSE upstream 2(C-gt)/n_total + reverse
+    sweep in ONE kernel.  Returns (rgb, mse_sum, cauchy_raw).
+
+    Pass a device float64[2] `sums` to accumulate the two scalars on the
+    device instead (then they are returned as that tensor, no host sync)."""
+    as_np = not isinstance(origins, torch.Tensor)
+    r, keep = _batch(grid, origins, dirs, viewdirs, target=gt_rgb)
+    jt = _jitter_offsets(r.n, opts.jitter, rng)
+    if jt is not None:
+        jtt = torch.from_numpy(jt).to(grid.device)
+        r.jitter = jtt.data_ptr()
+    rgb = torch.empty((r.n, 3), dtype=torch.float64, device=grid.device)
+    dev_sums = sums if sums is not None else torch.zeros(2, dtype=torch.float64,
+                                                         device=grid.device)
+    _launch_bwd(grid, r, opts, True, 2.0 / n_total, lam_cauchy, grads, rgb, dev_sums)
+    del keep
+    out_rgb = rgb.cpu().numpy() if as_np else rgb
+    if sums is not None:
+        return out_rgb, dev_sums, None
+    s = dev_sums.cpu().numpy()
+    return out_rgb, float(s[0]), float(s[1])
+
+
+def render_image(grid: SparseGrid, camera, opts: RenderOptions | None = None,
+                 chunk: int = 1 << 20) -> np.ndarray:
+    """R:282-293: full camera view -> (H, W, 3) float64 image."""
+    from .camera import generate_rays
+
+    opts = opts or RenderOptions()
+    origins, dirs = generate_rays(camera)
+    out = np.empty((camera.height * camera.width, 3))
+    for s in range(0, origins.shape[0], chunk):
+        rgb, _, _ = render_rays(grid, origins[s:s + chunk], dirs[s:s + chunk], opts)
+        out[s:s + chunk] = rgb
+    return out.reshape(camera.height, camera.width, 3)
