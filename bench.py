@@ -1,0 +1,420 @@
+#!/usr/bin/env python3
+"""Benchmark: Plenoxels training steps (fused forward + backward + TV +
+RMSProp update) on B200, BASELINE.json configs[1]:
+
+  synthetic Blender-style bounded scene (the reference's procedural toy scene,
+  100 hemisphere views x 200^2 px), dense 256^3 grid at the trainer's init
+  (sigma 0.1, rgb 0.1), SH degree 2, TV regularisation (1% cells), RMSProp
+  with default_config('bounded') schedules, 5000-ray batches per GPU.
+
+One JSON line on rank 0 (contract in the task statement):
+  value   rays/s of the device-resident step (ray pool in HBM, batch indices
+          drawn by the reference's EpochBatcher RNG), K steps timed with CUDA
+          events, max over ranks, weak scaling (5000 rays per GPU)
+  e2e     the same step through the public API with the batch arrays in
+          pinned HOST memory: H2D of o/d/viewdir/gt + the kernels + D2H of the
+          loss sums, every step
+  roofline the dominant kernel's algorithmic bytes / its event-timed duration
+  cpu_baseline the CPU oracle (sequential f64 C port of the reference
+          kernels, 1 core) on the same step, rank 0 at N=1
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train rays/sec (fwd+bwd+update) at 1/2/4/8 B200; HBM GB/s vs peak; PSNR match"
+WORKLOAD = "C2: bounded synthetic scene, dense 256^3 init, SH2, TV + RMSProp, 5000 rays/GPU"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--batch", type=int, default=5000)
+    p.add_argument("--dims", type=int, default=256)
+    p.add_argument("--views", type=int, default=100)
+    p.add_argument("--res", type=int, default=200)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-steps", type=int, default=2)
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ utils --
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def toy_scene(n_views, res, device):
+    """Synthetic training set: the reference's toy scene rendered on device."""
+    from paper_2112_05131_b200 import scenes
+
+    train, _, _ = scenes.make_toy_dataset(n_views=n_views, res=res, n_test=1, grid_dim=64,
+                                          device=device)
+    return train
+
+
+def bench_config(args):
+    from paper_2112_05131_b200 import trainer
+
+    cfg = trainer.default_config("bounded")
+    cfg.ladder = [trainer.LadderRung(0, (args.dims,) * 3)]
+    cfg.batch_size = args.batch * args.gpus      # global batch; 5000 rays per GPU
+    cfg.log_every = 0
+    cfg.eval_every = 0
+    return cfg
+
+
+# ------------------------------------------------------------ CPU oracle --
+def oracle_steps(args, n_steps, ds, time_budget_s=None):
+    """The reference's step body (T:455-486: fused_mse_backward + tv_loss +
+    optim.step + grads.clear) through the f64 C port, on one host core.
+    Returns (rays_per_s, steps_timed, sample description)."""
+    from oracle import oracle as orc
+    from paper_2112_05131_b200 import optim as popt
+    from paper_2112_05131_b200.camera import all_rays
+
+    o, m, v, gt = all_rays(ds.images, ds.cameras)
+    cfg = bench_config(args)
+    B = args.batch
+    lo, hi = np.array(cfg.aabb[:3]), np.array(cfg.aabb[3:])
+    g = orc.Grid.dense((args.dims,) * 3, lo, hi, sigma=cfg.init_sigma, rgb=cfg.init_rgb)
+    v_state = np.zeros_like(g.table)
+    buf = orc.GradBuf(g.n_rows)
+    rng = np.random.default_rng(cfg.seed)
+    perm = rng.permutation(o.shape[0])
+    times = []
+    t_start = time.perf_counter()
+    for step in range(n_steps + 1):
+        idx = perm[(step * B) % len(perm):][:B]
+        t0 = time.perf_counter()
+        orc.fused_mse_backward(g, o[idx], m[idx], v[idx], gt[idx], buf, B,
+                               step_frac=cfg.step_frac, stop_thresh=cfg.stop_thresh,
+                               background=cfg.background)
+        cells = orc.sample_tv_cells(g.dims, cfg.tv_sample_frac, rng)
+        orc.tv_loss(g, cells, cfg.lambda_tv_sigma, cfg.lambda_tv_sh, buf)
+        orc.opt_step(g, buf, v_state, popt.lr_at(cfg.lr_sigma, step), popt.lr_at(cfg.lr_sh, step))
+        buf.clear()
+        dt = time.perf_counter() - t0
+        if step > 0:     # discard the first step (first-touch page faults)
+            times.append(dt)
+        if time_budget_s and time.perf_counter() - t_start > time_budget_s and times:
+            break
+    sample = (f"{len(times)} timed step(s) of {B} rays (+1 discarded), dense {args.dims}^3 f64 "
+              f"grid, TV 1% cells, RMSProp; sequential C port of K:173-600, 1 thread")
+    return B / float(np.mean(times)), len(times), sample
+
+
+def oracle_scene(n_views, res):
+    """Scene for a box without a GPU (not used on the B200 box)."""
+    from oracle import oracle as orc
+    from paper_2112_05131_b200 import scenes
+    from paper_2112_05131_b200.camera import generate_rays
+
+    table, shape = scenes.toy_grid_arrays(64)
+    g = orc.Grid(np.arange(table.shape[0], dtype=np.int32).reshape(shape), table,
+                 (-1.1,) * 3, (1.1,) * 3)
+    g, _ = orc.prune(g, "density", 1e-6)
+    cams, _ = scenes.hemisphere_cameras(n_views, res, phase=1.0)
+    imgs = []
+    for cam in cams:
+        o, d = generate_rays(cam)
+        rgb, _, _ = orc.render_rays(g, o, d)
+        imgs.append((np.rint(np.clip(rgb, 0, 1) * 255) / 255.0).astype(np.float32)
+                    .reshape(res, res, 3))
+    return scenes.Dataset(np.stack(imgs), cams)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    budget = 150.0
+    # the scene is rendered by the oracle itself: nothing of ours on this arm
+    n_views = max(1, min(args.views, -(-(args.steps + 1) * args.batch // (args.res ** 2))))
+    ds = oracle_scene(n_views, args.res)
+    rps, k, sample = oracle_steps(args, max(1, args.steps), ds, time_budget_s=budget)
+    line = {"impl": "reference", "metric": METRIC, "value": rps, "unit": "rays/s",
+            "n_gpus": args.gpus, "steps": k, "warmup": 1, "ms_per_step": 1000.0 * args.batch / rps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "grid": f"{args.dims}^3",
+                                            "rays_per_step": args.batch},
+            "cpu_baseline": {"value": rps, "unit": "rays/s", "cores": 1, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": rps, "unit": "rays/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ our kernels --
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world_size = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world_size > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2112_05131_b200 import losses, optim, render, trainer
+    from paper_2112_05131_b200.dist import World, reduce_gradients, shard_range
+
+    world = World(rank, world_size) if world_size > 1 else World()
+    assert args.gpus == world_size, "--gpus must match the launched world size"
+
+    ds = toy_scene(args.views, args.res, dev)
+    cfg = bench_config(args)
+    tr = trainer.Trainer(ds, cfg, device=dev, world=world)
+    B_local = args.batch
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world_size > 1:
+            dist.barrier()
+
+    for s in range(args.warmup):
+        tr.step(s)
+    torch.cuda.synchronize()
+
+    # -- timed region: K device-resident steps -------------------------------
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(3)]
+    per_kernel = {"render_fused_bwd": [], "tv": [], "opt_step": []}
+    kernel_events = []
+    counts = torch.zeros(args.steps, dtype=torch.int64, device=dev)
+
+    # instrument the three launches of a step with events on the launching stream
+    orig_fused, orig_tv, orig_opt = render.fused_mse_backward_pool, losses.tv_loss, optim.step
+
+    def wrap(fn, name):
+        def inner(*a, **k):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out = fn(*a, **k)
+            e1.record(stream)
+            kernel_events.append((name, e0, e1))
+            return out
+        return inner
+
+    render.fused_mse_backward_pool = wrap(orig_fused, "render_fused_bwd")
+    losses.tv_loss = wrap(orig_tv, "tv")
+    optim.step = wrap(orig_opt, "opt_step")
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    t_ev0, t_ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_ev0.record(stream)
+    for k in range(args.steps):
+        tr.step(args.warmup + k)
+        counts[k].copy_(tr.count[0])
+    t_ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    render.fused_mse_backward_pool, losses.tv_loss, optim.step = orig_fused, orig_tv, orig_opt
+    ms = t_ev0.elapsed_time(t_ev1) / args.steps
+    for name, e0, e1 in kernel_events:
+        per_kernel[name].append(e0.elapsed_time(e1))
+    U = float(counts.double().mean().item())
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world_size > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    value = args.batch * world_size / (ms / 1000.0)
+
+    # -- per-kernel row counts at the same state (one extra, untimed step) ----
+    U_render = None
+    s_step = args.warmup + args.steps
+    idx = tr.batcher.next_device()
+    s0, c0 = shard_range(idx.numel(), rank, world_size)
+    tr.sums.zero_()
+    render.fused_mse_backward_pool(tr.grid, tr.pool, idx[s0:s0 + c0], tr.grads, tr.opts,
+                                   n_total=idx.numel(), lam_cauchy=0.0, sums=tr.sums[0:2])
+    U_render = tr.grads.n_touched
+    tr.grads.clear()
+
+    # -- e2e: public API with pinned host batches ------------------------------
+    from paper_2112_05131_b200.camera import all_rays
+    o, m, v, gt = all_rays(ds.images, ds.cameras)
+    rng = np.random.default_rng(1234 + rank)
+    K2, W2 = args.steps, min(args.warmup, 3)
+    host = []
+    for _ in range(K2 + W2):
+        sel = rng.integers(0, o.shape[0], B_local)
+        host.append([torch.from_numpy(np.ascontiguousarray(a[sel])).pin_memory()
+                     for a in (o, m, v, gt)])
+    dbuf = [torch.empty((B_local, 3), dtype=torch.float64, device=dev) for _ in range(4)]
+    sums = torch.zeros(4, dtype=torch.float64, device=dev)
+    hsums = torch.zeros(4, dtype=torch.float64).pin_memory()
+    h2d = 4 * B_local * 3 * 8
+    d2h = 4 * 8
+
+    def e2e_step(step, hb):
+        for dsti, src in zip(dbuf, hb):
+            dsti.copy_(src, non_blocking=True)
+        sums.zero_()
+        render.fused_mse_backward(tr.grid, dbuf[0], dbuf[1], dbuf[2], dbuf[3], tr.grads, tr.opts,
+                                  n_total=B_local * world_size, sums=sums[0:2])
+        run = losses.sample_tv_cells(tr.grid, cfg.tv_sample_frac, tr.rng)
+        losses.tv_loss(tr.grid, run.split(rank, world_size), cfg.lambda_tv_sigma,
+                       cfg.lambda_tv_sh, tr.grads, sums=sums[2:4], n_norm=run.count)
+        reduce_gradients(world, tr.grads.data, tr.grads.touched_mask, sums)
+        hsums.copy_(sums, non_blocking=True)
+        stream.synchronize()                      # the loss reaches the host every step
+        assert np.isfinite(hsums.numpy()).all()
+        optim.step(tr.grid, tr.grads, tr.state, optim.lr_at(cfg.lr_sigma, step),
+                   optim.lr_at(cfg.lr_sh, step), clear=True)
+
+    for i in range(W2):
+        e2e_step(s_step + i, host[i])
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(K2):
+        e2e_step(s_step + W2 + i, host[W2 + i])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = torch.tensor([e0.elapsed_time(e1) / K2], dtype=torch.float64, device=dev)
+    if world_size > 1:
+        dist.all_reduce(ms_e2e, op=dist.ReduceOp.MAX)
+    e2e_value = B_local * world_size / (float(ms_e2e.item()) / 1000.0)
+
+    # -- roofline of the dominant kernel ---------------------------------------
+    peak, peak_kind = load_peaks()
+    R = tr.grid.n_rows
+    n_tv = max(1, int(round(cfg.tv_sample_frac * R)))
+    n_tv_local = shard_range(n_tv, rank, world_size)[1]
+    alg = {   # algorithmic bytes per launch
+        "render_fused_bwd": B_local * 104 + U_render * (4 + 112 + 224),
+        "tv": n_tv_local * (16 + 4 * 112) + n_tv_local * 224,
+        "opt_step": R * 1 + U * (672 + 1),
+    }
+    avg = {k: float(np.mean(vs)) for k, vs in per_kernel.items() if vs}
+    dom = max(avg, key=lambda k: avg[k])
+    achieved = alg[dom] / (avg[dom] * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(dom)
+        except Exception:
+            traffic = None
+    step_bytes = 60 * args.batch + 8 * n_tv + U * (4 + 112 + 224 + 672)
+
+    cpu = None
+    if rank == 0 and world_size == 1 and not args.no_cpu_baseline:
+        rps, k, sample = oracle_steps(args, args.cpu_steps, ds)
+        cpu = {"value": rps, "unit": "rays/s", "cores": 1, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world_size,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference toy scene rendered on device, 8-bit)",
+            "config": {"workload": WORKLOAD, "grid": f"{args.dims}^3 dense init",
+                       "rays_per_gpu": args.batch, "global_batch": args.batch * world_size,
+                       "views": args.views, "res": args.res, "parallelism": f"dp{world_size}",
+                       "l2": "inputs_larger_than_l2 (table+grad+v = %.2f GB)" % (3 * R * 112 / 1e9),
+                       "touched_rows_U": U, "touched_rows_render": U_render, "tv_cells": n_tv,
+                       "step_bytes_model": step_bytes,
+                       "step_hbm_frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
+                       "kernel_ms": avg},
+            "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "algorithmic_bytes": alg[dom]},
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": 3 * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world_size > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

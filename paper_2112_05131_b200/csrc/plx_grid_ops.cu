@@ -133,8 +133,12 @@ __global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
 }
 
 // ------------------------------------------------------- optimiser --------
-// One warp serves 4 rows x 7 float4 (lanes 28..31 idle), so the touched
-// byte of a row is read and cleared inside one warp.
+// Persistent sweep over the touched mask (K:572-600).  A warp owns 128-row
+// segments: one coalesced 128-byte load of the mask, a warp prefix sum turns
+// the set bytes into a compact per-warp list in shared memory, and the
+// touched rows are then updated 4 at a time (lanes 0..27 = 4 rows x 7 float4,
+// fully coalesced 448-byte runs of table / grad / v).  Untouched rows cost
+// one mask byte; touched rows cost exactly their compulsory 672 B.
 struct OptArgs {
     float *table, *v, *grad;
     uint8_t *tmask;
@@ -144,53 +148,119 @@ struct OptArgs {
     unsigned long long *count;
 };
 
+__device__ __forceinline__ int nonzero_bytes(uint32_t m) {
+    m = (m | (m >> 4)) & 0x0f0f0f0fu;
+    m = (m | (m >> 2)) & 0x03030303u;
+    m = (m | (m >> 1)) & 0x01010101u;
+    return __popc(m);
+}
+
+__device__ __forceinline__ void opt_update_quad(const OptArgs &a, int64_t row, int quad) {
+    float4 *gp = reinterpret_cast<float4 *>(a.grad + row * PLX_ROW) + quad;
+    if (!a.update) {
+        if (a.clear) *gp = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
+    float4 *tp = reinterpret_cast<float4 *>(a.table + row * PLX_ROW) + quad;
+    const float4 g4 = *gp;
+    const float4 t4 = *tp;
+    float g[4] = {g4.x, g4.y, g4.z, g4.w};
+    float t[4] = {t4.x, t4.y, t4.z, t4.w};
+    if (a.rmsprop) {
+        float4 *vp = reinterpret_cast<float4 *>(a.v + row * PLX_ROW) + quad;
+        const float4 v4 = *vp;
+        float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (g[e] == 0.0f) continue;   // K:581-583: stale state
+            const double gd = (double)g[e];
+            const double lr = (quad == 0 && e == 0) ? a.lr_sigma : a.lr_sh;
+            const double nv = a.beta * (double)v[e] + (1.0 - a.beta) * gd * gd;
+            v[e] = (float)nv;
+            t[e] = (float)((double)t[e] - lr * gd / (sqrt(nv) + a.eps));
+        }
+        *vp = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (g[e] == 0.0f) continue;
+            const double lr = (quad == 0 && e == 0) ? a.lr_sigma : a.lr_sh;
+            t[e] = (float)((double)t[e] - lr * (double)g[e]);
+        }
+    }
+    *tp = make_float4(t[0], t[1], t[2], t[3]);
+    if (a.clear) *gp = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) opt_kernel(OptArgs a) {
-    const int lane = threadIdx.x & 31;
-    const int64_t wid = ((int64_t)blockIdx.x * NT + threadIdx.x) >> 5;
-    const int64_t row = wid * 4 + lane / 7;
-    const int quad = lane % 7;
-    const bool active = lane < 28 && row < a.rows;
-    bool touched = false;
-    if (active) touched = a.tmask[row] != 0;
-    if (touched && !a.update) {
-        if (a.clear) reinterpret_cast<float4 *>(a.grad + row * PLX_ROW)[quad] = make_float4(0.f, 0.f, 0.f, 0.f);
-    } else if (touched) {
-        float4 *gp = reinterpret_cast<float4 *>(a.grad + row * PLX_ROW) + quad;
-        float4 *tp = reinterpret_cast<float4 *>(a.table + row * PLX_ROW) + quad;
-        float4 *vp = reinterpret_cast<float4 *>(a.v + row * PLX_ROW) + quad;
-        const float4 g4 = *gp;
-        float4 t4 = *tp;
-        float g[4] = {g4.x, g4.y, g4.z, g4.w};
-        float t[4] = {t4.x, t4.y, t4.z, t4.w};
-        if (a.rmsprop) {
-            float4 v4 = *vp;
-            float v[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                if (g[e] == 0.0f) continue;   // K:581-583 stale state
-                const double gd = (double)g[e];
-                const double lr = (quad == 0 && e == 0) ? a.lr_sigma : a.lr_sh;
-                const double nv = a.beta * (double)v[e] + (1.0 - a.beta) * gd * gd;
-                v[e] = (float)nv;
-                t[e] = (float)((double)t[e] - lr * gd / (sqrt(nv) + a.eps));
-            }
-            *vp = make_float4(v[0], v[1], v[2], v[3]);
+    __shared__ uint8_t list[NT / 32][128];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t nseg = (a.rows + 127) >> 7;
+    const int64_t nw = (int64_t)gridDim.x * (NT / 32);
+    unsigned long long cnt = 0;
+    const int quad = lane % 7, sub = lane / 7;
+    auto load_mask = [&](int64_t seg) -> uint32_t {
+        const int64_t r0 = seg * 128 + lane * 4;
+        uint32_t m = 0;
+        if (seg >= nseg) return 0u;
+        if (r0 + 3 < a.rows) {
+            m = *reinterpret_cast<const volatile uint32_t *>(a.tmask + r0);
         } else {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                if (g[e] == 0.0f) continue;
-                const double lr = (quad == 0 && e == 0) ? a.lr_sigma : a.lr_sh;
-                t[e] = (float)((double)t[e] - lr * (double)g[e]);
+            for (int e = 0; e < 4; ++e)
+                if (r0 + e < a.rows && a.tmask[r0 + e]) m |= 0xffu << (8 * e);
+        }
+        return m;
+    };
+    int64_t seg = (int64_t)blockIdx.x * (NT / 32) + wib;
+    uint32_t m_next = load_mask(seg);
+    for (; seg < nseg; seg += nw) {
+        const int64_t r0 = seg * 128 + lane * 4;
+        const uint32_t m = m_next;
+        m_next = load_mask(seg + nw);   // prefetch the next segment's mask
+        const int c = nonzero_bytes(m);
+        int incl = c;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(PLX_FULL_MASK, incl, off);
+            if (lane >= off) incl += y;
+        }
+        const int total = __shfl_sync(PLX_FULL_MASK, incl, 31);
+        if (total == 0) continue;
+        int pos = incl - c;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if ((m >> (8 * e)) & 0xffu) list[wib][pos++] = (uint8_t)(lane * 4 + e);
+        __syncwarp();
+        cnt += (unsigned long long)total;
+        for (int gidx = 0; gidx < total; gidx += 8) {   // two 4-row groups in flight
+            const int j0 = gidx + sub, j1 = gidx + 4 + sub;
+            if (lane < 28 && j0 < total) opt_update_quad(a, seg * 128 + list[wib][j0], quad);
+            if (lane < 28 && j1 < total) opt_update_quad(a, seg * 128 + list[wib][j1], quad);
+        }
+        if (a.clear && m) {
+            if (r0 + 3 < a.rows) {
+                *reinterpret_cast<uint32_t *>(a.tmask + r0) = 0u;
+            } else {
+                for (int e = 0; e < 4; ++e)
+                    if (r0 + e < a.rows) a.tmask[r0 + e] = 0;
             }
         }
-        *tp = make_float4(t[0], t[1], t[2], t[3]);
-        if (a.clear) *gp = make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncwarp();
     }
-    const unsigned rows_touched = __ballot_sync(PLX_FULL_MASK, touched && quad == 0);
-    __syncwarp();
-    if (a.clear && touched && quad == 0) a.tmask[row] = 0;
-    if (a.count && lane == 0 && rows_touched) atomicAdd(a.count, (unsigned long long)__popc(rows_touched));
+    if (a.count && lane == 0 && cnt) atomicAdd(a.count, cnt);
+}
+
+static int g_num_sms = 0;
+static int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
 }
 
 template <int NT>
@@ -491,8 +561,10 @@ extern "C" int plx_opt_step(plx_grid *g, float *v, plx_grad *gb, double lr_sigma
     OptArgs a{g->table, v, gb->grad, gb->tmask, g->rows, lr_sigma, lr_sh, beta, eps, rmsprop, clear,
               1, reinterpret_cast<unsigned long long *>(out_count)};
     constexpr int NT = 256;
-    const int64_t warps = (g->rows + 3) / 4;
-    opt_kernel<NT><<<blocks(warps * 32, NT), NT, 0, (cudaStream_t)stream>>>(a);
+    const int64_t segs = (g->rows + 127) / 128;
+    int64_t nb = (segs + NT / 32 - 1) / (NT / 32);
+    if (nb > (int64_t)num_sms() * 4) nb = (int64_t)num_sms() * 4;   // persistent: 4 x 256 thr / SM
+    opt_kernel<NT><<<(unsigned)nb, NT, 0, (cudaStream_t)stream>>>(a);
     return status();
 }
 
@@ -502,8 +574,10 @@ extern "C" int plx_clear_grad(plx_grad *gb, int64_t rows, int64_t *out_count, vo
     OptArgs a{nullptr, nullptr, gb->grad, gb->tmask, rows, 0.0, 0.0, 0.0, 0.0, 0, 1, 0,
               reinterpret_cast<unsigned long long *>(out_count)};
     constexpr int NT = 256;
-    const int64_t warps = (rows + 3) / 4;
-    opt_kernel<NT><<<blocks(warps * 32, NT), NT, 0, (cudaStream_t)stream>>>(a);
+    const int64_t segs = (rows + 127) / 128;
+    int64_t nb = (segs + NT / 32 - 1) / (NT / 32);
+    if (nb > (int64_t)num_sms() * 4) nb = (int64_t)num_sms() * 4;
+    opt_kernel<NT><<<(unsigned)nb, NT, 0, (cudaStream_t)stream>>>(a);
     return status();
 }
 

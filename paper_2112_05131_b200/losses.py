@@ -47,6 +47,12 @@ class CellRun:
     def __len__(self) -> int:
         return self.count
 
+    def split(self, rank: int, size: int) -> "CellRun":
+        """Contiguous sub-run for one rank (dist.shard_range)."""
+        from .dist import shard_range
+        s, c = shard_range(self.count, rank, size)
+        return CellRun((self.start + s) % self.n_cells, c, self.n_cells)
+
     def __array__(self, dtype=None, copy=None):
         a = ((self.start + np.arange(self.count)) % self.n_cells).astype(np.int64)
         return a if dtype is None else a.astype(dtype)
@@ -62,11 +68,14 @@ def sample_tv_cells(grid: SparseGrid, fraction: float, rng) -> CellRun:
 
 def tv_loss(grid: SparseGrid, cells, lam_sigma: float, lam_sh: float,
             grads: GradientBuffer | None = None, eps: float = TV_EPS,
-            wrap=(False, False, False), sums: torch.Tensor | None = None):
+            wrap=(False, False, False), sums: torch.Tensor | None = None,
+            n_norm: int | None = None):
     """L:50-77 -> (lam_sigma * tv_sigma, lam_sh * tv_sh).
 
     With a device float64[2] `sums`, the raw (sigma_sum, sh_sum) are
-    accumulated there and (sums, n) is returned without a host sync."""
+    accumulated there and (sums, n) is returned without a host sync.
+    `n_norm` overrides the averaging count (a rank's sub-run of a larger run
+    normalises by the global count, dist.py)."""
     if isinstance(cells, CellRun):
         n, start, cptr, keep = cells.count, cells.start, None, None
     else:
@@ -77,20 +86,21 @@ def tv_loss(grid: SparseGrid, cells, lam_sigma: float, lam_sh: float,
     if n == 0:
         return 0.0, 0.0
     dims = grid.dims
+    nn = int(n_norm) if n_norm is not None else n
     dev_sums = sums if sums is not None else torch.zeros(2, dtype=torch.float64,
                                                          device=grid.device)
     gb = grads._c() if grads is not None else None
     c_ = grid._c(with_occ=False)
     _lib.check(_lib.lib().plx_tv(
         ctypes.byref(c_), cptr, start, n, dims[0] / 256.0, dims[1] / 256.0, dims[2] / 256.0,
-        float(eps), lam_sigma / n, lam_sh / n, int(wrap[0]), int(wrap[1]), int(wrap[2]),
+        float(eps), lam_sigma / nn, lam_sh / nn, int(wrap[0]), int(wrap[1]), int(wrap[2]),
         int(grads is not None), ctypes.byref(gb) if gb is not None else None,
         dev_sums.data_ptr(), _lib.stream_ptr()), "tv")
     del keep
     if sums is not None:
         return dev_sums, n
     s = dev_sums.cpu().numpy()
-    return lam_sigma * float(s[0]) / n, lam_sh * float(s[1]) / n
+    return lam_sigma * float(s[0]) / nn, lam_sh * float(s[1]) / nn
 
 
 def cauchy_sparsity_loss(sigmas, lam: float):

@@ -241,6 +241,47 @@ def fused_mse_backward(grid: SparseGrid, origins, dirs, viewdirs, gt_rgb,
     return out_rgb, float(s[0]), float(s[1])
 
 
+class RayPool:
+    """Device-resident training rays: origins, march dirs,
+    view dirs and gt colours as float64 (N, 3) in HBM; a batch is a device
+    int64 index vector gathered inside the kernel (no per-step host copy)."""
+
+    def __init__(self, origins, dirs, viewdirs, rgb, device=None):
+        dev = torch.device(device or "cuda")
+        self.origins = _ray_tensor(origins, dev)
+        self.dirs = _ray_tensor(dirs, dev)
+        self.viewdirs = _ray_tensor(viewdirs, dev)
+        self.rgb = _ray_tensor(rgb, dev)
+        self.n = self.origins.shape[0]
+
+    def rays(self, idx: torch.Tensor | None, n: int | None = None) -> _lib.PlxRays:
+        r = _lib.PlxRays()
+        r.origins, r.dirs = self.origins.data_ptr(), self.dirs.data_ptr()
+        r.viewdirs, r.target = self.viewdirs.data_ptr(), self.rgb.data_ptr()
+        r.jitter = None
+        r.idx = _lib.ptr(idx)
+        r.n = int(idx.numel()) if idx is not None else int(n if n is not None else self.n)
+        return r
+
+
+def fused_mse_backward_pool(grid: SparseGrid, pool: RayPool, idx: torch.Tensor,
+                            grads: GradientBuffer, opts: RenderOptions, n_total: int,
+                            lam_cauchy: float, sums: torch.Tensor, jitter=None,
+                            kopts: _lib.PlxRenderOpts | None = None,
+                            cgrid: _lib.PlxGrid | None = None) -> None:
+    """The trainer's form of fused_mse_backward (R:253-279, T:455-457): batch =
+    pool rows `idx` (device int64), sums (device f64[2]) accumulated, no sync."""
+    r = pool.rays(idx)
+    if jitter is not None:
+        r.jitter = jitter.data_ptr()
+    c = cgrid if cgrid is not None else grid._c(with_occ=opts.interp == "trilinear")
+    ko = kopts if kopts is not None else kernel_opts(grid, opts)
+    gb = grads._c()
+    _lib.check(_lib.lib().plx_render_fused_bwd(
+        ctypes.byref(c), ctypes.byref(r), ctypes.byref(ko), 1, 2.0 / n_total, float(lam_cauchy),
+        ctypes.byref(gb), None, sums.data_ptr(), _lib.stream_ptr()), "render_fused_bwd")
+
+
 def render_image(grid: SparseGrid, camera, opts: RenderOptions | None = None,
                  chunk: int = 1 << 20) -> np.ndarray:
     """R:282-293: full camera view -> (H, W, 3) float64 image."""

@@ -1,0 +1,439 @@
+"""End-to-end optimisation on the B200 (drop-in for pkg/src/plenoxel/trainer.py,
+bounded and forward-facing-NDC scenes; the 360° MSI background is out of
+scope).
+
+The step body (T:411-492) keeps the reference's order and RNG consumption --
+EpochBatcher permutations and sample_tv_cells draws come from the same
+numpy default_rng(seed) -- while the data path is device-resident:
+
+  batch   = pool rows idx (device permutation, uploaded once per epoch)
+  render  = plx_render_fused_bwd            (one kernel, sums stay on device)
+  TV      = plx_tv on (start, count)        (one kernel)
+  check   = one 32-byte D2H of the loss sums (finiteness, T:473-480)
+  update  = plx_opt_step with fused clear   (one kernel, counts n_touched)
+
+With a World of size N (dist.py) each rank renders its contiguous slice of
+the global batch and its sub-run of the TV cells, then the gradients are
+all-reduced and the (replicated) update runs everywhere.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import math
+import time
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+import torch
+import yaml
+
+from . import _lib, artifact_io, losses, optim, render
+from .camera import all_rays
+from .dist import World, max_reduce, reduce_gradients, shard_range
+from .grid import GradientBuffer, SparseGrid
+
+SCENE_TYPES = ("bounded", "forward_facing_ndc", "unbounded_360")
+
+
+class TrainingDiverged(RuntimeError):
+    pass
+
+
+class ResourceError(RuntimeError):
+    pass
+
+
+@dataclass
+class LadderRung:
+    step: int
+    dims: tuple
+
+
+@dataclass
+class TrainConfig:
+    """T:40-99 (same keys, same defaults)."""
+
+    scene_type: str = "bounded"
+    aabb: tuple = (-1.5, -1.5, -1.5, 1.5, 1.5, 1.5)
+    ladder: list = field(default_factory=lambda: [LadderRung(0, (256, 256, 256))])
+    total_steps: int = 128000
+    batch_size: int = 5000
+    step_frac: float = 0.5
+    stop_thresh: float = 1e-4
+    interp: str = "trilinear"
+    formula: str = "relative"
+    background: tuple = (1.0, 1.0, 1.0)
+    prune_criterion: str = "weight"
+    prune_threshold: float = 0.256
+    lambda_tv_sigma: float = 1e-5
+    lambda_tv_sh: float = 1e-3
+    tv_sample_frac: float = 0.01
+    tv_until_step: int = -1
+    lambda_sparsity: float = 0.0
+    lambda_beta: float = 0.0
+    lr_sigma: optim.LrSchedule = field(default_factory=lambda: optim.LrSchedule(
+        kind="delayed_exponential", lr_init=30.0, lr_final=0.05, total_steps=250000,
+        delay_steps=15000, delay_mult=0.01))
+    lr_sh: optim.LrSchedule = field(default_factory=lambda: optim.LrSchedule(
+        kind="exponential", lr_init=0.01, lr_final=5e-6, total_steps=250000))
+    optimizer: str = "rmsprop"
+    rms_beta: float = 0.95
+    rms_eps: float = 1e-8
+    init_sigma: float = 0.1
+    init_rgb: float = 0.1
+    seed: int = 0
+    eval_every: int = 1000
+    log_every: int = 100
+    checkpoint_every: int = 0
+    jitter: float = 0.0
+    ndc_z_pad: float = 0.0
+
+    def __post_init__(self):
+        if self.scene_type not in SCENE_TYPES:
+            raise ValueError(f"unknown scene type {self.scene_type!r}")
+        if self.batch_size < 1:
+            raise ValueError("batch size must be >= 1")
+        steps = [r.step for r in self.ladder]
+        if steps != sorted(steps) or len(set(steps)) != len(steps):
+            raise ValueError("ladder steps must be strictly increasing")
+        if steps and steps[0] != 0:
+            raise ValueError("first ladder rung must start at step 0")
+        if any(s >= self.total_steps for s in steps[1:]):
+            raise ValueError("ladder steps must be < total_steps")
+
+
+def default_config(scene_type: str) -> TrainConfig:
+    """T:102-154."""
+    if scene_type == "bounded":
+        return TrainConfig(scene_type="bounded", aabb=(-1.5, -1.5, -1.5, 1.5, 1.5, 1.5),
+                           ladder=[LadderRung(0, (256, 256, 256)),
+                                   LadderRung(38400, (512, 512, 512))],
+                           total_steps=128000, prune_criterion="weight", prune_threshold=0.256,
+                           lambda_tv_sigma=1e-5, lambda_tv_sh=1e-3, tv_until_step=38400,
+                           background=(1.0, 1.0, 1.0))
+    if scene_type == "forward_facing_ndc":
+        return TrainConfig(scene_type="forward_facing_ndc", aabb=(-1.0, -1.0, -1.0, 1.0, 1.0, 1.0),
+                           ladder=[LadderRung(0, (256, 256, 128)),
+                                   LadderRung(38400, (512, 512, 128)),
+                                   LadderRung(76800, (1408, 1156, 128))],
+                           total_steps=128000, prune_criterion="density", prune_threshold=5.0,
+                           lambda_tv_sigma=5e-4, lambda_tv_sh=5e-3, lambda_sparsity=1e-12,
+                           background=(0.0, 0.0, 0.0))
+    if scene_type == "unbounded_360":
+        raise NotImplementedError("unbounded_360 (MSI background) is out of scope, SURVEY §8(f)-4")
+    raise ValueError(f"unknown scene type {scene_type!r}")
+
+
+def toy_config(grid_dim: int = 64, step_frac: float = 0.5, total_steps: int = 5000,
+               batch_size: int = 3000, aabb: float = 1.1) -> TrainConfig:
+    """toy.py:37-62."""
+    return TrainConfig(
+        scene_type="bounded", aabb=(-aabb,) * 3 + (aabb,) * 3,
+        ladder=[LadderRung(0, (grid_dim,) * 3)], total_steps=total_steps,
+        batch_size=batch_size, step_frac=step_frac, lambda_tv_sigma=1e-6, lambda_tv_sh=1e-4,
+        tv_until_step=-1,
+        lr_sigma=optim.LrSchedule(kind="delayed_exponential", lr_init=2.0, lr_final=0.1,
+                                  total_steps=2 * total_steps, delay_steps=total_steps // 10,
+                                  delay_mult=0.01),
+        lr_sh=optim.LrSchedule(kind="exponential", lr_init=0.01, lr_final=1e-4,
+                               total_steps=2 * total_steps),
+        eval_every=0, log_every=100, background=(1.0, 1.0, 1.0))
+
+
+def config_to_dict(cfg: TrainConfig) -> dict:
+    d = dataclasses.asdict(cfg)
+    d["ladder"] = [{"step": r.step, "dims": list(r.dims)} for r in cfg.ladder]
+    d["aabb"], d["background"] = list(cfg.aabb), list(cfg.background)
+    return d
+
+
+def config_from_dict(d: dict) -> TrainConfig:
+    known = {f.name for f in dataclasses.fields(TrainConfig)}
+    unknown = set(d) - known
+    if unknown:
+        raise ValueError(f"unknown config keys: {sorted(unknown)}")
+    kw = dict(d)
+    if "ladder" in kw:
+        kw["ladder"] = [LadderRung(int(r["step"]), tuple(int(x) for x in r["dims"]))
+                        for r in kw["ladder"]]
+    for key in ("lr_sigma", "lr_sh"):
+        if key in kw and isinstance(kw[key], dict):
+            kw[key] = optim.LrSchedule(**kw[key])
+    for key in ("aabb", "background"):
+        if key in kw:
+            kw[key] = tuple(float(x) for x in kw[key])
+    return TrainConfig(**kw)
+
+
+def load_config(path) -> TrainConfig:
+    with open(path) as f:
+        return config_from_dict(yaml.safe_load(f))
+
+
+def save_config(cfg: TrainConfig, path) -> None:
+    with open(path, "w") as f:
+        yaml.safe_dump(config_to_dict(cfg), f, sort_keys=False)
+
+
+class EpochBatcher:
+    """T:233-255 (identical RNG use) with a device mirror of the permutation:
+    next_device() returns the same indices as next() as a CUDA int64 tensor,
+    uploading each permutation once per epoch."""
+
+    def __init__(self, n: int, batch_size: int, rng, device=None):
+        self.n = n
+        self.batch_size = batch_size
+        self.rng = rng
+        self.device = device
+        self.perm = rng.permutation(n)
+        self.cursor = 0
+        self._perm_dev = None
+
+    def _dev_perm(self):
+        if self._perm_dev is None:
+            self._perm_dev = torch.from_numpy(self.perm).to(self.device or "cuda")
+        return self._perm_dev
+
+    def next(self) -> np.ndarray:
+        chunks = []
+        need = self.batch_size
+        while need > 0:
+            if self.cursor >= self.n:
+                self.perm = self.rng.permutation(self.n)
+                self._perm_dev = None
+                self.cursor = 0
+            take = min(need, self.n - self.cursor)
+            chunks.append(self.perm[self.cursor:self.cursor + take])
+            self.cursor += take
+            need -= take
+        return np.concatenate(chunks) if len(chunks) > 1 else chunks[0]
+
+    def next_device(self) -> torch.Tensor:
+        chunks = []
+        need = self.batch_size
+        while need > 0:
+            if self.cursor >= self.n:
+                self.perm = self.rng.permutation(self.n)
+                self._perm_dev = None
+                self.cursor = 0
+            take = min(need, self.n - self.cursor)
+            chunks.append(self._dev_perm()[self.cursor:self.cursor + take])
+            self.cursor += take
+            need -= take
+        return torch.cat(chunks) if len(chunks) > 1 else chunks[0]
+
+
+@dataclass
+class TrainResult:
+    grid: SparseGrid
+    metrics: list
+    config: TrainConfig
+
+
+def _grid_aabb(cfg: TrainConfig, dims):
+    lo = np.array(cfg.aabb[:3], dtype=np.float64)
+    hi = np.array(cfg.aabb[3:], dtype=np.float64)
+    if cfg.scene_type == "forward_facing_ndc" and cfg.ndc_z_pad > 0:
+        pad = cfg.ndc_z_pad * (hi[2] - lo[2]) / (dims[2] - 1)
+        lo[2] -= pad
+        hi[2] += pad
+    return lo, hi
+
+
+def _estimate_table_bytes(dims) -> int:
+    """Device footprint of a dense rung: links + table + grad + v (f32)."""
+    cells = int(np.prod([int(d) for d in dims]))
+    return cells * (4 + 3 * 28 * 4 + 1)
+
+
+class Trainer:
+    """Owns the device state of one training run (grid, RMSProp state,
+    gradient buffer, ray pool, batcher) and executes steps."""
+
+    def __init__(self, train_ds, config: TrainConfig, device=None, world: World | None = None):
+        cfg = config
+        if cfg.scene_type == "unbounded_360":
+            raise NotImplementedError("unbounded_360 is out of scope (SURVEY §8(f)-4)")
+        self.cfg = cfg
+        self.world = world or World()
+        self.device = torch.device(device or "cuda")
+        self.rng = np.random.default_rng(cfg.seed)
+        o, m, v, gt = all_rays(train_ds.images, train_ds.cameras, train_ds.scene_type)
+        self.pool = render.RayPool(o, m, v, gt, device=self.device)
+        dims0 = cfg.ladder[0].dims
+        lo, hi = _grid_aabb(cfg, dims0)
+        self.grid = SparseGrid.dense(dims0, lo, hi, sigma=cfg.init_sigma, rgb=cfg.init_rgb,
+                                     device=self.device)
+        self.state = optim.OptimState(self.grid.n_rows, beta=cfg.rms_beta, eps=cfg.rms_eps,
+                                      device=self.device)
+        self.grads = GradientBuffer(self.grid.n_rows, device=self.device)
+        self.opts = render.RenderOptions(step_frac=cfg.step_frac, stop_thresh=cfg.stop_thresh,
+                                         background=tuple(cfg.background), interp=cfg.interp,
+                                         formula=cfg.formula, jitter=cfg.jitter)
+        self.batcher = EpochBatcher(self.pool.n, cfg.batch_size, self.rng, self.device)
+        self.rung_events = {r.step: tuple(r.dims) for r in cfg.ladder[1:]}
+        self.sums = torch.zeros(4, dtype=torch.float64, device=self.device)
+        self.count = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self._host_sums = torch.zeros(4, dtype=torch.float64).pin_memory()
+        self._refresh_cache()
+
+    def _refresh_cache(self):
+        self._cgrid = self.grid._c(with_occ=self.opts.interp == "trilinear")
+        self._kopts = render.kernel_opts(self.grid, self.opts)
+
+    # -- ladder event (T:412-439) ---------------------------------------------
+    def rung_event(self, new_dims, out_dir=None, step=0):
+        cfg = self.cfg
+        if cfg.prune_criterion == "weight":
+            w = self.max_weights()
+            self.grid, kept = self.grid.prune("weight", cfg.prune_threshold, w)
+        else:
+            self.grid, kept = self.grid.prune("density", cfg.prune_threshold)
+        self.state.reindex(kept)
+        need = _estimate_table_bytes(new_dims)
+        free, _ = torch.cuda.mem_get_info(self.device)
+        if need > free:
+            raise ResourceError(f"upsampling to {tuple(new_dims)} needs ~{need >> 20} MiB, "
+                                f"only {free >> 20} MiB free on the device")
+        self.grid = self.grid.upsample(new_dims)
+        self.state.reset(self.grid.n_rows)
+        self.grads = GradientBuffer(self.grid.n_rows, device=self.device)
+        self._refresh_cache()
+        if out_dir is not None:
+            artifact_io.save_checkpoint(Path(out_dir) / f"checkpoint_{step:07d}.plnx",
+                                        self.grid, self.state, step)
+
+    def max_weights(self) -> torch.Tensor:
+        """Max-weight over all training rays, sharded over ranks + max-reduce."""
+        s, c = shard_range(self.pool.n, self.world.rank, self.world.size)
+        w = self.grid.max_weight_accumulate(self.pool.origins[s:s + c], self.pool.dirs[s:s + c],
+                                            self.cfg.step_frac, self.cfg.stop_thresh,
+                                            self.cfg.interp)
+        max_reduce(self.world, w)
+        return w
+
+    # -- one optimisation step (T:441-492) ------------------------------------
+    def step(self, step: int, check_finite: bool = True) -> dict:
+        cfg = self.cfg
+        idx = self.batcher.next_device()
+        B = int(idx.numel())
+        jt = None
+        if self.opts.jitter > 0:
+            jt = torch.from_numpy(self.rng.random(B) * self.opts.jitter).to(self.device)
+        s0, c0 = shard_range(B, self.world.rank, self.world.size)
+        self.sums.zero_()
+        render.fused_mse_backward_pool(
+            self.grid, self.pool, idx[s0:s0 + c0], self.grads, self.opts, n_total=B,
+            lam_cauchy=cfg.lambda_sparsity, sums=self.sums[0:2],
+            jitter=None if jt is None else jt[s0:s0 + c0], kopts=self._kopts, cgrid=self._cgrid)
+        tv_on = (cfg.lambda_tv_sigma > 0 or cfg.lambda_tv_sh > 0) and (
+            cfg.tv_until_step < 0 or step < cfg.tv_until_step)
+        n_tv = 0
+        if tv_on:
+            run = losses.sample_tv_cells(self.grid, cfg.tv_sample_frac, self.rng)
+            n_tv = run.count
+            sub = run.split(self.world.rank, self.world.size)
+            if sub.count:
+                losses.tv_loss(self.grid, sub, cfg.lambda_tv_sigma, cfg.lambda_tv_sh,
+                               self.grads, sums=self.sums[2:4], n_norm=n_tv)
+        reduce_gradients(self.world, self.grads.data, self.grads.touched_mask, self.sums)
+        rec = {"B": B, "n_tv": n_tv}
+        if check_finite:
+            self._host_sums.copy_(self.sums, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            mse_sum, cauchy_raw, tv_s, tv_h = (float(x) for x in self._host_sums)
+            loss_mse = mse_sum / B
+            tv_sig = cfg.lambda_tv_sigma * tv_s / n_tv if n_tv else 0.0
+            tv_sh = cfg.lambda_tv_sh * tv_h / n_tv if n_tv else 0.0
+            loss = loss_mse + tv_sig + tv_sh + cfg.lambda_sparsity * cauchy_raw
+            if not math.isfinite(loss):
+                raise TrainingDiverged(f"non-finite loss at step {step}: mse={loss_mse!r} "
+                                       f"tv=({tv_sig!r}, {tv_sh!r})")
+            rec.update(loss=loss, mse=loss_mse)
+        self.count.zero_()
+        optim.step(self.grid, self.grads, self.state, optim.lr_at(cfg.lr_sigma, step),
+                   optim.lr_at(cfg.lr_sh, step), cfg.optimizer, clear=True,
+                   count_out=self.count)
+        return rec
+
+    def nnz_fraction(self) -> float:
+        """GradientBuffer.nnz_fraction of the last step (counted by the opt kernel)."""
+        return int(self.count.item()) / max(self.grid.n_rows, 1)
+
+    # -- evaluation (T:309-347) -------------------------------------------------
+    def evaluate(self, dataset, chunk: int = 1 << 20):
+        return evaluate(self.grid, dataset, self.opts, chunk)
+
+
+def evaluate(grid: SparseGrid, dataset, opts: render.RenderOptions, chunk: int = 1 << 20):
+    """Mean PSNR/SSIM over a dataset's views (T:309-347), device renders."""
+    from .camera import generate_rays, to_ndc
+
+    rows = []
+    for vi, (img, cam) in enumerate(zip(dataset.images, dataset.cameras)):
+        o, d = generate_rays(cam)
+        v = None
+        if dataset.scene_type == "forward_facing_ndc":
+            v = d
+            o, d, _ = to_ndc(o, d, cam)
+        ot = torch.from_numpy(o).to(grid.device)
+        dt = torch.from_numpy(np.ascontiguousarray(d)).to(grid.device)
+        vt = torch.from_numpy(np.ascontiguousarray(v)).to(grid.device) if v is not None else None
+        pred = torch.empty((o.shape[0], 3), dtype=torch.float64, device=grid.device)
+        for s in range(0, o.shape[0], chunk):
+            rgb, _, _ = render.render_rays(grid, ot[s:s + chunk], dt[s:s + chunk], opts,
+                                           viewdirs=None if vt is None else vt[s:s + chunk])
+            pred[s:s + chunk] = rgb
+        pred = pred.cpu().numpy().reshape(np.asarray(img).shape)
+        gt = np.asarray(img, dtype=np.float64)
+        rows.append({"view": vi, "psnr": losses.psnr(pred, gt), "ssim": losses.ssim(pred, gt)})
+    return (float(np.mean([r["psnr"] for r in rows])), float(np.mean([r["ssim"] for r in rows])),
+            rows)
+
+
+def train(train_ds, config: TrainConfig, test_ds=None, out_dir=None, metrics_sink=None,
+          device=None, world: World | None = None) -> TrainResult:
+    """T:350-518 on the device (bounded / forward-facing scenes)."""
+    cfg = config
+    tr = Trainer(train_ds, cfg, device=device, world=world)
+    out_dir = Path(out_dir) if out_dir is not None else None
+    if out_dir is not None:
+        out_dir.mkdir(parents=True, exist_ok=True)
+    metrics: list = []
+
+    def emit(rec):
+        metrics.append(rec)
+        if metrics_sink is not None:
+            metrics_sink(rec)
+
+    t_start = time.perf_counter()
+    last_eval = -1
+    for step in range(cfg.total_steps):
+        if step in tr.rung_events:
+            tr.rung_event(tr.rung_events[step], out_dir, step)
+        try:
+            rec = tr.step(step)
+        except TrainingDiverged:
+            if out_dir is not None:
+                artifact_io.save_grid(tr.grid, out_dir / "diverged.plnx")
+            raise
+        if cfg.log_every > 0 and step % cfg.log_every == 0:
+            emit({"step": step, "loss": rec["loss"], "mse": rec["mse"],
+                  "nnz_fraction": tr.nnz_fraction()})
+        if test_ds is not None and cfg.eval_every > 0 and (step + 1) % cfg.eval_every == 0:
+            p, s, _ = tr.evaluate(test_ds)
+            last_eval = step + 1
+            emit({"step": step + 1, "psnr": p, "ssim": s,
+                  "wall_time_s": time.perf_counter() - t_start})
+        if cfg.checkpoint_every > 0 and out_dir is not None and (step + 1) % cfg.checkpoint_every == 0:
+            artifact_io.save_checkpoint(out_dir / f"checkpoint_{step + 1:07d}.plnx", tr.grid,
+                                        tr.state, step + 1)
+    if test_ds is not None and last_eval != cfg.total_steps:
+        p, s, _ = tr.evaluate(test_ds)
+        emit({"step": cfg.total_steps, "psnr": p, "ssim": s,
+              "wall_time_s": time.perf_counter() - t_start})
+    if out_dir is not None:
+        artifact_io.save_checkpoint(out_dir / "final.plnx", tr.grid, tr.state, cfg.total_steps)
+    return TrainResult(grid=tr.grid, metrics=metrics, config=cfg)
