@@ -89,13 +89,17 @@ int plx_render_fwd(const plx_grid *g, const plx_rays *rays, const plx_render_opt
 /* render_backward (K:241-411) via fused_mse_backward (R:253-279, mse_mode=1,
  * up_scale = 2/n_total) and render_rays_backward (R:205-239, mse_mode=0,
  * target = upstream dL/dC).  Gradients are ADDED into gb->grad with f32
- * atomics; every occupied stencil row of every recorded sample is marked in
- * gb->tmask.  out_sums (device double[2]) is ACCUMULATED with
- * {mse_sum, cauchy_sum}; out_rgb may be NULL. */
+ * reductions; every occupied stencil row of every recorded sample is marked
+ * in gb->tmask.  out_sums (device double[2]) is ACCUMULATED with
+ * {mse_sum, cauchy_sum}; out_rgb may be NULL.  `scratch` is a device
+ * workspace of at least plx_render_scratch_bytes(g, o, rays->n) bytes (it
+ * replaces the reference's per-call s_* scratch arrays, R:277-278). */
+int64_t plx_render_scratch_bytes(const plx_grid *g, const plx_render_opts *o, int64_t n_rays);
 int plx_render_fused_bwd(const plx_grid *g, const plx_rays *rays,
                          const plx_render_opts *o, int32_t mse_mode, double up_scale,
                          double lam_cauchy, plx_grad *gb, double *out_rgb,
-                         double *out_sums, void *stream);
+                         double *out_sums, void *scratch, int64_t scratch_bytes,
+                         void *stream);
 
 /* max_weight_accum (K:414-453) via SparseGrid.max_weight_accumulate
  * (G:287-302).  out_w [rows] float64 is max-updated in place (caller zeroes). */
@@ -135,7 +139,8 @@ int plx_count_touched(const uint8_t *tmask, int64_t rows, int64_t *out_count,
  *   3. *_apply  -> new table (+ kept ids for prune)
  * plx_scan_scratch_bytes(n) sizes the scan workspace. */
 int plx_prune_mark(const plx_grid *g, const double *weights, double threshold,
-                   uint8_t *deemed_scratch, uint8_t *flags, void *stream);
+                   uint8_t *deemed_scratch /* 2 * ncell bytes */, uint8_t *flags,
+                   void *stream);
 int plx_prune_apply(const plx_grid *g, const int32_t *new_links, int64_t *kept_old,
                     float *new_table, void *stream);
 int plx_upsample_mark(const plx_grid *g, const int64_t new_dims[3], uint8_t *flags,

@@ -58,9 +58,10 @@ _D = ctypes.c_double
 _SIGS = {
     "plx_render_fwd": [ctypes.POINTER(PlxGrid), ctypes.POINTER(PlxRays),
                        ctypes.POINTER(PlxRenderOpts), _P, _P, _P, _P],
+    "plx_render_scratch_bytes": [ctypes.POINTER(PlxGrid), ctypes.POINTER(PlxRenderOpts), _I64],
     "plx_render_fused_bwd": [ctypes.POINTER(PlxGrid), ctypes.POINTER(PlxRays),
                              ctypes.POINTER(PlxRenderOpts), _I32, _D, _D,
-                             ctypes.POINTER(PlxGrad), _P, _P, _P],
+                             ctypes.POINTER(PlxGrad), _P, _P, _P, _I64, _P],
     "plx_max_weight": [ctypes.POINTER(PlxGrid), ctypes.POINTER(PlxRays),
                        ctypes.POINTER(PlxRenderOpts), _P, _P],
     "plx_tv": [ctypes.POINTER(PlxGrid), _P, _I64, _I64, _D, _D, _D, _D, _D, _D,
@@ -80,7 +81,7 @@ _SIGS = {
     "plx_version": [],
     "plx_device_check": [],
 }
-_RESTYPE = {"plx_scan_scratch_bytes": _I64, "plx_cell_occ_words": _I64,
+_RESTYPE = {"plx_scan_scratch_bytes": _I64, "plx_render_scratch_bytes": _I64, "plx_cell_occ_words": _I64,
             "plx_version": ctypes.c_char_p}
 
 EXPORTS = tuple(_SIGS)
@@ -145,6 +146,26 @@ def stream_ptr(stream=None) -> int:
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
+
+
+_scratch_cache: dict = {}
+
+
+def render_scratch(c_grid, c_opts, n_rays: int, device):
+    """Device workspace for plx_render_fused_bwd (cached per device, grown on
+    demand).  Returns (ptr, nbytes, tensor)."""
+    import torch
+    need = int(lib().plx_render_scratch_bytes(ctypes.byref(c_grid), ctypes.byref(c_opts),
+                                              int(n_rays)))
+    if need < 0:
+        raise ValueError("render_scratch: invalid grid / options")
+    key = str(device)
+    buf = _scratch_cache.get(key)
+    if buf is None or buf.numel() < need:
+        _scratch_cache.pop(key, None)
+        buf = torch.empty(max(need, 1 << 20), dtype=torch.uint8, device=device)
+        _scratch_cache[key] = buf
+    return buf.data_ptr(), buf.numel(), buf
 
 
 def dims_array(dims) -> ctypes.Array:

@@ -131,23 +131,24 @@ __device__ __forceinline__ void eval_sample(const DGrid &G, const RayMarch &rm, 
 }
 
 // Composite one chunk (K:213-233).  In: carry (T for relative, asum for
-// absolute), incl flags.  Out: per-lane T_i and w_i (valid on included
-// lanes; included lanes past the early stop are dropped), updated carry,
-// `stopped` (warp-uniform).
+// absolute), incl flags and att per lane.  Out: per-lane T_i and w_i (valid
+// on included lanes; included lanes past the early stop are dropped),
+// updated carry, `stopped` (warp-uniform).  Deterministic: pass 2 replays it
+// on the recorded (att, incl) and reproduces pass 1 bit-for-bit.
 template <bool ABS>
-__device__ __forceinline__ void composite_chunk(Sample &s, int lane, double stop,
+__device__ __forceinline__ void composite_chunk(bool &incl, double att, int lane, double stop,
                                                 double &Tcarry, double &Acarry, double &Ti,
                                                 double &wi, bool &stopped) {
     double Tn;
     if (!ABS) {
-        double a = s.incl ? s.att : 1.0;
+        double a = incl ? att : 1.0;
         double pinc = warp_scan_mul(a, lane);
         double pexc = __shfl_up_sync(PLX_FULL_MASK, pinc, 1);
         if (lane == 0) pexc = 1.0;
         Ti = Tcarry * pexc;
         Tn = Tcarry * pinc;
     } else {
-        double v = s.incl ? 1.0 - s.att : 0.0;
+        double v = incl ? 1.0 - att : 0.0;
         double sinc = warp_scan_add(v, lane);
         double sexc = __shfl_up_sync(PLX_FULL_MASK, sinc, 1);
         if (lane == 0) sexc = 0.0;
@@ -159,12 +160,12 @@ __device__ __forceinline__ void composite_chunk(Sample &s, int lane, double stop
         Acarry = before + v;   // lane-local; broadcast below
     }
     wi = Ti - Tn;
-    unsigned stopm = __ballot_sync(PLX_FULL_MASK, s.incl && Tn < stop);
+    unsigned stopm = __ballot_sync(PLX_FULL_MASK, incl && Tn < stop);
     int last = 31;
     if (stopm) {
         last = __ffs(stopm) - 1;
         stopped = true;
-        if (lane > last) s.incl = false;
+        if (lane > last) incl = false;
     }
     Tcarry = __shfl_sync(PLX_FULL_MASK, Tn, last);
     if (ABS) Acarry = __shfl_sync(PLX_FULL_MASK, Acarry, last);
@@ -172,15 +173,122 @@ __device__ __forceinline__ void composite_chunk(Sample &s, int lane, double stop
 
 __device__ __forceinline__ double relu(double x) { return x > 0.0 ? x : 0.0; }
 
+// Per-warp-slot scratch of the backward: pass 1 records, per included
+// sample, {att, c0, c1, c2} (+ sigma when the Cauchy term is on) and, per
+// chunk, {first position, included-lane mask}; pass 2 replays the
+// compositing from these records instead of re-gathering the grid.
+struct Scratch {
+    int *counter;      // dynamic ray scheduler (zeroed by the launcher)
+    double4 *rec;      // [slots][nrec]
+    double *rec_sig;   // [slots][nrec]
+    uint2 *meta;       // [slots][nchunk]
+    int64_t nrec, nchunk;
+};
+
+// Packed lattice cell (i, j, k) -> one 64-bit key (21 bits per axis).
+__device__ __forceinline__ long long pack_cell(int64_t i, int64_t j, int64_t k) {
+    return (long long)((i << 42) | (j << 21) | k);
+}
+
+// Register accumulators of the transposed scatter: lane c (< 28) holds
+// column c of the 8 stencil rows of the current cell.  When the ray steps
+// into a face/edge/corner-adjacent cell the shared corners are shifted
+// instead of flushed, so each grid row receives about one coalesced 28-lane
+// reduction per ray visit instead of one per sample x corner.
+template <bool NEAREST>
+struct RowAcc {
+    static constexpr int NQ = NEAREST ? 1 : 8;
+    float acc[NQ];
+    int32_t row[NQ];
+    long long cell;   // packed; -1 = none
+
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            acc[q] = 0.f;
+            row[q] = -1;
+        }
+        cell = -1;
+    }
+    __device__ __forceinline__ void flush(int q, float *grad, uint8_t *tmask, int lane) {
+        const int32_t r = row[q];
+        if (r >= 0) {
+            if (lane < PLX_ROW) red_add_f32(grad + (int64_t)r * PLX_ROW + lane, acc[q]);
+            if (lane == 0) tmask[r] = 1;
+        }
+        acc[q] = 0.f;
+    }
+    __device__ __forceinline__ void flush_all(float *grad, uint8_t *tmask, int lane) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) flush(q, grad, tmask, lane);
+        cell = -1;
+    }
+    // Corner bit `bit` of q (4 = x, 2 = y, 1 = z) moves by +-1.
+    __device__ __forceinline__ void shift(int bit, int delta, float *grad, uint8_t *tmask, int lane) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            if (q & bit) continue;
+            const int lo = q, hi = q | bit;
+            if (delta > 0) {   // lo corners leave, hi corners become lo
+                flush(lo, grad, tmask, lane);
+                acc[lo] = acc[hi];
+                row[lo] = row[hi];
+                acc[hi] = 0.f;
+                row[hi] = -1;
+            } else {           // hi corners leave, lo corners become hi
+                flush(hi, grad, tmask, lane);
+                acc[hi] = acc[lo];
+                row[hi] = row[lo];
+                acc[lo] = 0.f;
+                row[lo] = -1;
+            }
+        }
+    }
+    __device__ __forceinline__ void move_to(long long nc, const DGrid &G, float *grad,
+                                            uint8_t *tmask, int lane) {
+        const int64_t ni = nc >> 42, nj = (nc >> 21) & 0x1fffff, nk = nc & 0x1fffff;
+        if (NEAREST) {
+            flush(0, grad, tmask, lane);
+        } else if (cell >= 0) {
+            const int64_t ci = cell >> 42, cj = (cell >> 21) & 0x1fffff, ck = cell & 0x1fffff;
+            const int64_t di = ni - ci, dj = nj - cj, dk = nk - ck;
+            if (di >= -1 && di <= 1 && dj >= -1 && dj <= 1 && dk >= -1 && dk <= 1) {
+                if (di) shift(4, (int)di, grad, tmask, lane);
+                if (dj) shift(2, (int)dj, grad, tmask, lane);
+                if (dk) shift(1, (int)dk, grad, tmask, lane);
+            } else {
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) flush(q, grad, tmask, lane);
+            }
+        }
+        cell = nc;
+        const int32_t *base = G.links + flat(G, ni, nj, nk);
+        const int64_t sy = G.Dz, sx = (int64_t)G.Dy * G.Dz;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+            row[q] = __ldg(base + ((q >> 2) & 1) * sx + ((q >> 1) & 1) * sy + (q & 1));
+    }
+};
+
 template <int MODE, bool ABS, bool NEAREST>
-__global__ void __launch_bounds__(256) march_kernel(DGrid G, RayArgs R, KOpts O, Outs out) {
+__global__ void __launch_bounds__(256, 2)
+    march_kernel(DGrid G, RayArgs R, KOpts O, Outs out, Scratch S) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int64_t ray = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    const int64_t slot = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    const int64_t nslots = (int64_t)gridDim.x * (blockDim.x >> 5);
     __shared__ double red_mse[8], red_cau[8];
     double mse_part = 0.0, cau_part = 0.0;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    int64_t ray = slot;
 
-    if (ray < R.n) {
+    for (;;) {
+        if (MODE == BWD) {   // dynamic scheduling: rays differ widely in length
+            int r = 0;
+            if (lane == 0) r = atomicAdd(S.counter, 1);
+            ray = __shfl_sync(PLX_FULL_MASK, r, 0);
+        }
+        if (ray >= R.n) break;
         const int64_t src = R.idx ? R.idx[ray] : ray;
         RayMarch rm;
 #pragma unroll
@@ -198,13 +306,18 @@ __global__ void __launch_bounds__(256) march_kernel(DGrid G, RayArgs R, KOpts O,
         // ---------------- pass 1: forward ----------------
         double T = 1.0, A = 0.0, C0 = 0.0, C1 = 0.0, C2 = 0.0, wsum = 0.0;
         double Q0 = 0.0, Q1 = 0.0, Q2 = 0.0;   // absolute backward: sum c(bn - bi)
+        int64_t nch = 0, nrec = 0;              // recorded chunks / samples
+        double4 *rec = S.rec + slot * S.nrec;
+        double *rec_sig = S.rec_sig + slot * S.nrec;
+        uint2 *meta = S.meta + slot * S.nchunk;
         bool stopped = false;
         for (int64_t base = 0; base < rm.nsamp && !stopped; base += 32) {
             Sample s;
             eval_sample<MODE, NEAREST>(G, rm, O.step, base + lane, basis, s);
             if (!__any_sync(PLX_FULL_MASK, s.incl)) continue;
             double Ti, wi;
-            composite_chunk<(MODE == MAXW ? false : ABS)>(s, lane, O.stop, T, A, Ti, wi, stopped);
+            composite_chunk<(MODE == MAXW ? false : ABS)>(s.incl, s.att, lane, O.stop, T, A, Ti,
+                                                           wi, stopped);
             if (MODE == MAXW) {
                 if (s.incl) {
                     double w = Ti * (1.0 - s.att);   // K:446
@@ -218,6 +331,17 @@ __global__ void __launch_bounds__(256) march_kernel(DGrid G, RayArgs R, KOpts O,
                     }
                 }
                 continue;
+            }
+            if (MODE == BWD) {   // record the chunk for pass 2
+                const unsigned m = __ballot_sync(PLX_FULL_MASK, s.incl);
+                if (lane == 0) meta[nch] = make_uint2((unsigned)base, m);
+                if (s.incl) {
+                    const int64_t k = nrec + __popc(m & lt_mask);
+                    rec[k] = make_double4(s.att, s.c[0], s.c[1], s.c[2]);
+                    if (out.lam_cauchy > 0.0) rec_sig[k] = s.sig;
+                }
+                ++nch;
+                nrec += __popc(m);
             }
             double x0 = 0.0, x1 = 0.0, x2 = 0.0, xw = 0.0;
             if (s.incl) {
@@ -237,128 +361,181 @@ __global__ void __launch_bounds__(256) march_kernel(DGrid G, RayArgs R, KOpts O,
             C2 += warp_sum(x2);
             if (MODE == FWD) wsum += warp_sum(xw);
         }
-        if (MODE == MAXW) goto done;
-        {
-            const double rgb0 = C0 + T * O.bg[0], rgb1 = C1 + T * O.bg[1], rgb2 = C2 + T * O.bg[2];
-            if (lane == 0 && out.rgb) {
-                out.rgb[3 * ray + 0] = rgb0;
-                out.rgb[3 * ray + 1] = rgb1;
-                out.rgb[3 * ray + 2] = rgb2;
+        if (MODE == MAXW) {
+            ray += nslots;
+            continue;
+        }
+        const double rgb0 = C0 + T * O.bg[0], rgb1 = C1 + T * O.bg[1], rgb2 = C2 + T * O.bg[2];
+        if (lane == 0 && out.rgb) {
+            out.rgb[3 * ray + 0] = rgb0;
+            out.rgb[3 * ray + 1] = rgb1;
+            out.rgb[3 * ray + 2] = rgb2;
+        }
+        if (MODE == FWD) {
+            if (lane == 0) {
+                if (out.trans) out.trans[ray] = T;
+                if (out.wsum) out.wsum[ray] = wsum;
             }
-            if (MODE == FWD) {
-                if (lane == 0) {
-                    if (out.trans) out.trans[ray] = T;
-                    if (out.wsum) out.wsum[ray] = wsum;
-                }
-                goto done;
+            ray += nslots;
+            continue;
+        }
+        // ---------------- upstream (K:330-341) ----------------
+        double up0, up1, up2;
+        if (out.mse_mode) {
+            const double e0 = rgb0 - __ldg(R.target + 3 * src + 0);
+            const double e1 = rgb1 - __ldg(R.target + 3 * src + 1);
+            const double e2 = rgb2 - __ldg(R.target + 3 * src + 2);
+            if (lane == 0) mse_part += e0 * e0 + e1 * e1 + e2 * e2;
+            up0 = out.up_scale * e0;
+            up1 = out.up_scale * e1;
+            up2 = out.up_scale * e2;
+        } else {
+            up0 = __ldg(R.target + 3 * src + 0);
+            up1 = __ldg(R.target + 3 * src + 1);
+            up2 = __ldg(R.target + 3 * src + 2);
+        }
+        if (ABS) {
+            Q0 = warp_sum(Q0);
+            Q1 = warp_sum(Q1);
+            Q2 = warp_sum(Q2);
+        }
+        // ---------------- pass 2: replay + transposed scatter ----------------
+        // sf before sample i in the reference's reverse sweep:
+        //   relative: T bg + sum_{j>i} w_j c_j = rgb - P_i      (K:351-353, 381-383)
+        //   absolute: -bg [T>0] + sum_{j>i} c_j (bn_j - bi_j)   (K:346-349, 374-376)
+        const double bend = T > 0.0 ? 1.0 : 0.0;
+        // lane c's column: 0 = sigma, 1 + 9 ch + b = SH (channel-major, sh.py:3-7)
+        const int col_ch = lane >= 1 ? (lane - 1) / 9 : 0;
+        float col_basis = 0.f;
+        if (lane >= 1 && lane < PLX_ROW) {
+            const int b = (lane - 1) % 9;
+#pragma unroll
+            for (int bb = 0; bb < 9; ++bb)
+                if (bb == b) col_basis = (float)basis[bb];
+        }
+        RowAcc<NEAREST> ra;
+        ra.init();
+        double P0 = 0.0, P1 = 0.0, P2 = 0.0;
+        double T2 = 1.0, A2 = 0.0;
+        bool stopped2 = false;
+        int64_t k0 = 0;
+        for (int64_t c = 0; c < nch; ++c) {
+            const uint2 mt = meta[c];
+            const unsigned mask = mt.y;
+            const int64_t si = (int64_t)mt.x + lane;
+            bool incl = (mask >> lane) & 1u;
+            double att = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, sig = 0.0;
+            if (incl) {
+                const int64_t k = k0 + __popc(mask & lt_mask);
+                const double4 r4 = rec[k];
+                att = r4.x;
+                c0 = r4.y;
+                c1 = r4.z;
+                c2 = r4.w;
+                if (out.lam_cauchy > 0.0) sig = rec_sig[k];
             }
-            // ---------------- upstream (K:330-341) ----------------
-            double up0, up1, up2;
-            if (out.mse_mode) {
-                const double e0 = rgb0 - __ldg(R.target + 3 * src + 0);
-                const double e1 = rgb1 - __ldg(R.target + 3 * src + 1);
-                const double e2 = rgb2 - __ldg(R.target + 3 * src + 2);
-                mse_part = e0 * e0 + e1 * e1 + e2 * e2;
-                up0 = out.up_scale * e0;
-                up1 = out.up_scale * e1;
-                up2 = out.up_scale * e2;
+            k0 += __popc(mask);
+            double Ti, wi;
+            composite_chunk<ABS>(incl, att, lane, O.stop, T2, A2, Ti, wi, stopped2);
+            const double cc0 = relu(c0), cc1 = relu(c1), cc2 = relu(c2);
+            double t, dlt, g[3];
+            sample_coords(rm, G, O.step, si, t, dlt, g);
+            double gsig;
+            if (!ABS) {
+                double y0 = incl ? wi * cc0 : 0.0, y1 = incl ? wi * cc1 : 0.0,
+                       y2 = incl ? wi * cc2 : 0.0;
+                double i0 = P0 + warp_scan_add(y0, lane), i1 = P1 + warp_scan_add(y1, lane),
+                       i2 = P2 + warp_scan_add(y2, lane);
+                P0 = __shfl_sync(PLX_FULL_MASK, i0, 31);
+                P1 = __shfl_sync(PLX_FULL_MASK, i1, 31);
+                P2 = __shfl_sync(PLX_FULL_MASK, i2, 31);
+                const double sf0 = rgb0 - i0, sf1 = rgb1 - i1, sf2 = rgb2 - i2;
+                gsig = dlt * (up0 * (Ti * att * cc0 - sf0) + up1 * (Ti * att * cc1 - sf1) +
+                              up2 * (Ti * att * cc2 - sf2));
             } else {
-                up0 = __ldg(R.target + 3 * src + 0);
-                up1 = __ldg(R.target + 3 * src + 1);
-                up2 = __ldg(R.target + 3 * src + 2);
+                const double Tn = Ti - wi;
+                const double bn = Tn > 0.0 ? 1.0 : 0.0, bi = Ti > 0.0 ? 1.0 : 0.0;
+                double y0 = incl ? cc0 * (bn - bi) : 0.0, y1 = incl ? cc1 * (bn - bi) : 0.0,
+                       y2 = incl ? cc2 * (bn - bi) : 0.0;
+                double i0 = P0 + warp_scan_add(y0, lane), i1 = P1 + warp_scan_add(y1, lane),
+                       i2 = P2 + warp_scan_add(y2, lane);
+                P0 = __shfl_sync(PLX_FULL_MASK, i0, 31);
+                P1 = __shfl_sync(PLX_FULL_MASK, i1, 31);
+                P2 = __shfl_sync(PLX_FULL_MASK, i2, 31);
+                const double sf0 = -O.bg[0] * bend + (Q0 - i0);
+                const double sf1 = -O.bg[1] * bend + (Q1 - i1);
+                const double sf2 = -O.bg[2] * bend + (Q2 - i2);
+                const double galpha =
+                    (up0 * (cc0 * bn + sf0) + up1 * (cc1 * bn + sf1) + up2 * (cc2 * bn + sf2));
+                gsig = galpha * dlt * att;
             }
-            if (ABS) {   // sum over all lanes of the per-lane Q partials
-                Q0 = warp_sum(Q0);
-                Q1 = warp_sum(Q1);
-                Q2 = warp_sum(Q2);
+            if (incl && out.lam_cauchy > 0.0) {   // K:384-386
+                cau_part += log(1.0 + 2.0 * sig * sig);
+                gsig += out.lam_cauchy * 4.0 * sig / (1.0 + 2.0 * sig * sig);
             }
-            // sf before processing sample i in the reference's reverse sweep:
-            //   relative: T bg + sum_{j>i} w_j c_j = rgb - P_i      (K:351-353, 381-383)
-            //   absolute: -bg [T>0] + sum_{j>i} c_j (bn_j - bi_j)   (K:346-349, 374-376)
-            const double bend = T > 0.0 ? 1.0 : 0.0;
-            double P0 = 0.0, P1 = 0.0, P2 = 0.0;   // running prefix (carry)
-            double T2 = 1.0, A2 = 0.0;
-            bool stopped2 = false;
-            for (int64_t base = 0; base < rm.nsamp && !stopped2; base += 32) {
-                Sample s;
-                eval_sample<MODE, NEAREST>(G, rm, O.step, base + lane, basis, s);
-                if (!__any_sync(PLX_FULL_MASK, s.incl)) continue;
-                double Ti, wi;
-                composite_chunk<ABS>(s, lane, O.stop, T2, A2, Ti, wi, stopped2);
-                const double cc0 = relu(s.c[0]), cc1 = relu(s.c[1]), cc2 = relu(s.c[2]);
-                double gsig = 0.0;
-                if (!ABS) {
-                    double y0 = s.incl ? wi * cc0 : 0.0, y1 = s.incl ? wi * cc1 : 0.0,
-                           y2 = s.incl ? wi * cc2 : 0.0;
-                    double i0 = P0 + warp_scan_add(y0, lane), i1 = P1 + warp_scan_add(y1, lane),
-                           i2 = P2 + warp_scan_add(y2, lane);
-                    P0 = __shfl_sync(PLX_FULL_MASK, i0, 31);
-                    P1 = __shfl_sync(PLX_FULL_MASK, i1, 31);
-                    P2 = __shfl_sync(PLX_FULL_MASK, i2, 31);
-                    const double sf0 = rgb0 - i0, sf1 = rgb1 - i1, sf2 = rgb2 - i2;
-                    gsig = s.dlt * (up0 * (Ti * s.att * cc0 - sf0) + up1 * (Ti * s.att * cc1 - sf1) +
-                                    up2 * (Ti * s.att * cc2 - sf2));
+            // per-sample scatter payload (K:387-410): dL/dsigma, dL/dc per channel
+            const float gs_f = (float)gsig;
+            const float gc0_f = c0 > 0.0 ? (float)(up0 * wi) : 0.f;
+            const float gc1_f = c1 > 0.0 ? (float)(up1 * wi) : 0.f;
+            const float gc2_f = c2 > 0.0 ? (float)(up2 * wi) : 0.f;
+            // this lane's stencil cell and fractional offsets
+            long long cellkey;
+            float fx, fy, fz;
+            if (NEAREST) {
+                int64_t i = (int64_t)(g[0] + 0.5), j = (int64_t)(g[1] + 0.5), k = (int64_t)(g[2] + 0.5);
+                if (i > G.Dx - 1) i = G.Dx - 1;
+                if (j > G.Dy - 1) j = G.Dy - 1;
+                if (k > G.Dz - 1) k = G.Dz - 1;
+                cellkey = pack_cell(i, j, k);
+                fx = fy = fz = 0.f;
+            } else {
+                int64_t i0 = (int64_t)g[0], j0 = (int64_t)g[1], kk0 = (int64_t)g[2];
+                if (i0 > G.Dx - 2) i0 = G.Dx - 2;
+                if (j0 > G.Dy - 2) j0 = G.Dy - 2;
+                if (kk0 > G.Dz - 2) kk0 = G.Dz - 2;
+                cellkey = pack_cell(i0, j0, kk0);
+                fx = (float)(g[0] - (double)i0);
+                fy = (float)(g[1] - (double)j0);
+                fz = (float)(g[2] - (double)kk0);
+            }
+            unsigned m = mask;   // already truncated at the early stop in pass 1
+            while (m) {
+                const int j = __ffs(m) - 1;
+                m &= m - 1;
+                const long long cj = __shfl_sync(PLX_FULL_MASK, cellkey, j);
+                const float gsj = __shfl_sync(PLX_FULL_MASK, gs_f, j);
+                const float g0j = __shfl_sync(PLX_FULL_MASK, gc0_f, j);
+                const float g1j = __shfl_sync(PLX_FULL_MASK, gc1_f, j);
+                const float g2j = __shfl_sync(PLX_FULL_MASK, gc2_f, j);
+                if (cj != ra.cell) ra.move_to(cj, G, out.grad, out.tmask, lane);
+                const float gcol = lane == 0 ? gsj : (col_ch == 0 ? g0j : (col_ch == 1 ? g1j : g2j)) * col_basis;
+                if (NEAREST) {
+                    ra.acc[0] += gcol;
                 } else {
-                    const double Tn = Ti - wi;
-                    const double bn = Tn > 0.0 ? 1.0 : 0.0, bi = Ti > 0.0 ? 1.0 : 0.0;
-                    double y0 = s.incl ? cc0 * (bn - bi) : 0.0, y1 = s.incl ? cc1 * (bn - bi) : 0.0,
-                           y2 = s.incl ? cc2 * (bn - bi) : 0.0;
-                    double i0 = P0 + warp_scan_add(y0, lane), i1 = P1 + warp_scan_add(y1, lane),
-                           i2 = P2 + warp_scan_add(y2, lane);
-                    P0 = __shfl_sync(PLX_FULL_MASK, i0, 31);
-                    P1 = __shfl_sync(PLX_FULL_MASK, i1, 31);
-                    P2 = __shfl_sync(PLX_FULL_MASK, i2, 31);
-                    const double sf0 = -O.bg[0] * bend + (Q0 - i0);
-                    const double sf1 = -O.bg[1] * bend + (Q1 - i1);
-                    const double sf2 = -O.bg[2] * bend + (Q2 - i2);
-                    const double galpha =
-                        (up0 * (cc0 * bn + sf0) + up1 * (cc1 * bn + sf1) + up2 * (cc2 * bn + sf2));
-                    gsig = galpha * s.dlt * s.att;
-                }
-                if (!s.incl) continue;
-                if (out.lam_cauchy > 0.0) {   // K:384-386
-                    cau_part += log(1.0 + 2.0 * s.sig * s.sig);
-                    gsig += out.lam_cauchy * 4.0 * s.sig / (1.0 + 2.0 * s.sig * s.sig);
-                }
-                const double gc0 = s.c[0] > 0.0 ? up0 * wi : 0.0;   // K:387-389
-                const double gc1 = s.c[1] > 0.0 ? up1 * wi : 0.0;
-                const double gc2 = s.c[2] > 0.0 ? up2 * wi : 0.0;
-                const bool any_c = gc0 != 0.0 || gc1 != 0.0 || gc2 != 0.0;
-                constexpr int NQ = NEAREST ? 1 : 8;
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {   // K:395-410
-                    const int32_t r = s.rows[q];
-                    if (r < 0) continue;
-                    const double wq = s.ws[q];
-                    out.tmask[r] = 1;
-                    float *gr = out.grad + (int64_t)r * PLX_ROW;
-                    const float gs = (float)(wq * gsig);
-                    if (!any_c) {
-                        red_add_f32(gr, gs);
-                        continue;
-                    }
-                    const double k0 = wq * gc0, k1 = wq * gc1, k2 = wq * gc2;
-                    float v[PLX_ROW];
-                    v[0] = gs;
-#pragma unroll
-                    for (int b = 0; b < 9; ++b) {
-                        v[1 + b] = (float)(k0 * basis[b]);
-                        v[10 + b] = (float)(k1 * basis[b]);
-                        v[19 + b] = (float)(k2 * basis[b]);
-                    }
-#pragma unroll
-                    for (int m = 0; m < 7; ++m)
-                        red_add_v4(gr + 4 * m, v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]);
+                    const float fxj = __shfl_sync(PLX_FULL_MASK, fx, j);
+                    const float fyj = __shfl_sync(PLX_FULL_MASK, fy, j);
+                    const float fzj = __shfl_sync(PLX_FULL_MASK, fz, j);
+                    const float x0 = (1.f - fxj) * gcol, x1 = fxj * gcol;
+                    const float y0 = 1.f - fyj, y1 = fyj, z0 = 1.f - fzj, z1 = fzj;
+                    ra.acc[0] += x0 * y0 * z0;
+                    ra.acc[1] += x0 * y0 * z1;
+                    ra.acc[2] += x0 * y1 * z0;
+                    ra.acc[3] += x0 * y1 * z1;
+                    ra.acc[4] += x1 * y0 * z0;
+                    ra.acc[5] += x1 * y0 * z1;
+                    ra.acc[6] += x1 * y1 * z0;
+                    ra.acc[7] += x1 * y1 * z1;
                 }
             }
         }
+        ra.flush_all(out.grad, out.tmask, lane);
+        ray += nslots;
     }
-done:
     if (MODE == BWD) {
-        mse_part = warp_sum(mse_part);   // lanes hold identical mse_part; take lane 0's
         cau_part = warp_sum(cau_part);
+        mse_part = warp_sum(mse_part);   // only lane 0 contributed
         if (lane == 0) {
-            red_mse[warp] = mse_part / 32.0;
+            red_mse[warp] = mse_part;
             red_cau[warp] = cau_part;
         }
         __syncthreads();
@@ -381,35 +558,109 @@ using namespace plx;
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
 
 bool grid_ok(const plx_grid *g) {
     return g && g->links && g->dims[0] >= 2 && g->dims[1] >= 2 && g->dims[2] >= 2 &&
-           (g->rows == 0 || g->table) &&
-           g->dims[0] * g->dims[1] * g->dims[2] < (int64_t)1 << 31;
+           (g->rows == 0 || g->table) && g->dims[0] < (1 << 21) && g->dims[1] < (1 << 21) &&
+           g->dims[2] < (1 << 21) && g->dims[0] * g->dims[1] * g->dims[2] < (int64_t)1 << 31;
+}
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <int MODE, bool ABS, bool NEAREST>
+int blocks_per_sm() {
+    static int nb = 0;
+    if (!nb) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, march_kernel<MODE, ABS, NEAREST>, kThreads, 0);
+        if (nb <= 0) nb = 1;
+    }
+    return nb;
+}
+
+int bwd_blocks_per_sm(const plx_render_opts *o) {
+    if (o->nearest)
+        return o->absolute ? blocks_per_sm<BWD, true, true>() : blocks_per_sm<BWD, false, true>();
+    return o->absolute ? blocks_per_sm<BWD, true, false>() : blocks_per_sm<BWD, false, false>();
+}
+
+// Capacity of one warp slot: every march position of the longest chord (R:67-69).
+int64_t max_records(const plx_grid *g, double step) {
+    double d2 = 0.0;
+    for (int a = 0; a < 3; ++a) d2 += (g->hi[a] - g->lo[a]) * (g->hi[a] - g->lo[a]);
+    return (int64_t)ceil(sqrt(d2) / step) + 4;
+}
+
+struct ScratchLayout {
+    int64_t slots, nrec, nchunk, bytes, off_rec, off_sig, off_meta;
+};
+
+ScratchLayout layout(const plx_grid *g, const plx_render_opts *o, int64_t n_rays) {
+    ScratchLayout L;
+    int64_t blocks = (int64_t)num_sms() * bwd_blocks_per_sm(o);
+    const int64_t need = (n_rays + kWarps - 1) / kWarps;
+    if (n_rays > 0 && need < blocks) blocks = need;
+    L.slots = blocks * kWarps;
+    L.nrec = max_records(g, o->step);
+    L.nchunk = L.nrec / 32 + 2;
+    L.off_rec = 256;
+    L.off_sig = L.off_rec + L.slots * L.nrec * (int64_t)sizeof(double4);
+    L.off_meta = L.off_sig + L.slots * L.nrec * (int64_t)sizeof(double);
+    L.bytes = L.off_meta + L.slots * L.nchunk * (int64_t)sizeof(uint2);
+    return L;
 }
 
 template <int MODE>
 int launch_march(const plx_grid *g, const plx_rays *rays, const plx_render_opts *o, Outs out,
-                 void *stream) {
+                 void *scratch, int64_t scratch_bytes, void *stream) {
     if (!grid_ok(g) || !rays || !o || rays->n < 0 || !rays->origins || !rays->dirs) return PLX_EINVAL;
+    if (rays->n >= (int64_t)1 << 31) return PLX_EINVAL;
     if (MODE != MAXW && !rays->viewdirs) return PLX_EINVAL;
-    if (MODE == BWD && (!rays->target || !out.grad || !out.tmask || !out.sums)) return PLX_EINVAL;
+    if (MODE == BWD && (!rays->target || !out.grad || !out.tmask || !out.sums || !scratch))
+        return PLX_EINVAL;
     if (!(o->step > 0.0)) return PLX_EINVAL;
     if (rays->n == 0) return PLX_OK;
     DGrid G = make_dgrid(*g);
     RayArgs R{rays->origins, rays->dirs, rays->viewdirs, rays->target, rays->jitter, rays->idx,
               rays->n};
     KOpts K{o->step, o->stop_thresh, {o->bg[0], o->bg[1], o->bg[2]}};
-    const int warps = kThreads / 32;
-    dim3 grid((unsigned)((rays->n + warps - 1) / warps));
     cudaStream_t s = (cudaStream_t)stream;
+    Scratch S{};
+    int64_t blocks;
+    if (MODE == BWD) {
+        const ScratchLayout L = layout(g, o, rays->n);
+        if (scratch_bytes < L.bytes) return PLX_EINVAL;
+        char *base = reinterpret_cast<char *>(scratch);
+        S.counter = reinterpret_cast<int *>(base);
+        S.rec = reinterpret_cast<double4 *>(base + L.off_rec);
+        S.rec_sig = reinterpret_cast<double *>(base + L.off_sig);
+        S.meta = reinterpret_cast<uint2 *>(base + L.off_meta);
+        S.nrec = L.nrec;
+        S.nchunk = L.nchunk;
+        blocks = L.slots / kWarps;
+        if (cudaMemsetAsync(S.counter, 0, sizeof(int), s) != cudaSuccess) return PLX_ECUDA;
+    } else {   // static grid-stride over rays, occupancy-sized grid
+        blocks = (rays->n + kWarps - 1) / kWarps;
+        const int64_t cap = (int64_t)num_sms() * 4;
+        if (blocks > cap) blocks = cap;
+    }
     const bool ABSF = MODE != MAXW && o->absolute;
+    dim3 grid((unsigned)blocks);
     if (o->nearest) {
-        if (ABSF) march_kernel<MODE, true, true><<<grid, kThreads, 0, s>>>(G, R, K, out);
-        else march_kernel<MODE, false, true><<<grid, kThreads, 0, s>>>(G, R, K, out);
+        if (ABSF) march_kernel<MODE, true, true><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
+        else march_kernel<MODE, false, true><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
     } else {
-        if (ABSF) march_kernel<MODE, true, false><<<grid, kThreads, 0, s>>>(G, R, K, out);
-        else march_kernel<MODE, false, false><<<grid, kThreads, 0, s>>>(G, R, K, out);
+        if (ABSF) march_kernel<MODE, true, false><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
+        else march_kernel<MODE, false, false><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
     }
     return cudaPeekAtLastError() == cudaSuccess ? PLX_OK : PLX_ECUDA;
 }
@@ -423,13 +674,20 @@ extern "C" int plx_render_fwd(const plx_grid *g, const plx_rays *rays, const plx
     out.rgb = out_rgb;
     out.trans = out_trans;
     out.wsum = out_wsum;
-    return launch_march<FWD>(g, rays, o, out, stream);
+    return launch_march<FWD>(g, rays, o, out, nullptr, 0, stream);
+}
+
+extern "C" int64_t plx_render_scratch_bytes(const plx_grid *g, const plx_render_opts *o,
+                                            int64_t n_rays) {
+    if (!grid_ok(g) || !o || !(o->step > 0.0)) return -1;
+    return layout(g, o, n_rays).bytes;
 }
 
 extern "C" int plx_render_fused_bwd(const plx_grid *g, const plx_rays *rays,
                                     const plx_render_opts *o, int32_t mse_mode, double up_scale,
                                     double lam_cauchy, plx_grad *gb, double *out_rgb,
-                                    double *out_sums, void *stream) {
+                                    double *out_sums, void *scratch, int64_t scratch_bytes,
+                                    void *stream) {
     if (!gb) return PLX_EINVAL;
     Outs out{};
     out.rgb = out_rgb;
@@ -439,7 +697,7 @@ extern "C" int plx_render_fused_bwd(const plx_grid *g, const plx_rays *rays,
     out.mse_mode = mse_mode;
     out.up_scale = up_scale;
     out.lam_cauchy = lam_cauchy;
-    return launch_march<BWD>(g, rays, o, out, stream);
+    return launch_march<BWD>(g, rays, o, out, scratch, scratch_bytes, stream);
 }
 
 extern "C" int plx_max_weight(const plx_grid *g, const plx_rays *rays, const plx_render_opts *o,
@@ -447,5 +705,5 @@ extern "C" int plx_max_weight(const plx_grid *g, const plx_rays *rays, const plx
     if (!out_w) return PLX_EINVAL;
     Outs out{};
     out.maxw = out_w;
-    return launch_march<MAXW>(g, rays, o, out, stream);
+    return launch_march<MAXW>(g, rays, o, out, nullptr, 0, stream);
 }

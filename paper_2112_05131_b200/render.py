@@ -179,9 +179,10 @@ def _launch_bwd(grid, r, opts, mse_mode, up_scale, lam_cauchy, grads, rgb, sums)
     if grads.n_rows != grid.n_rows:
         raise ValueError("gradient buffer rows do not match the grid table")
     c, ko, gb = grid._c(with_occ=opts.interp == "trilinear"), kernel_opts(grid, opts), grads._c()
+    sp, sn, _keep = _lib.render_scratch(c, ko, r.n, grid.device)
     _lib.check(_lib.lib().plx_render_fused_bwd(
         ctypes.byref(c), ctypes.byref(r), ctypes.byref(ko), int(mse_mode), float(up_scale),
-        float(lam_cauchy), ctypes.byref(gb), _lib.ptr(rgb), sums.data_ptr(),
+        float(lam_cauchy), ctypes.byref(gb), _lib.ptr(rgb), sums.data_ptr(), sp, sn,
         _lib.stream_ptr()), "render_fused_bwd")
 
 
@@ -277,9 +278,10 @@ def fused_mse_backward_pool(grid: SparseGrid, pool: RayPool, idx: torch.Tensor,
     c = cgrid if cgrid is not None else grid._c(with_occ=opts.interp == "trilinear")
     ko = kopts if kopts is not None else kernel_opts(grid, opts)
     gb = grads._c()
+    sp, sn, _keep = _lib.render_scratch(c, ko, r.n, grid.device)
     _lib.check(_lib.lib().plx_render_fused_bwd(
         ctypes.byref(c), ctypes.byref(r), ctypes.byref(ko), 1, 2.0 / n_total, float(lam_cauchy),
-        ctypes.byref(gb), None, sums.data_ptr(), _lib.stream_ptr()), "render_fused_bwd")
+        ctypes.byref(gb), None, sums.data_ptr(), sp, sn, _lib.stream_ptr()), "render_fused_bwd")
 
 
 def render_image(grid: SparseGrid, camera, opts: RenderOptions | None = None,
