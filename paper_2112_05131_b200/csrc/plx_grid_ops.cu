@@ -155,41 +155,27 @@ __device__ __forceinline__ int nonzero_bytes(uint32_t m) {
     return __popc(m);
 }
 
-__device__ __forceinline__ void opt_update_quad(const OptArgs &a, int64_t row, int quad) {
-    float4 *gp = reinterpret_cast<float4 *>(a.grad + row * PLX_ROW) + quad;
-    if (!a.update) {
-        if (a.clear) *gp = make_float4(0.f, 0.f, 0.f, 0.f);
-        return;
-    }
-    float4 *tp = reinterpret_cast<float4 *>(a.table + row * PLX_ROW) + quad;
-    const float4 g4 = *gp;
-    const float4 t4 = *tp;
+// The update of one float4 of one row (K:578-590), float64 arithmetic.
+__device__ __forceinline__ void opt_apply(const OptArgs &a, int quad, float4 &g4, float4 &t4,
+                                          float4 &v4) {
     float g[4] = {g4.x, g4.y, g4.z, g4.w};
     float t[4] = {t4.x, t4.y, t4.z, t4.w};
-    if (a.rmsprop) {
-        float4 *vp = reinterpret_cast<float4 *>(a.v + row * PLX_ROW) + quad;
-        const float4 v4 = *vp;
-        float v[4] = {v4.x, v4.y, v4.z, v4.w};
+    float v[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            if (g[e] == 0.0f) continue;   // K:581-583: stale state
-            const double gd = (double)g[e];
-            const double lr = (quad == 0 && e == 0) ? a.lr_sigma : a.lr_sh;
+    for (int e = 0; e < 4; ++e) {
+        if (g[e] == 0.0f) continue;   // K:581-583: stale state
+        const double gd = (double)g[e];
+        const double lr = (quad == 0 && e == 0) ? a.lr_sigma : a.lr_sh;
+        if (a.rmsprop) {
             const double nv = a.beta * (double)v[e] + (1.0 - a.beta) * gd * gd;
             v[e] = (float)nv;
             t[e] = (float)((double)t[e] - lr * gd / (sqrt(nv) + a.eps));
-        }
-        *vp = make_float4(v[0], v[1], v[2], v[3]);
-    } else {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            if (g[e] == 0.0f) continue;
-            const double lr = (quad == 0 && e == 0) ? a.lr_sigma : a.lr_sh;
-            t[e] = (float)((double)t[e] - lr * (double)g[e]);
+        } else {
+            t[e] = (float)((double)t[e] - lr * gd);
         }
     }
-    *tp = make_float4(t[0], t[1], t[2], t[3]);
-    if (a.clear) *gp = make_float4(0.f, 0.f, 0.f, 0.f);
+    t4 = make_float4(t[0], t[1], t[2], t[3]);
+    v4 = make_float4(v[0], v[1], v[2], v[3]);
 }
 
 template <int NT>
@@ -234,10 +220,37 @@ __global__ void __launch_bounds__(NT) opt_kernel(OptArgs a) {
             if ((m >> (8 * e)) & 0xffu) list[wib][pos++] = (uint8_t)(lane * 4 + e);
         __syncwarp();
         cnt += (unsigned long long)total;
-        for (int gidx = 0; gidx < total; gidx += 8) {   // two 4-row groups in flight
-            const int j0 = gidx + sub, j1 = gidx + 4 + sub;
-            if (lane < 28 && j0 < total) opt_update_quad(a, seg * 128 + list[wib][j0], quad);
-            if (lane < 28 && j1 < total) opt_update_quad(a, seg * 128 + list[wib][j1], quad);
+        constexpr int U = 2;   // 2 groups x 4 rows: 6 float4 loads in flight per lane
+        for (int gidx = 0; gidx < total; gidx += 4 * U) {
+            float4 g4[U], t4[U], v4[U];
+            int64_t rw[U];
+            bool act[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = gidx + 4 * u + sub;
+                act[u] = lane < 28 && j < total;
+                rw[u] = act[u] ? seg * 128 + list[wib][j] : 0;
+                if (act[u]) {
+                    g4[u] = reinterpret_cast<const float4 *>(a.grad + rw[u] * PLX_ROW)[quad];
+                    if (a.update) {
+                        t4[u] = reinterpret_cast<const float4 *>(a.table + rw[u] * PLX_ROW)[quad];
+                        if (a.rmsprop)
+                            v4[u] = reinterpret_cast<const float4 *>(a.v + rw[u] * PLX_ROW)[quad];
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (!act[u]) continue;
+                if (a.update) {
+                    opt_apply(a, quad, g4[u], t4[u], v4[u]);
+                    reinterpret_cast<float4 *>(a.table + rw[u] * PLX_ROW)[quad] = t4[u];
+                    if (a.rmsprop) reinterpret_cast<float4 *>(a.v + rw[u] * PLX_ROW)[quad] = v4[u];
+                }
+                if (a.clear)
+                    reinterpret_cast<float4 *>(a.grad + rw[u] * PLX_ROW)[quad] =
+                        make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         }
         if (a.clear && m) {
             if (r0 + 3 < a.rows) {
@@ -261,6 +274,15 @@ static int num_sms() {
         if (g_num_sms <= 0) g_num_sms = 148;
     }
     return g_num_sms;
+}
+
+static int opt_blocks_per_sm() {
+    static int nb = 0;
+    if (!nb) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, opt_kernel<256>, 256, 0);
+        if (nb <= 0) nb = 1;
+    }
+    return nb;
 }
 
 template <int NT>
@@ -563,7 +585,7 @@ extern "C" int plx_opt_step(plx_grid *g, float *v, plx_grad *gb, double lr_sigma
     constexpr int NT = 256;
     const int64_t segs = (g->rows + 127) / 128;
     int64_t nb = (segs + NT / 32 - 1) / (NT / 32);
-    if (nb > (int64_t)num_sms() * 4) nb = (int64_t)num_sms() * 4;   // persistent: 4 x 256 thr / SM
+    if (nb > (int64_t)num_sms() * opt_blocks_per_sm()) nb = (int64_t)num_sms() * opt_blocks_per_sm();
     opt_kernel<NT><<<(unsigned)nb, NT, 0, (cudaStream_t)stream>>>(a);
     return status();
 }
@@ -576,7 +598,7 @@ extern "C" int plx_clear_grad(plx_grad *gb, int64_t rows, int64_t *out_count, vo
     constexpr int NT = 256;
     const int64_t segs = (rows + 127) / 128;
     int64_t nb = (segs + NT / 32 - 1) / (NT / 32);
-    if (nb > (int64_t)num_sms() * 4) nb = (int64_t)num_sms() * 4;
+    if (nb > (int64_t)num_sms() * opt_blocks_per_sm()) nb = (int64_t)num_sms() * opt_blocks_per_sm();
     opt_kernel<NT><<<(unsigned)nb, NT, 0, (cudaStream_t)stream>>>(a);
     return status();
 }

@@ -18,6 +18,8 @@
 // equals (rgb - prefix_i) and is formed in float64, where the cancellation is
 // harmless (|error| ~ 1e-16 |rgb|).  Gradients are scattered with vector
 // f32 reductions (red.global.add.v4.f32, 7 per stencil row).
+#include <stdlib.h>
+
 #include "plx_common.cuh"
 
 namespace plx {
@@ -270,8 +272,8 @@ struct RowAcc {
     }
 };
 
-template <int MODE, bool ABS, bool NEAREST>
-__global__ void __launch_bounds__(256, 2)
+template <int MODE, bool ABS, bool NEAREST, int MINB>
+__global__ void __launch_bounds__(256, MINB)
     march_kernel(DGrid G, RayArgs R, KOpts O, Outs out, Scratch S) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -577,20 +579,51 @@ int num_sms() {
     return n;
 }
 
-template <int MODE, bool ABS, bool NEAREST>
+// Minimum resident blocks per SM the backward is compiled for (register
+// budget 128 vs 80 per thread); PLX_BWD_MINB=2|3 selects (default 2).
+int bwd_minb() {
+    static int m = 0;
+    if (!m) {
+        const char *e = getenv("PLX_BWD_MINB");
+        m = (e && atoi(e) == 3) ? 3 : 2;
+    }
+    return m;
+}
+
+template <int MODE, bool ABS, bool NEAREST, int MINB>
 int blocks_per_sm() {
     static int nb = 0;
     if (!nb) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, march_kernel<MODE, ABS, NEAREST>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, march_kernel<MODE, ABS, NEAREST, MINB>,
+                                                      kThreads, 0);
         if (nb <= 0) nb = 1;
     }
     return nb;
 }
 
-int bwd_blocks_per_sm(const plx_render_opts *o) {
+template <int MINB>
+int bwd_blocks_per_sm_t(const plx_render_opts *o) {
     if (o->nearest)
-        return o->absolute ? blocks_per_sm<BWD, true, true>() : blocks_per_sm<BWD, false, true>();
-    return o->absolute ? blocks_per_sm<BWD, true, false>() : blocks_per_sm<BWD, false, false>();
+        return o->absolute ? blocks_per_sm<BWD, true, true, MINB>()
+                           : blocks_per_sm<BWD, false, true, MINB>();
+    return o->absolute ? blocks_per_sm<BWD, true, false, MINB>()
+                       : blocks_per_sm<BWD, false, false, MINB>();
+}
+
+int bwd_blocks_per_sm(const plx_render_opts *o) {
+    return bwd_minb() == 3 ? bwd_blocks_per_sm_t<3>(o) : bwd_blocks_per_sm_t<2>(o);
+}
+
+template <int MODE, int MINB>
+void launch_variant(const plx_render_opts *o, bool ABSF, dim3 grid, cudaStream_t s, DGrid G,
+                    RayArgs R, KOpts K, Outs out, Scratch S) {
+    if (o->nearest) {
+        if (ABSF) march_kernel<MODE, true, true, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
+        else march_kernel<MODE, false, true, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
+    } else {
+        if (ABSF) march_kernel<MODE, true, false, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
+        else march_kernel<MODE, false, false, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
+    }
 }
 
 // Capacity of one warp slot: every march position of the longest chord (R:67-69).
@@ -655,13 +688,8 @@ int launch_march(const plx_grid *g, const plx_rays *rays, const plx_render_opts 
     }
     const bool ABSF = MODE != MAXW && o->absolute;
     dim3 grid((unsigned)blocks);
-    if (o->nearest) {
-        if (ABSF) march_kernel<MODE, true, true><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
-        else march_kernel<MODE, false, true><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
-    } else {
-        if (ABSF) march_kernel<MODE, true, false><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
-        else march_kernel<MODE, false, false><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
-    }
+    if (MODE == BWD && bwd_minb() == 2) launch_variant<MODE, 2>(o, ABSF, grid, s, G, R, K, out, S);
+    else launch_variant<MODE, 3>(o, ABSF, grid, s, G, R, K, out, S);
     return cudaPeekAtLastError() == cudaSuccess ? PLX_OK : PLX_ECUDA;
 }
 
