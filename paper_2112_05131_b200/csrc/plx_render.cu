@@ -192,83 +192,117 @@ __device__ __forceinline__ long long pack_cell(int64_t i, int64_t j, int64_t k) 
     return (long long)((i << 42) | (j << 21) | k);
 }
 
-// Register accumulators of the transposed scatter: lane c (< 28) holds
-// column c of the 8 stencil rows of the current cell.  When the ray steps
-// into a face/edge/corner-adjacent cell the shared corners are shifted
-// instead of flushed, so each grid row receives about one coalesced 28-lane
-// reduction per ray visit instead of one per sample x corner.
-template <bool NEAREST>
-struct RowAcc {
-    static constexpr int NQ = NEAREST ? 1 : 8;
-    float acc[NQ];
-    int32_t row[NQ];
-    long long cell;   // packed; -1 = none
+// Per-sample scatter payload staged in shared memory by the lane-parallel
+// phase of pass 2 and consumed in sample order by the accumulator below.
+struct SmemSample {
+    long long key;      // packed stencil cell (or lattice point for nearest)
+    float f[4];         // fx, fy, fz, -
+    float g[4];         // dL/dsigma, dL/dc_R, dL/dc_G, dL/dc_B  (K:384-389)
+    int32_t rows[8];    // stencil rows (K:84-123), -1 = empty
+};
 
-    __device__ __forceinline__ void init() {
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            acc[q] = 0.f;
-            row[q] = -1;
-        }
+// Lane-distributed accumulator of the backward scatter.  The gradient of
+// a stencil row factorises as
+//   d table[r, 0]          = sum_s w_q(s) dL/dsigma(s)
+//   d table[r, 1+9ch+b]    = basis_b * sum_s w_q(s) dL/dc_ch(s)
+// (basis_b is per ray), so a cell needs only 8 corners x 4 scalars = 32
+// accumulators: lane L holds corner q = L/4, component k = L%4.  A sample
+// costs one FMA per lane.  When the ray steps into a face/edge/corner-
+// adjacent cell the shared corners are shifted between lanes (one shuffle)
+// instead of flushed; a flushed corner becomes one coalesced 28-lane
+// reduction on its 112-byte gradient row (lane c = column c).
+template <bool NEAREST>
+struct LaneAcc {
+    float acc;          // this lane's (corner, component) partial sum
+    int32_t row;        // row of this lane's corner, -1 = empty / none
+    long long cell;     // packed current cell, -1 = none
+    int q, k;           // lane's corner and component
+    int kcol;           // source component of column `lane` at flush time
+    float col_basis;    // basis factor of column `lane` (1 for sigma)
+
+    __device__ __forceinline__ void init(int lane, const double *basis) {
+        acc = 0.f;
+        row = -1;
         cell = -1;
+        q = lane >> 2;
+        k = lane & 3;
+        kcol = lane == 0 ? 0 : (lane < PLX_ROW ? 1 + (lane - 1) / 9 : 0);
+        col_basis = lane == 0 ? 1.f : 0.f;
+        if (lane >= 1 && lane < PLX_ROW) {
+            const int b = (lane - 1) % 9;
+#pragma unroll
+            for (int bb = 0; bb < 9; ++bb)
+                if (bb == b) col_basis = (float)basis[bb];
+        }
     }
-    __device__ __forceinline__ void flush(int q, float *grad, uint8_t *tmask, int lane) {
-        const int32_t r = row[q];
+    __device__ __forceinline__ void flush_corner(int qq, float *grad, uint8_t *tmask, int lane) {
+        const int32_t r = __shfl_sync(PLX_FULL_MASK, row, 4 * qq);
+        const float a = __shfl_sync(PLX_FULL_MASK, acc, 4 * qq + kcol);
         if (r >= 0) {
-            if (lane < PLX_ROW) red_add_f32(grad + (int64_t)r * PLX_ROW + lane, acc[q]);
+            if (lane < PLX_ROW) red_add_f32(grad + (int64_t)r * PLX_ROW + lane, a * col_basis);
             if (lane == 0) tmask[r] = 1;
         }
-        acc[q] = 0.f;
     }
     __device__ __forceinline__ void flush_all(float *grad, uint8_t *tmask, int lane) {
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) flush(q, grad, tmask, lane);
+        for (int qq = 0; qq < (NEAREST ? 1 : 8); ++qq) flush_corner(qq, grad, tmask, lane);
+        acc = 0.f;
+        row = -1;
         cell = -1;
     }
-    // Corner bit `bit` of q (4 = x, 2 = y, 1 = z) moves by +-1.
-    __device__ __forceinline__ void shift(int bit, int delta, float *grad, uint8_t *tmask, int lane) {
+    // corner bit `bit` (4 = x, 2 = y, 1 = z) moves by delta = +-1
+    __device__ __forceinline__ void shift(int bit, int delta, float *grad, uint8_t *tmask,
+                                          int lane) {
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            if (q & bit) continue;
-            const int lo = q, hi = q | bit;
-            if (delta > 0) {   // lo corners leave, hi corners become lo
-                flush(lo, grad, tmask, lane);
-                acc[lo] = acc[hi];
-                row[lo] = row[hi];
-                acc[hi] = 0.f;
-                row[hi] = -1;
-            } else {           // hi corners leave, lo corners become hi
-                flush(hi, grad, tmask, lane);
-                acc[hi] = acc[lo];
-                row[hi] = row[lo];
-                acc[lo] = 0.f;
-                row[lo] = -1;
-            }
+        for (int qq = 0; qq < 8; ++qq) {
+            const bool leaving = delta > 0 ? !(qq & bit) : (qq & bit);
+            if (leaving) flush_corner(qq, grad, tmask, lane);
+        }
+        const int off = 4 * bit;
+        if (delta > 0) {   // hi corners become lo, new hi corners start empty
+            const float a = __shfl_down_sync(PLX_FULL_MASK, acc, off);
+            const int32_t r = __shfl_down_sync(PLX_FULL_MASK, row, off);
+            acc = (q & bit) ? 0.f : a;
+            row = (q & bit) ? -1 : r;
+        } else {
+            const float a = __shfl_up_sync(PLX_FULL_MASK, acc, off);
+            const int32_t r = __shfl_up_sync(PLX_FULL_MASK, row, off);
+            acc = (q & bit) ? a : 0.f;
+            row = (q & bit) ? r : -1;
         }
     }
-    __device__ __forceinline__ void move_to(long long nc, const DGrid &G, float *grad,
+    __device__ __forceinline__ void move_to(long long nc, const SmemSample &smp, float *grad,
                                             uint8_t *tmask, int lane) {
-        const int64_t ni = nc >> 42, nj = (nc >> 21) & 0x1fffff, nk = nc & 0x1fffff;
         if (NEAREST) {
-            flush(0, grad, tmask, lane);
+            flush_corner(0, grad, tmask, lane);
+            acc = 0.f;
         } else if (cell >= 0) {
-            const int64_t ci = cell >> 42, cj = (cell >> 21) & 0x1fffff, ck = cell & 0x1fffff;
-            const int64_t di = ni - ci, dj = nj - cj, dk = nk - ck;
+            const long long di = (nc >> 42) - (cell >> 42);
+            const long long dj = ((nc >> 21) & 0x1fffff) - ((cell >> 21) & 0x1fffff);
+            const long long dk = (nc & 0x1fffff) - (cell & 0x1fffff);
             if (di >= -1 && di <= 1 && dj >= -1 && dj <= 1 && dk >= -1 && dk <= 1) {
                 if (di) shift(4, (int)di, grad, tmask, lane);
                 if (dj) shift(2, (int)dj, grad, tmask, lane);
                 if (dk) shift(1, (int)dk, grad, tmask, lane);
             } else {
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) flush(q, grad, tmask, lane);
+                for (int qq = 0; qq < 8; ++qq) flush_corner(qq, grad, tmask, lane);
+                acc = 0.f;
             }
         }
         cell = nc;
-        const int32_t *base = G.links + flat(G, ni, nj, nk);
-        const int64_t sy = G.Dz, sx = (int64_t)G.Dy * G.Dz;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q)
-            row[q] = __ldg(base + ((q >> 2) & 1) * sx + ((q >> 1) & 1) * sy + (q & 1));
+        row = smp.rows[NEAREST ? 0 : q];
+    }
+    __device__ __forceinline__ void add(const SmemSample &smp) {
+        const float gk = smp.g[k];
+        if (NEAREST) {
+            acc += q == 0 ? gk : 0.f;
+        } else {
+            const float wx = (q & 4) ? smp.f[0] : 1.f - smp.f[0];
+            const float wy = (q & 2) ? smp.f[1] : 1.f - smp.f[1];
+            const float wz = (q & 1) ? smp.f[2] : 1.f - smp.f[2];
+            acc += wx * wy * wz * gk;
+        }
     }
 };
 
@@ -279,10 +313,11 @@ __global__ void __launch_bounds__(256, MINB)
     const int warp = threadIdx.x >> 5;
     const int64_t slot = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     const int64_t nslots = (int64_t)gridDim.x * (blockDim.x >> 5);
-    __shared__ double red_mse[8], red_cau[8];
     double mse_part = 0.0, cau_part = 0.0;
     const unsigned lt_mask = (1u << lane) - 1u;
     int64_t ray = slot;
+    __shared__ SmemSample smem_all[MODE == BWD ? 8 : 1][32];
+    SmemSample *sm = smem_all[MODE == BWD ? warp : 0];
 
     for (;;) {
         if (MODE == BWD) {   // dynamic scheduling: rays differ widely in length
@@ -406,17 +441,8 @@ __global__ void __launch_bounds__(256, MINB)
         //   relative: T bg + sum_{j>i} w_j c_j = rgb - P_i      (K:351-353, 381-383)
         //   absolute: -bg [T>0] + sum_{j>i} c_j (bn_j - bi_j)   (K:346-349, 374-376)
         const double bend = T > 0.0 ? 1.0 : 0.0;
-        // lane c's column: 0 = sigma, 1 + 9 ch + b = SH (channel-major, sh.py:3-7)
-        const int col_ch = lane >= 1 ? (lane - 1) / 9 : 0;
-        float col_basis = 0.f;
-        if (lane >= 1 && lane < PLX_ROW) {
-            const int b = (lane - 1) % 9;
-#pragma unroll
-            for (int bb = 0; bb < 9; ++bb)
-                if (bb == b) col_basis = (float)basis[bb];
-        }
-        RowAcc<NEAREST> ra;
-        ra.init();
+        LaneAcc<NEAREST> ra;
+        ra.init(lane, basis);
         double P0 = 0.0, P1 = 0.0, P2 = 0.0;
         double T2 = 1.0, A2 = 0.0;
         bool stopped2 = false;
@@ -475,80 +501,56 @@ __global__ void __launch_bounds__(256, MINB)
                 cau_part += log(1.0 + 2.0 * sig * sig);
                 gsig += out.lam_cauchy * 4.0 * sig / (1.0 + 2.0 * sig * sig);
             }
-            // per-sample scatter payload (K:387-410): dL/dsigma, dL/dc per channel
-            const float gs_f = (float)gsig;
-            const float gc0_f = c0 > 0.0 ? (float)(up0 * wi) : 0.f;
-            const float gc1_f = c1 > 0.0 ? (float)(up1 * wi) : 0.f;
-            const float gc2_f = c2 > 0.0 ? (float)(up2 * wi) : 0.f;
-            // this lane's stencil cell and fractional offsets
-            long long cellkey;
-            float fx, fy, fz;
-            if (NEAREST) {
-                int64_t i = (int64_t)(g[0] + 0.5), j = (int64_t)(g[1] + 0.5), k = (int64_t)(g[2] + 0.5);
-                if (i > G.Dx - 1) i = G.Dx - 1;
-                if (j > G.Dy - 1) j = G.Dy - 1;
-                if (k > G.Dz - 1) k = G.Dz - 1;
-                cellkey = pack_cell(i, j, k);
-                fx = fy = fz = 0.f;
-            } else {
-                int64_t i0 = (int64_t)g[0], j0 = (int64_t)g[1], kk0 = (int64_t)g[2];
-                if (i0 > G.Dx - 2) i0 = G.Dx - 2;
-                if (j0 > G.Dy - 2) j0 = G.Dy - 2;
-                if (kk0 > G.Dz - 2) kk0 = G.Dz - 2;
-                cellkey = pack_cell(i0, j0, kk0);
-                fx = (float)(g[0] - (double)i0);
-                fy = (float)(g[1] - (double)j0);
-                fz = (float)(g[2] - (double)kk0);
+            // per-sample scatter payload (K:387-410), staged for the in-order accumulator
+            if (incl) {
+                SmemSample &me = sm[lane];
+                me.g[0] = (float)gsig;
+                me.g[1] = c0 > 0.0 ? (float)(up0 * wi) : 0.f;
+                me.g[2] = c1 > 0.0 ? (float)(up1 * wi) : 0.f;
+                me.g[3] = c2 > 0.0 ? (float)(up2 * wi) : 0.f;
+                if (NEAREST) {
+                    int64_t i = (int64_t)(g[0] + 0.5), j = (int64_t)(g[1] + 0.5), k = (int64_t)(g[2] + 0.5);
+                    if (i > G.Dx - 1) i = G.Dx - 1;
+                    if (j > G.Dy - 1) j = G.Dy - 1;
+                    if (k > G.Dz - 1) k = G.Dz - 1;
+                    me.key = pack_cell(i, j, k);
+                    me.rows[0] = __ldg(G.links + flat(G, i, j, k));
+                } else {
+                    int64_t i0 = (int64_t)g[0], j0 = (int64_t)g[1], kk0 = (int64_t)g[2];
+                    if (i0 > G.Dx - 2) i0 = G.Dx - 2;
+                    if (j0 > G.Dy - 2) j0 = G.Dy - 2;
+                    if (kk0 > G.Dz - 2) kk0 = G.Dz - 2;
+                    me.key = pack_cell(i0, j0, kk0);
+                    me.f[0] = (float)(g[0] - (double)i0);
+                    me.f[1] = (float)(g[1] - (double)j0);
+                    me.f[2] = (float)(g[2] - (double)kk0);
+                    const int32_t *base = G.links + flat(G, i0, j0, kk0);
+                    const int64_t sy = G.Dz, sx = (int64_t)G.Dy * G.Dz;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        me.rows[q] = __ldg(base + ((q >> 2) & 1) * sx + ((q >> 1) & 1) * sy + (q & 1));
+                }
             }
+            __syncwarp();
             unsigned m = mask;   // already truncated at the early stop in pass 1
             while (m) {
                 const int j = __ffs(m) - 1;
                 m &= m - 1;
-                const long long cj = __shfl_sync(PLX_FULL_MASK, cellkey, j);
-                const float gsj = __shfl_sync(PLX_FULL_MASK, gs_f, j);
-                const float g0j = __shfl_sync(PLX_FULL_MASK, gc0_f, j);
-                const float g1j = __shfl_sync(PLX_FULL_MASK, gc1_f, j);
-                const float g2j = __shfl_sync(PLX_FULL_MASK, gc2_f, j);
-                if (cj != ra.cell) ra.move_to(cj, G, out.grad, out.tmask, lane);
-                const float gcol = lane == 0 ? gsj : (col_ch == 0 ? g0j : (col_ch == 1 ? g1j : g2j)) * col_basis;
-                if (NEAREST) {
-                    ra.acc[0] += gcol;
-                } else {
-                    const float fxj = __shfl_sync(PLX_FULL_MASK, fx, j);
-                    const float fyj = __shfl_sync(PLX_FULL_MASK, fy, j);
-                    const float fzj = __shfl_sync(PLX_FULL_MASK, fz, j);
-                    const float x0 = (1.f - fxj) * gcol, x1 = fxj * gcol;
-                    const float y0 = 1.f - fyj, y1 = fyj, z0 = 1.f - fzj, z1 = fzj;
-                    ra.acc[0] += x0 * y0 * z0;
-                    ra.acc[1] += x0 * y0 * z1;
-                    ra.acc[2] += x0 * y1 * z0;
-                    ra.acc[3] += x0 * y1 * z1;
-                    ra.acc[4] += x1 * y0 * z0;
-                    ra.acc[5] += x1 * y0 * z1;
-                    ra.acc[6] += x1 * y1 * z0;
-                    ra.acc[7] += x1 * y1 * z1;
-                }
+                const SmemSample &smp = sm[j];
+                const long long key = smp.key;
+                if (key != ra.cell) ra.move_to(key, smp, out.grad, out.tmask, lane);
+                ra.add(smp);
             }
+            __syncwarp();
         }
         ra.flush_all(out.grad, out.tmask, lane);
         ray += nslots;
     }
-    if (MODE == BWD) {
+    if (MODE == BWD) {   // one pair of f64 atomics per warp (no block barrier)
         cau_part = warp_sum(cau_part);
-        mse_part = warp_sum(mse_part);   // only lane 0 contributed
         if (lane == 0) {
-            red_mse[warp] = mse_part;
-            red_cau[warp] = cau_part;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double a = 0.0, b = 0.0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-                a += red_mse[w];
-                b += red_cau[w];
-            }
-            if (a != 0.0) atomicAdd(out.sums + 0, a);
-            if (b != 0.0) atomicAdd(out.sums + 1, b);
+            if (mse_part != 0.0) atomicAdd(out.sums + 0, mse_part);
+            if (cau_part != 0.0) atomicAdd(out.sums + 1, cau_part);
         }
     }
 }
