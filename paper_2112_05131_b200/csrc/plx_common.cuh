@@ -132,9 +132,11 @@ __device__ __forceinline__ void sample_coords(const RayMarch &rm, const DGrid &G
     for (int a = 0; a < 3; ++a) g[a] = clamp_coord(rm.o[a] + t * rm.d[a], G.lo[a], G.scale[a], G.dmax[a]);
 }
 
-// Stencil (K:84-123): rows[8] (-1 = empty) and weights; returns 1 or 8.
+// Stencil (K:84-123): rows[8] (-1 = empty) and the fractional offsets f[3];
+// the corner weight is stencil_w(f, q) (recomputed instead of stored, to save
+// registers; same float64 products as K:115-121).  Returns 1 or 8.
 template <bool NEAREST>
-__device__ __forceinline__ int stencil(const DGrid &G, const double *g, int32_t *rows, double *ws,
+__device__ __forceinline__ int stencil(const DGrid &G, const double *g, int32_t *rows, double *f,
                                        bool &any_occ) {
     if (NEAREST) {
         int64_t i = (int64_t)(g[0] + 0.5), j = (int64_t)(g[1] + 0.5), k = (int64_t)(g[2] + 0.5);
@@ -142,7 +144,6 @@ __device__ __forceinline__ int stencil(const DGrid &G, const double *g, int32_t 
         if (j > G.Dy - 1) j = G.Dy - 1;
         if (k > G.Dz - 1) k = G.Dz - 1;
         rows[0] = __ldg(G.links + flat(G, i, j, k));
-        ws[0] = 1.0;
         any_occ = rows[0] >= 0;
         return 1;
     }
@@ -157,30 +158,30 @@ __device__ __forceinline__ int stencil(const DGrid &G, const double *g, int32_t 
             return 8;
         }
     }
-    double fx = g[0] - (double)i0, fy = g[1] - (double)j0, fz = g[2] - (double)k0;
+    f[0] = g[0] - (double)i0;
+    f[1] = g[1] - (double)j0;
+    f[2] = g[2] - (double)k0;
     const int32_t *base = G.links + flat(G, i0, j0, k0);
     const int64_t sy = G.Dz, sx = (int64_t)G.Dy * G.Dz;
     bool occ = false;
-    int n = 0;
 #pragma unroll
-    for (int di = 0; di < 2; ++di) {
-        double wx = di == 1 ? fx : 1.0 - fx;
-#pragma unroll
-        for (int dj = 0; dj < 2; ++dj) {
-            double wy = dj == 1 ? fy : 1.0 - fy;
-#pragma unroll
-            for (int dk = 0; dk < 2; ++dk) {
-                double wz = dk == 1 ? fz : 1.0 - fz;
-                int32_t r = __ldg(base + di * sx + dj * sy + dk);
-                rows[n] = r;
-                ws[n] = wx * wy * wz;
-                occ |= r >= 0;
-                ++n;
-            }
-        }
+    for (int q = 0; q < 8; ++q) {
+        const int32_t r = __ldg(base + ((q >> 2) & 1) * sx + ((q >> 1) & 1) * sy + (q & 1));
+        rows[q] = r;
+        occ |= r >= 0;
     }
     any_occ = occ;
     return 8;
+}
+
+// Trilinear corner weight (K:114-121): corner q = (di, dj, dk) = bits (4, 2, 1).
+template <bool NEAREST>
+__device__ __forceinline__ double stencil_w(const double *f, int q) {
+    if (NEAREST) return 1.0;
+    const double wx = (q & 4) ? f[0] : 1.0 - f[0];
+    const double wy = (q & 2) ? f[1] : 1.0 - f[1];
+    const double wz = (q & 1) ? f[2] : 1.0 - f[2];
+    return wx * wy * wz;
 }
 
 // ---- warp collectives (f64) ----------------------------------------------

@@ -53,7 +53,7 @@ struct Outs {
 // One march position evaluated by one lane.
 struct Sample {
     int32_t rows[8];
-    double ws[8];
+    double f[3];   // fractional lattice offsets; weights via stencil_w
     double sig, att, dlt;
     double c[3];   // pre-clamp colour (K:305)
     bool incl;
@@ -70,14 +70,14 @@ __device__ __forceinline__ void eval_sample(const DGrid &G, const RayMarch &rm, 
     sample_coords(rm, G, step, si, t, s.dlt, g);
     bool occ;
     constexpr int NQ = NEAREST ? 1 : 8;
-    stencil<NEAREST>(G, g, s.rows, s.ws, occ);
+    stencil<NEAREST>(G, g, s.rows, s.f, occ);
     if (!occ) return;
     // _sigma_at (K:126-135): float64 sum over occupied corners in order.
     double sig = 0.0;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         int32_t r = s.rows[q];
-        if (r >= 0) sig += s.ws[q] * (double)__ldg(G.table + (int64_t)r * PLX_ROW);
+        if (r >= 0) sig += stencil_w<NEAREST>(s.f, q) * (double)__ldg(G.table + (int64_t)r * PLX_ROW);
     }
     s.sig = sig;
     if (MODE == BWD ? !(sig >= 0.0) : !(sig > 0.0)) return;
@@ -122,7 +122,7 @@ __device__ __forceinline__ void eval_sample(const DGrid &G, const RayMarch &rm, 
         a2 += basis[6] * (double)v6.y;
         a2 += basis[7] * (double)v6.z;
         a2 += basis[8] * (double)v6.w;
-        double w = s.ws[q];
+        const double w = stencil_w<NEAREST>(s.f, q);
         c0 += w * a0;
         c1 += w * a1;
         c2 += w * a2;
