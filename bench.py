@@ -252,7 +252,7 @@ def run_ours(args):
         tr.step(s)
     torch.cuda.synchronize()
     # the e2e leg replays from this same training state (fair comparison)
-    snap_table, snap_v = tr.grid.table.clone(), tr.state.v.clone()
+    snap_den, snap_sh, snap_v = tr.grid.density.clone(), tr.grid.sh.clone(), tr.state.v.clone()
 
     # -- timed region: K device-resident steps -------------------------------
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -282,6 +282,7 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     t_ev0, t_ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st0 = tr.march_stats.clone()
     t_ev0.record(stream)
     for k in range(args.steps):
         tr.step(args.warmup + k)
@@ -291,6 +292,7 @@ def run_ours(args):
     barrier()
     clk = clocks.stop()
     render.fused_mse_backward_pool, losses.tv_loss, optim.step = orig_fused, orig_tv, orig_opt
+    march = ((tr.march_stats - st0).double() / args.steps).cpu().numpy()
     ms = t_ev0.elapsed_time(t_ev1) / args.steps
     for name, e0, e1 in kernel_events:
         per_kernel[name].append(e0.elapsed_time(e1))
@@ -346,9 +348,10 @@ def run_ours(args):
 
     for i in range(W2):
         e2e_step(args.warmup - W2 + i, host[i])
-    tr.grid.table.copy_(snap_table)     # replay from the value leg's starting state
+    tr.grid.density.copy_(snap_den)     # replay from the value leg's starting state
+    tr.grid.sh.copy_(snap_sh)
     tr.state.v.copy_(snap_v)
-    del snap_table, snap_v
+    del snap_den, snap_sh, snap_v
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -399,8 +402,11 @@ def run_ours(args):
             "config": {"workload": WORKLOAD, "grid": f"{args.dims}^3 dense init",
                        "rays_per_gpu": args.batch, "global_batch": args.batch * world_size,
                        "views": args.views, "res": args.res, "parallelism": f"dp{world_size}",
-                       "l2": "inputs_larger_than_l2 (table+grad+v = %.2f GB)" % (3 * R * 112 / 1e9),
+                       "l2": "inputs_larger_than_l2 (sh+density+grad+v = %.2f GB)" % (R * (3 * 112 + 4) / 1e9),
                        "touched_rows_U": U, "touched_rows_render": U_render, "tv_cells": n_tv,
+                       "march_positions_per_step": float(march[0]),
+                       "samples_per_step": float(march[1]),
+                       "chunks_per_step": float(march[2]),
                        "step_bytes_model": step_bytes,
                        "step_hbm_frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
                        "kernel_ms": avg},
@@ -411,7 +417,8 @@ def run_ours(args):
                          "traffic": traffic, "algorithmic_bytes": alg[dom]},
             "cpu_baseline": cpu,
             "clocks": clk,
-            "gpu_launches": 3 * args.steps,
+            # per step: fused render+backward, TV, touched-set compaction, update
+            "gpu_launches": 4 * args.steps,
         }
         print(json.dumps(line), flush=True)
     if world_size > 1:

@@ -13,9 +13,12 @@
  *     `stream` (a cudaStream_t, NULL = legacy default stream) and is
  *     asynchronous -- nothing here synchronises the host.
  *
- * Storage differs from the reference only in precision: the data table, the
- * gradient buffer and the RMSProp state are float32 (rows x 28, 112 B / row,
- * column 0 = sigma, 1..27 = SH channel-major), all arithmetic is float64.
+ * Storage differs from the reference in precision and layout: the grid's
+ * data are float32 in two arrays, `density` [rows] (sigma) and `table`
+ * [rows x 28] (SH channel-major in columns 1..27, column 0 padding), so the
+ * sigma gathers of the march touch a compact 4 B/row array instead of 112-
+ * byte rows; the gradient buffer and RMSProp state are float32 (rows x 28,
+ * column 0 = sigma).  Arithmetic is float64 except the colour dot products.
  * Rays are float64 (N x 3).  The touched-row set of GradientBuffer (G:25-68:
  * touched_mask + insertion-ordered touched_ids + count) is kept as the byte
  * mask alone; the count is produced by plx_opt_step / plx_count_touched.
@@ -42,7 +45,10 @@ enum {
  * (K:174-177, K:242-248, K:415-416, K:457-459) and SparseGrid (G:71-92). */
 typedef struct {
     const int32_t *links;  /* [Dx*Dy*Dz] C-order (z fastest), -1 = empty     */
-    float *table;          /* [rows*28]                                      */
+    float *table;          /* [rows*28] SH rows: columns 1..27 = the
+                              reference table's SH columns; column 0 is
+                              padding (16-byte rows), never read          */
+    float *density;        /* [rows] sigma = the reference table column 0  */
     int64_t dims[3];       /* Dx, Dy, Dz (each >= 2)                         */
     int64_t rows;
     double lo[3], hi[3];   /* aabb_min / aabb_max                            */
@@ -53,10 +59,15 @@ typedef struct {
                                  (plx_build_cell_occ); NULL = test the links */
 } plx_grid;
 
-/* GradientBuffer (G:25-68): data + touched mask. */
+/* GradientBuffer (G:25-68): data + touched mask, and optionally the
+ * touched-id list + count (touched_ids / _count).  When tids/tcnt are set,
+ * plx_opt_step compacts the mask into them and updates the list (two-phase);
+ * when both are NULL it sweeps the mask in place. */
 typedef struct {
     float *grad;           /* [rows*28] */
     uint8_t *tmask;        /* [rows]    */
+    int32_t *tids;         /* [rows] scratch, or NULL (order unspecified)  */
+    int64_t *tcnt;         /* [1] length of tids after plx_opt_step, or NULL */
 } plx_grad;
 
 /* RenderOptions (R:27-42) resolved to kernel scalars (R:63-64, R:132-139). */
@@ -66,6 +77,10 @@ typedef struct {
     double bg[3];
     int32_t nearest;       /* interp == "nearest"                            */
     int32_t absolute;      /* formula == "absolute"                          */
+    int64_t *stats;        /* optional device int64[4], ACCUMULATED by the
+                              march kernels: {march positions evaluated (up
+                              to the early stop), samples composited, 32-
+                              position chunks, rays}; NULL = off          */
 } plx_render_opts;
 
 /* A ray batch.  If idx != NULL ray r of the batch is pool row idx[r] of
@@ -142,11 +157,12 @@ int plx_prune_mark(const plx_grid *g, const double *weights, double threshold,
                    uint8_t *deemed_scratch /* 2 * ncell bytes */, uint8_t *flags,
                    void *stream);
 int plx_prune_apply(const plx_grid *g, const int32_t *new_links, int64_t *kept_old,
-                    float *new_table, void *stream);
+                    float *new_table, float *new_density, void *stream);
 int plx_upsample_mark(const plx_grid *g, const int64_t new_dims[3], uint8_t *flags,
                       void *stream);
 int plx_upsample_apply(const plx_grid *g, const int64_t new_dims[3],
-                       const int32_t *new_links, float *new_table, void *stream);
+                       const int32_t *new_links, float *new_table, float *new_density,
+                       void *stream);
 int64_t plx_scan_scratch_bytes(int64_t n);
 int plx_scan_ids(const uint8_t *flags, int64_t n, int32_t *ids, int64_t *count,
                  void *scratch, void *stream);

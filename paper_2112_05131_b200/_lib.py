@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libplx.so")
+# PLX_LIB: development override (A/B of kernel variants built elsewhere in-tree)
+LIB_PATH = os.environ.get("PLX_LIB") or os.path.join(_HERE, "libplx.so")
 
 PLX_OK, PLX_EINVAL, PLX_ECUDA = 0, 1, 2
 ROW = 28
@@ -26,20 +27,21 @@ class PlxError(RuntimeError):
 
 class PlxGrid(ctypes.Structure):
     _fields_ = [("links", ctypes.c_void_p), ("table", ctypes.c_void_p),
-                ("dims", ctypes.c_int64 * 3), ("rows", ctypes.c_int64),
+                ("density", ctypes.c_void_p), ("dims", ctypes.c_int64 * 3), ("rows", ctypes.c_int64),
                 ("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3),
                 ("scale", ctypes.c_double * 3), ("dmax", ctypes.c_double * 3),
                 ("cell_occ", ctypes.c_void_p)]
 
 
 class PlxGrad(ctypes.Structure):
-    _fields_ = [("grad", ctypes.c_void_p), ("tmask", ctypes.c_void_p)]
+    _fields_ = [("grad", ctypes.c_void_p), ("tmask", ctypes.c_void_p),
+                ("tids", ctypes.c_void_p), ("tcnt", ctypes.c_void_p)]
 
 
 class PlxRenderOpts(ctypes.Structure):
     _fields_ = [("step", ctypes.c_double), ("stop_thresh", ctypes.c_double),
                 ("bg", ctypes.c_double * 3), ("nearest", ctypes.c_int32),
-                ("absolute", ctypes.c_int32)]
+                ("absolute", ctypes.c_int32), ("stats", ctypes.c_void_p)]
 
 
 class PlxRays(ctypes.Structure):
@@ -71,9 +73,9 @@ _SIGS = {
     "plx_clear_grad": [ctypes.POINTER(PlxGrad), _I64, _P, _P],
     "plx_count_touched": [_P, _I64, _P, _P],
     "plx_prune_mark": [ctypes.POINTER(PlxGrid), _P, _D, _P, _P, _P],
-    "plx_prune_apply": [ctypes.POINTER(PlxGrid), _P, _P, _P, _P],
+    "plx_prune_apply": [ctypes.POINTER(PlxGrid), _P, _P, _P, _P, _P],
     "plx_upsample_mark": [ctypes.POINTER(PlxGrid), ctypes.POINTER(_I64), _P, _P],
-    "plx_upsample_apply": [ctypes.POINTER(PlxGrid), ctypes.POINTER(_I64), _P, _P, _P],
+    "plx_upsample_apply": [ctypes.POINTER(PlxGrid), ctypes.POINTER(_I64), _P, _P, _P, _P],
     "plx_scan_scratch_bytes": [_I64],
     "plx_scan_ids": [_P, _I64, _P, _P, _P, _P],
     "plx_cell_occ_words": [ctypes.POINTER(_I64)],

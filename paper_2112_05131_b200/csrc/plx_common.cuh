@@ -20,7 +20,8 @@ namespace plx {
 // Kernel-side copy of plx_grid (passed by value).
 struct DGrid {
     const int32_t *__restrict__ links;
-    const float *__restrict__ table;
+    const float *__restrict__ table;     // SH rows (column 0 unused)
+    const float *__restrict__ density;   // sigma per row
     const uint32_t *__restrict__ cell_occ;
     int32_t Dx, Dy, Dz;
     double lo[3], hi[3], scale[3], dmax[3];
@@ -30,6 +31,7 @@ inline DGrid make_dgrid(const plx_grid &g) {
     DGrid d;
     d.links = g.links;
     d.table = g.table;
+    d.density = g.density;
     d.cell_occ = g.cell_occ;
     d.Dx = (int32_t)g.dims[0];
     d.Dy = (int32_t)g.dims[1];

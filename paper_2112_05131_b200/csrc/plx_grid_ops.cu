@@ -46,10 +46,10 @@ __global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
         const double e2 = a.eps * a.eps;
         const float *T = G.table;
         // opacity term (K:505-532): missing neighbours read as 0
-        const double s0 = r0 >= 0 ? (double)__ldg(T + (int64_t)r0 * PLX_ROW) : 0.0;
-        const double sx = rx >= 0 ? (double)__ldg(T + (int64_t)rx * PLX_ROW) : 0.0;
-        const double sy = ry >= 0 ? (double)__ldg(T + (int64_t)ry * PLX_ROW) : 0.0;
-        const double sz = rz >= 0 ? (double)__ldg(T + (int64_t)rz * PLX_ROW) : 0.0;
+        const double s0 = r0 >= 0 ? (double)__ldg(G.density + r0) : 0.0;
+        const double sx = rx >= 0 ? (double)__ldg(G.density + rx) : 0.0;
+        const double sy = ry >= 0 ? (double)__ldg(G.density + ry) : 0.0;
+        const double sz = rz >= 0 ? (double)__ldg(G.density + rz) : 0.0;
         const double dxv = (sx - s0) * a.fac[0], dyv = (sy - s0) * a.fac[1], dzv = (sz - s0) * a.fac[2];
         const double val = sqrt(dxv * dxv + dyv * dyv + dzv * dzv + e2);
         sig_sum = val;
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
 // fully coalesced 448-byte runs of table / grad / v).  Untouched rows cost
 // one mask byte; touched rows cost exactly their compulsory 672 B.
 struct OptArgs {
-    float *table, *v, *grad;
+    float *table, *density, *v, *grad;
     uint8_t *tmask;
     int64_t rows;
     double lr_sigma, lr_sh, beta, eps;
@@ -153,6 +153,31 @@ __device__ __forceinline__ int nonzero_bytes(uint32_t m) {
     m = (m | (m >> 2)) & 0x03030303u;
     m = (m | (m >> 1)) & 0x01010101u;
     return __popc(m);
+}
+
+// lr*g / (sqrt(nv) + eps) in float64 without the IEEE div/sqrt subroutines
+// (they were ~60 % of this kernel's instructions): MUFU reciprocal-sqrt and
+// reciprocal seeds, Newton steps with explicit FMAs, and one residual
+// correction each, so both the root and the quotient are within ~1 ulp of
+// float64.  The result is rounded to the f32 table afterwards, where it
+// equals the correctly rounded float64 path except at f32 rounding ties
+// (~2^-29 of values).  nv > 0 and sqrt(nv) + eps >= 1e-8 here (g != 0).
+__device__ __forceinline__ double rms_quot(double num, double nv, double eps) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(nv));
+    const double hn = 0.5 * nv;
+    y = y * fma(-hn * y, y, 1.5);
+    y = y * fma(-hn * y, y, 1.5);
+    double s = nv * y;
+    s = fma(0.5 * y, fma(-s, s, nv), s);   // sqrt(nv), corrected
+    const double den = s + eps;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+    r = r * fma(-den, r, 2.0);
+    r = r * fma(-den, r, 2.0);
+    double q = num * r;
+    q = fma(r, fma(-den, q, num), q);      // num / den, corrected
+    return q;
 }
 
 // The update of one float4 of one row (K:578-590), float64 arithmetic.
@@ -169,7 +194,7 @@ __device__ __forceinline__ void opt_apply(const OptArgs &a, int quad, float4 &g4
         if (a.rmsprop) {
             const double nv = a.beta * (double)v[e] + (1.0 - a.beta) * gd * gd;
             v[e] = (float)nv;
-            t[e] = (float)((double)t[e] - lr * gd / (sqrt(nv) + a.eps));
+            t[e] = (float)((double)t[e] - rms_quot(lr * gd, nv, a.eps));
         } else {
             t[e] = (float)((double)t[e] - lr * gd);
         }
@@ -223,6 +248,7 @@ __global__ void __launch_bounds__(NT) opt_kernel(OptArgs a) {
         constexpr int U = 2;   // 2 groups x 4 rows: 6 float4 loads in flight per lane
         for (int gidx = 0; gidx < total; gidx += 4 * U) {
             float4 g4[U], t4[U], v4[U];
+            float den[U];
             int64_t rw[U];
             bool act[U];
 #pragma unroll
@@ -234,6 +260,7 @@ __global__ void __launch_bounds__(NT) opt_kernel(OptArgs a) {
                     g4[u] = reinterpret_cast<const float4 *>(a.grad + rw[u] * PLX_ROW)[quad];
                     if (a.update) {
                         t4[u] = reinterpret_cast<const float4 *>(a.table + rw[u] * PLX_ROW)[quad];
+                        if (quad == 0) den[u] = a.density[rw[u]];
                         if (a.rmsprop)
                             v4[u] = reinterpret_cast<const float4 *>(a.v + rw[u] * PLX_ROW)[quad];
                     }
@@ -243,7 +270,12 @@ __global__ void __launch_bounds__(NT) opt_kernel(OptArgs a) {
             for (int u = 0; u < U; ++u) {
                 if (!act[u]) continue;
                 if (a.update) {
+                    if (quad == 0) t4[u].x = den[u];
                     opt_apply(a, quad, g4[u], t4[u], v4[u]);
+                    if (quad == 0) {
+                        a.density[rw[u]] = t4[u].x;
+                        t4[u].x = 0.f;
+                    }
                     reinterpret_cast<float4 *>(a.table + rw[u] * PLX_ROW)[quad] = t4[u];
                     if (a.rmsprop) reinterpret_cast<float4 *>(a.v + rw[u] * PLX_ROW)[quad] = v4[u];
                 }
@@ -263,6 +295,125 @@ __global__ void __launch_bounds__(NT) opt_kernel(OptArgs a) {
         __syncwarp();
     }
     if (a.count && lane == 0 && cnt) atomicAdd(a.count, cnt);
+}
+
+// Two-phase variant used when the caller provides the touched-id list of
+// GradientBuffer (G:25-68 touched_ids / _count, plx_grad.tids / tcnt):
+//   phase 1 (touched_compact_kernel): the mask -> a compact list of touched
+//            row ids (one atomic per warp per 2048-row range; order within
+//            the list does not matter, every row is updated independently)
+//            and the mask clear;
+//   phase 2 (opt_rows_kernel): grid-stride over the list, 4 rows x 7 float4
+//            per warp group, kOptU groups in flight per lane, so every lane
+//            keeps 3*kOptU independent 16-byte loads outstanding -- the sweep
+//            above serialises mask scan -> loads -> update per segment.
+constexpr int kCompactSegs = 16;   // 128-row segments per warp range
+constexpr int kOptU = 4;
+
+__global__ void __launch_bounds__(256) touched_compact_kernel(uint8_t *tmask, int64_t rows,
+                                                              int32_t *tids, int64_t *tcnt,
+                                                              int clear) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nseg = (rows + 127) >> 7;
+    const int64_t nrange = (nseg + kCompactSegs - 1) / kCompactSegs;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t rg = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); rg < nrange;
+         rg += nw) {
+        const int64_t s0 = rg * kCompactSegs;
+        const int64_t s1 = min(nseg, s0 + kCompactSegs);
+        uint32_t m[kCompactSegs];
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < kCompactSegs; ++i) {
+            m[i] = 0u;
+            const int64_t r0 = (s0 + i) * 128 + lane * 4;
+            if (s0 + i < s1) {
+                if (r0 + 3 < rows) {
+                    m[i] = *reinterpret_cast<const uint32_t *>(tmask + r0);
+                } else {
+                    for (int e = 0; e < 4; ++e)
+                        if (r0 + e < rows && tmask[r0 + e]) m[i] |= 0xffu << (8 * e);
+                }
+            }
+            c += nonzero_bytes(m[i]);
+        }
+        int incl = c;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(PLX_FULL_MASK, incl, off);
+            if (lane >= off) incl += y;
+        }
+        const int total = __shfl_sync(PLX_FULL_MASK, incl, 31);
+        if (total == 0) continue;
+        unsigned long long base = 0;
+        if (lane == 31) base = atomicAdd(reinterpret_cast<unsigned long long *>(tcnt),
+                                         (unsigned long long)total);
+        base = __shfl_sync(PLX_FULL_MASK, base, 31);
+        int64_t pos = (int64_t)base + incl - c;
+#pragma unroll
+        for (int i = 0; i < kCompactSegs; ++i) {
+            if (!m[i]) continue;
+            const int64_t r0 = (s0 + i) * 128 + lane * 4;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if ((m[i] >> (8 * e)) & 0xffu) tids[pos++] = (int32_t)(r0 + e);
+            if (clear) {
+                if (r0 + 3 < rows) {
+                    *reinterpret_cast<uint32_t *>(tmask + r0) = 0u;
+                } else {
+                    for (int e = 0; e < 4; ++e)
+                        if (r0 + e < rows) tmask[r0 + e] = 0;
+                }
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256, 3) opt_rows_kernel(OptArgs a, const int32_t *tids,
+                                                       const int64_t *tcnt) {
+    const int lane = threadIdx.x & 31;
+    const int quad = lane % 7, sub = lane / 7;
+    const int64_t n = *tcnt;
+    const int64_t ngroups = (n + 3) >> 2;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (a.count && w == 0 && lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(a.count),
+                                                  (unsigned long long)n);
+    for (int64_t g0 = w; g0 < ngroups; g0 += nw * kOptU) {
+        float4 g4[kOptU], t4[kOptU], v4[kOptU];
+        float den[kOptU];
+        int64_t rw[kOptU];
+        bool act[kOptU];
+#pragma unroll
+        for (int u = 0; u < kOptU; ++u) {
+            const int64_t j = (g0 + u * nw) * 4 + sub;
+            act[u] = lane < 28 && g0 + u * nw < ngroups && j < n;
+            rw[u] = act[u] ? (int64_t)__ldg(tids + j) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kOptU; ++u) {
+            if (!act[u]) continue;
+            g4[u] = reinterpret_cast<const float4 *>(a.grad + rw[u] * PLX_ROW)[quad];
+            t4[u] = reinterpret_cast<const float4 *>(a.table + rw[u] * PLX_ROW)[quad];
+            if (quad == 0) den[u] = a.density[rw[u]];   // merged after all loads are issued
+            if (a.rmsprop) v4[u] = reinterpret_cast<const float4 *>(a.v + rw[u] * PLX_ROW)[quad];
+        }
+#pragma unroll
+        for (int u = 0; u < kOptU; ++u) {
+            if (!act[u]) continue;
+            if (quad == 0) t4[u].x = den[u];
+            opt_apply(a, quad, g4[u], t4[u], v4[u]);
+            if (quad == 0) {   // sigma lives in the density array (column 0 unused)
+                a.density[rw[u]] = t4[u].x;
+                t4[u].x = 0.f;
+            }
+            reinterpret_cast<float4 *>(a.table + rw[u] * PLX_ROW)[quad] = t4[u];
+            if (a.rmsprop) reinterpret_cast<float4 *>(a.v + rw[u] * PLX_ROW)[quad] = v4[u];
+            if (a.clear)
+                reinterpret_cast<float4 *>(a.grad + rw[u] * PLX_ROW)[quad] =
+                    make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
 }
 
 static int g_num_sms = 0;
@@ -321,7 +472,7 @@ __global__ void prune_deem_kernel(DGrid G, const double *weights, double thr, ui
     const int32_t r = G.links[c];
     uint8_t d = 0;
     if (r >= 0) {
-        const double v = weights ? weights[r] : (double)G.table[(int64_t)r * PLX_ROW];
+        const double v = weights ? weights[r] : (double)G.density[r];
         d = v >= thr;
     }
     deemed[c] = d;
@@ -341,7 +492,7 @@ __global__ void dilate_axis_kernel(const uint8_t *in, uint8_t *out, int64_t ncel
 }
 
 __global__ void prune_apply_kernel(DGrid G, const int32_t *new_links, int64_t ncell,
-                                   int64_t *kept_old, float *new_table) {
+                                   int64_t *kept_old, float *new_table, float *new_density) {
     // one warp-quarter (8 lanes) per cell: 7 lanes copy the row as float4
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t c = t >> 3;
@@ -352,6 +503,7 @@ __global__ void prune_apply_kernel(DGrid G, const int32_t *new_links, int64_t nc
     const int32_t old = G.links[c];
     if (part == 7) {
         if (kept_old) kept_old[id] = old;
+        new_density[id] = G.density[old];
         return;
     }
     reinterpret_cast<float4 *>(new_table + (int64_t)id * PLX_ROW)[part] =
@@ -414,8 +566,9 @@ __global__ void upsample_mark_kernel(DGrid G, UpArgs u, uint8_t *flags, int64_t 
 }
 
 __global__ void upsample_apply_kernel(DGrid G, UpArgs u, const int32_t *new_links, int64_t ncell,
-                                      float *new_table) {
-    // 7 lanes per new cell, each producing one float4 of the row
+                                      float *new_table, float *new_density) {
+    // 7 lanes per new cell, each producing one float4 of the row (part 0
+    // carries sigma from the density array in its first component)
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t c = t >> 3;
     const int part = t & 7;
@@ -429,11 +582,16 @@ __global__ void upsample_apply_kernel(DGrid G, UpArgs u, const int32_t *new_link
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         if (rows[q] < 0) continue;   // empty corners read 0, no renormalisation
-        const float4 v = __ldg(reinterpret_cast<const float4 *>(G.table + (int64_t)rows[q] * PLX_ROW) + part);
+        float4 v = __ldg(reinterpret_cast<const float4 *>(G.table + (int64_t)rows[q] * PLX_ROW) + part);
+        if (part == 0) v.x = __ldg(G.density + rows[q]);
         acc[0] += ws[q] * (double)v.x;
         acc[1] += ws[q] * (double)v.y;
         acc[2] += ws[q] * (double)v.z;
         acc[3] += ws[q] * (double)v.w;
+    }
+    if (part == 0) {
+        new_density[id] = (float)acc[0];
+        acc[0] = 0.0;
     }
     reinterpret_cast<float4 *>(new_table + (int64_t)id * PLX_ROW)[part] =
         make_float4((float)acc[0], (float)acc[1], (float)acc[2], (float)acc[3]);
@@ -537,7 +695,8 @@ using namespace plx;
 namespace {
 bool grid_ok(const plx_grid *g) {
     return g && g->links && g->dims[0] >= 2 && g->dims[1] >= 2 && g->dims[2] >= 2 &&
-           (g->rows == 0 || g->table) && g->dims[0] * g->dims[1] * g->dims[2] < (int64_t)1 << 31;
+           (g->rows == 0 || (g->table && g->density)) &&
+           g->dims[0] * g->dims[1] * g->dims[2] < (int64_t)1 << 31;
 }
 int status() { return cudaPeekAtLastError() == cudaSuccess ? PLX_OK : PLX_ECUDA; }
 unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -577,23 +736,41 @@ extern "C" int plx_tv(const plx_grid *g, const int64_t *cells, int64_t start, in
 extern "C" int plx_opt_step(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, double lr_sh,
                             double beta, double eps, int32_t rmsprop, int32_t clear,
                             int64_t *out_count, void *stream) {
-    if (!g || !gb || !gb->grad || !gb->tmask || (rmsprop && !v) || (g->rows > 0 && !g->table))
+    if (!g || !gb || !gb->grad || !gb->tmask || (rmsprop && !v) ||
+        (g->rows > 0 && (!g->table || !g->density)))
         return PLX_EINVAL;
+    if ((gb->tids == nullptr) != (gb->tcnt == nullptr)) return PLX_EINVAL;
     if (g->rows == 0) return PLX_OK;
-    OptArgs a{g->table, v, gb->grad, gb->tmask, g->rows, lr_sigma, lr_sh, beta, eps, rmsprop, clear,
-              1, reinterpret_cast<unsigned long long *>(out_count)};
+    OptArgs a{g->table, g->density, v, gb->grad, gb->tmask, g->rows, lr_sigma, lr_sh, beta, eps,
+              rmsprop, clear, 1, reinterpret_cast<unsigned long long *>(out_count)};
     constexpr int NT = 256;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (gb->tids) {   // two-phase: compact the touched set, then update the list
+        if (cudaMemsetAsync(gb->tcnt, 0, sizeof(int64_t), s) != cudaSuccess) return PLX_ECUDA;
+        const int64_t nrange = ((g->rows + 127) / 128 + kCompactSegs - 1) / kCompactSegs;
+        int64_t nb = (nrange + NT / 32 - 1) / (NT / 32);
+        if (nb > (int64_t)num_sms() * 8) nb = (int64_t)num_sms() * 8;
+        touched_compact_kernel<<<(unsigned)nb, NT, 0, s>>>(gb->tmask, g->rows, gb->tids, gb->tcnt,
+                                                          clear);
+        static int nbr = 0;
+        if (!nbr) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbr, opt_rows_kernel, NT, 0);
+            if (nbr <= 0) nbr = 1;
+        }
+        opt_rows_kernel<<<(unsigned)(num_sms() * nbr), NT, 0, s>>>(a, gb->tids, gb->tcnt);
+        return status();
+    }
     const int64_t segs = (g->rows + 127) / 128;
     int64_t nb = (segs + NT / 32 - 1) / (NT / 32);
     if (nb > (int64_t)num_sms() * opt_blocks_per_sm()) nb = (int64_t)num_sms() * opt_blocks_per_sm();
-    opt_kernel<NT><<<(unsigned)nb, NT, 0, (cudaStream_t)stream>>>(a);
+    opt_kernel<NT><<<(unsigned)nb, NT, 0, s>>>(a);
     return status();
 }
 
 extern "C" int plx_clear_grad(plx_grad *gb, int64_t rows, int64_t *out_count, void *stream) {
     if (!gb || !gb->grad || !gb->tmask || rows < 0) return PLX_EINVAL;
     if (rows == 0) return PLX_OK;
-    OptArgs a{nullptr, nullptr, gb->grad, gb->tmask, rows, 0.0, 0.0, 0.0, 0.0, 0, 1, 0,
+    OptArgs a{nullptr, nullptr, nullptr, gb->grad, gb->tmask, rows, 0.0, 0.0, 0.0, 0.0, 0, 1, 0,
               reinterpret_cast<unsigned long long *>(out_count)};
     constexpr int NT = 256;
     const int64_t segs = (rows + 127) / 128;
@@ -631,11 +808,11 @@ extern "C" int plx_prune_mark(const plx_grid *g, const double *weights, double t
 }
 
 extern "C" int plx_prune_apply(const plx_grid *g, const int32_t *new_links, int64_t *kept_old,
-                               float *new_table, void *stream) {
-    if (!grid_ok(g) || !new_links) return PLX_EINVAL;
+                               float *new_table, float *new_density, void *stream) {
+    if (!grid_ok(g) || !new_links || !new_table || !new_density) return PLX_EINVAL;
     const int64_t n = ncell(g);
     prune_apply_kernel<<<blocks(n * 8, 256), 256, 0, (cudaStream_t)stream>>>(
-        make_dgrid(*g), new_links, n, kept_old, new_table);
+        make_dgrid(*g), new_links, n, kept_old, new_table, new_density);
     return status();
 }
 
@@ -661,11 +838,12 @@ extern "C" int plx_upsample_mark(const plx_grid *g, const int64_t new_dims[3], u
 }
 
 extern "C" int plx_upsample_apply(const plx_grid *g, const int64_t new_dims[3],
-                                  const int32_t *new_links, float *new_table, void *stream) {
-    if (!grid_ok(g) || !new_dims || !new_links) return PLX_EINVAL;
+                                  const int32_t *new_links, float *new_table, float *new_density,
+                                  void *stream) {
+    if (!grid_ok(g) || !new_dims || !new_links || !new_table || !new_density) return PLX_EINVAL;
     const int64_t n = new_dims[0] * new_dims[1] * new_dims[2];
     upsample_apply_kernel<<<blocks(n * 8, 256), 256, 0, (cudaStream_t)stream>>>(
-        make_dgrid(*g), make_up(g, new_dims), new_links, n, new_table);
+        make_dgrid(*g), make_up(g, new_dims), new_links, n, new_table, new_density);
     return status();
 }
 

@@ -47,15 +47,21 @@ class GradientBuffer:
         self.data = torch.zeros((int(n_rows), ROW), dtype=torch.float32, device=dev)
         self.touched_mask = torch.zeros(int(n_rows), dtype=torch.uint8, device=dev)
         self._count = torch.zeros(1, dtype=torch.int64, device=dev)
+        # touched_ids / _count (G:25-68): filled by the two-phase optimiser step
+        self.touched_ids = torch.empty(max(int(n_rows), 1), dtype=torch.int32, device=dev)
+        self._tcnt = torch.zeros(1, dtype=torch.int64, device=dev)
 
     @property
     def n_rows(self) -> int:
         return self.data.shape[0]
 
-    def _c(self) -> _lib.PlxGrad:
+    def _c(self, with_ids: bool = True) -> _lib.PlxGrad:
         g = _lib.PlxGrad()
         g.grad = self.data.data_ptr()
         g.tmask = self.touched_mask.data_ptr()
+        if with_ids:
+            g.tids = self.touched_ids.data_ptr()
+            g.tcnt = self._tcnt.data_ptr()
         return g
 
     def count_touched_async(self) -> torch.Tensor:
@@ -96,7 +102,14 @@ class GradientBuffer:
 
 
 class SparseGrid:
-    """Dense int32 pointer lattice + f32 data table in HBM (G:71-320)."""
+    """Dense int32 pointer lattice + f32 data in HBM (G:71-320).
+
+    The reference's (rows, 28) `table` (column 0 sigma, 1..27 SH) is stored
+    as two arrays: `density` (rows,) and `sh` (rows, 28) with column 0 unused
+    (kept zero; 16-byte rows for float4 access).  The sigma gathers of the
+    march then read a compact 4 B/row array.  `table` is the reference's
+    combined view, materialised as a COPY (assign `grid.table = t` to write
+    it back)."""
 
     def __init__(self, links, table, aabb_min, aabb_max, device=None):
         dev = _dev(device if device is not None else
@@ -110,7 +123,7 @@ class SparseGrid:
         if table.dim() != 2 or table.shape[1] != ROW:
             raise ValueError(f"table must be (rows, {ROW})")
         self._links = links.to(device=dev, dtype=torch.int32).contiguous()
-        self.table = table.to(device=dev, dtype=torch.float32).contiguous()
+        self.table = table.to(device=dev, dtype=torch.float32)
         self.aabb_min = np.asarray(aabb_min, dtype=np.float64).reshape(3).copy()
         self.aabb_max = np.asarray(aabb_max, dtype=np.float64).reshape(3).copy()
         if np.any(self.aabb_max <= self.aabb_min):
@@ -120,6 +133,19 @@ class SparseGrid:
         self._cell_occ = None
 
     # -- constructors -------------------------------------------------------
+    @classmethod
+    def _from_parts(cls, links, n_rows, aabb_min, aabb_max, device) -> "SparseGrid":
+        """Grid over device links with uninitialised density / sh of n_rows
+        (filled by a structure-op kernel)."""
+        g = cls.__new__(cls)
+        g._links = links.to(torch.int32).contiguous()
+        g.density = torch.empty(int(n_rows), dtype=torch.float32, device=device)
+        g.sh = torch.empty((int(n_rows), ROW), dtype=torch.float32, device=device)
+        g.aabb_min = np.asarray(aabb_min, dtype=np.float64).reshape(3).copy()
+        g.aabb_max = np.asarray(aabb_max, dtype=np.float64).reshape(3).copy()
+        g._cell_occ = None
+        return g
+
     @classmethod
     def dense(cls, dims, aabb_min, aabb_max, sigma: float = 0.0, rgb: float | None = None,
               device=None) -> "SparseGrid":
@@ -154,8 +180,25 @@ class SparseGrid:
         self._cell_occ = None
 
     @property
+    def table(self) -> torch.Tensor:
+        """The reference's (rows, 28) table: a fresh tensor, column 0 = sigma."""
+        t = self.sh.clone()
+        t[:, 0] = self.density
+        return t
+
+    @table.setter
+    def table(self, value) -> None:
+        t = torch.as_tensor(value)
+        dev = self._links.device
+        if t.dim() != 2 or t.shape[1] != ROW:
+            raise ValueError(f"table must be (rows, {ROW})")
+        self.density = t[:, 0].to(device=dev, dtype=torch.float32).contiguous()
+        self.sh = t.to(device=dev, dtype=torch.float32).clone().contiguous()
+        self.sh[:, 0] = 0.0
+
+    @property
     def device(self):
-        return self.table.device
+        return self._links.device
 
     @property
     def dims(self) -> tuple[int, int, int]:
@@ -163,7 +206,7 @@ class SparseGrid:
 
     @property
     def n_rows(self) -> int:
-        return int(self.table.shape[0])
+        return int(self.density.shape[0])
 
     @property
     def extent(self) -> np.ndarray:
@@ -200,7 +243,8 @@ class SparseGrid:
     def _c(self, with_occ: bool = True) -> _lib.PlxGrid:
         g = _lib.PlxGrid()
         g.links = self._links.data_ptr()
-        g.table = self.table.data_ptr() if self.n_rows else None
+        g.table = self.sh.data_ptr() if self.n_rows else None
+        g.density = self.density.data_ptr() if self.n_rows else None
         g.dims = _lib.dims_array(self.dims)
         g.rows = self.n_rows
         g.lo = (ctypes.c_double * 3)(*self.aabb_min)
@@ -215,7 +259,7 @@ class SparseGrid:
         return self._links.cpu().numpy(), self.table.cpu().numpy()
 
     def copy(self) -> "SparseGrid":
-        return SparseGrid(self._links.clone(), self.table.clone(), self.aabb_min.copy(),
+        return SparseGrid(self._links.clone(), self.table, self.aabb_min.copy(),
                           self.aabb_max.copy(), device=self.device)
 
     def occupancy(self) -> torch.Tensor:
@@ -257,12 +301,12 @@ class SparseGrid:
         del scratch
         ids, n_keep = self._compact(flags)
         kept = torch.empty(max(n_keep, 1), dtype=torch.int64, device=self.device)
-        table = torch.empty((n_keep, ROW), dtype=torch.float32, device=self.device)
+        grid = SparseGrid._from_parts(ids.reshape(self.dims), n_keep, self.aabb_min,
+                                      self.aabb_max, self.device)
         if n_keep:
             _lib.check(L.plx_prune_apply(ctypes.byref(c), ids.data_ptr(), kept.data_ptr(),
-                                         table.data_ptr(), s), "prune_apply")
-        grid = SparseGrid(ids.reshape(self.dims), table, self.aabb_min, self.aabb_max,
-                          device=self.device)
+                                         grid.sh.data_ptr(), grid.density.data_ptr(), s),
+                       "prune_apply")
         return grid, kept[:n_keep]
 
     def upsample(self, new_dims) -> "SparseGrid":
@@ -283,12 +327,13 @@ class SparseGrid:
                    "upsample_mark")
         ids, n_new = self._compact(flags)
         del flags
-        table = torch.empty((n_new, ROW), dtype=torch.float32, device=self.device)
+        grid = SparseGrid._from_parts(ids.reshape(new_dims), n_new, self.aabb_min,
+                                      self.aabb_max, self.device)
         if n_new:
             _lib.check(L.plx_upsample_apply(ctypes.byref(c), nd, ids.data_ptr(),
-                                            table.data_ptr(), s), "upsample_apply")
-        return SparseGrid(ids.reshape(new_dims), table, self.aabb_min, self.aabb_max,
-                          device=self.device)
+                                            grid.sh.data_ptr(), grid.density.data_ptr(), s),
+                       "upsample_apply")
+        return grid
 
     def max_weight_accumulate(self, origins, dirs, step_frac: float = 0.5,
                               stop_thresh: float = 1e-4, interp: str = "trilinear",
@@ -323,5 +368,6 @@ class SparseGrid:
             counts = torch.bincount(rows, minlength=self.n_rows)
             if int(rows.max()) >= self.n_rows or not bool(torch.all(counts == 1)):
                 raise AssertionError("links and table rows are not a bijection")
-        if not bool(torch.all(torch.isfinite(self.table))):
+        if not (bool(torch.all(torch.isfinite(self.sh))) and
+                bool(torch.all(torch.isfinite(self.density)))):
             raise AssertionError("non-finite values in data table")

@@ -243,9 +243,10 @@ def _grid_aabb(cfg: TrainConfig, dims):
 
 
 def _estimate_table_bytes(dims) -> int:
-    """Device footprint of a dense rung: links + table + grad + v (f32)."""
+    """Device footprint of a dense rung: links + density + sh + grad + v (f32)
+    + touched mask and id list."""
     cells = int(np.prod([int(d) for d in dims]))
-    return cells * (4 + 3 * 28 * 4 + 1)
+    return cells * (4 + 4 + 3 * 28 * 4 + 1 + 4)
 
 
 class Trainer:
@@ -276,12 +277,16 @@ class Trainer:
         self.rung_events = {r.step: tuple(r.dims) for r in cfg.ladder[1:]}
         self.sums = torch.zeros(4, dtype=torch.float64, device=self.device)
         self.count = torch.zeros(1, dtype=torch.int64, device=self.device)
+        # march counters of the fused kernel, accumulated over steps:
+        # {positions, samples, chunks, rays} (plx_render_opts.stats)
+        self.march_stats = torch.zeros(4, dtype=torch.int64, device=self.device)
         self._host_sums = torch.zeros(4, dtype=torch.float64).pin_memory()
         self._refresh_cache()
 
     def _refresh_cache(self):
         self._cgrid = self.grid._c(with_occ=self.opts.interp == "trilinear")
         self._kopts = render.kernel_opts(self.grid, self.opts)
+        self._kopts.stats = self.march_stats.data_ptr()
 
     # -- ladder event (T:412-439) ---------------------------------------------
     def rung_event(self, new_dims, out_dir=None, step=0):

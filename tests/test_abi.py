@@ -45,3 +45,27 @@ def test_scan_scratch_sizing_is_host_only():
     assert lib.plx_scan_scratch_bytes(4096) == 16
     d = (ctypes.c_int64 * 3)(64, 64, 64)
     assert lib.plx_cell_occ_words(d) == 64 ** 3 // 32
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """The ctypes mirrors in _lib.py have the C layout include/plx.h declares
+    (sizeof and every field offset, checked by compiling the header)."""
+    structs = {"plx_grid": _lib.PlxGrid, "plx_grad": _lib.PlxGrad,
+               "plx_render_opts": _lib.PlxRenderOpts, "plx_rays": _lib.PlxRays}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "plx.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True,
+                                                       text=True, check=True).stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(got[cname]) == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(py, fname).offset, (cname, fname)

@@ -16,6 +16,10 @@ from helpers import golden_grid, grad_close, load, random_grid, ray_batch
 pytestmark = pytest.mark.gpu
 
 RGB_TOL = 1e-4
+# The colour dot products are f32 FMAs (~3e-7 from float64, far inside
+# RGB_TOL); sigma, transmittance and the sample set stay float64-exact, so the
+# Cauchy sums keep 1e-9 while the MSE sum carries the colour rounding.
+MSE_REL = 1e-6
 
 
 def px():
@@ -104,7 +108,7 @@ def _check_bwd(g, o, d, gt, kw, lam=0.0, upstream=None):
                                                      lam_cauchy=lam, **kw)
         rgb_d, mse_d, cau_d = px().fused_mse_backward(dg, o, d, vd, gt, buf_d, opts,
                                                       n_total=len(o), lam_cauchy=lam)
-        assert mse_d == pytest.approx(mse_o, rel=1e-9, abs=1e-12)
+        assert mse_d == pytest.approx(mse_o, rel=MSE_REL, abs=1e-12)
     else:
         rgb_o, cau_o = orc.render_rays_backward(g, o, d, upstream, buf_o, lam_cauchy=lam, **kw)
         rgb_d, cau_d = px().render_rays_backward(dg, o, d, upstream, buf_d, opts,
@@ -131,7 +135,7 @@ def test_fused_backward_golden(cell_occ):
                                                 buf, px().RenderOptions(**kw), n_total=len(o),
                                                 lam_cauchy=lam)
         assert np.max(np.abs(rgb - z[f"c{ci}_rgb"])) < RGB_TOL
-        assert mse == pytest.approx(z[f"c{ci}_sums"][0], rel=1e-9)
+        assert mse == pytest.approx(z[f"c{ci}_sums"][0], rel=MSE_REL)
         assert cau == pytest.approx(z[f"c{ci}_sums"][1], rel=1e-9, abs=1e-15)
         np.testing.assert_array_equal(buf.touched_rows(), z[f"c{ci}_touched"])
         ok, worst, nbad = grad_close(buf.dense(), z[f"c{ci}_grad"])
@@ -237,6 +241,45 @@ def test_opt_step_golden():
         assert buf.n_touched == 0 and float(buf.data.abs().sum()) == 0.0
 
 
+@pytest.mark.parametrize("method", ["rmsprop", "sgd"])
+def test_opt_step_bitwise_after_f32_rounding(method):
+    """The kernel's float64 update (MUFU-seeded Newton root/quotient, no IEEE
+    div/sqrt subroutines) rounded to f32 equals the oracle's float64 result
+    (K:572-590) rounded to f32 on ~1.8 M values spanning 12 decades; only
+    f32 rounding ties may differ."""
+    rng = np.random.default_rng(11)
+    n = 64000
+    t0 = rng.normal(size=(n, 28)).astype(np.float32).astype(np.float64)
+    v0 = (10.0 ** rng.uniform(-12, 0, (n, 28))).astype(np.float32).astype(np.float64)
+    gr = (rng.normal(size=(n, 28)) * 10.0 ** rng.uniform(-6, 2, (n, 28)))
+    gr[rng.random((n, 28)) < 0.1] = 0.0       # stale-state entries (g == 0)
+    gr = gr.astype(np.float32).astype(np.float64)
+    touched = np.sort(rng.permutation(n)[: n // 2])
+    gr[np.setdiff1d(np.arange(n), touched)] = 0.0
+    g = px().SparseGrid(np.arange(n, dtype=np.int32).reshape(40, 40, 40), t0.astype(np.float32),
+                        (0, 0, 0), (1, 1, 1))
+    st = px().OptimState(n)
+    st.v.copy_(torch.as_tensor(v0, dtype=torch.float32))
+    buf = px().GradientBuffer(n)
+    buf.data.copy_(torch.as_tensor(gr, dtype=torch.float32))
+    buf.touched_mask[torch.as_tensor(touched).cuda()] = 1
+    from paper_2112_05131_b200 import optim
+    optim.step(g, buf, st, 30.0, 0.01, method)
+    og = orc.Grid(np.arange(n, dtype=np.int32).reshape(40, 40, 40), t0.copy(), (0, 0, 0),
+                  (1, 1, 1))
+    ob = orc.GradBuf(n)
+    ob.data[:] = gr
+    ob.touched_ids[: len(touched)] = touched
+    ob._count[0] = len(touched)
+    vo = v0.copy()
+    orc.opt_step(og, ob, vo, 30.0, 0.01, method)
+    got = g.table.cpu().numpy()
+    want = og.table.astype(np.float32)
+    assert np.count_nonzero(got != want) <= 4, np.count_nonzero(got != want)
+    if method == "rmsprop":
+        assert np.count_nonzero(st.v.cpu().numpy() != vo.astype(np.float32)) == 0
+
+
 def test_opt_step_fused_clear_counts():
     rng = np.random.default_rng(3)
     g = px().SparseGrid.dense((6, 7, 8), (0, 0, 0), (1, 1, 1), sigma=0.3, rgb=0.2)
@@ -320,3 +363,16 @@ def test_upsample_empty_grid_is_graceful():
     g = px().SparseGrid.empty((4, 4, 4), (0, 0, 0), (1, 1, 1))
     u = g.upsample((8, 8, 8))
     assert u.n_rows == 0 and u.dims == (8, 8, 8)
+
+
+@pytest.mark.parametrize("interp", ["trilinear", "nearest"])
+def test_fused_backward_long_rays_vs_oracle(interp):
+    """Rays of several hundred positions (many 32-position chunks, face, edge
+    and corner crossings, holes) through a 40^3 grid: exercises the scatter
+    accumulator's carried state across chunks against the oracle."""
+    rng = np.random.default_rng(300)
+    g = random_grid(rng, dims=(40, 37, 43), holes=0.3, sigma_range=(-0.3, 0.6))
+    o, d = ray_batch(rng, 200)
+    gt = rng.uniform(0, 1, (200, 3))
+    _check_bwd(g, o, d, gt, dict(step_frac=0.37, stop_thresh=1e-4,
+                                 background=(0.2, 0.5, 0.9), interp=interp), lam=1e-4)
