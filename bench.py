@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--res", type=int, default=200)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--steady-step", type=int, default=2000,
+                   help="also time K steps after training to this step (0 = off)")
     return p.parse_args()
 
 
@@ -350,6 +352,7 @@ def run_ours(args):
         e2e_step(args.warmup - W2 + i, host[i])
     tr.grid.density.copy_(snap_den)     # replay from the value leg's starting state
     tr.grid.sh.copy_(snap_sh)
+    tr.grid.invalidate()                # density edited in place: rebuild the sign bitmask
     tr.state.v.copy_(snap_v)
     del snap_den, snap_sh, snap_v
     torch.cuda.synchronize()
@@ -365,6 +368,39 @@ def run_ours(args):
     if world_size > 1:
         dist.all_reduce(ms_e2e, op=dist.ReduceOp.MAX)
     e2e_value = B_local * world_size / (float(ms_e2e.item()) / 1000.0)
+
+    # -- the same step later in training (reported beside the headline) -------
+    # The headline is timed at steps W..W+K of a run from the dense init, the
+    # most expensive regime (most of the grid still has sigma >= 0).  Training
+    # spends nearly all of its 38,400 256^3 steps in the sparse regime, so the
+    # same K-step measurement is repeated after training on to --steady-step.
+    steady = None
+    if args.steady_step > args.warmup + args.steps:
+        s_next = args.warmup + args.steps
+        while s_next < args.steady_step:
+            tr.step(s_next, check_finite=False)
+            s_next += 1
+        torch.cuda.synchronize()
+        barrier()
+        st1 = tr.march_stats.clone()
+        c_acc = torch.zeros(1, dtype=torch.int64, device=dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(args.steps):
+            tr.step(s_next + k)
+            c_acc += tr.count
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms_s = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+        if world_size > 1:
+            dist.all_reduce(ms_s, op=dist.ReduceOp.MAX)
+        ms_s = float(ms_s.item())
+        mst = ((tr.march_stats - st1).double() / args.steps).cpu().numpy()
+        steady = {"from_step": s_next, "steps": args.steps, "ms_per_step": ms_s,
+                  "rays_per_s": args.batch * world_size / (ms_s / 1000.0),
+                  "touched_rows_U": float(c_acc.item()) / args.steps,
+                  "march_positions_per_step": float(mst[0]), "samples_per_step": float(mst[1])}
 
     # -- roofline of the dominant kernel ---------------------------------------
     peak, peak_kind = load_peaks()
@@ -408,6 +444,7 @@ def run_ours(args):
                        "samples_per_step": float(march[1]),
                        "chunks_per_step": float(march[2]),
                        "step_bytes_model": step_bytes,
+                       "steady_state": steady,
                        "step_hbm_frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
                        "kernel_ms": avg},
             "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": h2d,

@@ -57,6 +57,16 @@ typedef struct {
     const uint32_t *cell_occ; /* optional: 1 bit per trilinear base cell,
                                  set iff any of its 8 corners is occupied
                                  (plx_build_cell_occ); NULL = test the links */
+    uint32_t *neg_bits;    /* optional: 1 bit per lattice point, set iff it
+                              is occupied with density < 0
+                              (plx_build_neg_bits).  A trilinear cell whose
+                              8 corners are all set cannot hold a composited
+                              sample, so the march skips its gathers.
+                              plx_opt_step keeps it current (needs row_cell);
+                              rebuild after editing density or links.     */
+    const int32_t *row_cell; /* [rows] lattice point of each row (inverse of
+                              links, plx_build_row_cell); required with
+                              neg_bits by plx_opt_step                    */
 } plx_grid;
 
 /* GradientBuffer (G:25-68): data + touched mask, and optionally the
@@ -134,10 +144,15 @@ int plx_tv(const plx_grid *g, const int64_t *cells, int64_t start, int64_t count
 /* opt_step (K:572-590) via optim.step (O:81-97), fused with clear_grad
  * (K:593-600) when clear != 0.  Visits rows whose tmask is set; entries with
  * g == 0 keep their stale state.  out_count (device int64, may be NULL)
- * receives the number of touched rows (GradientBuffer.n_touched). */
+ * receives the number of touched rows (GradientBuffer.n_touched).
+ * guard (device double[5], may be NULL) moves the trainer's divergence check
+ * (T:473-480) onto the device: guard[0..3] = the step's loss sums {mse,
+ * cauchy, tv_sigma, tv_sh}, guard[4] = sticky halt flag; if any sum is
+ * non-finite or guard[4] != 0, nothing is updated or cleared and guard[4]
+ * is set to 1, so the host can check asynchronously. */
 int plx_opt_step(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, double lr_sh,
                  double beta, double eps, int32_t rmsprop, int32_t clear,
-                 int64_t *out_count, void *stream);
+                 double *guard, int64_t *out_count, void *stream);
 
 /* clear_grad (K:593-600) alone (GradientBuffer.clear, G:62-64): zero the
  * touched rows of gb->grad and reset gb->tmask.  out_count as above. */
@@ -172,6 +187,9 @@ int plx_scan_ids(const uint8_t *flags, int64_t n, int32_t *ids, int64_t *count,
  * = any of the 8 corner links >= 0.  Must be rebuilt after prune/upsample. */
 int64_t plx_cell_occ_words(const int64_t dims[3]);
 int plx_build_cell_occ(const plx_grid *g, uint32_t *cell_occ, void *stream);
+/* neg_bits (plx_cell_occ_words words, same lattice indexing) and row_cell. */
+int plx_build_neg_bits(const plx_grid *g, uint32_t *neg_bits, void *stream);
+int plx_build_row_cell(const plx_grid *g, int32_t *row_cell, void *stream);
 
 /* Library identification / self-check. */
 const char *plx_version(void);

@@ -30,7 +30,8 @@ class PlxGrid(ctypes.Structure):
                 ("density", ctypes.c_void_p), ("dims", ctypes.c_int64 * 3), ("rows", ctypes.c_int64),
                 ("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3),
                 ("scale", ctypes.c_double * 3), ("dmax", ctypes.c_double * 3),
-                ("cell_occ", ctypes.c_void_p)]
+                ("cell_occ", ctypes.c_void_p), ("neg_bits", ctypes.c_void_p),
+                ("row_cell", ctypes.c_void_p)]
 
 
 class PlxGrad(ctypes.Structure):
@@ -69,7 +70,7 @@ _SIGS = {
     "plx_tv": [ctypes.POINTER(PlxGrid), _P, _I64, _I64, _D, _D, _D, _D, _D, _D,
                _I32, _I32, _I32, _I32, ctypes.POINTER(PlxGrad), _P, _P],
     "plx_opt_step": [ctypes.POINTER(PlxGrid), _P, ctypes.POINTER(PlxGrad), _D, _D, _D,
-                     _D, _I32, _I32, _P, _P],
+                     _D, _I32, _I32, _P, _P, _P],
     "plx_clear_grad": [ctypes.POINTER(PlxGrad), _I64, _P, _P],
     "plx_count_touched": [_P, _I64, _P, _P],
     "plx_prune_mark": [ctypes.POINTER(PlxGrid), _P, _D, _P, _P, _P],
@@ -80,6 +81,8 @@ _SIGS = {
     "plx_scan_ids": [_P, _I64, _P, _P, _P, _P],
     "plx_cell_occ_words": [ctypes.POINTER(_I64)],
     "plx_build_cell_occ": [ctypes.POINTER(PlxGrid), _P, _P],
+    "plx_build_neg_bits": [ctypes.POINTER(PlxGrid), _P, _P],
+    "plx_build_row_cell": [ctypes.POINTER(PlxGrid), _P, _P],
     "plx_version": [],
     "plx_device_check": [],
 }

@@ -23,6 +23,7 @@ struct DGrid {
     const float *__restrict__ table;     // SH rows (column 0 unused)
     const float *__restrict__ density;   // sigma per row
     const uint32_t *__restrict__ cell_occ;
+    const uint32_t *neg_bits;            // lattice points occupied with sigma < 0 (mutable)
     int32_t Dx, Dy, Dz;
     double lo[3], hi[3], scale[3], dmax[3];
 };
@@ -33,6 +34,7 @@ inline DGrid make_dgrid(const plx_grid &g) {
     d.table = g.table;
     d.density = g.density;
     d.cell_occ = g.cell_occ;
+    d.neg_bits = g.neg_bits;
     d.Dx = (int32_t)g.dims[0];
     d.Dy = (int32_t)g.dims[1];
     d.Dz = (int32_t)g.dims[2];
@@ -134,17 +136,37 @@ __device__ __forceinline__ void sample_coords(const RayMarch &rm, const DGrid &G
     for (int a = 0; a < 3; ++a) g[a] = clamp_coord(rm.o[a] + t * rm.d[a], G.lo[a], G.scale[a], G.dmax[a]);
 }
 
-// Stencil (K:84-123): rows[8] (-1 = empty) and the fractional offsets f[3];
-// the corner weight is stencil_w(f, q) (recomputed instead of stored, to save
+// Two consecutive bits c, c+1 of a lattice bitmask (3 = both set).
+__device__ __forceinline__ unsigned bits2(const uint32_t *m, int64_t c) {
+    const uint32_t w = m[c >> 5];
+    const int b = (int)(c & 31);
+    return b < 31 ? (w >> b) & 3u : (w >> 31) | ((m[(c >> 5) + 1] & 1u) << 1);
+}
+
+// Trilinear cell with base lattice point c whose 8 corners are all set in
+// neg_bits (occupied, sigma < 0).  The bitmask is updated in place by the
+// optimiser, so it is read with plain (not read-only-path) loads.
+__device__ __forceinline__ bool dead_cell(const DGrid &G, int64_t c) {
+    const int64_t sy = G.Dz, sx = (int64_t)G.Dy * G.Dz;
+    return (bits2(G.neg_bits, c) & bits2(G.neg_bits, c + sy) & bits2(G.neg_bits, c + sx) &
+            bits2(G.neg_bits, c + sx + sy)) == 3u;
+}
+
+// Stencil (K:84-123): rows[8] (-1 = empty), the fractional offsets f[3] and
+// the base cell (trilinear) or lattice point (nearest) ijk[3]; the corner
+// weight is stencil_w(f, q) (recomputed instead of stored, to save
 // registers; same float64 products as K:115-121).  Returns 1 or 8.
 template <bool NEAREST>
 __device__ __forceinline__ int stencil(const DGrid &G, const double *g, int32_t *rows, double *f,
-                                       bool &any_occ) {
+                                       bool &any_occ, int *ijk) {
     if (NEAREST) {
         int64_t i = (int64_t)(g[0] + 0.5), j = (int64_t)(g[1] + 0.5), k = (int64_t)(g[2] + 0.5);
         if (i > G.Dx - 1) i = G.Dx - 1;
         if (j > G.Dy - 1) j = G.Dy - 1;
         if (k > G.Dz - 1) k = G.Dz - 1;
+        ijk[0] = (int)i;
+        ijk[1] = (int)j;
+        ijk[2] = (int)k;
         rows[0] = __ldg(G.links + flat(G, i, j, k));
         any_occ = rows[0] >= 0;
         return 1;
@@ -153,12 +175,22 @@ __device__ __forceinline__ int stencil(const DGrid &G, const double *g, int32_t 
     if (i0 > G.Dx - 2) i0 = G.Dx - 2;
     if (j0 > G.Dy - 2) j0 = G.Dy - 2;
     if (k0 > G.Dz - 2) k0 = G.Dz - 2;
+    ijk[0] = (int)i0;
+    ijk[1] = (int)j0;
+    ijk[2] = (int)k0;
     if (G.cell_occ) {
         int64_t c = flat(G, i0, j0, k0);
         if (!((__ldg(G.cell_occ + (c >> 5)) >> (c & 31)) & 1u)) {
             any_occ = false;
             return 8;
         }
+    }
+    if (G.neg_bits && dead_cell(G, flat(G, i0, j0, k0))) {
+        // all 8 corners occupied with sigma < 0: the interpolated sigma is a
+        // convex combination of negatives, so the sample is excluded (K:211,
+        // K:293) -- skip the link and density gathers
+        any_occ = false;
+        return 8;
     }
     f[0] = g[0] - (double)i0;
     f[1] = g[1] - (double)j0;

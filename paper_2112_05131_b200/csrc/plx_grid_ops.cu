@@ -141,6 +141,9 @@ __global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
 // one mask byte; touched rows cost exactly their compulsory 672 B.
 struct OptArgs {
     float *table, *density, *v, *grad;
+    double *guard;             // optional divergence guard (see guard_halts)
+    uint32_t *neg_bits;        // optional: kept current when sigma changes sign
+    const int32_t *row_cell;   // row -> lattice point (required with neg_bits)
     uint8_t *tmask;
     int64_t rows;
     double lr_sigma, lr_sh, beta, eps;
@@ -180,6 +183,25 @@ __device__ __forceinline__ double rms_quot(double num, double nv, double eps) {
     return q;
 }
 
+// Divergence guard (trainer.py T:473-480 on the device): guard[0..3] are
+// the step's loss sums, guard[4] a sticky halt flag.  True = skip the step.
+__device__ __forceinline__ bool guard_halts(double *guard) {
+    if (!guard) return false;
+    bool bad = guard[4] != 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) bad |= !isfinite(guard[i]);
+    return bad;
+}
+
+// sigma of a row at lattice point c went from `before` to `after`: keep its
+// neg bit current.
+__device__ __forceinline__ void neg_update(const OptArgs &a, int32_t c, float before, float after) {
+    if (!a.neg_bits || ((before < 0.f) == (after < 0.f))) return;
+    const uint32_t bit = 1u << (c & 31);
+    if (after < 0.f) atomicOr(a.neg_bits + (c >> 5), bit);
+    else atomicAnd(a.neg_bits + (c >> 5), ~bit);
+}
+
 // The update of one float4 of one row (K:578-590), float64 arithmetic.
 __device__ __forceinline__ void opt_apply(const OptArgs &a, int quad, float4 &g4, float4 &t4,
                                           float4 &v4) {
@@ -205,6 +227,10 @@ __device__ __forceinline__ void opt_apply(const OptArgs &a, int quad, float4 &g4
 
 template <int NT>
 __global__ void __launch_bounds__(NT) opt_kernel(OptArgs a) {
+    if (guard_halts(a.guard)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.guard[4] = 1.0;
+        return;
+    }
     __shared__ uint8_t list[NT / 32][128];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nseg = (a.rows + 127) >> 7;
@@ -274,6 +300,7 @@ __global__ void __launch_bounds__(NT) opt_kernel(OptArgs a) {
                     opt_apply(a, quad, g4[u], t4[u], v4[u]);
                     if (quad == 0) {
                         a.density[rw[u]] = t4[u].x;
+                        if (a.neg_bits) neg_update(a, a.row_cell[rw[u]], den[u], t4[u].x);
                         t4[u].x = 0.f;
                     }
                     reinterpret_cast<float4 *>(a.table + rw[u] * PLX_ROW)[quad] = t4[u];
@@ -312,15 +339,22 @@ constexpr int kOptU = 4;
 
 __global__ void __launch_bounds__(256) touched_compact_kernel(uint8_t *tmask, int64_t rows,
                                                               int32_t *tids, int64_t *tcnt,
-                                                              int clear) {
-    const int lane = threadIdx.x & 31;
+                                                              int clear, double *guard) {
+    __shared__ int warp_tot[8];
+    __shared__ unsigned long long blk_base;
+    if (guard_halts(guard)) {   // non-finite loss: no update, no clear (T:473-480)
+        if (blockIdx.x == 0 && threadIdx.x == 0) guard[4] = 1.0;
+        return;
+    }
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nseg = (rows + 127) >> 7;
     const int64_t nrange = (nseg + kCompactSegs - 1) / kCompactSegs;
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t rg = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); rg < nrange;
-         rg += nw) {
+    // block-uniform trip count: one range per warp per iteration, one atomic
+    // per block per iteration (a single global counter serialises at L2)
+    for (int64_t rg0 = (int64_t)blockIdx.x * 8; rg0 < nrange; rg0 += (int64_t)gridDim.x * 8) {
+        const int64_t rg = rg0 + wib;
         const int64_t s0 = rg * kCompactSegs;
-        const int64_t s1 = min(nseg, s0 + kCompactSegs);
+        const int64_t s1 = rg < nrange ? min(nseg, s0 + kCompactSegs) : s0;
         uint32_t m[kCompactSegs];
         int c = 0;
 #pragma unroll
@@ -343,13 +377,21 @@ __global__ void __launch_bounds__(256) touched_compact_kernel(uint8_t *tmask, in
             const int y = __shfl_up_sync(PLX_FULL_MASK, incl, off);
             if (lane >= off) incl += y;
         }
-        const int total = __shfl_sync(PLX_FULL_MASK, incl, 31);
-        if (total == 0) continue;
-        unsigned long long base = 0;
-        if (lane == 31) base = atomicAdd(reinterpret_cast<unsigned long long *>(tcnt),
-                                         (unsigned long long)total);
-        base = __shfl_sync(PLX_FULL_MASK, base, 31);
-        int64_t pos = (int64_t)base + incl - c;
+        if (lane == 31) warp_tot[wib] = incl;
+        __syncthreads();
+        int before = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            const int t = warp_tot[w];
+            before += w < wib ? t : 0;
+            total += t;
+        }
+        if (threadIdx.x == 0)
+            blk_base = total ? atomicAdd(reinterpret_cast<unsigned long long *>(tcnt),
+                                         (unsigned long long)total)
+                             : 0ull;
+        __syncthreads();
+        int64_t pos = (int64_t)blk_base + before + incl - c;
 #pragma unroll
         for (int i = 0; i < kCompactSegs; ++i) {
             if (!m[i]) continue;
@@ -366,11 +408,12 @@ __global__ void __launch_bounds__(256) touched_compact_kernel(uint8_t *tmask, in
                 }
             }
         }
+        __syncthreads();   // warp_tot / blk_base reuse
     }
 }
 
-__global__ void __launch_bounds__(256, 3) opt_rows_kernel(OptArgs a, const int32_t *tids,
-                                                       const int64_t *tcnt) {
+__global__ void __launch_bounds__(256, 2) opt_rows_kernel(OptArgs a, const int32_t *tids,
+                                                          const int64_t *tcnt) {
     const int lane = threadIdx.x & 31;
     const int quad = lane % 7, sub = lane / 7;
     const int64_t n = *tcnt;
@@ -379,40 +422,55 @@ __global__ void __launch_bounds__(256, 3) opt_rows_kernel(OptArgs a, const int32
     const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (a.count && w == 0 && lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(a.count),
                                                   (unsigned long long)n);
+    // row ids of the groups g0 + u*nw (u < kOptU); -1 = none.  The ids of the
+    // next iteration are loaded before this iteration's rows are used, so
+    // the id -> row dependency is off the critical path.
+    auto load_ids = [&](int64_t g0, int32_t *ids) {
+#pragma unroll
+        for (int u = 0; u < kOptU; ++u) {
+            const int64_t gi = g0 + u * nw;
+            const int64_t j = gi * 4 + sub;
+            ids[u] = (lane < 28 && gi < ngroups && j < n) ? __ldg(tids + j) : -1;
+        }
+    };
+    int32_t cur[kOptU], nxt[kOptU];
+    load_ids(w, cur);
     for (int64_t g0 = w; g0 < ngroups; g0 += nw * kOptU) {
         float4 g4[kOptU], t4[kOptU], v4[kOptU];
         float den[kOptU];
-        int64_t rw[kOptU];
-        bool act[kOptU];
+        int32_t cell[kOptU];
 #pragma unroll
         for (int u = 0; u < kOptU; ++u) {
-            const int64_t j = (g0 + u * nw) * 4 + sub;
-            act[u] = lane < 28 && g0 + u * nw < ngroups && j < n;
-            rw[u] = act[u] ? (int64_t)__ldg(tids + j) : 0;
+            if (cur[u] < 0) continue;
+            const int64_t r = cur[u];
+            g4[u] = reinterpret_cast<const float4 *>(a.grad + r * PLX_ROW)[quad];
+            t4[u] = reinterpret_cast<const float4 *>(a.table + r * PLX_ROW)[quad];
+            if (quad == 0) {   // merged after all loads are issued
+                den[u] = a.density[r];
+                cell[u] = a.neg_bits ? a.row_cell[r] : 0;
+            }
+            if (a.rmsprop) v4[u] = reinterpret_cast<const float4 *>(a.v + r * PLX_ROW)[quad];
         }
+        load_ids(g0 + nw * kOptU, nxt);
 #pragma unroll
         for (int u = 0; u < kOptU; ++u) {
-            if (!act[u]) continue;
-            g4[u] = reinterpret_cast<const float4 *>(a.grad + rw[u] * PLX_ROW)[quad];
-            t4[u] = reinterpret_cast<const float4 *>(a.table + rw[u] * PLX_ROW)[quad];
-            if (quad == 0) den[u] = a.density[rw[u]];   // merged after all loads are issued
-            if (a.rmsprop) v4[u] = reinterpret_cast<const float4 *>(a.v + rw[u] * PLX_ROW)[quad];
-        }
-#pragma unroll
-        for (int u = 0; u < kOptU; ++u) {
-            if (!act[u]) continue;
+            if (cur[u] < 0) continue;
+            const int64_t r = cur[u];
             if (quad == 0) t4[u].x = den[u];
             opt_apply(a, quad, g4[u], t4[u], v4[u]);
             if (quad == 0) {   // sigma lives in the density array (column 0 unused)
-                a.density[rw[u]] = t4[u].x;
+                a.density[r] = t4[u].x;
+                neg_update(a, cell[u], den[u], t4[u].x);
                 t4[u].x = 0.f;
             }
-            reinterpret_cast<float4 *>(a.table + rw[u] * PLX_ROW)[quad] = t4[u];
-            if (a.rmsprop) reinterpret_cast<float4 *>(a.v + rw[u] * PLX_ROW)[quad] = v4[u];
+            reinterpret_cast<float4 *>(a.table + r * PLX_ROW)[quad] = t4[u];
+            if (a.rmsprop) reinterpret_cast<float4 *>(a.v + r * PLX_ROW)[quad] = v4[u];
             if (a.clear)
-                reinterpret_cast<float4 *>(a.grad + rw[u] * PLX_ROW)[quad] =
+                reinterpret_cast<float4 *>(a.grad + r * PLX_ROW)[quad] =
                     make_float4(0.f, 0.f, 0.f, 0.f);
         }
+#pragma unroll
+        for (int u = 0; u < kOptU; ++u) cur[u] = nxt[u];
     }
 }
 
@@ -688,6 +746,27 @@ __global__ void cell_occ_kernel(DGrid G, uint32_t *words, int64_t nwords, int64_
     words[w] = bits;
 }
 
+// neg_bits word w: bit b set iff lattice point 32w+b is occupied with sigma < 0.
+__global__ void neg_bits_kernel(DGrid G, uint32_t *words, int64_t nwords, int64_t ncell) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= nwords) return;
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; ++b) {
+        const int64_t c = w * 32 + b;
+        if (c >= ncell) break;
+        const int32_t r = G.links[c];
+        if (r >= 0 && G.density[r] < 0.f) bits |= 1u << b;
+    }
+    words[w] = bits;
+}
+
+__global__ void row_cell_kernel(const int32_t *links, int64_t ncell, int32_t *row_cell) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncell) return;
+    const int32_t r = links[c];
+    if (r >= 0) row_cell[r] = (int32_t)c;
+}
+
 }  // namespace plx
 
 using namespace plx;
@@ -735,23 +814,24 @@ extern "C" int plx_tv(const plx_grid *g, const int64_t *cells, int64_t start, in
 
 extern "C" int plx_opt_step(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, double lr_sh,
                             double beta, double eps, int32_t rmsprop, int32_t clear,
-                            int64_t *out_count, void *stream) {
+                            double *guard, int64_t *out_count, void *stream) {
     if (!g || !gb || !gb->grad || !gb->tmask || (rmsprop && !v) ||
         (g->rows > 0 && (!g->table || !g->density)))
         return PLX_EINVAL;
     if ((gb->tids == nullptr) != (gb->tcnt == nullptr)) return PLX_EINVAL;
     if (g->rows == 0) return PLX_OK;
-    OptArgs a{g->table, g->density, v, gb->grad, gb->tmask, g->rows, lr_sigma, lr_sh, beta, eps,
-              rmsprop, clear, 1, reinterpret_cast<unsigned long long *>(out_count)};
+    if (g->neg_bits && !g->row_cell) return PLX_EINVAL;
+    OptArgs a{g->table, g->density, v, gb->grad, guard, g->neg_bits, g->row_cell, gb->tmask, g->rows,
+              lr_sigma, lr_sh, beta, eps, rmsprop, clear, 1, reinterpret_cast<unsigned long long *>(out_count)};
     constexpr int NT = 256;
     cudaStream_t s = (cudaStream_t)stream;
     if (gb->tids) {   // two-phase: compact the touched set, then update the list
         if (cudaMemsetAsync(gb->tcnt, 0, sizeof(int64_t), s) != cudaSuccess) return PLX_ECUDA;
         const int64_t nrange = ((g->rows + 127) / 128 + kCompactSegs - 1) / kCompactSegs;
         int64_t nb = (nrange + NT / 32 - 1) / (NT / 32);
-        if (nb > (int64_t)num_sms() * 8) nb = (int64_t)num_sms() * 8;
+        if (nb > (int64_t)num_sms() * 6) nb = (int64_t)num_sms() * 6;
         touched_compact_kernel<<<(unsigned)nb, NT, 0, s>>>(gb->tmask, g->rows, gb->tids, gb->tcnt,
-                                                          clear);
+                                                          clear, guard);
         static int nbr = 0;
         if (!nbr) {
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbr, opt_rows_kernel, NT, 0);
@@ -770,7 +850,8 @@ extern "C" int plx_opt_step(plx_grid *g, float *v, plx_grad *gb, double lr_sigma
 extern "C" int plx_clear_grad(plx_grad *gb, int64_t rows, int64_t *out_count, void *stream) {
     if (!gb || !gb->grad || !gb->tmask || rows < 0) return PLX_EINVAL;
     if (rows == 0) return PLX_OK;
-    OptArgs a{nullptr, nullptr, nullptr, gb->grad, gb->tmask, rows, 0.0, 0.0, 0.0, 0.0, 0, 1, 0,
+    OptArgs a{nullptr, nullptr, nullptr, gb->grad, nullptr, nullptr, nullptr, gb->tmask, rows, 0.0, 0.0,
+              0.0, 0.0, 0, 1, 0,
               reinterpret_cast<unsigned long long *>(out_count)};
     constexpr int NT = 256;
     const int64_t segs = (rows + 127) / 128;
@@ -875,6 +956,20 @@ extern "C" int plx_build_cell_occ(const plx_grid *g, uint32_t *cell_occ, void *s
     if (!grid_ok(g) || !cell_occ) return PLX_EINVAL;
     const int64_t n = ncell(g), nw = (n + 31) / 32;
     cell_occ_kernel<<<blocks(nw, 256), 256, 0, (cudaStream_t)stream>>>(make_dgrid(*g), cell_occ, nw, n);
+    return status();
+}
+
+extern "C" int plx_build_neg_bits(const plx_grid *g, uint32_t *neg_bits, void *stream) {
+    if (!grid_ok(g) || !neg_bits) return PLX_EINVAL;
+    const int64_t n = ncell(g), nw = (n + 31) / 32;
+    neg_bits_kernel<<<blocks(nw, 256), 256, 0, (cudaStream_t)stream>>>(make_dgrid(*g), neg_bits, nw, n);
+    return status();
+}
+
+extern "C" int plx_build_row_cell(const plx_grid *g, int32_t *row_cell, void *stream) {
+    if (!grid_ok(g) || !row_cell) return PLX_EINVAL;
+    const int64_t n = ncell(g);
+    row_cell_kernel<<<blocks(n, 256), 256, 0, (cudaStream_t)stream>>>(g->links, n, row_cell);
     return status();
 }
 

@@ -5,19 +5,24 @@
 // render_backward (K:241-411), max_weight_accum (K:414-453).
 //
 // Parallel decomposition (B200-first, not a translation of the sequential
-// loop): one warp per ray, one lane per march position.  A ray is walked in
-// chunks of 32 consecutive positions: every lane evaluates its own sample
-// (stencil through `links`, float64 trilinear sigma and SH colour from f32
-// rows gathered as float4), then the chunk is composited with warp scans
-// (product scan of exp(-sigma*delta) for "relative", sum scan of alpha for
-// "absolute"), early termination is a ballot on T < stop_thresh (T is
-// monotone, so the first such lane is the reference's break point).
+// loop): one warp per ray.  The march is walked in chunks of 32 consecutive
+// positions, one lane per position: stencil through `links`, float64
+// trilinear sigma from the density array, then the chunk is composited with
+// warp scans (product scan of exp(-sigma*delta) for "relative", sum scan of
+// alpha for "absolute"); early termination is a ballot on T < stop_thresh
+// (T is monotone, so the first such lane is the reference's break point).
 //
-// The backward replays the march a second time instead of storing per-sample
-// records: the reference's reverse suffix sum S_i = sum_{j>i} w_j c_j + T bg
-// equals (rgb - prefix_i) and is formed in float64, where the cancellation is
-// harmless (|error| ~ 1e-16 |rgb|).  Gradients are scattered with vector
-// f32 reductions (red.global.add.v4.f32, 7 per stencil row).
+// The fused backward (bwd_kernel) runs three phases per ray:
+//   A  sigma march + compositing over positions; each composited sample is
+//      appended to the warp's record list {att, T, w, cell, f, rows};
+//   B  colour over the DENSE sample list (32 samples per iteration, every
+//      lane busy): 8 SH rows gathered as float4, f32 FMAs, rgb = sum w c+;
+//   C  the reverse sweep over the dense list: suffix S_i = rgb - prefix_i
+//      (float64, |error| ~ 1e-16 |rgb|), dL/dsigma and dL/dc, and the
+//      lane-distributed scatter accumulator (LaneAcc) that reduces each
+//      touched gradient row once per ray visit with red.global.add.v4.f32.
+// Only ~1/8 of march positions are composited samples on the training
+// grids, so B and C iterate over samples, not positions.
 #include <stdlib.h>
 
 #include "plx_common.cuh"
@@ -60,8 +65,8 @@ struct Sample {
     bool incl;
 };
 
-// Evaluate position si (K:286-305): stencil, sigma, and for included samples
-// the colour.  FWD/MAXW include sigma > 0, BWD sigma >= 0 (K:211 vs K:293).
+// Evaluate position si for the forward render / max-weight (K:200-229):
+// stencil, sigma, and for included samples (sigma > 0, K:211) the colour.
 // Positions, stencil rows/weights, sigma and exp(-sigma delta) are float64
 // in the reference's operation order (bit-exact on f32 grids: the sample
 // set, the early stop and the touched rows match the reference exactly).
@@ -78,7 +83,8 @@ __device__ __forceinline__ void eval_sample(const DGrid &G, const RayMarch &rm, 
     sample_coords(rm, G, step, si, t, s.dlt, g);
     bool occ;
     constexpr int NQ = NEAREST ? 1 : 8;
-    stencil<NEAREST>(G, g, s.rows, s.f, occ);
+    int ijk[3];
+    stencil<NEAREST>(G, g, s.rows, s.f, occ, ijk);
     if (!occ) return;
     // _sigma_at (K:126-135): float64 sum over occupied corners in order.
     double sig = 0.0;
@@ -88,7 +94,7 @@ __device__ __forceinline__ void eval_sample(const DGrid &G, const RayMarch &rm, 
         if (r >= 0) sig += stencil_w<NEAREST>(s.f, q) * (double)__ldg(G.density + r);
     }
     s.sig = sig;
-    if (MODE == BWD ? !(sig >= 0.0) : !(sig > 0.0)) return;
+    if (!(sig > 0.0)) return;   // K:211 (render_forward / max_weight_accum)
     s.incl = true;
     s.att = exp(-sig * s.dlt);
     if (MODE == MAXW) return;
@@ -180,18 +186,22 @@ __device__ __forceinline__ void composite_chunk(bool &incl, double att, int lane
 
 __device__ __forceinline__ double relu(double x) { return x > 0.0 ? x : 0.0; }
 
-// Per-warp-slot scratch of the backward: pass 1 records, per included
-// sample, att (f64) and {c0, c1, c2} (f32), 24 B (+ sigma when the Cauchy
-// term is on) and, per
-// chunk, {first position, included-lane mask}; pass 2 replays the
-// compositing from these records instead of re-gathering the grid.
+// Per-warp-slot record list of the backward (SoA; capacity nrec = every
+// march position of the longest chord, R:67-69).  Phase A appends one
+// record per composited sample, B adds the colour, C consumes them.  These
+// replace the reference's per-call s_t / s_dlt / s_sig / s_T / s_w / s_cpre
+// scratch (K:259-264, R:277-278).
 struct Scratch {
     int *counter;      // dynamic ray scheduler (zeroed by the launcher)
-    double *rec_att;   // [slots][nrec]  exp(-sigma delta), float64 (replayed bit-exactly)
-    float4 *rec_c;     // [slots][nrec]  pre-clamp colour (f32, as computed)
-    double *rec_sig;   // [slots][nrec]
-    uint2 *meta;       // [slots][nchunk]
-    int64_t nrec, nchunk;
+    double *att;       // exp(-sigma delta)                 [slots][nrec]
+    double *T;         // transmittance before the sample
+    double *w;         // compositing weight
+    float4 *c;         // pre-clamp colour (phase B)
+    int4 *cell;        // {i, j, k, position index}
+    float4 *f;         // fractional offsets in the cell
+    int4 *rows;        // 8 stencil rows                     [slots][nrec][2]
+    double *sig;       // sigma (Cauchy term only)
+    int64_t nrec;
 };
 
 // Per-warp shared staging of one chunk's scatter payload (pass 2).  The
@@ -324,27 +334,16 @@ struct LaneAcc {
     }
 };
 
-template <int MODE, bool ABS, bool NEAREST, int MINB>
-__global__ void __launch_bounds__(128, MINB)
-    march_kernel(DGrid G, RayArgs R, KOpts O, Outs out, Scratch S) {
+// Forward render / max-weight: one pass over the positions (K:173-238,
+// K:414-453).  Static grid-stride over rays.
+template <int MODE, bool ABS, bool NEAREST>
+__global__ void __launch_bounds__(128, 6)
+    march_kernel(DGrid G, RayArgs R, KOpts O, Outs out) {
     const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int64_t slot = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    const int64_t slot = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int64_t nslots = (int64_t)gridDim.x * (blockDim.x >> 5);
-    double mse_part = 0.0, cau_part = 0.0;
     unsigned st_pos = 0, st_samp = 0, st_chunks = 0, st_rays = 0;   // warp-uniform
-    const unsigned lt_mask = (1u << lane) - 1u;
-    int64_t ray = slot;
-    __shared__ SmemChunk smem_all[MODE == BWD ? 4 : 1];
-    SmemChunk &sc = smem_all[MODE == BWD ? warp : 0];
-
-    for (;;) {
-        if (MODE == BWD) {   // dynamic scheduling: rays differ widely in length
-            int r = 0;
-            if (lane == 0) r = atomicAdd(S.counter, 1);
-            ray = __shfl_sync(PLX_FULL_MASK, r, 0);
-        }
-        if (ray >= R.n) break;
+    for (int64_t ray = slot; ray < R.n; ray += nslots) {
         ++st_rays;
         const int64_t src = R.idx ? R.idx[ray] : ray;
         RayMarch rm;
@@ -353,44 +352,33 @@ __global__ void __launch_bounds__(128, MINB)
             rm.o[a] = __ldg(R.origins + 3 * src + a);
             rm.d[a] = __ldg(R.dirs + 3 * src + a);
         }
-        float bf[9];   // SH basis (K:27-37) in float64, used as f32 by the colour FMAs
-        if (MODE != MAXW) {
+        float bf[9];
+        if (MODE == FWD) {
             double basis[9];
             sh_basis9(__ldg(R.viewdirs + 3 * src), __ldg(R.viewdirs + 3 * src + 1),
                       __ldg(R.viewdirs + 3 * src + 2), basis);
 #pragma unroll
             for (int b = 0; b < 9; ++b) bf[b] = (float)basis[b];
         }
-        const double jit = (MODE != MAXW && R.jitter) ? R.jitter[ray] : 0.0;
+        const double jit = (MODE == FWD && R.jitter) ? R.jitter[ray] : 0.0;
         ray_march_setup(rm, G, O.step, jit);
-
-        // ---------------- pass 1: forward ----------------
         double T = 1.0, A = 0.0, C0 = 0.0, C1 = 0.0, C2 = 0.0, wsum = 0.0;
-        double Q0 = 0.0, Q1 = 0.0, Q2 = 0.0;   // absolute backward: sum c(bn - bi)
-        int64_t nch = 0, nrec = 0;              // recorded chunks / samples
-        double *rec_att = S.rec_att + slot * S.nrec;
-        float4 *rec_c = S.rec_c + slot * S.nrec;
-        double *rec_sig = S.rec_sig + slot * S.nrec;
-        uint2 *meta = S.meta + slot * S.nchunk;
         bool stopped = false;
         for (int64_t base = 0; base < rm.nsamp && !stopped; base += 32) {
             Sample s;
             eval_sample<MODE, NEAREST>(G, rm, O.step, base + lane, bf, s);
             const int npos = (int)min((int64_t)32, rm.nsamp - base);
+            st_chunks += 1;
             if (!__any_sync(PLX_FULL_MASK, s.incl)) {
                 st_pos += npos;
-                st_chunks += 1;
                 continue;
             }
             double Ti, wi;
             composite_chunk<(MODE == MAXW ? false : ABS)>(s.incl, s.att, lane, O.stop, T, A, Ti,
                                                            wi, stopped);
-            {   // positions up to the early stop, samples that contribute
-                const unsigned im = __ballot_sync(PLX_FULL_MASK, s.incl);
-                st_pos += stopped ? 32 - __clz(im) : npos;
-                st_samp += __popc(im);
-                st_chunks += 1;
-            }
+            const unsigned im = __ballot_sync(PLX_FULL_MASK, s.incl);
+            st_pos += stopped ? 32 - __clz(im) : npos;
+            st_samp += __popc(im);
             if (MODE == MAXW) {
                 if (s.incl) {
                     double w = Ti * (1.0 - s.att);   // K:446
@@ -405,28 +393,199 @@ __global__ void __launch_bounds__(128, MINB)
                 }
                 continue;
             }
-            const double cr0 = relu((double)s.c[0]), cr1 = relu((double)s.c[1]),
-                         cr2 = relu((double)s.c[2]);
-            if (MODE == BWD) {   // record the chunk for pass 2
-                const unsigned m = __ballot_sync(PLX_FULL_MASK, s.incl);
-                if (lane == 0) meta[nch] = make_uint2((unsigned)base, m);
-                if (s.incl) {
-                    const int64_t k = nrec + __popc(m & lt_mask);
-                    rec_att[k] = s.att;
-                    rec_c[k] = make_float4(s.c[0], s.c[1], s.c[2], 0.f);
-                    if (out.lam_cauchy > 0.0) rec_sig[k] = s.sig;
-                }
-                ++nch;
-                nrec += __popc(m);
-            }
             double x0 = 0.0, x1 = 0.0, x2 = 0.0, xw = 0.0;
-            if (s.incl) {
+            if (s.incl) {   // K:224-229: only the positive part is accumulated
+                x0 = wi * relu((double)s.c[0]);
+                x1 = wi * relu((double)s.c[1]);
+                x2 = wi * relu((double)s.c[2]);
+                xw = wi;
+            }
+            C0 += warp_sum(x0);
+            C1 += warp_sum(x1);
+            C2 += warp_sum(x2);
+            wsum += warp_sum(xw);
+        }
+        if (MODE == FWD && lane == 0) {   // K:234-238
+            out.rgb[3 * ray + 0] = C0 + T * O.bg[0];
+            out.rgb[3 * ray + 1] = C1 + T * O.bg[1];
+            out.rgb[3 * ray + 2] = C2 + T * O.bg[2];
+            if (out.trans) out.trans[ray] = T;
+            if (out.wsum) out.wsum[ray] = wsum;
+        }
+    }
+    if (O.stats && lane == 0) {
+        atomicAdd(O.stats + 0, (unsigned long long)st_pos);
+        atomicAdd(O.stats + 1, (unsigned long long)st_samp);
+        atomicAdd(O.stats + 2, (unsigned long long)st_chunks);
+        atomicAdd(O.stats + 3, (unsigned long long)st_rays);
+    }
+}
+
+// The fused forward + MSE + backward (K:241-411), phases A / B / C above.
+template <bool ABS, bool NEAREST, int MINB>
+__global__ void __launch_bounds__(128, MINB)
+    bwd_kernel(DGrid G, RayArgs R, KOpts O, Outs out, Scratch S) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int64_t slot = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    double mse_part = 0.0, cau_part = 0.0;
+    unsigned st_pos = 0, st_samp = 0, st_chunks = 0, st_rays = 0;   // warp-uniform
+    const unsigned lt_mask = (1u << lane) - 1u;
+    __shared__ SmemChunk smem_all[4];
+    SmemChunk &sc = smem_all[warp];
+    const bool cauchy = out.lam_cauchy > 0.0;
+    double *const r_att = S.att + slot * S.nrec;
+    double *const r_T = S.T + slot * S.nrec;
+    double *const r_w = S.w + slot * S.nrec;
+    float4 *const r_c = S.c + slot * S.nrec;
+    int4 *const r_cell = S.cell + slot * S.nrec;
+    float4 *const r_f = S.f + slot * S.nrec;
+    int4 *const r_rows = S.rows + 2 * slot * S.nrec;
+    double *const r_sig = S.sig + slot * S.nrec;
+
+    for (;;) {
+        int rr = 0;   // dynamic scheduling: rays differ widely in length
+        if (lane == 0) rr = atomicAdd(S.counter, 1);
+        const int64_t ray = __shfl_sync(PLX_FULL_MASK, rr, 0);
+        if (ray >= R.n) break;
+        ++st_rays;
+        const int64_t src = R.idx ? R.idx[ray] : ray;
+        RayMarch rm;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            rm.o[a] = __ldg(R.origins + 3 * src + a);
+            rm.d[a] = __ldg(R.dirs + 3 * src + a);
+        }
+        const double jit = R.jitter ? R.jitter[ray] : 0.0;
+        ray_march_setup(rm, G, O.step, jit);
+
+        // ---------------- A: sigma march + compositing (K:285-323) ----------------
+        double T = 1.0, A = 0.0;
+        int ns = 0;   // composited samples (records)
+        bool stopped = false;
+        for (int64_t base = 0; base < rm.nsamp && !stopped; base += 32) {
+            const int64_t si = base + lane;
+            bool incl = false;
+            double att = 1.0, sig = 0.0, t, dlt, g[3], fd[3];
+            int32_t rows[8];
+            int ijk[3];
+            if (si < rm.nsamp) {
+                sample_coords(rm, G, O.step, si, t, dlt, g);
+                bool occ;
+                constexpr int NQ = NEAREST ? 1 : 8;
+                stencil<NEAREST>(G, g, rows, fd, occ, ijk);
+                if (occ) {   // _sigma_at (K:126-135), float64, reference order
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q)
+                        if (rows[q] >= 0)
+                            sig += stencil_w<NEAREST>(fd, q) * (double)__ldg(G.density + rows[q]);
+                    incl = sig >= 0.0;   // K:293: recorded unless sigma < 0
+                    if (incl) att = exp(-sig * dlt);
+                }
+            }
+            const int npos = (int)min((int64_t)32, rm.nsamp - base);
+            st_chunks += 1;
+            if (!__any_sync(PLX_FULL_MASK, incl)) {
+                st_pos += npos;
+                continue;
+            }
+            double Ti, wi;
+            composite_chunk<ABS>(incl, att, lane, O.stop, T, A, Ti, wi, stopped);
+            const unsigned m = __ballot_sync(PLX_FULL_MASK, incl);
+            st_pos += stopped ? 32 - __clz(m) : npos;
+            st_samp += __popc(m);
+            if (incl) {
+                const int k = ns + __popc(m & lt_mask);
+                r_att[k] = att;
+                r_T[k] = Ti;
+                r_w[k] = wi;
+                r_cell[k] = make_int4(ijk[0], ijk[1], ijk[2], (int)si);
+                if (!NEAREST) {
+                    r_f[k] = make_float4((float)fd[0], (float)fd[1], (float)fd[2], 0.f);
+                    r_rows[2 * k] = make_int4(rows[0], rows[1], rows[2], rows[3]);
+                    r_rows[2 * k + 1] = make_int4(rows[4], rows[5], rows[6], rows[7]);
+                } else {
+                    r_rows[2 * k] = make_int4(rows[0], -1, -1, -1);
+                }
+                if (cauchy) r_sig[k] = sig;
+            }
+            ns += __popc(m);
+        }
+
+        // ---------------- B: colour over the dense sample list (K:305-320) ----------------
+        float bf[9];   // SH basis (K:27-37) in float64, used as f32 by the colour FMAs
+        {
+            double basis[9];
+            sh_basis9(__ldg(R.viewdirs + 3 * src), __ldg(R.viewdirs + 3 * src + 1),
+                      __ldg(R.viewdirs + 3 * src + 2), basis);
+#pragma unroll
+            for (int b = 0; b < 9; ++b) bf[b] = (float)basis[b];
+        }
+        double C0 = 0.0, C1 = 0.0, C2 = 0.0;
+        double Q0 = 0.0, Q1 = 0.0, Q2 = 0.0;   // absolute backward: sum c(bn - bi)
+        __syncwarp();
+        for (int g0 = 0; g0 < ns; g0 += 32) {
+            const int j = g0 + lane;
+            double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+            if (j < ns) {
+                const int4 ra = r_rows[2 * j];
+                const int4 rb = NEAREST ? make_int4(-1, -1, -1, -1) : r_rows[2 * j + 1];
+                const int32_t rows[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+                float4 f4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (!NEAREST) f4 = r_f[j];
+                float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+                constexpr int NQ = NEAREST ? 1 : 8;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const int32_t r = rows[q];
+                    if (r < 0) continue;
+                    const float4 *row = reinterpret_cast<const float4 *>(G.table + (int64_t)r * PLX_ROW);
+                    const float4 v0 = __ldg(row + 0), v1 = __ldg(row + 1), v2 = __ldg(row + 2),
+                                 v3 = __ldg(row + 3), v4 = __ldg(row + 4), v5 = __ldg(row + 5),
+                                 v6 = __ldg(row + 6);
+                    // row layout: [-, R0..R8, G0..G8, B0..B8]  (_color_at, K:138-152)
+                    float a0 = bf[0] * v0.y, a1 = bf[0] * v2.z, a2 = bf[0] * v4.w;
+                    a0 = __fmaf_rn(bf[1], v0.z, a0);
+                    a1 = __fmaf_rn(bf[1], v2.w, a1);
+                    a2 = __fmaf_rn(bf[1], v5.x, a2);
+                    a0 = __fmaf_rn(bf[2], v0.w, a0);
+                    a1 = __fmaf_rn(bf[2], v3.x, a1);
+                    a2 = __fmaf_rn(bf[2], v5.y, a2);
+                    a0 = __fmaf_rn(bf[3], v1.x, a0);
+                    a1 = __fmaf_rn(bf[3], v3.y, a1);
+                    a2 = __fmaf_rn(bf[3], v5.z, a2);
+                    a0 = __fmaf_rn(bf[4], v1.y, a0);
+                    a1 = __fmaf_rn(bf[4], v3.z, a1);
+                    a2 = __fmaf_rn(bf[4], v5.w, a2);
+                    a0 = __fmaf_rn(bf[5], v1.z, a0);
+                    a1 = __fmaf_rn(bf[5], v3.w, a1);
+                    a2 = __fmaf_rn(bf[5], v6.x, a2);
+                    a0 = __fmaf_rn(bf[6], v1.w, a0);
+                    a1 = __fmaf_rn(bf[6], v4.x, a1);
+                    a2 = __fmaf_rn(bf[6], v6.y, a2);
+                    a0 = __fmaf_rn(bf[7], v2.x, a0);
+                    a1 = __fmaf_rn(bf[7], v4.y, a1);
+                    a2 = __fmaf_rn(bf[7], v6.z, a2);
+                    a0 = __fmaf_rn(bf[8], v2.y, a0);
+                    a1 = __fmaf_rn(bf[8], v4.z, a1);
+                    a2 = __fmaf_rn(bf[8], v6.w, a2);
+                    float w = 1.f;
+                    if (!NEAREST)
+                        w = ((q & 4) ? f4.x : 1.f - f4.x) * ((q & 2) ? f4.y : 1.f - f4.y) *
+                            ((q & 1) ? f4.z : 1.f - f4.z);
+                    c0 = __fmaf_rn(w, a0, c0);
+                    c1 = __fmaf_rn(w, a1, c1);
+                    c2 = __fmaf_rn(w, a2, c2);
+                }
+                r_c[j] = make_float4(c0, c1, c2, 0.f);
+                const double wi = r_w[j];
+                const double cr0 = relu((double)c0), cr1 = relu((double)c1), cr2 = relu((double)c2);
                 x0 = wi * cr0;
                 x1 = wi * cr1;
                 x2 = wi * cr2;
-                xw = wi;
-                if (MODE == BWD && ABS) {
-                    double bn = (Ti - wi) > 0.0 ? 1.0 : 0.0, bi = Ti > 0.0 ? 1.0 : 0.0;
+                if (ABS) {
+                    const double Ti = r_T[j];
+                    const double bn = (Ti - wi) > 0.0 ? 1.0 : 0.0, bi = Ti > 0.0 ? 1.0 : 0.0;
                     Q0 += cr0 * (bn - bi);
                     Q1 += cr1 * (bn - bi);
                     Q2 += cr2 * (bn - bi);
@@ -435,25 +594,12 @@ __global__ void __launch_bounds__(128, MINB)
             C0 += warp_sum(x0);
             C1 += warp_sum(x1);
             C2 += warp_sum(x2);
-            if (MODE == FWD) wsum += warp_sum(xw);
-        }
-        if (MODE == MAXW) {
-            ray += nslots;
-            continue;
         }
         const double rgb0 = C0 + T * O.bg[0], rgb1 = C1 + T * O.bg[1], rgb2 = C2 + T * O.bg[2];
         if (lane == 0 && out.rgb) {
             out.rgb[3 * ray + 0] = rgb0;
             out.rgb[3 * ray + 1] = rgb1;
             out.rgb[3 * ray + 2] = rgb2;
-        }
-        if (MODE == FWD) {
-            if (lane == 0) {
-                if (out.trans) out.trans[ray] = T;
-                if (out.wsum) out.wsum[ray] = wsum;
-            }
-            ray += nslots;
-            continue;
         }
         // ---------------- upstream (K:330-341) ----------------
         double up0, up1, up2;
@@ -475,48 +621,50 @@ __global__ void __launch_bounds__(128, MINB)
             Q1 = warp_sum(Q1);
             Q2 = warp_sum(Q2);
         }
-        // ---------------- pass 2: replay + transposed scatter ----------------
+
+        // ---------------- C: reverse sweep + scatter (K:343-410) ----------------
         // sf before sample i in the reference's reverse sweep:
         //   relative: T bg + sum_{j>i} w_j c_j = rgb - P_i      (K:351-353, 381-383)
         //   absolute: -bg [T>0] + sum_{j>i} c_j (bn_j - bi_j)   (K:346-349, 374-376)
         const double bend = T > 0.0 ? 1.0 : 0.0;
+        const double dlt_last = rm.L - O.step * (double)(rm.nsamp - 1);
         LaneAcc<NEAREST> ra;
         ra.init(lane, bf);
         double P0 = 0.0, P1 = 0.0, P2 = 0.0;
-        double T2 = 1.0, A2 = 0.0;
-        bool stopped2 = false;
-        int64_t k0 = 0;
-        // carried across chunks: last included sample's cell and the flip
-        int pci = 0, pcj = 0, pck = 0;
+        int pci = 0, pcj = 0, pck = 0;   // carried: previous sample's cell
         bool pvalid = false;
-        int cflip = 0;
-        for (int64_t c = 0; c < nch; ++c) {
-            const uint2 mt = meta[c];
-            const unsigned mask = mt.y;
-            const int64_t si = (int64_t)mt.x + lane;
-            bool incl = (mask >> lane) & 1u;
-            double att = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, sig = 0.0;
+        int cflip = 0;                   // carried corner relabelling
+        for (int g0 = 0; g0 < ns; g0 += 32) {
+            const int j = g0 + lane;
+            const bool incl = j < ns;
+            const unsigned mask = __ballot_sync(PLX_FULL_MASK, incl);
+            double att = 1.0, Ti = 0.0, wi = 0.0, sig = 0.0;
+            float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f), f4 = c4;
+            int4 cl = make_int4(0, 0, 0, 0);
             if (incl) {
-                const int64_t k = k0 + __popc(mask & lt_mask);
-                att = rec_att[k];
-                const float4 c4 = rec_c[k];
-                c0 = c4.x;
-                c1 = c4.y;
-                c2 = c4.z;
-                if (out.lam_cauchy > 0.0) sig = rec_sig[k];
+                att = r_att[j];
+                Ti = r_T[j];
+                wi = r_w[j];
+                c4 = r_c[j];
+                cl = r_cell[j];
+                if (!NEAREST) {
+                    f4 = r_f[j];
+                    *reinterpret_cast<int4 *>(&sc.rows[lane][0]) = r_rows[2 * j];
+                    *reinterpret_cast<int4 *>(&sc.rows[lane][4]) = r_rows[2 * j + 1];
+                } else {
+                    sc.rows[lane][0] = r_rows[2 * j].x;
+                }
+                if (cauchy) sig = r_sig[j];
             }
-            k0 += __popc(mask);
-            double Ti, wi;
-            composite_chunk<ABS>(incl, att, lane, O.stop, T2, A2, Ti, wi, stopped2);
-            const double cc0 = relu(c0), cc1 = relu(c1), cc2 = relu(c2);
-            double t, dlt, g[3];
-            sample_coords(rm, G, O.step, si, t, dlt, g);
+            const double dlt = cl.w < rm.nsamp - 1 ? O.step : dlt_last;   // K:200-205
+            const double cc0 = relu((double)c4.x), cc1 = relu((double)c4.y),
+                         cc2 = relu((double)c4.z);
             double gsig;
             if (!ABS) {
-                double y0 = incl ? wi * cc0 : 0.0, y1 = incl ? wi * cc1 : 0.0,
-                       y2 = incl ? wi * cc2 : 0.0;
-                double i0 = P0 + warp_scan_add(y0, lane), i1 = P1 + warp_scan_add(y1, lane),
-                       i2 = P2 + warp_scan_add(y2, lane);
+                const double y0 = incl ? wi * cc0 : 0.0, y1 = incl ? wi * cc1 : 0.0,
+                             y2 = incl ? wi * cc2 : 0.0;
+                const double i0 = P0 + warp_scan_add(y0, lane), i1 = P1 + warp_scan_add(y1, lane),
+                             i2 = P2 + warp_scan_add(y2, lane);
                 P0 = __shfl_sync(PLX_FULL_MASK, i0, 31);
                 P1 = __shfl_sync(PLX_FULL_MASK, i1, 31);
                 P2 = __shfl_sync(PLX_FULL_MASK, i2, 31);
@@ -526,10 +674,10 @@ __global__ void __launch_bounds__(128, MINB)
             } else {
                 const double Tn = Ti - wi;
                 const double bn = Tn > 0.0 ? 1.0 : 0.0, bi = Ti > 0.0 ? 1.0 : 0.0;
-                double y0 = incl ? cc0 * (bn - bi) : 0.0, y1 = incl ? cc1 * (bn - bi) : 0.0,
-                       y2 = incl ? cc2 * (bn - bi) : 0.0;
-                double i0 = P0 + warp_scan_add(y0, lane), i1 = P1 + warp_scan_add(y1, lane),
-                       i2 = P2 + warp_scan_add(y2, lane);
+                const double y0 = incl ? cc0 * (bn - bi) : 0.0, y1 = incl ? cc1 * (bn - bi) : 0.0,
+                             y2 = incl ? cc2 * (bn - bi) : 0.0;
+                const double i0 = P0 + warp_scan_add(y0, lane), i1 = P1 + warp_scan_add(y1, lane),
+                             i2 = P2 + warp_scan_add(y2, lane);
                 P0 = __shfl_sync(PLX_FULL_MASK, i0, 31);
                 P1 = __shfl_sync(PLX_FULL_MASK, i1, 31);
                 P2 = __shfl_sync(PLX_FULL_MASK, i2, 31);
@@ -540,56 +688,17 @@ __global__ void __launch_bounds__(128, MINB)
                     (up0 * (cc0 * bn + sf0) + up1 * (cc1 * bn + sf1) + up2 * (cc2 * bn + sf2));
                 gsig = galpha * dlt * att;
             }
-            if (incl && out.lam_cauchy > 0.0) {   // K:384-386
+            if (incl && cauchy) {   // K:384-386
                 cau_part += log(1.0 + 2.0 * sig * sig);
                 gsig += out.lam_cauchy * 4.0 * sig / (1.0 + 2.0 * sig * sig);
             }
             // ---- lane-parallel staging of the scatter payload (K:387-410) ----
-            // mask is already truncated at the early stop (pass 1)
-            int ci = 0, cj = 0, ck = 0;
-            float f0 = 0.f, f1 = 0.f, f2 = 0.f;
-            if (incl) {
-                if (NEAREST) {
-                    int64_t i = (int64_t)(g[0] + 0.5), j = (int64_t)(g[1] + 0.5), k = (int64_t)(g[2] + 0.5);
-                    if (i > G.Dx - 1) i = G.Dx - 1;
-                    if (j > G.Dy - 1) j = G.Dy - 1;
-                    if (k > G.Dz - 1) k = G.Dz - 1;
-                    ci = (int)i;
-                    cj = (int)j;
-                    ck = (int)k;
-                    sc.rows[lane][0] = __ldg(G.links + flat(G, i, j, k));
-                } else {
-                    int64_t i0 = (int64_t)g[0], j0 = (int64_t)g[1], kk0 = (int64_t)g[2];
-                    if (i0 > G.Dx - 2) i0 = G.Dx - 2;
-                    if (j0 > G.Dy - 2) j0 = G.Dy - 2;
-                    if (kk0 > G.Dz - 2) kk0 = G.Dz - 2;
-                    ci = (int)i0;
-                    cj = (int)j0;
-                    ck = (int)kk0;
-                    f0 = (float)(g[0] - (double)i0);
-                    f1 = (float)(g[1] - (double)j0);
-                    f2 = (float)(g[2] - (double)kk0);
-                    const int32_t *lb = G.links + flat(G, i0, j0, kk0);
-                    const int64_t sy = G.Dz, sx = (int64_t)G.Dy * G.Dz;
-                    int4 ra4, rb4;
-                    ra4.x = __ldg(lb);
-                    ra4.y = __ldg(lb + 1);
-                    ra4.z = __ldg(lb + sy);
-                    ra4.w = __ldg(lb + sy + 1);
-                    rb4.x = __ldg(lb + sx);
-                    rb4.y = __ldg(lb + sx + 1);
-                    rb4.z = __ldg(lb + sx + sy);
-                    rb4.w = __ldg(lb + sx + sy + 1);
-                    *reinterpret_cast<int4 *>(&sc.rows[lane][0]) = ra4;
-                    *reinterpret_cast<int4 *>(&sc.rows[lane][4]) = rb4;
-                }
-            }
-            // move code vs the previous included sample (this chunk or carried)
+            // move code vs the previous sample (this group or carried)
             const unsigned below = mask & lt_mask;
-            const int pl = below ? 31 - __clz(below) : lane;
-            const int qi = __shfl_sync(PLX_FULL_MASK, ci, pl);
-            const int qj = __shfl_sync(PLX_FULL_MASK, cj, pl);
-            const int qk = __shfl_sync(PLX_FULL_MASK, ck, pl);
+            const int pl = below ? lane - 1 : lane;   // the list is dense
+            const int qi = __shfl_sync(PLX_FULL_MASK, cl.x, pl);
+            const int qj = __shfl_sync(PLX_FULL_MASK, cl.y, pl);
+            const int qk = __shfl_sync(PLX_FULL_MASK, cl.z, pl);
             int mv = 0;
             if (incl) {
                 const bool hasp = below != 0u || pvalid;
@@ -597,7 +706,7 @@ __global__ void __launch_bounds__(128, MINB)
                 if (!hasp) {
                     mv = MV_FAR;
                 } else {
-                    const int di = ci - pi, dj = cj - pj, dk = ck - pk;
+                    const int di = cl.x - pi, dj = cl.y - pj, dk = cl.z - pk;
                     if (di | dj | dk) {
                         const bool adj = !NEAREST && di >= -1 && di <= 1 && dj >= -1 && dj <= 1 &&
                                          dk >= -1 && dk <= 1;
@@ -615,50 +724,45 @@ __global__ void __launch_bounds__(128, MINB)
             }
             const int fl = cflip ^ fx;
             if (incl) {
-                const float gk[4] = {(float)gsig, c0 > 0.0 ? (float)(up0 * wi) : 0.f,
-                                     c1 > 0.0 ? (float)(up1 * wi) : 0.f,
-                                     c2 > 0.0 ? (float)(up2 * wi) : 0.f};
+                const float gk[4] = {(float)gsig, c4.x > 0.f ? (float)(up0 * wi) : 0.f,
+                                     c4.y > 0.f ? (float)(up1 * wi) : 0.f,
+                                     c4.z > 0.f ? (float)(up2 * wi) : 0.f};
                 if (NEAREST) {
 #pragma unroll
                     for (int L = 0; L < 32; ++L) sc.val[L][lane] = L < 4 ? gk[L] : 0.f;
                 } else {
-                    float wq[8];
+                    // corner e = q ^ fl of physical slot q: xor-ing a bit of the
+                    // corner index swaps (1 - f, f) on that axis
+                    const float lx = (fl & 4) ? f4.x : 1.f - f4.x, hx = (fl & 4) ? 1.f - f4.x : f4.x;
+                    const float ly = (fl & 2) ? f4.y : 1.f - f4.y, hy = (fl & 2) ? 1.f - f4.y : f4.y;
+                    const float lz = (fl & 1) ? f4.z : 1.f - f4.z, hz = (fl & 1) ? 1.f - f4.z : f4.z;
 #pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        wq[e] = ((e & 4) ? f0 : 1.f - f0) * ((e & 2) ? f1 : 1.f - f1) *
-                                ((e & 1) ? f2 : 1.f - f2);
+                    for (int qs = 0; qs < 8; ++qs) {
+                        const float w = ((qs & 4) ? hx : lx) * ((qs & 2) ? hy : ly) *
+                                        ((qs & 1) ? hz : lz);
 #pragma unroll
-                    for (int L = 0; L < 32; ++L) {
-                        // lane L's corner is (L/4) ^ fl; select among the 8 weights
-                        const int e = (L >> 2) ^ fl;
-                        float w = wq[0];
-#pragma unroll
-                        for (int ee = 1; ee < 8; ++ee) w = e == ee ? wq[ee] : w;
-                        sc.val[L][lane] = w * gk[L & 3];
+                        for (int kk = 0; kk < 4; ++kk) sc.val[4 * qs + kk][lane] = w * gk[kk];
                     }
                 }
             }
-            // carry to the next chunk
-            const int hl = 31 - __clz(mask);   // mask != 0 for recorded chunks
+            // carry to the next group
+            const int hl = 31 - __clz(mask);
             cflip = __shfl_sync(PLX_FULL_MASK, fl, hl);
-            pci = __shfl_sync(PLX_FULL_MASK, ci, hl);
-            pcj = __shfl_sync(PLX_FULL_MASK, cj, hl);
-            pck = __shfl_sync(PLX_FULL_MASK, ck, hl);
+            pci = __shfl_sync(PLX_FULL_MASK, cl.x, hl);
+            pcj = __shfl_sync(PLX_FULL_MASK, cl.y, hl);
+            pck = __shfl_sync(PLX_FULL_MASK, cl.z, hl);
             pvalid = true;
             __syncwarp();
             // ---- serial, in sample order: moves (flushes) + one add ----
-            unsigned m = mask;
-            while (m) {
-                const int j = __ffs(m) - 1;
-                m &= m - 1;
-                const int mvj = sc.mv[j];
-                if (mvj) ra.move(mvj, sc, j, out.grad, out.tmask, lane);
-                ra.acc += sc.val[lane][j];
+            const int n = __popc(mask);
+            for (int jj = 0; jj < n; ++jj) {
+                const int mvj = sc.mv[jj];
+                if (mvj) ra.move(mvj, sc, jj, out.grad, out.tmask, lane);
+                ra.acc += sc.val[lane][jj];
             }
             __syncwarp();
         }
         ra.flush_all(out.grad, out.tmask, lane);
-        ray += nslots;
     }
     if (O.stats && lane == 0) {
         atomicAdd(O.stats + 0, (unsigned long long)st_pos);
@@ -666,12 +770,10 @@ __global__ void __launch_bounds__(128, MINB)
         atomicAdd(O.stats + 2, (unsigned long long)st_chunks);
         atomicAdd(O.stats + 3, (unsigned long long)st_rays);
     }
-    if (MODE == BWD) {   // one pair of f64 atomics per warp (no block barrier)
-        cau_part = warp_sum(cau_part);
-        if (lane == 0) {
-            if (mse_part != 0.0) atomicAdd(out.sums + 0, mse_part);
-            if (cau_part != 0.0) atomicAdd(out.sums + 1, cau_part);
-        }
+    cau_part = warp_sum(cau_part);   // one pair of f64 atomics per warp
+    if (lane == 0) {
+        if (mse_part != 0.0) atomicAdd(out.sums + 0, mse_part);
+        if (cau_part != 0.0) atomicAdd(out.sums + 1, cau_part);
     }
 }
 
@@ -686,8 +788,9 @@ constexpr int kWarps = kThreads / 32;
 
 bool grid_ok(const plx_grid *g) {
     return g && g->links && g->dims[0] >= 2 && g->dims[1] >= 2 && g->dims[2] >= 2 &&
-           (g->rows == 0 || (g->table && g->density)) && g->dims[0] < (1 << 21) && g->dims[1] < (1 << 21) &&
-           g->dims[2] < (1 << 21) && g->dims[0] * g->dims[1] * g->dims[2] < (int64_t)1 << 31;
+           (g->rows == 0 || (g->table && g->density)) && g->dims[0] < (1 << 21) &&
+           g->dims[1] < (1 << 21) && g->dims[2] < (1 << 21) &&
+           g->dims[0] * g->dims[1] * g->dims[2] < (int64_t)1 << 31;
 }
 
 int num_sms() {
@@ -702,23 +805,22 @@ int num_sms() {
 }
 
 // Minimum resident 128-thread blocks per SM the backward is compiled for:
-// 4 / 5 / 6 = register budget 128 / 96 / 80 per thread (16 / 20 / 24
-// warps per SM); PLX_BWD_MINB selects, default 4.
+// 4 / 5 = register budget 128 / 96 per thread (16 / 20 warps per SM);
+// PLX_BWD_MINB selects, default 4.
 int bwd_minb() {
     static int m = 0;
     if (!m) {
         const char *e = getenv("PLX_BWD_MINB");
-        const int v = e ? atoi(e) : 0;
-        m = (v == 5 || v == 6) ? v : 4;
+        m = (e && atoi(e) == 5) ? 5 : 4;
     }
     return m;
 }
 
-template <int MODE, bool ABS, bool NEAREST, int MINB>
-int blocks_per_sm() {
+template <bool ABS, bool NEAREST, int MINB>
+int bwd_blocks_per_sm_t() {
     static int nb = 0;
     if (!nb) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, march_kernel<MODE, ABS, NEAREST, MINB>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bwd_kernel<ABS, NEAREST, MINB>,
                                                       kThreads, 0);
         if (nb <= 0) nb = 1;
     }
@@ -726,31 +828,39 @@ int blocks_per_sm() {
 }
 
 template <int MINB>
-int bwd_blocks_per_sm_t(const plx_render_opts *o) {
+int bwd_blocks_per_sm_m(const plx_render_opts *o) {
     if (o->nearest)
-        return o->absolute ? blocks_per_sm<BWD, true, true, MINB>()
-                           : blocks_per_sm<BWD, false, true, MINB>();
-    return o->absolute ? blocks_per_sm<BWD, true, false, MINB>()
-                       : blocks_per_sm<BWD, false, false, MINB>();
+        return o->absolute ? bwd_blocks_per_sm_t<true, true, MINB>()
+                           : bwd_blocks_per_sm_t<false, true, MINB>();
+    return o->absolute ? bwd_blocks_per_sm_t<true, false, MINB>()
+                       : bwd_blocks_per_sm_t<false, false, MINB>();
 }
 
 int bwd_blocks_per_sm(const plx_render_opts *o) {
-    switch (bwd_minb()) {
-        case 5: return bwd_blocks_per_sm_t<5>(o);
-        case 6: return bwd_blocks_per_sm_t<6>(o);
-        default: return bwd_blocks_per_sm_t<4>(o);
+    return bwd_minb() == 5 ? bwd_blocks_per_sm_m<5>(o) : bwd_blocks_per_sm_m<4>(o);
+}
+
+template <int MINB>
+void launch_bwd(const plx_render_opts *o, dim3 grid, cudaStream_t s, DGrid G, RayArgs R, KOpts K,
+                Outs out, Scratch S) {
+    if (o->nearest) {
+        if (o->absolute) bwd_kernel<true, true, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
+        else bwd_kernel<false, true, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
+    } else {
+        if (o->absolute) bwd_kernel<true, false, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
+        else bwd_kernel<false, false, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
     }
 }
 
-template <int MODE, int MINB>
-void launch_variant(const plx_render_opts *o, bool ABSF, dim3 grid, cudaStream_t s, DGrid G,
-                    RayArgs R, KOpts K, Outs out, Scratch S) {
+template <int MODE>
+void launch_fwd(const plx_render_opts *o, bool ABSF, dim3 grid, cudaStream_t s, DGrid G,
+                RayArgs R, KOpts K, Outs out) {
     if (o->nearest) {
-        if (ABSF) march_kernel<MODE, true, true, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
-        else march_kernel<MODE, false, true, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
+        if (ABSF) march_kernel<MODE, true, true><<<grid, kThreads, 0, s>>>(G, R, K, out);
+        else march_kernel<MODE, false, true><<<grid, kThreads, 0, s>>>(G, R, K, out);
     } else {
-        if (ABSF) march_kernel<MODE, true, false, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
-        else march_kernel<MODE, false, false, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
+        if (ABSF) march_kernel<MODE, true, false><<<grid, kThreads, 0, s>>>(G, R, K, out);
+        else march_kernel<MODE, false, false><<<grid, kThreads, 0, s>>>(G, R, K, out);
     }
 }
 
@@ -762,7 +872,8 @@ int64_t max_records(const plx_grid *g, double step) {
 }
 
 struct ScratchLayout {
-    int64_t slots, nrec, nchunk, bytes, off_att, off_c, off_sig, off_meta;
+    int64_t slots, nrec, bytes;
+    int64_t off_att, off_T, off_w, off_c, off_cell, off_f, off_rows, off_sig;
 };
 
 ScratchLayout layout(const plx_grid *g, const plx_render_opts *o, int64_t n_rays) {
@@ -772,58 +883,49 @@ ScratchLayout layout(const plx_grid *g, const plx_render_opts *o, int64_t n_rays
     if (n_rays > 0 && need < blocks) blocks = need;
     L.slots = blocks * kWarps;
     L.nrec = max_records(g, o->step);
-    L.nchunk = L.nrec / 32 + 2;
-    L.off_att = 256;
-    L.off_c = L.off_att + L.slots * L.nrec * (int64_t)sizeof(double);
-    L.off_c = (L.off_c + 15) & ~(int64_t)15;
-    L.off_sig = L.off_c + L.slots * L.nrec * (int64_t)sizeof(float4);
-    L.off_meta = L.off_sig + L.slots * L.nrec * (int64_t)sizeof(double);
-    L.bytes = L.off_meta + L.slots * L.nchunk * (int64_t)sizeof(uint2);
+    const int64_t n = L.slots * L.nrec;
+    int64_t off = 256;
+    auto take = [&](int64_t bytes) {
+        const int64_t at = off;
+        off = (off + bytes + 255) & ~(int64_t)255;
+        return at;
+    };
+    L.off_att = take(n * 8);
+    L.off_T = take(n * 8);
+    L.off_w = take(n * 8);
+    L.off_c = take(n * 16);
+    L.off_cell = take(n * 16);
+    L.off_f = take(n * 16);
+    L.off_rows = take(n * 32);
+    L.off_sig = take(n * 8);
+    L.bytes = off;
     return L;
+}
+
+int check_rays(const plx_grid *g, const plx_rays *rays, const plx_render_opts *o, bool views) {
+    if (!grid_ok(g) || !rays || !o || rays->n < 0 || !rays->origins || !rays->dirs) return PLX_EINVAL;
+    if (rays->n >= (int64_t)1 << 31) return PLX_EINVAL;
+    if (views && !rays->viewdirs) return PLX_EINVAL;
+    if (!(o->step > 0.0)) return PLX_EINVAL;
+    return PLX_OK;
 }
 
 template <int MODE>
 int launch_march(const plx_grid *g, const plx_rays *rays, const plx_render_opts *o, Outs out,
-                 void *scratch, int64_t scratch_bytes, void *stream) {
-    if (!grid_ok(g) || !rays || !o || rays->n < 0 || !rays->origins || !rays->dirs) return PLX_EINVAL;
-    if (rays->n >= (int64_t)1 << 31) return PLX_EINVAL;
-    if (MODE != MAXW && !rays->viewdirs) return PLX_EINVAL;
-    if (MODE == BWD && (!rays->target || !out.grad || !out.tmask || !out.sums || !scratch))
-        return PLX_EINVAL;
-    if (!(o->step > 0.0)) return PLX_EINVAL;
+                 void *stream) {
+    const int rc = check_rays(g, rays, o, MODE == FWD);
+    if (rc != PLX_OK) return rc;
     if (rays->n == 0) return PLX_OK;
     DGrid G = make_dgrid(*g);
     RayArgs R{rays->origins, rays->dirs, rays->viewdirs, rays->target, rays->jitter, rays->idx,
               rays->n};
     KOpts K{o->step, o->stop_thresh, {o->bg[0], o->bg[1], o->bg[2]},
             reinterpret_cast<unsigned long long *>(o->stats)};
-    cudaStream_t s = (cudaStream_t)stream;
-    Scratch S{};
-    int64_t blocks;
-    if (MODE == BWD) {
-        const ScratchLayout L = layout(g, o, rays->n);
-        if (scratch_bytes < L.bytes) return PLX_EINVAL;
-        char *base = reinterpret_cast<char *>(scratch);
-        S.counter = reinterpret_cast<int *>(base);
-        S.rec_att = reinterpret_cast<double *>(base + L.off_att);
-        S.rec_c = reinterpret_cast<float4 *>(base + L.off_c);
-        S.rec_sig = reinterpret_cast<double *>(base + L.off_sig);
-        S.meta = reinterpret_cast<uint2 *>(base + L.off_meta);
-        S.nrec = L.nrec;
-        S.nchunk = L.nchunk;
-        blocks = L.slots / kWarps;
-        if (cudaMemsetAsync(S.counter, 0, sizeof(int), s) != cudaSuccess) return PLX_ECUDA;
-    } else {   // static grid-stride over rays, occupancy-sized grid
-        blocks = (rays->n + kWarps - 1) / kWarps;
-        const int64_t cap = (int64_t)num_sms() * 8;
-        if (blocks > cap) blocks = cap;
-    }
-    const bool ABSF = MODE != MAXW && o->absolute;
-    dim3 grid((unsigned)blocks);
-    if (MODE != BWD) launch_variant<MODE, 6>(o, ABSF, grid, s, G, R, K, out, S);
-    else if (bwd_minb() == 5) launch_variant<MODE, 5>(o, ABSF, grid, s, G, R, K, out, S);
-    else if (bwd_minb() == 6) launch_variant<MODE, 6>(o, ABSF, grid, s, G, R, K, out, S);
-    else launch_variant<MODE, 4>(o, ABSF, grid, s, G, R, K, out, S);
+    int64_t blocks = (rays->n + kWarps - 1) / kWarps;   // static grid-stride over rays
+    const int64_t cap = (int64_t)num_sms() * 12;
+    if (blocks > cap) blocks = cap;
+    launch_fwd<MODE>(o, MODE == FWD && o->absolute, dim3((unsigned)blocks), (cudaStream_t)stream,
+                     G, R, K, out);
     return cudaPeekAtLastError() == cudaSuccess ? PLX_OK : PLX_ECUDA;
 }
 
@@ -836,7 +938,7 @@ extern "C" int plx_render_fwd(const plx_grid *g, const plx_rays *rays, const plx
     out.rgb = out_rgb;
     out.trans = out_trans;
     out.wsum = out_wsum;
-    return launch_march<FWD>(g, rays, o, out, nullptr, 0, stream);
+    return launch_march<FWD>(g, rays, o, out, stream);
 }
 
 extern "C" int64_t plx_render_scratch_bytes(const plx_grid *g, const plx_render_opts *o,
@@ -850,7 +952,13 @@ extern "C" int plx_render_fused_bwd(const plx_grid *g, const plx_rays *rays,
                                     double lam_cauchy, plx_grad *gb, double *out_rgb,
                                     double *out_sums, void *scratch, int64_t scratch_bytes,
                                     void *stream) {
-    if (!gb) return PLX_EINVAL;
+    if (!gb || !gb->grad || !gb->tmask || !out_sums || !scratch) return PLX_EINVAL;
+    const int rc = check_rays(g, rays, o, true);
+    if (rc != PLX_OK) return rc;
+    if (!rays->target) return PLX_EINVAL;
+    if (rays->n == 0) return PLX_OK;
+    const ScratchLayout L = layout(g, o, rays->n);
+    if (scratch_bytes < L.bytes) return PLX_EINVAL;
     Outs out{};
     out.rgb = out_rgb;
     out.sums = out_sums;
@@ -859,7 +967,29 @@ extern "C" int plx_render_fused_bwd(const plx_grid *g, const plx_rays *rays,
     out.mse_mode = mse_mode;
     out.up_scale = up_scale;
     out.lam_cauchy = lam_cauchy;
-    return launch_march<BWD>(g, rays, o, out, scratch, scratch_bytes, stream);
+    DGrid G = make_dgrid(*g);
+    RayArgs R{rays->origins, rays->dirs, rays->viewdirs, rays->target, rays->jitter, rays->idx,
+              rays->n};
+    KOpts K{o->step, o->stop_thresh, {o->bg[0], o->bg[1], o->bg[2]},
+            reinterpret_cast<unsigned long long *>(o->stats)};
+    char *base = reinterpret_cast<char *>(scratch);
+    Scratch S;
+    S.counter = reinterpret_cast<int *>(base);
+    S.att = reinterpret_cast<double *>(base + L.off_att);
+    S.T = reinterpret_cast<double *>(base + L.off_T);
+    S.w = reinterpret_cast<double *>(base + L.off_w);
+    S.c = reinterpret_cast<float4 *>(base + L.off_c);
+    S.cell = reinterpret_cast<int4 *>(base + L.off_cell);
+    S.f = reinterpret_cast<float4 *>(base + L.off_f);
+    S.rows = reinterpret_cast<int4 *>(base + L.off_rows);
+    S.sig = reinterpret_cast<double *>(base + L.off_sig);
+    S.nrec = L.nrec;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemsetAsync(S.counter, 0, sizeof(int), s) != cudaSuccess) return PLX_ECUDA;
+    const dim3 grid((unsigned)(L.slots / kWarps));
+    if (bwd_minb() == 5) launch_bwd<5>(o, grid, s, G, R, K, out, S);
+    else launch_bwd<4>(o, grid, s, G, R, K, out, S);
+    return cudaPeekAtLastError() == cudaSuccess ? PLX_OK : PLX_ECUDA;
 }
 
 extern "C" int plx_max_weight(const plx_grid *g, const plx_rays *rays, const plx_render_opts *o,
@@ -867,5 +997,5 @@ extern "C" int plx_max_weight(const plx_grid *g, const plx_rays *rays, const plx
     if (!out_w) return PLX_EINVAL;
     Outs out{};
     out.maxw = out_w;
-    return launch_march<MAXW>(g, rays, o, out, nullptr, 0, stream);
+    return launch_march<MAXW>(g, rays, o, out, stream);
 }

@@ -131,6 +131,8 @@ class SparseGrid:
         if int(np.prod(self.dims)) >= 2 ** 31:
             raise ValueError("lattice too large for int32 cell ids")
         self._cell_occ = None
+        self._neg = None
+        self._row_cell = None
 
     # -- constructors -------------------------------------------------------
     @classmethod
@@ -144,6 +146,8 @@ class SparseGrid:
         g.aabb_min = np.asarray(aabb_min, dtype=np.float64).reshape(3).copy()
         g.aabb_max = np.asarray(aabb_max, dtype=np.float64).reshape(3).copy()
         g._cell_occ = None
+        g._neg = None
+        g._row_cell = None
         return g
 
     @classmethod
@@ -178,6 +182,8 @@ class SparseGrid:
     def links(self, value) -> None:
         self._links = torch.as_tensor(value).to(self._links.device, torch.int32).contiguous()
         self._cell_occ = None
+        self._neg = None
+        self._row_cell = None
 
     @property
     def table(self) -> torch.Tensor:
@@ -192,9 +198,19 @@ class SparseGrid:
         dev = self._links.device
         if t.dim() != 2 or t.shape[1] != ROW:
             raise ValueError(f"table must be (rows, {ROW})")
+        same_rows = hasattr(self, "density") and int(self.density.shape[0]) == int(t.shape[0])
+        if same_rows:   # in place: descriptors cached by callers stay valid
+            self.density.copy_(t[:, 0])
+            self.sh.copy_(t)
+            self.sh[:, 0] = 0.0
+            if getattr(self, "_neg", None) is not None:
+                self.invalidate()
+            return
         self.density = t[:, 0].to(device=dev, dtype=torch.float32).contiguous()
         self.sh = t.to(device=dev, dtype=torch.float32).clone().contiguous()
         self.sh[:, 0] = 0.0
+        self._neg = None
+        self._row_cell = None
 
     @property
     def device(self):
@@ -227,20 +243,54 @@ class SparseGrid:
         return self.aabb_min + np.asarray(ijk, dtype=np.float64) * self.voxel_size
 
     def invalidate(self) -> None:
-        """Call after editing `links` in place (drops the cell bitmask)."""
-        self._cell_occ = None
+        """Call after editing `links` or `density` in place: rebuilds the
+        derived bitmasks (cell occupancy, negative-density lattice points,
+        row -> cell map) in their existing buffers, so descriptors cached by
+        a caller stay valid."""
+        c = self._c(with_occ=False, with_neg=False)
+        L, s = _lib.lib(), _lib.stream_ptr()
+        if self._cell_occ is not None:
+            _lib.check(L.plx_build_cell_occ(ctypes.byref(c), self._cell_occ.data_ptr(), s),
+                       "build_cell_occ")
+        if self._row_cell is not None and self.n_rows:
+            _lib.check(L.plx_build_row_cell(ctypes.byref(c), self._row_cell.data_ptr(), s),
+                       "build_row_cell")
+        if self._neg is not None:
+            _lib.check(L.plx_build_neg_bits(ctypes.byref(c), self._neg.data_ptr(), s),
+                       "build_neg_bits")
 
     def cell_occ(self) -> torch.Tensor:
         if self._cell_occ is None:
             words = _lib.load().plx_cell_occ_words(_lib.dims_array(self.dims))
             occ = torch.empty(int(words), dtype=torch.int32, device=self.device)
-            c = self._c(with_occ=False)
+            c = self._c(with_occ=False, with_neg=False)
             _lib.check(_lib.lib().plx_build_cell_occ(ctypes.byref(c), occ.data_ptr(),
                                                      _lib.stream_ptr()), "build_cell_occ")
             self._cell_occ = occ
         return self._cell_occ
 
-    def _c(self, with_occ: bool = True) -> _lib.PlxGrid:
+    def neg_masks(self):
+        """(neg_bits, row_cell): lattice points occupied with density < 0 and
+        the row -> lattice point map.  Built on first use; from then on every
+        descriptor of this grid carries them, the march skips cells whose 8
+        corners are negative, and the optimiser keeps the bits current."""
+        if self._neg is None:
+            words = _lib.load().plx_cell_occ_words(_lib.dims_array(self.dims))
+            c = self._c(with_occ=False, with_neg=False)
+            L, s = _lib.lib(), _lib.stream_ptr()
+            rc = torch.empty(max(self.n_rows, 1), dtype=torch.int32, device=self.device)
+            if self.n_rows:
+                _lib.check(L.plx_build_row_cell(ctypes.byref(c), rc.data_ptr(), s),
+                           "build_row_cell")
+            neg = torch.empty(int(words), dtype=torch.int32, device=self.device)
+            _lib.check(L.plx_build_neg_bits(ctypes.byref(c), neg.data_ptr(), s), "build_neg_bits")
+            self._row_cell, self._neg = rc, neg
+        return self._neg, self._row_cell
+
+    def _c(self, with_occ: bool = True, with_neg: bool | None = None) -> _lib.PlxGrid:
+        """Kernel descriptor.  with_neg (default: with_occ) builds the
+        negative-density bitmask; once built it is always attached, so that
+        the optimiser keeps it current."""
         g = _lib.PlxGrid()
         g.links = self._links.data_ptr()
         g.table = self.sh.data_ptr() if self.n_rows else None
@@ -252,6 +302,12 @@ class SparseGrid:
         g.scale = (ctypes.c_double * 3)(*self.lattice_scale)
         g.dmax = (ctypes.c_double * 3)(*(np.array(self.dims, dtype=np.float64) - 1.0))
         g.cell_occ = self.cell_occ().data_ptr() if (with_occ and USE_CELL_OCC) else None
+        if with_neg is None:
+            with_neg = with_occ and USE_CELL_OCC
+        if (with_neg or self._neg is not None) and self.n_rows:
+            neg, rc = self.neg_masks()
+            g.neg_bits = neg.data_ptr()
+            g.row_cell = rc.data_ptr()
         return g
 
     def to_numpy(self):

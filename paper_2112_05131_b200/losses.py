@@ -69,7 +69,7 @@ def sample_tv_cells(grid: SparseGrid, fraction: float, rng) -> CellRun:
 def tv_loss(grid: SparseGrid, cells, lam_sigma: float, lam_sh: float,
             grads: GradientBuffer | None = None, eps: float = TV_EPS,
             wrap=(False, False, False), sums: torch.Tensor | None = None,
-            n_norm: int | None = None):
+            n_norm: int | None = None, _cgrid=None, _cgrad=None):
     """L:50-77 -> (lam_sigma * tv_sigma, lam_sh * tv_sh).
 
     With a device float64[2] `sums`, the raw (sigma_sum, sh_sum) are
@@ -89,8 +89,8 @@ def tv_loss(grid: SparseGrid, cells, lam_sigma: float, lam_sh: float,
     nn = int(n_norm) if n_norm is not None else n
     dev_sums = sums if sums is not None else torch.zeros(2, dtype=torch.float64,
                                                          device=grid.device)
-    gb = grads._c() if grads is not None else None
-    c_ = grid._c(with_occ=False)
+    gb = (_cgrad if _cgrad is not None else grads._c()) if grads is not None else None
+    c_ = _cgrid if _cgrid is not None else grid._c(with_occ=False)
     _lib.check(_lib.lib().plx_tv(
         ctypes.byref(c_), cptr, start, n, dims[0] / 256.0, dims[1] / 256.0, dims[2] / 256.0,
         float(eps), lam_sigma / nn, lam_sh / nn, int(wrap[0]), int(wrap[1]), int(wrap[2]),

@@ -269,7 +269,8 @@ def fused_mse_backward_pool(grid: SparseGrid, pool: RayPool, idx: torch.Tensor,
                             grads: GradientBuffer, opts: RenderOptions, n_total: int,
                             lam_cauchy: float, sums: torch.Tensor, jitter=None,
                             kopts: _lib.PlxRenderOpts | None = None,
-                            cgrid: _lib.PlxGrid | None = None) -> None:
+                            cgrid: _lib.PlxGrid | None = None,
+                            cgrad: _lib.PlxGrad | None = None) -> None:
     """The trainer's form of fused_mse_backward (R:253-279, T:455-457): batch =
     pool rows `idx` (device int64), sums (device f64[2]) accumulated, no sync."""
     r = pool.rays(idx)
@@ -277,7 +278,7 @@ def fused_mse_backward_pool(grid: SparseGrid, pool: RayPool, idx: torch.Tensor,
         r.jitter = jitter.data_ptr()
     c = cgrid if cgrid is not None else grid._c(with_occ=opts.interp == "trilinear")
     ko = kopts if kopts is not None else kernel_opts(grid, opts)
-    gb = grads._c()
+    gb = cgrad if cgrad is not None else grads._c()
     sp, sn, _keep = _lib.render_scratch(c, ko, r.n, grid.device)
     _lib.check(_lib.lib().plx_render_fused_bwd(
         ctypes.byref(c), ctypes.byref(r), ctypes.byref(ko), 1, 2.0 / n_total, float(lam_cauchy),

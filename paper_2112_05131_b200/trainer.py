@@ -275,16 +275,23 @@ class Trainer:
                                          formula=cfg.formula, jitter=cfg.jitter)
         self.batcher = EpochBatcher(self.pool.n, cfg.batch_size, self.rng, self.device)
         self.rung_events = {r.step: tuple(r.dims) for r in cfg.ladder[1:]}
-        self.sums = torch.zeros(4, dtype=torch.float64, device=self.device)
+        # {mse_sum, cauchy_sum, tv_sigma_sum, tv_sh_sum, halt}: the loss sums of
+        # the current step and the sticky divergence flag of the device guard
+        self.sums = torch.zeros(5, dtype=torch.float64, device=self.device)
         self.count = torch.zeros(1, dtype=torch.int64, device=self.device)
         # march counters of the fused kernel, accumulated over steps:
         # {positions, samples, chunks, rays} (plx_render_opts.stats)
         self.march_stats = torch.zeros(4, dtype=torch.int64, device=self.device)
-        self._host_sums = torch.zeros(4, dtype=torch.float64).pin_memory()
+        self._host_sums = [torch.zeros(4, dtype=torch.float64).pin_memory() for _ in range(2)]
+        self._sums_ready = [torch.cuda.Event(), torch.cuda.Event()]
+        self._pending = None
+        self.diverged_step = None
         self._refresh_cache()
 
     def _refresh_cache(self):
         self._cgrid = self.grid._c(with_occ=self.opts.interp == "trilinear")
+        self._cgrid_plain = self.grid._c(with_occ=False)
+        self._cgrad = self.grads._c()
         self._kopts = render.kernel_opts(self.grid, self.opts)
         self._kopts.stats = self.march_stats.data_ptr()
 
@@ -320,7 +327,17 @@ class Trainer:
         return w
 
     # -- one optimisation step (T:441-492) ------------------------------------
-    def step(self, step: int, check_finite: bool = True) -> dict:
+    def step(self, step: int, check_finite: bool = True, sync: bool = False) -> dict:
+        """One step: batch, fused render+backward, TV, (exchange), update.
+
+        The divergence check (T:473-480) runs on the device: plx_opt_step is
+        handed the step's loss sums and skips the update (stickily) when one
+        is non-finite, so the grid is left exactly as the reference leaves it
+        when it raises.  The host learns of it one step later: each call
+        checks the PREVIOUS step's sums (copied asynchronously), so the host
+        never waits for the step it just enqueued and the GPU never idles
+        between steps.  sync=True (logging steps) waits for this step's loss
+        and returns it in the record."""
         cfg = self.cfg
         idx = self.batcher.next_device()
         B = int(idx.numel())
@@ -328,11 +345,12 @@ class Trainer:
         if self.opts.jitter > 0:
             jt = torch.from_numpy(self.rng.random(B) * self.opts.jitter).to(self.device)
         s0, c0 = shard_range(B, self.world.rank, self.world.size)
-        self.sums.zero_()
+        self.sums[0:4].zero_()
         render.fused_mse_backward_pool(
             self.grid, self.pool, idx[s0:s0 + c0], self.grads, self.opts, n_total=B,
             lam_cauchy=cfg.lambda_sparsity, sums=self.sums[0:2],
-            jitter=None if jt is None else jt[s0:s0 + c0], kopts=self._kopts, cgrid=self._cgrid)
+            jitter=None if jt is None else jt[s0:s0 + c0], kopts=self._kopts, cgrid=self._cgrid,
+            cgrad=self._cgrad)
         tv_on = (cfg.lambda_tv_sigma > 0 or cfg.lambda_tv_sh > 0) and (
             cfg.tv_until_step < 0 or step < cfg.tv_until_step)
         n_tv = 0
@@ -342,26 +360,47 @@ class Trainer:
             sub = run.split(self.world.rank, self.world.size)
             if sub.count:
                 losses.tv_loss(self.grid, sub, cfg.lambda_tv_sigma, cfg.lambda_tv_sh,
-                               self.grads, sums=self.sums[2:4], n_norm=n_tv)
+                               self.grads, sums=self.sums[2:4], n_norm=n_tv,
+                               _cgrid=self._cgrid_plain, _cgrad=self._cgrad)
         reduce_gradients(self.world, self.grads.data, self.grads.touched_mask, self.sums)
-        rec = {"B": B, "n_tv": n_tv}
-        if check_finite:
-            self._host_sums.copy_(self.sums, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            mse_sum, cauchy_raw, tv_s, tv_h = (float(x) for x in self._host_sums)
-            loss_mse = mse_sum / B
-            tv_sig = cfg.lambda_tv_sigma * tv_s / n_tv if n_tv else 0.0
-            tv_sh = cfg.lambda_tv_sh * tv_h / n_tv if n_tv else 0.0
-            loss = loss_mse + tv_sig + tv_sh + cfg.lambda_sparsity * cauchy_raw
-            if not math.isfinite(loss):
-                raise TrainingDiverged(f"non-finite loss at step {step}: mse={loss_mse!r} "
-                                       f"tv=({tv_sig!r}, {tv_sh!r})")
-            rec.update(loss=loss, mse=loss_mse)
+        slot = step & 1
+        self._host_sums[slot].copy_(self.sums[0:4], non_blocking=True)
+        self._sums_ready[slot].record()
         self.count.zero_()
         optim.step(self.grid, self.grads, self.state, optim.lr_at(cfg.lr_sigma, step),
                    optim.lr_at(cfg.lr_sh, step), cfg.optimizer, clear=True,
-                   count_out=self.count)
+                   count_out=self.count, guard=self.sums, _cgrid=self._cgrid,
+                   _cgrad=self._cgrad)
+        rec = {"B": B, "n_tv": n_tv}
+        if sync:
+            self.check_pending()
+            self._sums_ready[slot].synchronize()
+            rec.update(self._loss(step, slot, B, n_tv))
+        elif check_finite:
+            self.check_pending()
+            self._pending = (step, slot, B, n_tv)
         return rec
+
+    def _loss(self, step, slot, B, n_tv) -> dict:
+        cfg = self.cfg
+        mse_sum, cauchy_raw, tv_s, tv_h = (float(x) for x in self._host_sums[slot])
+        loss_mse = mse_sum / B
+        tv_sig = cfg.lambda_tv_sigma * tv_s / n_tv if n_tv else 0.0
+        tv_sh = cfg.lambda_tv_sh * tv_h / n_tv if n_tv else 0.0
+        loss = loss_mse + tv_sig + tv_sh + cfg.lambda_sparsity * cauchy_raw
+        if not math.isfinite(loss):
+            self.diverged_step = step
+            raise TrainingDiverged(f"non-finite loss at step {step}: mse={loss_mse!r} "
+                                   f"tv=({tv_sig!r}, {tv_sh!r})")
+        return {"loss": loss, "mse": loss_mse}
+
+    def check_pending(self) -> None:
+        """Check the loss of the last unchecked step (waits for that step only)."""
+        if self._pending is not None:
+            step, slot, B, n_tv = self._pending
+            self._pending = None
+            self._sums_ready[slot].synchronize()
+            self._loss(step, slot, B, n_tv)
 
     def nnz_fraction(self) -> float:
         """GradientBuffer.nnz_fraction of the last step (counted by the opt kernel)."""
@@ -418,13 +457,16 @@ def train(train_ds, config: TrainConfig, test_ds=None, out_dir=None, metrics_sin
     for step in range(cfg.total_steps):
         if step in tr.rung_events:
             tr.rung_event(tr.rung_events[step], out_dir, step)
+        log_now = cfg.log_every > 0 and step % cfg.log_every == 0
         try:
-            rec = tr.step(step)
+            rec = tr.step(step, sync=log_now)
+            if step == cfg.total_steps - 1:
+                tr.check_pending()
         except TrainingDiverged:
-            if out_dir is not None:
+            if out_dir is not None:   # the device guard kept the pre-update grid
                 artifact_io.save_grid(tr.grid, out_dir / "diverged.plnx")
             raise
-        if cfg.log_every > 0 and step % cfg.log_every == 0:
+        if log_now:
             emit({"step": step, "loss": rec["loss"], "mse": rec["mse"],
                   "nnz_fraction": tr.nnz_fraction()})
         if test_ds is not None and cfg.eval_every > 0 and (step + 1) % cfg.eval_every == 0:

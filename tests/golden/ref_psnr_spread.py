@@ -12,9 +12,12 @@ only) several times:
   stock    : as published (expect 34.64);
   f32      : table and RMSProp state rounded to float32 after every
              optimiser step (our storage precision), init perturbed by a
-             random +-1 f32 ulp per value with seeds 1..K.
+             random +-1 f32 ulp per value with seeds 1..K;
+  REF_GRAD_F32=1: additionally the gradients rounded to float32 before each
+             update (-> psnr_spread_grad32.json).
 Writes tests/golden/psnr_spread.json.  Usage: python ref_psnr_spread.py K
-(runs K+1 trainings in parallel processes, ~4 min each on one core)."""
+[FIRST] (runs the stock run plus seeds FIRST..FIRST+K-1 in parallel
+processes, ~4 min each on one core; seeds already in the file are kept)."""
 import json
 import os
 import sys
@@ -26,6 +29,9 @@ sys.path.insert(0, "/root/reference/pkg/src")
 OUT = Path(__file__).resolve().parent
 
 
+GRAD32 = os.environ.get("REF_GRAD_F32") == "1"
+
+
 def run(seed):
     import numpy as np
     import plenoxel as px
@@ -35,6 +41,8 @@ def run(seed):
         orig_step = popt.step
 
         def step_f32(grid, grads, state, *a, **k):
+            if GRAD32:   # gradients as an f32 accumulator would hold them
+                grads.data[:] = grads.data.astype(np.float32)
             out = orig_step(grid, grads, state, *a, **k)
             grid.table[:] = grid.table.astype(np.float32)
             state.v[:] = state.v.astype(np.float32)
@@ -66,10 +74,22 @@ def run(seed):
 
 def main():
     k = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-    with ProcessPoolExecutor(max_workers=min(k + 1, os.cpu_count() or 1)) as ex:
-        res = dict(ex.map(run, range(k + 1)))
-    out = {"stock": res[0], "f32_perturbed": [res[s] for s in range(1, k + 1)]}
-    (OUT / "psnr_spread.json").write_text(json.dumps(out, indent=1))
+    first = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    path = OUT / ("psnr_spread_grad32.json" if GRAD32 else "psnr_spread.json")
+    old = json.loads(path.read_text()) if path.exists() else {}
+    seeds = list(range(first, first + k)) + ([] if "stock" in old else [0])
+    with ProcessPoolExecutor(max_workers=min(len(seeds), os.cpu_count() or 1)) as ex:
+        res = dict(ex.map(run, seeds))
+    per_seed = {int(s): v for s, v in old.get("f32_perturbed_by_seed", {}).items()}
+    if not per_seed and "f32_perturbed" in old:   # first format: seeds 1..n
+        per_seed = {i + 1: v for i, v in enumerate(old["f32_perturbed"])}
+    per_seed.update({s: v for s, v in res.items() if s > 0})
+    vals = [per_seed[s] for s in sorted(per_seed)]
+    out = {"stock": res.get(0, old.get("stock")),
+           "f32_perturbed_by_seed": {str(s): per_seed[s] for s in sorted(per_seed)},
+           "f32_perturbed_mean": sum(vals) / len(vals),
+           "f32_perturbed_min": min(vals), "f32_perturbed_max": max(vals)}
+    path.write_text(json.dumps(out, indent=1))
     print(out)
 
 

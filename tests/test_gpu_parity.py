@@ -376,3 +376,36 @@ def test_fused_backward_long_rays_vs_oracle(interp):
     gt = rng.uniform(0, 1, (200, 3))
     _check_bwd(g, o, d, gt, dict(step_frac=0.37, stop_thresh=1e-4,
                                  background=(0.2, 0.5, 0.9), interp=interp), lam=1e-4)
+
+
+def test_negative_density_bitmask_tracks_optimiser():
+    """neg_bits (lattice points occupied with density < 0) are kept current
+    by the optimiser as sigma changes sign, equal a from-scratch rebuild, and
+    the march with the dead-cell skip renders exactly like the march without."""
+    from paper_2112_05131_b200 import optim
+    rng = np.random.default_rng(17)
+    g = dev_grid(random_grid(rng, dims=(13, 11, 12), holes=0.25, sigma_range=(-1.0, 1.0)))
+    neg, _ = g.neg_masks()
+    st = px().OptimState(g.n_rows)
+    for it in range(4):
+        buf = px().GradientBuffer(g.n_rows)
+        rows = rng.permutation(g.n_rows)[: g.n_rows // 2]
+        buf.data[torch.as_tensor(rows).cuda(), 0] = torch.as_tensor(
+            rng.normal(size=len(rows)), dtype=torch.float32).cuda()
+        buf.touched_mask[torch.as_tensor(rows).cuda()] = 1
+        optim.step(g, buf, st, 0.5, 0.01, clear=True)
+        kept = neg.clone()
+        g.invalidate()                     # rebuild from scratch into the same buffer
+        assert torch.equal(kept, neg), it
+    o, d = ray_batch(rng, 128)
+    with_skip = px().render_rays(g, o, d, px().RenderOptions(stop_thresh=0.0))
+    from paper_2112_05131_b200 import grid as gmod
+    h = px().SparseGrid(g.links, g.table, g.aabb_min, g.aabb_max)   # fresh: no bitmasks
+    old = gmod.USE_CELL_OCC
+    gmod.USE_CELL_OCC = False
+    try:
+        plain = px().render_rays(h, o, d, px().RenderOptions(stop_thresh=0.0))
+    finally:
+        gmod.USE_CELL_OCC = old
+    for a, b in zip(with_skip, plain):
+        np.testing.assert_array_equal(a, b)
