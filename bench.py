@@ -235,7 +235,7 @@ def run_ours(args):
     if world_size > 1:
         dist.init_process_group("nccl", device_id=dev)
     from paper_2112_05131_b200 import losses, optim, render, trainer
-    from paper_2112_05131_b200.dist import World, reduce_gradients, shard_range
+    from paper_2112_05131_b200.dist import World, shard_range
 
     world = World(rank, world_size) if world_size > 1 else World()
     assert args.gpus == world_size, "--gpus must match the launched world size"
@@ -327,7 +327,6 @@ def run_ours(args):
         host.append([torch.from_numpy(np.ascontiguousarray(a[sel])).pin_memory()
                      for a in (o, m, v, gt)])
     dbuf = [torch.empty((B_local, 3), dtype=torch.float64, device=dev) for _ in range(4)]
-    sums = torch.zeros(4, dtype=torch.float64, device=dev)
     hsums = torch.zeros(4, dtype=torch.float64).pin_memory()
     h2d = 4 * B_local * 3 * 8
     d2h = 4 * 8
@@ -335,18 +334,16 @@ def run_ours(args):
     def e2e_step(step, hb):
         for dsti, src in zip(dbuf, hb):
             dsti.copy_(src, non_blocking=True)
-        sums.zero_()
+        tr.sums[0:4].zero_()
         render.fused_mse_backward(tr.grid, dbuf[0], dbuf[1], dbuf[2], dbuf[3], tr.grads, tr.opts,
-                                  n_total=B_local * world_size, sums=sums[0:2])
+                                  n_total=B_local * world_size, sums=tr.sums[0:2])
         run = losses.sample_tv_cells(tr.grid, cfg.tv_sample_frac, tr.rng)
         losses.tv_loss(tr.grid, run.split(rank, world_size), cfg.lambda_tv_sigma,
-                       cfg.lambda_tv_sh, tr.grads, sums=sums[2:4], n_norm=run.count)
-        reduce_gradients(world, tr.grads.data, tr.grads.touched_mask, sums)
-        hsums.copy_(sums, non_blocking=True)
+                       cfg.lambda_tv_sh, tr.grads, sums=tr.sums[2:4], n_norm=run.count)
+        tr.exchange_update(step)                 # (all-reduce of sums,) exchange, update
+        hsums.copy_(tr.sums[0:4], non_blocking=True)
         stream.synchronize()                      # the loss reaches the host every step
         assert np.isfinite(hsums.numpy()).all()
-        optim.step(tr.grid, tr.grads, tr.state, optim.lr_at(cfg.lr_sigma, step),
-                   optim.lr_at(cfg.lr_sh, step), clear=True)
 
     for i in range(W2):
         e2e_step(args.warmup - W2 + i, host[i])

@@ -158,6 +158,57 @@ int plx_opt_step(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, double lr
  * touched rows of gb->grad and reset gb->tmask.  out_count as above. */
 int plx_clear_grad(plx_grad *gb, int64_t rows, int64_t *out_count, void *stream);
 
+/* ---- data-parallel exchange (no reference counterpart: the
+ * reference is single-process, K:267 "for ri in range(nray)").  Rays shard
+ * across ranks, the grid is replicated, and the per-step gradient exchange +
+ * update replaces T:483-486 (optim.step + grads.clear) on every rank. ---- */
+
+/* Ordered (ascending) list of the set bytes of tmask[rows] -> ids[*count]
+ * (device), e.g. the union of the ranks' touched rows after an all_reduce
+ * MAX of the masks.  scratch: plx_scan_scratch_bytes(rows) bytes. */
+int plx_touched_list(const uint8_t *tmask, int64_t rows, int32_t *ids, int64_t *count,
+                     void *scratch, void *stream);
+/* dst[j] = src row ids[j] (28 floats) for j < *count (device); cap bounds
+ * the launch (rows). */
+int plx_pack_rows(const float *src, const int32_t *ids, const int64_t *count, int64_t cap,
+                  float *dst, void *stream);
+/* opt_step over the rows ids[0..*count): gradients from gpack[j] (packed,
+ * e.g. all-reduced) or, if gpack == NULL, from gb->grad rows; clear != 0
+ * zeroes gb->grad and gb->tmask of the listed rows.  guard / out_count as in
+ * plx_opt_step. */
+int plx_opt_step_list(plx_grid *g, float *v, plx_grad *gb, const int32_t *ids,
+                      const int64_t *count, const float *gpack, double lr_sigma, double lr_sh,
+                      double beta, double eps, int32_t rmsprop, int32_t clear, double *guard,
+                      int64_t *out_count, void *stream);
+
+/* The ranks' buffers as seen from this process (own ones local, the others
+ * CUDA-IPC-mapped peer memory over NVLink). */
+#define PLX_MAX_PEERS 8
+typedef struct {
+    int32_t n, rank;
+    int64_t rows;
+    float *grad[PLX_MAX_PEERS];        /* rows x 28 each */
+    uint8_t *tmask[PLX_MAX_PEERS];
+    float *table[PLX_MAX_PEERS];       /* SH rows (column 0 unused) */
+    float *density[PLX_MAX_PEERS];
+    uint32_t *neg_bits[PLX_MAX_PEERS]; /* may be NULL (no dead-cell mask) */
+} plx_dp_peers;
+/* Fused reduce + update + broadcast over peer memory: rank `rank` owns the
+ * 128-row-aligned slice [rows*rank/n, rows*(rank+1)/n); for every row of it
+ * touched on ANY rank it sums the n gradient rows (rank order), applies the
+ * update with its own RMSProp state v, and stores the new sigma / SH row
+ * (and neg bit) into all n grids.  Gradients and masks are NOT cleared
+ * (each rank clears its own with plx_clear_grad after all ranks finished:
+ * the caller orders the ranks with a collective before and after).
+ * out_count (local) accumulates the slice's union count. */
+int plx_dp_owner_update(const plx_dp_peers *p, float *v, const int32_t *row_cell,
+                        double lr_sigma, double lr_sh, double beta, double eps, int32_t rmsprop,
+                        double *guard, int64_t *out_count, void *stream);
+/* CUDA IPC of a device buffer that may sit inside a larger allocation. */
+int plx_ipc_export(const void *ptr, uint8_t handle[64], int64_t *offset);
+int plx_ipc_import(const uint8_t handle[64], int64_t offset, void **base_out, void **ptr_out);
+int plx_ipc_close(void *base);
+
 /* GradientBuffer.n_touched (G:42-44): out_count (device int64) = popcount. */
 int plx_count_touched(const uint8_t *tmask, int64_t rows, int64_t *out_count,
                       void *stream);

@@ -39,6 +39,16 @@ class PlxGrad(ctypes.Structure):
                 ("tids", ctypes.c_void_p), ("tcnt", ctypes.c_void_p)]
 
 
+MAX_PEERS = 8
+
+
+class PlxDpPeers(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("rank", ctypes.c_int32), ("rows", ctypes.c_int64),
+                ("grad", ctypes.c_void_p * MAX_PEERS), ("tmask", ctypes.c_void_p * MAX_PEERS),
+                ("table", ctypes.c_void_p * MAX_PEERS), ("density", ctypes.c_void_p * MAX_PEERS),
+                ("neg_bits", ctypes.c_void_p * MAX_PEERS)]
+
+
 class PlxRenderOpts(ctypes.Structure):
     _fields_ = [("step", ctypes.c_double), ("stop_thresh", ctypes.c_double),
                 ("bg", ctypes.c_double * 3), ("nearest", ctypes.c_int32),
@@ -73,6 +83,15 @@ _SIGS = {
                      _D, _I32, _I32, _P, _P, _P],
     "plx_clear_grad": [ctypes.POINTER(PlxGrad), _I64, _P, _P],
     "plx_count_touched": [_P, _I64, _P, _P],
+    "plx_touched_list": [_P, _I64, _P, _P, _P, _P],
+    "plx_pack_rows": [_P, _P, _P, _I64, _P, _P],
+    "plx_opt_step_list": [ctypes.POINTER(PlxGrid), _P, ctypes.POINTER(PlxGrad), _P, _P, _P, _D,
+                          _D, _D, _D, _I32, _I32, _P, _P, _P],
+    "plx_dp_owner_update": [ctypes.POINTER(PlxDpPeers), _P, _P, _D, _D, _D, _D, _I32, _P, _P,
+                            _P],
+    "plx_ipc_export": [_P, ctypes.c_char_p, ctypes.POINTER(_I64)],
+    "plx_ipc_import": [ctypes.c_char_p, _I64, ctypes.POINTER(_P), ctypes.POINTER(_P)],
+    "plx_ipc_close": [_P],
     "plx_prune_mark": [ctypes.POINTER(PlxGrid), _P, _D, _P, _P, _P],
     "plx_prune_apply": [ctypes.POINTER(PlxGrid), _P, _P, _P, _P, _P],
     "plx_upsample_mark": [ctypes.POINTER(PlxGrid), ctypes.POINTER(_I64), _P, _P],

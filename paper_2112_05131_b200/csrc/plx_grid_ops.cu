@@ -8,7 +8,7 @@
 // row access, one pass, grids sized in multiples of the 148 SMs.
 #include <cub/block/block_reduce.cuh>
 
-#include "plx_common.cuh"
+#include "plx_optim.cuh"
 
 namespace plx {
 
@@ -158,41 +158,6 @@ __device__ __forceinline__ int nonzero_bytes(uint32_t m) {
     return __popc(m);
 }
 
-// lr*g / (sqrt(nv) + eps) in float64 without the IEEE div/sqrt subroutines
-// (they were ~60 % of this kernel's instructions): MUFU reciprocal-sqrt and
-// reciprocal seeds, Newton steps with explicit FMAs, and one residual
-// correction each, so both the root and the quotient are within ~1 ulp of
-// float64.  The result is rounded to the f32 table afterwards, where it
-// equals the correctly rounded float64 path except at f32 rounding ties
-// (~2^-29 of values).  nv > 0 and sqrt(nv) + eps >= 1e-8 here (g != 0).
-__device__ __forceinline__ double rms_quot(double num, double nv, double eps) {
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(nv));
-    const double hn = 0.5 * nv;
-    y = y * fma(-hn * y, y, 1.5);
-    y = y * fma(-hn * y, y, 1.5);
-    double s = nv * y;
-    s = fma(0.5 * y, fma(-s, s, nv), s);   // sqrt(nv), corrected
-    const double den = s + eps;
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
-    r = r * fma(-den, r, 2.0);
-    r = r * fma(-den, r, 2.0);
-    double q = num * r;
-    q = fma(r, fma(-den, q, num), q);      // num / den, corrected
-    return q;
-}
-
-// Divergence guard (trainer.py T:473-480 on the device): guard[0..3] are
-// the step's loss sums, guard[4] a sticky halt flag.  True = skip the step.
-__device__ __forceinline__ bool guard_halts(double *guard) {
-    if (!guard) return false;
-    bool bad = guard[4] != 0.0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) bad |= !isfinite(guard[i]);
-    return bad;
-}
-
 // sigma of a row at lattice point c went from `before` to `after`: keep its
 // neg bit current.
 __device__ __forceinline__ void neg_update(const OptArgs &a, int32_t c, float before, float after) {
@@ -205,24 +170,7 @@ __device__ __forceinline__ void neg_update(const OptArgs &a, int32_t c, float be
 // The update of one float4 of one row (K:578-590), float64 arithmetic.
 __device__ __forceinline__ void opt_apply(const OptArgs &a, int quad, float4 &g4, float4 &t4,
                                           float4 &v4) {
-    float g[4] = {g4.x, g4.y, g4.z, g4.w};
-    float t[4] = {t4.x, t4.y, t4.z, t4.w};
-    float v[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        if (g[e] == 0.0f) continue;   // K:581-583: stale state
-        const double gd = (double)g[e];
-        const double lr = (quad == 0 && e == 0) ? a.lr_sigma : a.lr_sh;
-        if (a.rmsprop) {
-            const double nv = a.beta * (double)v[e] + (1.0 - a.beta) * gd * gd;
-            v[e] = (float)nv;
-            t[e] = (float)((double)t[e] - rms_quot(lr * gd, nv, a.eps));
-        } else {
-            t[e] = (float)((double)t[e] - lr * gd);
-        }
-    }
-    t4 = make_float4(t[0], t[1], t[2], t[3]);
-    v4 = make_float4(v[0], v[1], v[2], v[3]);
+    opt_apply4(OptHyper{a.lr_sigma, a.lr_sh, a.beta, a.eps, a.rmsprop}, quad, g4, t4, v4);
 }
 
 template <int NT>
@@ -726,6 +674,33 @@ __global__ void __launch_bounds__(kScanThreads) scan_write_kernel(const uint8_t 
     }
 }
 
+// Ordered variant: list[rank] = i for every flagged element (ascending).
+__global__ void __launch_bounds__(kScanThreads) scan_list_kernel(const uint8_t *flags, int64_t n,
+                                                                 const int64_t *partial,
+                                                                 int32_t *list) {
+    __shared__ int sh[kScanThreads];
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    uint8_t f[kScanItems];
+    int c = 0;
+#pragma unroll
+    for (int e = 0; e < kScanItems; ++e) {
+        f[e] = (base + e < n) ? flags[base + e] : 0;
+        c += f[e] != 0;
+    }
+    sh[threadIdx.x] = c;
+    __syncthreads();
+    for (int off = 1; off < kScanThreads; off <<= 1) {
+        int y = threadIdx.x >= (unsigned)off ? sh[threadIdx.x - off] : 0;
+        __syncthreads();
+        sh[threadIdx.x] += y;
+        __syncthreads();
+    }
+    int64_t id = partial[blockIdx.x] + sh[threadIdx.x] - c;
+#pragma unroll
+    for (int e = 0; e < kScanItems; ++e)
+        if (f[e]) list[id++] = (int32_t)(base + e);
+}
+
 // ---------------------------------------------------- cell bitmask --------
 __global__ void cell_occ_kernel(DGrid G, uint32_t *words, int64_t nwords, int64_t ncell) {
     const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -945,6 +920,22 @@ extern "C" int plx_scan_ids(const uint8_t *flags, int64_t n, int32_t *ids, int64
     scan_count_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(flags, n, partial);
     scan_partials_kernel<<<1, 1024, 0, s>>>(partial, nb, count);
     scan_write_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(flags, n, partial, ids);
+    return status();
+}
+
+extern "C" int plx_touched_list(const uint8_t *tmask, int64_t rows, int32_t *ids, int64_t *count,
+                                void *scratch, void *stream) {
+    if (!tmask || !ids || !count || !scratch || rows < 0) return PLX_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nb = (rows + kScanTile - 1) / kScanTile;
+    int64_t *partial = reinterpret_cast<int64_t *>(scratch);
+    if (nb == 0) {
+        cudaMemsetAsync(count, 0, sizeof(int64_t), s);
+        return status();
+    }
+    scan_count_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(tmask, rows, partial);
+    scan_partials_kernel<<<1, 1024, 0, s>>>(partial, nb, count);
+    scan_list_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(tmask, rows, partial, ids);
     return status();
 }
 

@@ -31,7 +31,11 @@ import yaml
 
 from . import _lib, artifact_io, losses, optim, render
 from .camera import all_rays
-from .dist import World, max_reduce, reduce_gradients, shard_range
+import ctypes
+
+import torch.distributed as dist
+
+from .dist import PeerMap, World, max_reduce, reduce_gradients, shard_range, union_rows
 from .grid import GradientBuffer, SparseGrid
 
 SCENE_TYPES = ("bounded", "forward_facing_ndc", "unbounded_360")
@@ -286,6 +290,8 @@ class Trainer:
         self._sums_ready = [torch.cuda.Event(), torch.cuda.Event()]
         self._pending = None
         self.diverged_step = None
+        self._peers = None
+        self._dp_pack = None
         self._refresh_cache()
 
     def _refresh_cache(self):
@@ -294,6 +300,19 @@ class Trainer:
         self._cgrad = self.grads._c()
         self._kopts = render.kernel_opts(self.grid, self.opts)
         self._kopts.stats = self.march_stats.data_ptr()
+        w = self.world
+        if w.active and w.mode == "union":
+            R = self.grid.n_rows
+            self._dp_ids = torch.empty(max(R, 1), dtype=torch.int32, device=self.device)
+            self._dp_cnt = torch.zeros(1, dtype=torch.int64, device=self.device)
+            self._dp_scratch = torch.empty(int(_lib.load().plx_scan_scratch_bytes(R)),
+                                           dtype=torch.uint8, device=self.device)
+        if w.active and w.mode == "p2p":
+            if self._peers is not None:
+                torch.cuda.synchronize()
+                self._peers.close()
+            self._peers = PeerMap(w, self.grid, self.grads)
+            self._cgrid = self.grid._c(with_occ=self.opts.interp == "trilinear")
 
     # -- ladder event (T:412-439) ---------------------------------------------
     def rung_event(self, new_dims, out_dir=None, step=0):
@@ -362,15 +381,8 @@ class Trainer:
                 losses.tv_loss(self.grid, sub, cfg.lambda_tv_sigma, cfg.lambda_tv_sh,
                                self.grads, sums=self.sums[2:4], n_norm=n_tv,
                                _cgrid=self._cgrid_plain, _cgrad=self._cgrad)
-        reduce_gradients(self.world, self.grads.data, self.grads.touched_mask, self.sums)
         slot = step & 1
-        self._host_sums[slot].copy_(self.sums[0:4], non_blocking=True)
-        self._sums_ready[slot].record()
-        self.count.zero_()
-        optim.step(self.grid, self.grads, self.state, optim.lr_at(cfg.lr_sigma, step),
-                   optim.lr_at(cfg.lr_sh, step), cfg.optimizer, clear=True,
-                   count_out=self.count, guard=self.sums, _cgrid=self._cgrid,
-                   _cgrad=self._cgrad)
+        self.exchange_update(step, slot)
         rec = {"B": B, "n_tv": n_tv}
         if sync:
             self.check_pending()
@@ -380,6 +392,54 @@ class Trainer:
             self.check_pending()
             self._pending = (step, slot, B, n_tv)
         return rec
+
+    def exchange_update(self, step: int, slot: int | None = None) -> None:
+        """After the ranks' renders + TV: reduce the loss sums, exchange the
+        touched rows' gradients (World.mode, dist.py) and apply the update
+        with the fused clear (T:483-486).  The loss sums are copied to the
+        pinned slot `slot` for the asynchronous divergence check."""
+        cfg, w = self.cfg, self.world
+        lr_s, lr_c = optim.lr_at(cfg.lr_sigma, step), optim.lr_at(cfg.lr_sh, step)
+        if w.active:
+            dist.all_reduce(self.sums[0:4], group=w.group)
+        if slot is not None:
+            self._host_sums[slot].copy_(self.sums[0:4], non_blocking=True)
+            self._sums_ready[slot].record()
+        self.count.zero_()
+        if not w.active or w.mode == "dense":
+            reduce_gradients(w, self.grads.data, self.grads.touched_mask)
+            optim.step(self.grid, self.grads, self.state, lr_s, lr_c, cfg.optimizer, clear=True,
+                       count_out=self.count, guard=self.sums, _cgrid=self._cgrid,
+                       _cgrad=self._cgrad)
+            return
+        L, st = _lib.lib(), _lib.stream_ptr()
+        rms = int(cfg.optimizer == "rmsprop")
+        if w.mode == "union":
+            n = union_rows(w, self.grads.touched_mask, self._dp_scratch, self._dp_ids,
+                           self._dp_cnt)
+            if n == 0:
+                return
+            if self._dp_pack is None or self._dp_pack.numel() < n * 28:
+                self._dp_pack = torch.empty(int(n * 1.25) * 28, dtype=torch.float32,
+                                            device=self.device)
+            _lib.check(L.plx_pack_rows(self.grads.data.data_ptr(), self._dp_ids.data_ptr(),
+                                       self._dp_cnt.data_ptr(), n, self._dp_pack.data_ptr(),
+                                       st), "pack_rows")
+            dist.all_reduce(self._dp_pack[:n * 28], group=w.group)
+            _lib.check(L.plx_opt_step_list(
+                ctypes.byref(self._cgrid), self.state.v.data_ptr(), ctypes.byref(self._cgrad),
+                self._dp_ids.data_ptr(), self._dp_cnt.data_ptr(), self._dp_pack.data_ptr(),
+                lr_s, lr_c, self.state.beta, self.state.eps, rms, 1, self.sums.data_ptr(),
+                self.count.data_ptr(), st), "opt_step_list")
+            return
+        # p2p: owner-computes update over NVLink peer memory, then local clear
+        rc = self.grid.neg_masks()[1]
+        _lib.check(L.plx_dp_owner_update(
+            ctypes.byref(self._peers.peers), self.state.v.data_ptr(), rc.data_ptr(), lr_s, lr_c,
+            self.state.beta, self.state.eps, rms, self.sums.data_ptr(), self.count.data_ptr(),
+            st), "dp_owner_update")
+        dist.all_reduce(self.count, group=w.group)   # orders every owner before any clear
+        self.grads.clear()
 
     def _loss(self, step, slot, B, n_tv) -> dict:
         cfg = self.cfg

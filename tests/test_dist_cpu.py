@@ -91,3 +91,14 @@ def test_two_rank_gradient_exchange_equals_full_batch():
     assert np.all(np.abs(grad - full.data) <= 1e-6 * np.abs(full.data) + 1e-6 * scale)
     assert sums[0] == np.float64(mse) or abs(sums[0] - mse) < 1e-12 * abs(mse)
     assert abs(sums[1] - a) < 1e-9 * abs(a) and abs(sums[2] - b) < 1e-9 * abs(b)
+
+
+def test_owner_slices_tile_the_rows():
+    """p2p mode: the owners' 128-row-aligned slices partition [0, rows)."""
+    from paper_2112_05131_b200.dist import owner_slice
+    for rows in (1, 127, 128, 129, 5000, 16777216, 18680476):
+        for n in (1, 2, 3, 4, 8):
+            spans = [owner_slice(rows, r, n) for r in range(n)]
+            assert spans[0][0] == 0 and spans[-1][1] == rows
+            for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+                assert a1 == b0 and a0 % 128 == 0
