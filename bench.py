@@ -434,7 +434,7 @@ def run_ours(args):
             "data": "synthetic (reference toy scene rendered on device, 8-bit)",
             "config": {"workload": WORKLOAD, "grid": f"{args.dims}^3 dense init",
                        "rays_per_gpu": args.batch, "global_batch": args.batch * world_size,
-                       "views": args.views, "res": args.res, "parallelism": f"dp{world_size}",
+                       "views": args.views, "res": args.res, "parallelism": f"dp{world_size}" + (f"-{world.mode}" if world_size > 1 else ""),
                        "l2": "inputs_larger_than_l2 (sh+density+grad+v = %.2f GB)" % (R * (3 * 112 + 4) / 1e9),
                        "touched_rows_U": U, "touched_rows_render": U_render, "tv_cells": n_tv,
                        "march_positions_per_step": float(march[0]),

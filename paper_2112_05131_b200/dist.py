@@ -43,7 +43,7 @@ class World:
     rank: int = 0
     size: int = 1
     group: object = None
-    mode: str = field(default_factory=lambda: os.environ.get("PLX_DP", "union"))
+    mode: str = field(default_factory=lambda: os.environ.get("PLX_DP", "p2p"))
 
     def __post_init__(self):
         if self.mode not in MODES:
