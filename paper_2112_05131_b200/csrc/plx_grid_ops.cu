@@ -24,103 +24,152 @@ struct TvArgs {
     double *sums;
 };
 
+// sqrt(s) and 1/sqrt(s) for s > 0 in float64 to ~1 ulp, without the IEEE
+// sqrt and division subroutines (MUFU seed + Newton steps with explicit FMAs;
+// -fmad=false does not touch fma()).
+__device__ __forceinline__ void root_and_rinv(double s, double &root, double &rinv) {
+    if (s < 2.2250738585072014e-308) {   // subnormal (eps = 0 only): IEEE path
+        root = sqrt(s);
+        rinv = 1.0 / root;
+        return;
+    }
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
+    const double hs = 0.5 * s;
+    y = y * fma(-hs * y, y, 1.5);
+    y = y * fma(-hs * y, y, 1.5);
+    y = y * fma(-hs * y, y, 1.5);
+    double r = s * y;
+    r = fma(0.5 * y, fma(-r, r, s), r);
+    root = r;
+    rinv = y;
+}
+
+// Warp-cooperative TV: 4 cells per warp iteration, lane = (cell, column
+// quad): the 7 lanes of a cell own its 7 float4 column groups, so the 4 rows
+// (self, +x, +y, +z) of a cell are read and reduced as 7 parallel float4s
+// instead of a 7-step loop per thread.  Per column the arithmetic is the
+// reference's (float64, one sqrt per coefficient, K:534-568); the sigma term
+// (K:505-532) is column 0, owned by quad 0.
 template <int NT>
 __global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
     using BR = cub::BlockReduce<double, NT>;
     __shared__ typename BR::TempStorage tmp;
-    const int64_t ci = (int64_t)blockIdx.x * NT + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / 7, quad = lane % 7;
+    const int64_t nw = (int64_t)gridDim.x * (NT / 32);
+    const double e2 = a.eps * a.eps;
+    const float *T = G.table;
     double sig_sum = 0.0, sh_sum = 0.0;
-    if (ci < a.count) {
-        int64_t cid = a.cells ? a.cells[ci] : (a.start + ci) % a.ncell;   // L:41-47
-        const int64_t Dyz = (int64_t)G.Dy * G.Dz;
-        const int64_t i = cid / Dyz, rem = cid % Dyz, j = rem / G.Dz, k = rem % G.Dz;
-        const int32_t r0 = __ldg(G.links + cid);
-        int64_t ii = i + 1, jj = j + 1, kk = k + 1;
-        bool hx = true, hy = true, hz = true;
-        if (ii >= G.Dx) { if (a.wrap[0]) ii = 0; else hx = false; }
-        if (jj >= G.Dy) { if (a.wrap[1]) jj = 0; else hy = false; }
-        if (kk >= G.Dz) { if (a.wrap[2]) kk = 0; else hz = false; }
-        const int32_t rx = hx ? __ldg(G.links + flat(G, ii, j, k)) : -1;
-        const int32_t ry = hy ? __ldg(G.links + flat(G, i, jj, k)) : -1;
-        const int32_t rz = hz ? __ldg(G.links + flat(G, i, j, kk)) : -1;
-        const double e2 = a.eps * a.eps;
-        const float *T = G.table;
-        // opacity term (K:505-532): missing neighbours read as 0
-        const double s0 = r0 >= 0 ? (double)__ldg(G.density + r0) : 0.0;
-        const double sx = rx >= 0 ? (double)__ldg(G.density + rx) : 0.0;
-        const double sy = ry >= 0 ? (double)__ldg(G.density + ry) : 0.0;
-        const double sz = rz >= 0 ? (double)__ldg(G.density + rz) : 0.0;
-        const double dxv = (sx - s0) * a.fac[0], dyv = (sy - s0) * a.fac[1], dzv = (sz - s0) * a.fac[2];
-        const double val = sqrt(dxv * dxv + dyv * dyv + dzv * dzv + e2);
-        sig_sum = val;
-        // per-row gradient accumulators for the current 4-column group
-        float gx[4], gy[4], gz[4], g0v[4];
+    for (int64_t w = (int64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); w * 4 < a.count;
+         w += nw) {
+        const int64_t ci = w * 4 + sub;
+        const bool valid = lane < 28 && ci < a.count;
+        int32_t r0 = -1, rx = -1, ry = -1, rz = -1;
         bool tx = false, ty = false, tz = false, t0 = false;
-        const bool okx = rx >= 0, oky = ry >= 0, okz = rz >= 0;
-        const bool sh_on = r0 >= 0 && (okx || oky || okz);
-        if (!sh_on) sh_sum = 27.0 * a.eps;
-#pragma unroll 1
-        for (int m = 0; m < 7; ++m) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) gx[e] = gy[e] = gz[e] = g0v[e] = 0.0f;
+        float gx[4] = {0.f, 0.f, 0.f, 0.f}, gy[4] = {0.f, 0.f, 0.f, 0.f};
+        float gz[4] = {0.f, 0.f, 0.f, 0.f}, g0v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (valid) {
+            int64_t cid;   // L:41-47 (lattice < 2^31 cells: 32-bit index math)
+            if (a.cells) {
+                cid = a.cells[ci];
+            } else {
+                cid = a.start + ci;
+                if (cid >= a.ncell) cid %= a.ncell;   // wrapped run (rare branch)
+            }
+            const uint32_t c32 = (uint32_t)cid, dz = (uint32_t)G.Dz;
+            const uint32_t ij = c32 / dz, k = c32 - ij * dz;
+            const uint32_t i = ij / (uint32_t)G.Dy, j = ij - i * (uint32_t)G.Dy;
+            r0 = __ldg(G.links + cid);
+            int64_t ii = i + 1, jj = j + 1, kk = k + 1;
+            bool hx = true, hy = true, hz = true;
+            if (ii >= G.Dx) { if (a.wrap[0]) ii = 0; else hx = false; }
+            if (jj >= G.Dy) { if (a.wrap[1]) jj = 0; else hy = false; }
+            if (kk >= G.Dz) { if (a.wrap[2]) kk = 0; else hz = false; }
+            rx = hx ? __ldg(G.links + flat(G, ii, j, k)) : -1;
+            ry = hy ? __ldg(G.links + flat(G, i, jj, k)) : -1;
+            rz = hz ? __ldg(G.links + flat(G, i, j, kk)) : -1;
+            const bool okx = rx >= 0, oky = ry >= 0, okz = rz >= 0;
+            const bool sh_on = r0 >= 0 && (okx || oky || okz);
             float4 v0 = make_float4(0, 0, 0, 0), vx = v0, vy = v0, vz = v0;
             if (sh_on) {
-                v0 = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)r0 * PLX_ROW) + m);
-                if (okx) vx = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)rx * PLX_ROW) + m);
-                if (oky) vy = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)ry * PLX_ROW) + m);
-                if (okz) vz = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)rz * PLX_ROW) + m);
+                v0 = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)r0 * PLX_ROW) + quad);
+                if (okx) vx = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)rx * PLX_ROW) + quad);
+                if (oky) vy = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)ry * PLX_ROW) + quad);
+                if (okz) vz = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)rz * PLX_ROW) + quad);
             }
-            const float c0[4] = {v0.x, v0.y, v0.z, v0.w}, cx[4] = {vx.x, vx.y, vx.z, vx.w};
-            const float cy[4] = {vy.x, vy.y, vy.z, vy.w}, cz[4] = {vz.x, vz.y, vz.z, vz.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int d = 4 * m + e;
-                if (d == 0) {
-                    if (a.with_grad && val > 0.0) {
-                        const double inv = a.f_sigma / val;
-                        double g0 = 0.0;
-                        if (rx >= 0) { tx = true; gx[0] = (float)(dxv * a.fac[0] * inv); }
-                        g0 -= dxv * a.fac[0] * inv;
-                        if (ry >= 0) { ty = true; gy[0] = (float)(dyv * a.fac[1] * inv); }
-                        g0 -= dyv * a.fac[1] * inv;
-                        if (rz >= 0) { tz = true; gz[0] = (float)(dzv * a.fac[2] * inv); }
-                        g0 -= dzv * a.fac[2] * inv;
-                        if (r0 >= 0 && g0 != 0.0) { t0 = true; g0v[0] = (float)g0; }
-                    }
-                    continue;
-                }
-                if (!sh_on) continue;   // K:534-568
-                const double v0d = (double)c0[e];
-                const double ax = okx ? ((double)cx[e] - v0d) * a.fac[0] : 0.0;
-                const double ay = oky ? ((double)cy[e] - v0d) * a.fac[1] : 0.0;
-                const double az = okz ? ((double)cz[e] - v0d) * a.fac[2] : 0.0;
-                const double v = sqrt(ax * ax + ay * ay + az * az + e2);
-                sh_sum += v;
-                if (a.with_grad && v > 0.0) {
-                    const double inv = a.f_sh / v;
+            if (quad == 0) {
+                // opacity term (K:505-532): missing neighbours read as 0
+                const double s0 = r0 >= 0 ? (double)__ldg(G.density + r0) : 0.0;
+                const double sx = rx >= 0 ? (double)__ldg(G.density + rx) : 0.0;
+                const double sy = ry >= 0 ? (double)__ldg(G.density + ry) : 0.0;
+                const double sz = rz >= 0 ? (double)__ldg(G.density + rz) : 0.0;
+                const double dxv = (sx - s0) * a.fac[0], dyv = (sy - s0) * a.fac[1],
+                             dzv = (sz - s0) * a.fac[2];
+                const double s2v = dxv * dxv + dyv * dyv + dzv * dzv + e2;
+                double val = 0.0, rinv = 0.0;
+                if (s2v > 0.0) root_and_rinv(s2v, val, rinv);
+                sig_sum += val;
+                if (a.with_grad && val > 0.0) {
+                    const double inv = a.f_sigma * rinv;
                     double g0 = 0.0;
-                    if (okx) { tx = true; gx[e] = (float)(ax * a.fac[0] * inv); g0 -= ax * a.fac[0] * inv; }
-                    if (oky) { ty = true; gy[e] = (float)(ay * a.fac[1] * inv); g0 -= ay * a.fac[1] * inv; }
-                    if (okz) { tz = true; gz[e] = (float)(az * a.fac[2] * inv); g0 -= az * a.fac[2] * inv; }
-                    if (g0 != 0.0) { t0 = true; g0v[e] = (float)g0; }
+                    if (rx >= 0) { tx = true; gx[0] = (float)(dxv * a.fac[0] * inv); }
+                    g0 -= dxv * a.fac[0] * inv;
+                    if (ry >= 0) { ty = true; gy[0] = (float)(dyv * a.fac[1] * inv); }
+                    g0 -= dyv * a.fac[1] * inv;
+                    if (rz >= 0) { tz = true; gz[0] = (float)(dzv * a.fac[2] * inv); }
+                    g0 -= dzv * a.fac[2] * inv;
+                    if (r0 >= 0 && g0 != 0.0) { t0 = true; g0v[0] = (float)g0; }
+                }
+                if (!sh_on) sh_sum += 27.0 * a.eps;   // empty self / no neighbour
+            }
+            if (sh_on) {   // K:534-568, columns 4*quad .. 4*quad+3 (column 0 is sigma)
+                const float c0[4] = {v0.x, v0.y, v0.z, v0.w}, cx[4] = {vx.x, vx.y, vx.z, vx.w};
+                const float cy[4] = {vy.x, vy.y, vy.z, vy.w}, cz[4] = {vz.x, vz.y, vz.z, vz.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (quad == 0 && e == 0) continue;
+                    const double v0d = (double)c0[e];
+                    const double ax = okx ? ((double)cx[e] - v0d) * a.fac[0] : 0.0;
+                    const double ay = oky ? ((double)cy[e] - v0d) * a.fac[1] : 0.0;
+                    const double az = okz ? ((double)cz[e] - v0d) * a.fac[2] : 0.0;
+                    const double s2v = ax * ax + ay * ay + az * az + e2;
+                    double v = 0.0, rinv = 0.0;
+                    if (s2v > 0.0) root_and_rinv(s2v, v, rinv);
+                    sh_sum += v;
+                    if (a.with_grad && v > 0.0) {
+                        const double inv = a.f_sh * rinv;
+                        double g0 = 0.0;
+                        if (okx) { tx = true; gx[e] = (float)(ax * a.fac[0] * inv); g0 -= ax * a.fac[0] * inv; }
+                        if (oky) { ty = true; gy[e] = (float)(ay * a.fac[1] * inv); g0 -= ay * a.fac[1] * inv; }
+                        if (okz) { tz = true; gz[e] = (float)(az * a.fac[2] * inv); g0 -= az * a.fac[2] * inv; }
+                        if (g0 != 0.0) { t0 = true; g0v[e] = (float)g0; }
+                    }
                 }
             }
             if (a.with_grad) {
                 if (rx >= 0 && (gx[0] != 0.f || gx[1] != 0.f || gx[2] != 0.f || gx[3] != 0.f))
-                    red_add_v4(a.grad + (int64_t)rx * PLX_ROW + 4 * m, gx[0], gx[1], gx[2], gx[3]);
+                    red_add_v4(a.grad + (int64_t)rx * PLX_ROW + 4 * quad, gx[0], gx[1], gx[2], gx[3]);
                 if (ry >= 0 && (gy[0] != 0.f || gy[1] != 0.f || gy[2] != 0.f || gy[3] != 0.f))
-                    red_add_v4(a.grad + (int64_t)ry * PLX_ROW + 4 * m, gy[0], gy[1], gy[2], gy[3]);
+                    red_add_v4(a.grad + (int64_t)ry * PLX_ROW + 4 * quad, gy[0], gy[1], gy[2], gy[3]);
                 if (rz >= 0 && (gz[0] != 0.f || gz[1] != 0.f || gz[2] != 0.f || gz[3] != 0.f))
-                    red_add_v4(a.grad + (int64_t)rz * PLX_ROW + 4 * m, gz[0], gz[1], gz[2], gz[3]);
+                    red_add_v4(a.grad + (int64_t)rz * PLX_ROW + 4 * quad, gz[0], gz[1], gz[2], gz[3]);
                 if (r0 >= 0 && (g0v[0] != 0.f || g0v[1] != 0.f || g0v[2] != 0.f || g0v[3] != 0.f))
-                    red_add_v4(a.grad + (int64_t)r0 * PLX_ROW + 4 * m, g0v[0], g0v[1], g0v[2], g0v[3]);
+                    red_add_v4(a.grad + (int64_t)r0 * PLX_ROW + 4 * quad, g0v[0], g0v[1], g0v[2], g0v[3]);
             }
         }
-        if (a.with_grad) {   // _touch (K:155-160) semantics, idempotent byte stores
-            if (tx) a.tmask[rx] = 1;
-            if (ty) a.tmask[ry] = 1;
-            if (tz) a.tmask[rz] = 1;
-            if (t0) a.tmask[r0] = 1;
+        if (a.with_grad) {   // _touch (K:155-160): a row is touched if any column got a value
+            const unsigned cell_lanes = 0x7fu << (7 * (sub & 3));
+            const bool bx = __ballot_sync(PLX_FULL_MASK, tx) & cell_lanes;
+            const bool by = __ballot_sync(PLX_FULL_MASK, ty) & cell_lanes;
+            const bool bz = __ballot_sync(PLX_FULL_MASK, tz) & cell_lanes;
+            const bool b0 = __ballot_sync(PLX_FULL_MASK, t0) & cell_lanes;
+            if (valid && quad == 0) {
+                if (bx) a.tmask[rx] = 1;
+                if (by) a.tmask[ry] = 1;
+                if (bz) a.tmask[rz] = 1;
+                if (b0) a.tmask[r0] = 1;
+            }
         }
     }
     double s1 = BR(tmp).Sum(sig_sum);
@@ -305,20 +354,27 @@ __global__ void __launch_bounds__(256) touched_compact_kernel(uint8_t *tmask, in
         const int64_t s1 = rg < nrange ? min(nseg, s0 + kCompactSegs) : s0;
         uint32_t m[kCompactSegs];
         int c = 0;
+        if (s1 - s0 == kCompactSegs && s1 * 128 <= rows) {   // interior: 16 loads in flight
+            const uint32_t *p = reinterpret_cast<const uint32_t *>(tmask + s0 * 128) + lane;
 #pragma unroll
-        for (int i = 0; i < kCompactSegs; ++i) {
-            m[i] = 0u;
-            const int64_t r0 = (s0 + i) * 128 + lane * 4;
-            if (s0 + i < s1) {
-                if (r0 + 3 < rows) {
-                    m[i] = *reinterpret_cast<const uint32_t *>(tmask + r0);
-                } else {
-                    for (int e = 0; e < 4; ++e)
-                        if (r0 + e < rows && tmask[r0 + e]) m[i] |= 0xffu << (8 * e);
+            for (int i = 0; i < kCompactSegs; ++i) m[i] = __ldcs(p + 32 * i);
+        } else {
+#pragma unroll
+            for (int i = 0; i < kCompactSegs; ++i) {
+                m[i] = 0u;
+                const int64_t r0 = (s0 + i) * 128 + lane * 4;
+                if (s0 + i < s1) {
+                    if (r0 + 3 < rows) {
+                        m[i] = *reinterpret_cast<const uint32_t *>(tmask + r0);
+                    } else {
+                        for (int e = 0; e < 4; ++e)
+                            if (r0 + e < rows && tmask[r0 + e]) m[i] |= 0xffu << (8 * e);
+                    }
                 }
             }
-            c += nonzero_bytes(m[i]);
         }
+#pragma unroll
+        for (int i = 0; i < kCompactSegs; ++i) c += nonzero_bytes(m[i]);
         int incl = c;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -340,13 +396,27 @@ __global__ void __launch_bounds__(256) touched_compact_kernel(uint8_t *tmask, in
                              : 0ull;
         __syncthreads();
         int64_t pos = (int64_t)blk_base + before + incl - c;
+        // 4 bits per mask word (one per nonzero byte) -> visit set rows only
+        uint64_t bits = 0;
+#pragma unroll
+        for (int i = 0; i < kCompactSegs; ++i) {
+            uint32_t x = m[i];
+            x = (x | (x >> 4)) & 0x0f0f0f0fu;
+            x = (x | (x >> 2)) & 0x03030303u;
+            x = (x | (x >> 1)) & 0x01010101u;                 // bit 8e = byte e nonzero
+            x = (x | (x >> 7)) & 0x00030003u;
+            x = (x | (x >> 14)) & 0xfu;                        // bits 0..3
+            bits |= (uint64_t)x << (4 * i);
+        }
+        while (bits) {
+            const int b = __ffsll((long long)bits) - 1;
+            bits &= bits - 1;
+            tids[pos++] = (int32_t)((s0 + (b >> 2)) * 128 + lane * 4 + (b & 3));
+        }
 #pragma unroll
         for (int i = 0; i < kCompactSegs; ++i) {
             if (!m[i]) continue;
             const int64_t r0 = (s0 + i) * 128 + lane * 4;
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if ((m[i] >> (8 * e)) & 0xffu) tids[pos++] = (int32_t)(r0 + e);
             if (clear) {
                 if (r0 + 3 < rows) {
                     *reinterpret_cast<uint32_t *>(tmask + r0) = 0u;
@@ -783,7 +853,9 @@ extern "C" int plx_tv(const plx_grid *g, const int64_t *cells, int64_t start, in
     a.tmask = gb ? gb->tmask : nullptr;
     a.sums = out_sums;
     constexpr int NT = 256;
-    tv_kernel<NT><<<blocks(count, NT), NT, 0, (cudaStream_t)stream>>>(make_dgrid(*g), a);
+    int64_t nb = (count + 31) / 32;   // 8 warps x 4 cells per block iteration
+    if (nb > (int64_t)num_sms() * 8) nb = (int64_t)num_sms() * 8;
+    tv_kernel<NT><<<(unsigned)nb, NT, 0, (cudaStream_t)stream>>>(make_dgrid(*g), a);
     return status();
 }
 

@@ -1,0 +1,44 @@
+#!/usr/bin/env python3
+"""Per-kernel device times of the C2 training step in steady operation (warm
+caches, normal overlap) via torch.profiler/CUPTI -- complements the ncu
+launch list, whose per-launch times are serialised and cold-cache.
+
+usage: python scripts/kernel_times.py [steps] [warm_to_step]"""
+import os
+import sys
+from collections import defaultdict
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2112_05131_b200 import trainer  # noqa: E402
+
+steps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+warm = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+dev = torch.device("cuda", 0)
+ds = bench.toy_scene(100, 200, dev)
+
+
+class A:
+    batch, gpus, dims = 5000, 1, 256
+
+
+tr = trainer.Trainer(ds, bench.bench_config(A), device=dev)
+for s in range(warm):
+    tr.step(s)
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    for s in range(warm, warm + steps):
+        tr.step(s)
+    torch.cuda.synchronize()
+agg = defaultdict(list)
+for e in prof.events():
+    if e.device_type.name == "CUDA":
+        agg[e.name[:70]].append(e.device_time)
+tot = 0.0
+for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+    tot += sum(v)
+    print(f"{sum(v) / steps:9.1f} us/step  n/step={len(v) / steps:4.1f}  {k}")
+print(f"{tot / steps:9.1f} us/step total device time")

@@ -30,6 +30,8 @@ OUT = Path(__file__).resolve().parent
 
 
 GRAD32 = os.environ.get("REF_GRAD_F32") == "1"
+# per-step noise of the order of f32 atomic-accumulation reordering
+NOISE = os.environ.get("REF_GRAD_NOISE") == "1"
 
 
 def run(seed):
@@ -41,7 +43,13 @@ def run(seed):
         orig_step = popt.step
 
         def step_f32(grid, grads, state, *a, **k):
-            if GRAD32:   # gradients as an f32 accumulator would hold them
+            if NOISE:    # f32 accumulation in a nondeterministic order
+                rs = np.random.default_rng(seed * 1000003 + int(state.step_count))
+                g32 = grads.data.astype(np.float32).astype(np.float64)
+                ulp = np.spacing(np.abs(g32).astype(np.float32)).astype(np.float64)
+                grads.data[:] = np.where(g32 != 0.0, g32 + ulp * rs.integers(-2, 3, g32.shape),
+                                         0.0)
+            elif GRAD32:   # gradients as an f32 accumulator would hold them
                 grads.data[:] = grads.data.astype(np.float32)
             out = orig_step(grid, grads, state, *a, **k)
             grid.table[:] = grid.table.astype(np.float32)
@@ -75,7 +83,8 @@ def run(seed):
 def main():
     k = int(sys.argv[1]) if len(sys.argv) > 1 else 4
     first = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-    path = OUT / ("psnr_spread_grad32.json" if GRAD32 else "psnr_spread.json")
+    path = OUT / ("psnr_spread_noise.json" if NOISE else
+                  "psnr_spread_grad32.json" if GRAD32 else "psnr_spread.json")
     old = json.loads(path.read_text()) if path.exists() else {}
     seeds = list(range(first, first + k)) + ([] if "stock" in old else [0])
     with ProcessPoolExecutor(max_workers=min(len(seeds), os.cpu_count() or 1)) as ex:
