@@ -57,16 +57,19 @@ typedef struct {
     const uint32_t *cell_occ; /* optional: 1 bit per trilinear base cell,
                                  set iff any of its 8 corners is occupied
                                  (plx_build_cell_occ); NULL = test the links */
-    uint32_t *neg_bits;    /* optional: 1 bit per lattice point, set iff it
-                              is occupied with density < 0
-                              (plx_build_neg_bits).  A trilinear cell whose
-                              8 corners are all set cannot hold a composited
-                              sample, so the march skips its gathers.
-                              plx_opt_step keeps it current (needs row_cell);
-                              rebuild after editing density or links.     */
+    float *sigma_lat;      /* optional [Dx*Dy*Dz] lattice-indexed mirror of
+                              density: the sigma of the row at each lattice
+                              point, NaN where empty (plx_build_sigma_lat).
+                              The march then reads the 8 corner sigmas in
+                              ONE gather level (no links, no rows) and loads
+                              links only for the samples it keeps.  The
+                              optimisers keep it current (need row_cell);
+                              rebuild after editing density or links.  For
+                              an identity-linked dense grid it may simply
+                              alias `density` (then nothing is maintained). */
     const int32_t *row_cell; /* [rows] lattice point of each row (inverse of
                               links, plx_build_row_cell); required with
-                              neg_bits by plx_opt_step                    */
+                              sigma_lat by the optimisers                 */
 } plx_grid;
 
 /* GradientBuffer (G:25-68): data + touched mask, and optionally the
@@ -191,13 +194,13 @@ typedef struct {
     uint8_t *tmask[PLX_MAX_PEERS];
     float *table[PLX_MAX_PEERS];       /* SH rows (column 0 unused) */
     float *density[PLX_MAX_PEERS];
-    uint32_t *neg_bits[PLX_MAX_PEERS]; /* may be NULL (no dead-cell mask) */
+    float *sigma_lat[PLX_MAX_PEERS];   /* lattice sigma mirrors, may be NULL */
 } plx_dp_peers;
 /* Fused reduce + update + broadcast over peer memory: rank `rank` owns the
  * 128-row-aligned slice [rows*rank/n, rows*(rank+1)/n); for every row of it
  * touched on ANY rank it sums the n gradient rows (rank order), applies the
  * update with its own RMSProp state v, and stores the new sigma / SH row
- * (and neg bit) into all n grids.  Gradients and masks are NOT cleared
+ * (and lattice sigma) into all n grids.  Gradients and masks are NOT cleared
  * (each rank clears its own with plx_clear_grad after all ranks finished:
  * the caller orders the ranks with a collective before and after).
  * out_count (local) accumulates the slice's union count. */
@@ -238,8 +241,8 @@ int plx_scan_ids(const uint8_t *flags, int64_t n, int32_t *ids, int64_t *count,
  * = any of the 8 corner links >= 0.  Must be rebuilt after prune/upsample. */
 int64_t plx_cell_occ_words(const int64_t dims[3]);
 int plx_build_cell_occ(const plx_grid *g, uint32_t *cell_occ, void *stream);
-/* neg_bits (plx_cell_occ_words words, same lattice indexing) and row_cell. */
-int plx_build_neg_bits(const plx_grid *g, uint32_t *neg_bits, void *stream);
+/* sigma_lat ([Dx*Dy*Dz] floats) and row_cell ([rows] int32). */
+int plx_build_sigma_lat(const plx_grid *g, float *sigma_lat, void *stream);
 int plx_build_row_cell(const plx_grid *g, int32_t *row_cell, void *stream);
 
 /* Library identification / self-check. */

@@ -30,7 +30,7 @@ class PlxGrid(ctypes.Structure):
                 ("density", ctypes.c_void_p), ("dims", ctypes.c_int64 * 3), ("rows", ctypes.c_int64),
                 ("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3),
                 ("scale", ctypes.c_double * 3), ("dmax", ctypes.c_double * 3),
-                ("cell_occ", ctypes.c_void_p), ("neg_bits", ctypes.c_void_p),
+                ("cell_occ", ctypes.c_void_p), ("sigma_lat", ctypes.c_void_p),
                 ("row_cell", ctypes.c_void_p)]
 
 
@@ -46,7 +46,7 @@ class PlxDpPeers(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("rank", ctypes.c_int32), ("rows", ctypes.c_int64),
                 ("grad", ctypes.c_void_p * MAX_PEERS), ("tmask", ctypes.c_void_p * MAX_PEERS),
                 ("table", ctypes.c_void_p * MAX_PEERS), ("density", ctypes.c_void_p * MAX_PEERS),
-                ("neg_bits", ctypes.c_void_p * MAX_PEERS)]
+                ("sigma_lat", ctypes.c_void_p * MAX_PEERS)]
 
 
 class PlxRenderOpts(ctypes.Structure):
@@ -100,7 +100,7 @@ _SIGS = {
     "plx_scan_ids": [_P, _I64, _P, _P, _P, _P],
     "plx_cell_occ_words": [ctypes.POINTER(_I64)],
     "plx_build_cell_occ": [ctypes.POINTER(PlxGrid), _P, _P],
-    "plx_build_neg_bits": [ctypes.POINTER(PlxGrid), _P, _P],
+    "plx_build_sigma_lat": [ctypes.POINTER(PlxGrid), _P, _P],
     "plx_build_row_cell": [ctypes.POINTER(PlxGrid), _P, _P],
     "plx_version": [],
     "plx_device_check": [],

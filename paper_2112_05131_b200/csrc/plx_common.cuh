@@ -23,7 +23,7 @@ struct DGrid {
     const float *__restrict__ table;     // SH rows (column 0 unused)
     const float *__restrict__ density;   // sigma per row
     const uint32_t *__restrict__ cell_occ;
-    const uint32_t *neg_bits;            // lattice points occupied with sigma < 0 (mutable)
+    const float *sigma_lat;              // lattice-indexed sigma mirror, NaN = empty (mutable)
     int32_t Dx, Dy, Dz;
     double lo[3], hi[3], scale[3], dmax[3];
 };
@@ -34,7 +34,7 @@ inline DGrid make_dgrid(const plx_grid &g) {
     d.table = g.table;
     d.density = g.density;
     d.cell_occ = g.cell_occ;
-    d.neg_bits = g.neg_bits;
+    d.sigma_lat = g.sigma_lat;
     d.Dx = (int32_t)g.dims[0];
     d.Dy = (int32_t)g.dims[1];
     d.Dz = (int32_t)g.dims[2];
@@ -136,22 +136,6 @@ __device__ __forceinline__ void sample_coords(const RayMarch &rm, const DGrid &G
     for (int a = 0; a < 3; ++a) g[a] = clamp_coord(rm.o[a] + t * rm.d[a], G.lo[a], G.scale[a], G.dmax[a]);
 }
 
-// Two consecutive bits c, c+1 of a lattice bitmask (3 = both set).
-__device__ __forceinline__ unsigned bits2(const uint32_t *m, int64_t c) {
-    const uint32_t w = m[c >> 5];
-    const int b = (int)(c & 31);
-    return b < 31 ? (w >> b) & 3u : (w >> 31) | ((m[(c >> 5) + 1] & 1u) << 1);
-}
-
-// Trilinear cell with base lattice point c whose 8 corners are all set in
-// neg_bits (occupied, sigma < 0).  The bitmask is updated in place by the
-// optimiser, so it is read with plain (not read-only-path) loads.
-__device__ __forceinline__ bool dead_cell(const DGrid &G, int64_t c) {
-    const int64_t sy = G.Dz, sx = (int64_t)G.Dy * G.Dz;
-    return (bits2(G.neg_bits, c) & bits2(G.neg_bits, c + sy) & bits2(G.neg_bits, c + sx) &
-            bits2(G.neg_bits, c + sx + sy)) == 3u;
-}
-
 // Stencil (K:84-123): rows[8] (-1 = empty), the fractional offsets f[3] and
 // the base cell (trilinear) or lattice point (nearest) ijk[3]; the corner
 // weight is stencil_w(f, q) (recomputed instead of stored, to save
@@ -185,13 +169,6 @@ __device__ __forceinline__ int stencil(const DGrid &G, const double *g, int32_t 
             return 8;
         }
     }
-    if (G.neg_bits && dead_cell(G, flat(G, i0, j0, k0))) {
-        // all 8 corners occupied with sigma < 0: the interpolated sigma is a
-        // convex combination of negatives, so the sample is excluded (K:211,
-        // K:293) -- skip the link and density gathers
-        any_occ = false;
-        return 8;
-    }
     f[0] = g[0] - (double)i0;
     f[1] = g[1] - (double)j0;
     f[2] = g[2] - (double)k0;
@@ -206,6 +183,19 @@ __device__ __forceinline__ int stencil(const DGrid &G, const double *g, int32_t 
     }
     any_occ = occ;
     return 8;
+}
+
+// Stencil rows of a base cell / lattice point (K:84-123), -1 = empty.
+template <bool NEAREST>
+__device__ __forceinline__ void load_rows(const DGrid &G, const int *ijk, int32_t *rows) {
+    const int32_t *base = G.links + flat(G, ijk[0], ijk[1], ijk[2]);
+    if (NEAREST) {
+        rows[0] = __ldg(base);
+        return;
+    }
+    const int64_t sy = G.Dz, sx = (int64_t)G.Dy * G.Dz;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) rows[q] = __ldg(base + ((q >> 2) & 1) * sx + ((q >> 1) & 1) * sy + (q & 1));
 }
 
 // Trilinear corner weight (K:114-121): corner q = (di, dj, dk) = bits (4, 2, 1).
@@ -252,6 +242,72 @@ __device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float 
 
 __device__ __forceinline__ void red_add_f32(float *addr, float a) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(a) : "memory");
+}
+
+}  // namespace plx
+
+namespace plx {
+
+// _sigma_at (K:126-135) of the stencil at lattice coordinates g: float64 sum
+// over occupied corners in corner order; occ = any corner occupied.  With the
+// lattice-indexed mirror G.sigma_lat (NaN = empty point) the corner values
+// are ONE gather level -- no links, no rows -- and an empty corner simply
+// adds nothing, exactly as the reference skips it.  rows[] is filled only on
+// the links path (rows_ok = true); otherwise the caller loads it with
+// load_rows() for the samples it keeps.
+template <bool NEAREST>
+__device__ __forceinline__ bool sigma_at(const DGrid &G, const double *g, double *f, int *ijk,
+                                         int32_t *rows, double &sig, bool &rows_ok) {
+    sig = 0.0;
+    rows_ok = false;
+    bool occ = false;
+    if (!G.sigma_lat) {
+        stencil<NEAREST>(G, g, rows, f, occ, ijk);
+        rows_ok = true;
+        if (!occ) return false;
+        constexpr int NQ = NEAREST ? 1 : 8;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+            if (rows[q] >= 0) sig += stencil_w<NEAREST>(f, q) * (double)__ldg(G.density + rows[q]);
+        return true;
+    }
+    if (NEAREST) {
+        int64_t i = (int64_t)(g[0] + 0.5), j = (int64_t)(g[1] + 0.5), k = (int64_t)(g[2] + 0.5);
+        if (i > G.Dx - 1) i = G.Dx - 1;
+        if (j > G.Dy - 1) j = G.Dy - 1;
+        if (k > G.Dz - 1) k = G.Dz - 1;
+        ijk[0] = (int)i;
+        ijk[1] = (int)j;
+        ijk[2] = (int)k;
+        const float s = G.sigma_lat[flat(G, i, j, k)];
+        if (s != s) return false;
+        sig = stencil_w<NEAREST>(f, 0) * (double)s;
+        return true;
+    }
+    int64_t i0 = (int64_t)g[0], j0 = (int64_t)g[1], k0 = (int64_t)g[2];
+    if (i0 > G.Dx - 2) i0 = G.Dx - 2;
+    if (j0 > G.Dy - 2) j0 = G.Dy - 2;
+    if (k0 > G.Dz - 2) k0 = G.Dz - 2;
+    ijk[0] = (int)i0;
+    ijk[1] = (int)j0;
+    ijk[2] = (int)k0;
+    const int64_t c = flat(G, i0, j0, k0);
+    if (G.cell_occ && !((__ldg(G.cell_occ + (c >> 5)) >> (c & 31)) & 1u)) return false;
+    f[0] = g[0] - (double)i0;
+    f[1] = g[1] - (double)j0;
+    f[2] = g[2] - (double)k0;
+    const float *base = G.sigma_lat + c;
+    const int64_t sy = G.Dz, sx = (int64_t)G.Dy * G.Dz;
+    float s[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s[q] = base[((q >> 2) & 1) * sx + ((q >> 1) & 1) * sy + (q & 1)];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        if (s[q] != s[q]) continue;   // empty corner (K:131: skipped)
+        occ = true;
+        sig += stencil_w<NEAREST>(f, q) * (double)s[q];
+    }
+    return occ;
 }
 
 }  // namespace plx

@@ -40,7 +40,7 @@ struct ListArgs {
     float *table, *density, *v, *grad;
     const float *gpack;        // packed gradients of the list (NULL = grad rows)
     uint8_t *tmask;
-    uint32_t *neg_bits;
+    float *sigma_lat;
     const int32_t *row_cell;
     const int32_t *ids;
     const int64_t *count;
@@ -49,13 +49,6 @@ struct ListArgs {
     OptHyper h;
     int clear;
 };
-
-__device__ __forceinline__ void neg_flip(uint32_t *neg, int32_t c, float before, float after) {
-    if (!neg || ((before < 0.f) == (after < 0.f))) return;
-    const uint32_t bit = 1u << (c & 31);
-    if (after < 0.f) atomicOr(neg + (c >> 5), bit);
-    else atomicAnd(neg + (c >> 5), ~bit);
-}
 
 // Update the rows ids[0..count) (4 rows x 7 float4 per warp iteration).
 __global__ void __launch_bounds__(256, 2) opt_list_kernel(ListArgs a) {
@@ -83,13 +76,13 @@ __global__ void __launch_bounds__(256, 2) opt_list_kernel(ListArgs a) {
         int32_t cell = 0;
         if (quad == 0) {
             den = a.density[r];
-            cell = a.neg_bits ? a.row_cell[r] : 0;
+            cell = a.sigma_lat ? a.row_cell[r] : 0;
             t4.x = den;
         }
         opt_apply4(a.h, quad, g4, t4, v4);
         if (quad == 0) {   // sigma lives in the density array (column 0 unused)
             a.density[r] = t4.x;
-            neg_flip(a.neg_bits, cell, den, t4.x);
+            if (a.sigma_lat) a.sigma_lat[cell] = t4.x;
             t4.x = 0.f;
             if (a.clear) a.tmask[r] = 0;
         }
@@ -109,7 +102,7 @@ struct DpArgs {  // kernel-side copy of plx_dp_peers + update scalars
     const uint8_t *tmask[kMaxPeers];
     float *table[kMaxPeers];
     float *density[kMaxPeers];
-    uint32_t *neg[kMaxPeers];
+    float *lat[kMaxPeers];                // lattice sigma mirrors (may be NULL)
     float *v;                             // this rank's RMSProp state (owned rows only)
     const int32_t *row_cell;
     double *guard;
@@ -180,10 +173,10 @@ __global__ void __launch_bounds__(256) dp_owner_update_kernel(DpArgs a) {
                 float4 t4 = reinterpret_cast<const float4 *>(a.table[a.rank] + r * PLX_ROW)[quad];
                 float4 v4 = a.h.rmsprop ? reinterpret_cast<const float4 *>(a.v + r * PLX_ROW)[quad]
                                         : make_float4(0.f, 0.f, 0.f, 0.f);
-                float den = 0.f;
+                int32_t cell = 0;
                 if (quad == 0) {
-                    den = a.density[a.rank][r];
-                    t4.x = den;
+                    t4.x = a.density[a.rank][r];
+                    if (a.row_cell) cell = a.row_cell[r];
                 }
                 opt_apply4(a.h, quad, g4, t4, v4);
                 if (a.h.rmsprop) reinterpret_cast<float4 *>(a.v + r * PLX_ROW)[quad] = v4;
@@ -193,12 +186,7 @@ __global__ void __launch_bounds__(256) dp_owner_update_kernel(DpArgs a) {
                     reinterpret_cast<float4 *>(a.table[k] + r * PLX_ROW)[quad] = t4;
                     if (quad == 0) {
                         a.density[k][r] = sig;
-                        if (a.neg[k] && ((den < 0.f) != (sig < 0.f))) {
-                            const int32_t cc = a.row_cell[r];
-                            const uint32_t bit = 1u << (cc & 31);
-                            if (sig < 0.f) atomicOr_system(a.neg[k] + (cc >> 5), bit);
-                            else atomicAnd_system(a.neg[k] + (cc >> 5), ~bit);
-                        }
+                        if (a.lat[k]) a.lat[k][cell] = sig;
                     }
                 }
             }
@@ -243,7 +231,8 @@ extern "C" int plx_opt_step_list(plx_grid *g, float *v, plx_grad *gb, const int3
                                  int32_t clear, double *guard, int64_t *out_count, void *stream) {
     if (!g || !gb || !gb->grad || !gb->tmask || !ids || !count || (rmsprop && !v)) return PLX_EINVAL;
     if (g->rows > 0 && (!g->table || !g->density)) return PLX_EINVAL;
-    if (g->neg_bits && !g->row_cell) return PLX_EINVAL;
+    float *lat = g->sigma_lat == g->density ? nullptr : g->sigma_lat;   // aliased: no upkeep
+    if (lat && !g->row_cell) return PLX_EINVAL;
     if (g->rows == 0) return PLX_OK;
     ListArgs a;
     a.table = g->table;
@@ -252,7 +241,7 @@ extern "C" int plx_opt_step_list(plx_grid *g, float *v, plx_grad *gb, const int3
     a.grad = gb->grad;
     a.gpack = gpack;
     a.tmask = gb->tmask;
-    a.neg_bits = g->neg_bits;
+    a.sigma_lat = lat;
     a.row_cell = g->row_cell;
     a.ids = ids;
     a.count = count;
@@ -292,8 +281,8 @@ extern "C" int plx_dp_owner_update(const plx_dp_peers *p, float *v, const int32_
         a.tmask[k] = p->tmask[k];
         a.table[k] = p->table[k];
         a.density[k] = p->density[k];
-        a.neg[k] = p->neg_bits[k];
-        need_cell |= p->neg_bits[k] != nullptr;
+        a.lat[k] = p->sigma_lat[k] == p->density[k] ? nullptr : p->sigma_lat[k];
+        need_cell |= a.lat[k] != nullptr;
     }
     if (need_cell && !row_cell) return PLX_EINVAL;
     a.v = v;

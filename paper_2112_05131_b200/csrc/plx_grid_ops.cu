@@ -191,8 +191,8 @@ __global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
 struct OptArgs {
     float *table, *density, *v, *grad;
     double *guard;             // optional divergence guard (see guard_halts)
-    uint32_t *neg_bits;        // optional: kept current when sigma changes sign
-    const int32_t *row_cell;   // row -> lattice point (required with neg_bits)
+    float *sigma_lat;          // optional lattice sigma mirror: kept current
+    const int32_t *row_cell;   // row -> lattice point (required with sigma_lat)
     uint8_t *tmask;
     int64_t rows;
     double lr_sigma, lr_sh, beta, eps;
@@ -207,13 +207,9 @@ __device__ __forceinline__ int nonzero_bytes(uint32_t m) {
     return __popc(m);
 }
 
-// sigma of a row at lattice point c went from `before` to `after`: keep its
-// neg bit current.
-__device__ __forceinline__ void neg_update(const OptArgs &a, int32_t c, float before, float after) {
-    if (!a.neg_bits || ((before < 0.f) == (after < 0.f))) return;
-    const uint32_t bit = 1u << (c & 31);
-    if (after < 0.f) atomicOr(a.neg_bits + (c >> 5), bit);
-    else atomicAnd(a.neg_bits + (c >> 5), ~bit);
+// sigma of a row at lattice point c changed: keep the lattice mirror current.
+__device__ __forceinline__ void lat_update(const OptArgs &a, int32_t c, float sigma) {
+    if (a.sigma_lat) a.sigma_lat[c] = sigma;
 }
 
 // The update of one float4 of one row (K:578-590), float64 arithmetic.
@@ -297,7 +293,7 @@ __global__ void __launch_bounds__(NT) opt_kernel(OptArgs a) {
                     opt_apply(a, quad, g4[u], t4[u], v4[u]);
                     if (quad == 0) {
                         a.density[rw[u]] = t4[u].x;
-                        if (a.neg_bits) neg_update(a, a.row_cell[rw[u]], den[u], t4[u].x);
+                        if (a.sigma_lat) lat_update(a, a.row_cell[rw[u]], t4[u].x);
                         t4[u].x = 0.f;
                     }
                     reinterpret_cast<float4 *>(a.table + rw[u] * PLX_ROW)[quad] = t4[u];
@@ -465,7 +461,7 @@ __global__ void __launch_bounds__(256, 2) opt_rows_kernel(OptArgs a, const int32
             t4[u] = reinterpret_cast<const float4 *>(a.table + r * PLX_ROW)[quad];
             if (quad == 0) {   // merged after all loads are issued
                 den[u] = a.density[r];
-                cell[u] = a.neg_bits ? a.row_cell[r] : 0;
+                cell[u] = a.sigma_lat ? a.row_cell[r] : 0;
             }
             if (a.rmsprop) v4[u] = reinterpret_cast<const float4 *>(a.v + r * PLX_ROW)[quad];
         }
@@ -478,7 +474,7 @@ __global__ void __launch_bounds__(256, 2) opt_rows_kernel(OptArgs a, const int32
             opt_apply(a, quad, g4[u], t4[u], v4[u]);
             if (quad == 0) {   // sigma lives in the density array (column 0 unused)
                 a.density[r] = t4[u].x;
-                neg_update(a, cell[u], den[u], t4[u].x);
+                lat_update(a, cell[u], t4[u].x);
                 t4[u].x = 0.f;
             }
             reinterpret_cast<float4 *>(a.table + r * PLX_ROW)[quad] = t4[u];
@@ -791,18 +787,12 @@ __global__ void cell_occ_kernel(DGrid G, uint32_t *words, int64_t nwords, int64_
     words[w] = bits;
 }
 
-// neg_bits word w: bit b set iff lattice point 32w+b is occupied with sigma < 0.
-__global__ void neg_bits_kernel(DGrid G, uint32_t *words, int64_t nwords, int64_t ncell) {
-    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= nwords) return;
-    uint32_t bits = 0;
-    for (int b = 0; b < 32; ++b) {
-        const int64_t c = w * 32 + b;
-        if (c >= ncell) break;
-        const int32_t r = G.links[c];
-        if (r >= 0 && G.density[r] < 0.f) bits |= 1u << b;
-    }
-    words[w] = bits;
+// Lattice sigma mirror: point c -> density of its row, NaN where empty.
+__global__ void sigma_lat_kernel(DGrid G, float *out, int64_t ncell) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncell) return;
+    const int32_t r = G.links[c];
+    out[c] = r >= 0 ? G.density[r] : __int_as_float(0x7fc00000);
 }
 
 __global__ void row_cell_kernel(const int32_t *links, int64_t ncell, int32_t *row_cell) {
@@ -867,8 +857,10 @@ extern "C" int plx_opt_step(plx_grid *g, float *v, plx_grad *gb, double lr_sigma
         return PLX_EINVAL;
     if ((gb->tids == nullptr) != (gb->tcnt == nullptr)) return PLX_EINVAL;
     if (g->rows == 0) return PLX_OK;
-    if (g->neg_bits && !g->row_cell) return PLX_EINVAL;
-    OptArgs a{g->table, g->density, v, gb->grad, guard, g->neg_bits, g->row_cell, gb->tmask, g->rows,
+    // a mirror aliased to density (identity-linked dense grid) needs no upkeep
+    float *lat = g->sigma_lat == g->density ? nullptr : g->sigma_lat;
+    if (lat && !g->row_cell) return PLX_EINVAL;
+    OptArgs a{g->table, g->density, v, gb->grad, guard, lat, g->row_cell, gb->tmask, g->rows,
               lr_sigma, lr_sh, beta, eps, rmsprop, clear, 1, reinterpret_cast<unsigned long long *>(out_count)};
     constexpr int NT = 256;
     cudaStream_t s = (cudaStream_t)stream;
@@ -1022,10 +1014,10 @@ extern "C" int plx_build_cell_occ(const plx_grid *g, uint32_t *cell_occ, void *s
     return status();
 }
 
-extern "C" int plx_build_neg_bits(const plx_grid *g, uint32_t *neg_bits, void *stream) {
-    if (!grid_ok(g) || !neg_bits) return PLX_EINVAL;
-    const int64_t n = ncell(g), nw = (n + 31) / 32;
-    neg_bits_kernel<<<blocks(nw, 256), 256, 0, (cudaStream_t)stream>>>(make_dgrid(*g), neg_bits, nw, n);
+extern "C" int plx_build_sigma_lat(const plx_grid *g, float *sigma_lat, void *stream) {
+    if (!grid_ok(g) || !sigma_lat) return PLX_EINVAL;
+    const int64_t n = ncell(g);
+    sigma_lat_kernel<<<blocks(n, 256), 256, 0, (cudaStream_t)stream>>>(make_dgrid(*g), sigma_lat, n);
     return status();
 }
 

@@ -81,24 +81,18 @@ __device__ __forceinline__ void eval_sample(const DGrid &G, const RayMarch &rm, 
     if (si >= rm.nsamp) return;
     double t, g[3];
     sample_coords(rm, G, step, si, t, s.dlt, g);
-    bool occ;
-    constexpr int NQ = NEAREST ? 1 : 8;
     int ijk[3];
-    stencil<NEAREST>(G, g, s.rows, s.f, occ, ijk);
-    if (!occ) return;
-    // _sigma_at (K:126-135): float64 sum over occupied corners in order.
-    double sig = 0.0;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        int32_t r = s.rows[q];
-        if (r >= 0) sig += stencil_w<NEAREST>(s.f, q) * (double)__ldg(G.density + r);
-    }
+    bool rows_ok;
+    double sig;
+    if (!sigma_at<NEAREST>(G, g, s.f, ijk, s.rows, sig, rows_ok)) return;
     s.sig = sig;
     if (!(sig > 0.0)) return;   // K:211 (render_forward / max_weight_accum)
     s.incl = true;
     s.att = exp(-sig * s.dlt);
+    if (!rows_ok) load_rows<NEAREST>(G, ijk, s.rows);
     if (MODE == MAXW) return;
     // _color_at (K:138-152): per corner the 3 SH dots, then weight.
+    constexpr int NQ = NEAREST ? 1 : 8;
     float c0 = 0.f, c1 = 0.f, c2 = 0.f;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -469,16 +463,11 @@ __global__ void __launch_bounds__(128, MINB)
             double att = 1.0, sig = 0.0, t, dlt, g[3], fd[3];
             int32_t rows[8];
             int ijk[3];
+            bool rows_ok = true;
             if (si < rm.nsamp) {
                 sample_coords(rm, G, O.step, si, t, dlt, g);
-                bool occ;
-                constexpr int NQ = NEAREST ? 1 : 8;
-                stencil<NEAREST>(G, g, rows, fd, occ, ijk);
-                if (occ) {   // _sigma_at (K:126-135), float64, reference order
-#pragma unroll
-                    for (int q = 0; q < NQ; ++q)
-                        if (rows[q] >= 0)
-                            sig += stencil_w<NEAREST>(fd, q) * (double)__ldg(G.density + rows[q]);
+                // _sigma_at (K:126-135), float64, reference order
+                if (sigma_at<NEAREST>(G, g, fd, ijk, rows, sig, rows_ok)) {
                     incl = sig >= 0.0;   // K:293: recorded unless sigma < 0
                     if (incl) att = exp(-sig * dlt);
                 }
@@ -495,6 +484,7 @@ __global__ void __launch_bounds__(128, MINB)
             st_pos += stopped ? 32 - __clz(m) : npos;
             st_samp += __popc(m);
             if (incl) {
+                if (!rows_ok) load_rows<NEAREST>(G, ijk, rows);
                 const int k = ns + __popc(m & lt_mask);
                 r_att[k] = att;
                 r_T[k] = Ti;

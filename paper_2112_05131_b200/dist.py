@@ -114,14 +114,16 @@ class PeerMap:
     peers' buffers are opened in this process.  `peers` is the plx_dp_peers
     descriptor for plx_dp_owner_update."""
 
-    KEYS = ("grad", "tmask", "table", "density", "neg_bits")
+    KEYS = ("grad", "tmask", "table", "density", "sigma_lat")
 
     def __init__(self, world: World, grid, grads):
         L = _lib.lib()
         mine = {}
-        neg, _ = grid.neg_masks() if grid.n_rows else (None, None)
+        lat, _ = grid.lattice_sigma() if grid.n_rows else (None, None)
+        if lat is not None and lat.data_ptr() == grid.density.data_ptr():
+            lat = None   # aliased mirror (dense grid): updating density is enough
         local = {"grad": grads.data, "tmask": grads.touched_mask, "table": grid.sh,
-                 "density": grid.density, "neg_bits": neg}
+                 "density": grid.density, "sigma_lat": lat}
         for k in self.KEYS:
             t = local[k]
             if t is None or t.numel() == 0:

@@ -131,7 +131,7 @@ class SparseGrid:
         if int(np.prod(self.dims)) >= 2 ** 31:
             raise ValueError("lattice too large for int32 cell ids")
         self._cell_occ = None
-        self._neg = None
+        self._lat = None
         self._row_cell = None
 
     # -- constructors -------------------------------------------------------
@@ -146,7 +146,7 @@ class SparseGrid:
         g.aabb_min = np.asarray(aabb_min, dtype=np.float64).reshape(3).copy()
         g.aabb_max = np.asarray(aabb_max, dtype=np.float64).reshape(3).copy()
         g._cell_occ = None
-        g._neg = None
+        g._lat = None
         g._row_cell = None
         return g
 
@@ -182,7 +182,7 @@ class SparseGrid:
     def links(self, value) -> None:
         self._links = torch.as_tensor(value).to(self._links.device, torch.int32).contiguous()
         self._cell_occ = None
-        self._neg = None
+        self._lat = None
         self._row_cell = None
 
     @property
@@ -203,13 +203,13 @@ class SparseGrid:
             self.density.copy_(t[:, 0])
             self.sh.copy_(t)
             self.sh[:, 0] = 0.0
-            if getattr(self, "_neg", None) is not None:
+            if getattr(self, "_lat", None) is not None:
                 self.invalidate()
             return
         self.density = t[:, 0].to(device=dev, dtype=torch.float32).contiguous()
         self.sh = t.to(device=dev, dtype=torch.float32).clone().contiguous()
         self.sh[:, 0] = 0.0
-        self._neg = None
+        self._lat = None
         self._row_cell = None
 
     @property
@@ -244,10 +244,10 @@ class SparseGrid:
 
     def invalidate(self) -> None:
         """Call after editing `links` or `density` in place: rebuilds the
-        derived bitmasks (cell occupancy, negative-density lattice points,
+        derived structures (cell occupancy bitmask, lattice sigma mirror,
         row -> cell map) in their existing buffers, so descriptors cached by
         a caller stay valid."""
-        c = self._c(with_occ=False, with_neg=False)
+        c = self._c(with_occ=False, with_lat=False)
         L, s = _lib.lib(), _lib.stream_ptr()
         if self._cell_occ is not None:
             _lib.check(L.plx_build_cell_occ(ctypes.byref(c), self._cell_occ.data_ptr(), s),
@@ -255,42 +255,51 @@ class SparseGrid:
         if self._row_cell is not None and self.n_rows:
             _lib.check(L.plx_build_row_cell(ctypes.byref(c), self._row_cell.data_ptr(), s),
                        "build_row_cell")
-        if self._neg is not None:
-            _lib.check(L.plx_build_neg_bits(ctypes.byref(c), self._neg.data_ptr(), s),
-                       "build_neg_bits")
+        if self._lat is not None and self._lat.data_ptr() != self.density.data_ptr():
+            _lib.check(L.plx_build_sigma_lat(ctypes.byref(c), self._lat.data_ptr(), s),
+                       "build_sigma_lat")
 
     def cell_occ(self) -> torch.Tensor:
         if self._cell_occ is None:
             words = _lib.load().plx_cell_occ_words(_lib.dims_array(self.dims))
             occ = torch.empty(int(words), dtype=torch.int32, device=self.device)
-            c = self._c(with_occ=False, with_neg=False)
+            c = self._c(with_occ=False, with_lat=False)
             _lib.check(_lib.lib().plx_build_cell_occ(ctypes.byref(c), occ.data_ptr(),
                                                      _lib.stream_ptr()), "build_cell_occ")
             self._cell_occ = occ
         return self._cell_occ
 
-    def neg_masks(self):
-        """(neg_bits, row_cell): lattice points occupied with density < 0 and
-        the row -> lattice point map.  Built on first use; from then on every
-        descriptor of this grid carries them, the march skips cells whose 8
-        corners are negative, and the optimiser keeps the bits current."""
-        if self._neg is None:
-            words = _lib.load().plx_cell_occ_words(_lib.dims_array(self.dims))
-            c = self._c(with_occ=False, with_neg=False)
+    def lattice_sigma(self):
+        """(sigma_lat, row_cell): the lattice-indexed density mirror (NaN at
+        empty points) and the row -> lattice point map.  Built on first use;
+        from then on every descriptor of this grid carries them, the march
+        reads corner sigmas from the mirror in one gather level, and the
+        optimisers keep it current."""
+        if self._lat is None:
+            ncell = int(np.prod(self.dims))
+            if self.n_rows == ncell and bool(torch.equal(
+                    self._links.view(-1), torch.arange(ncell, dtype=torch.int32,
+                                                       device=self.device))):
+                # identity-linked dense grid: the mirror IS the density array
+                self._row_cell = torch.arange(ncell, dtype=torch.int32, device=self.device)
+                self._lat = self.density
+                return self._lat, self._row_cell
+            c = self._c(with_occ=False, with_lat=False)
             L, s = _lib.lib(), _lib.stream_ptr()
             rc = torch.empty(max(self.n_rows, 1), dtype=torch.int32, device=self.device)
             if self.n_rows:
                 _lib.check(L.plx_build_row_cell(ctypes.byref(c), rc.data_ptr(), s),
                            "build_row_cell")
-            neg = torch.empty(int(words), dtype=torch.int32, device=self.device)
-            _lib.check(L.plx_build_neg_bits(ctypes.byref(c), neg.data_ptr(), s), "build_neg_bits")
-            self._row_cell, self._neg = rc, neg
-        return self._neg, self._row_cell
+            lat = torch.empty(int(np.prod(self.dims)), dtype=torch.float32, device=self.device)
+            _lib.check(L.plx_build_sigma_lat(ctypes.byref(c), lat.data_ptr(), s),
+                       "build_sigma_lat")
+            self._row_cell, self._lat = rc, lat
+        return self._lat, self._row_cell
 
-    def _c(self, with_occ: bool = True, with_neg: bool | None = None) -> _lib.PlxGrid:
-        """Kernel descriptor.  with_neg (default: with_occ) builds the
-        negative-density bitmask; once built it is always attached, so that
-        the optimiser keeps it current."""
+    def _c(self, with_occ: bool = True, with_lat: bool | None = None) -> _lib.PlxGrid:
+        """Kernel descriptor.  with_lat (default: with_occ) builds the
+        lattice sigma mirror; once built it is always attached, so that the
+        optimisers keep it current."""
         g = _lib.PlxGrid()
         g.links = self._links.data_ptr()
         g.table = self.sh.data_ptr() if self.n_rows else None
@@ -302,11 +311,11 @@ class SparseGrid:
         g.scale = (ctypes.c_double * 3)(*self.lattice_scale)
         g.dmax = (ctypes.c_double * 3)(*(np.array(self.dims, dtype=np.float64) - 1.0))
         g.cell_occ = self.cell_occ().data_ptr() if (with_occ and USE_CELL_OCC) else None
-        if with_neg is None:
-            with_neg = with_occ and USE_CELL_OCC
-        if (with_neg or self._neg is not None) and self.n_rows:
-            neg, rc = self.neg_masks()
-            g.neg_bits = neg.data_ptr()
+        if with_lat is None:
+            with_lat = with_occ and USE_CELL_OCC
+        if (with_lat or self._lat is not None) and self.n_rows:
+            lat, rc = self.lattice_sigma()
+            g.sigma_lat = lat.data_ptr()
             g.row_cell = rc.data_ptr()
         return g
 

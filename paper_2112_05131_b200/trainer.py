@@ -433,7 +433,7 @@ class Trainer:
                 self.count.data_ptr(), st), "opt_step_list")
             return
         # p2p: owner-computes update over NVLink peer memory, then local clear
-        rc = self.grid.neg_masks()[1]
+        rc = self.grid.lattice_sigma()[1]
         _lib.check(L.plx_dp_owner_update(
             ctypes.byref(self._peers.peers), self.state.v.data_ptr(), rc.data_ptr(), lr_s, lr_c,
             self.state.beta, self.state.eps, rms, self.sums.data_ptr(), self.count.data_ptr(),

@@ -49,7 +49,7 @@ def _bounds(n, k, total=96):
 def _reference(grid_fn, rays, steps, method):
     from paper_2112_05131_b200 import optim
     g = grid_fn()
-    g.neg_masks()
+    g.lattice_sigma()
     st = px().OptimState(g.n_rows)
     touched = []
     for it in range(steps):
@@ -79,9 +79,9 @@ def _close(got, want, method):
 def _assert_same(got, want, method, st_got=None, st_want=None, rows=None):
     _close(got.density.cpu().numpy(), want.density.cpu().numpy(), method)
     _close(got.sh.cpu().numpy(), want.sh.cpu().numpy(), method)
-    neg = got.neg_masks()[0].clone()
-    got.invalidate()
-    assert torch.equal(neg, got.neg_masks()[0])
+    lat = got.lattice_sigma()[0].clone()
+    got.invalidate()   # the mirror kept by the exchange kernels == a rebuild
+    assert torch.equal(lat.view(torch.int32), got.lattice_sigma()[0].view(torch.int32))
     if st_got is not None and method == "rmsprop":
         lo, hi = rows
         _close(st_got.v[lo:hi].cpu().numpy(), st_want.v[lo:hi].cpu().numpy(), method)
@@ -108,12 +108,12 @@ def test_p2p_owner_update_equals_full_batch_step(n_ranks, method):
             p.tmask[k] = bufs[k].touched_mask.data_ptr()
             p.table[k] = reps[k].sh.data_ptr()
             p.density[k] = reps[k].density.data_ptr()
-            p.neg_bits[k] = reps[k].neg_masks()[0].data_ptr()
+            p.sigma_lat[k] = reps[k].lattice_sigma()[0].data_ptr()
         count = torch.zeros(1, dtype=torch.int64, device="cuda")
         for o in range(n_ranks):          # every owner reads all ranks' grads first
             p.rank = o
             _lib.check(L.plx_dp_owner_update(
-                ctypes.byref(p), states[o].v.data_ptr(), reps[o].neg_masks()[1].data_ptr(),
+                ctypes.byref(p), states[o].v.data_ptr(), reps[o].lattice_sigma()[1].data_ptr(),
                 0.7, 0.02, 0.95, 1e-8, int(method == "rmsprop"), None, count.data_ptr(),
                 _lib.stream_ptr()), "dp")
         torch.cuda.synchronize()
@@ -135,7 +135,7 @@ def test_union_packed_update_equals_full_batch_step(n_ranks, method):
     ref, ref_st, ref_touched = _reference(grid_fn, rays, steps=2, method=method)
     reps = [grid_fn() for _ in range(n_ranks)]
     for r in reps:
-        r.neg_masks()
+        r.lattice_sigma()
     states = [px().OptimState(reps[0].n_rows) for _ in range(n_ranks)]
     L, st = _lib.lib(), _lib.stream_ptr()
     R = reps[0].n_rows

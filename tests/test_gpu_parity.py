@@ -378,14 +378,15 @@ def test_fused_backward_long_rays_vs_oracle(interp):
                                  background=(0.2, 0.5, 0.9), interp=interp), lam=1e-4)
 
 
-def test_negative_density_bitmask_tracks_optimiser():
-    """neg_bits (lattice points occupied with density < 0) are kept current
-    by the optimiser as sigma changes sign, equal a from-scratch rebuild, and
-    the march with the dead-cell skip renders exactly like the march without."""
+def test_lattice_sigma_mirror_tracks_optimiser():
+    """sigma_lat (the lattice-indexed density mirror, NaN at empty points) is
+    kept current by the optimiser, equals a from-scratch rebuild bit for bit,
+    and the march reading corner sigmas from it renders exactly like the
+    march through links -> density."""
     from paper_2112_05131_b200 import optim
     rng = np.random.default_rng(17)
     g = dev_grid(random_grid(rng, dims=(13, 11, 12), holes=0.25, sigma_range=(-1.0, 1.0)))
-    neg, _ = g.neg_masks()
+    neg, _ = g.lattice_sigma()
     st = px().OptimState(g.n_rows)
     for it in range(4):
         buf = px().GradientBuffer(g.n_rows)
@@ -396,11 +397,11 @@ def test_negative_density_bitmask_tracks_optimiser():
         optim.step(g, buf, st, 0.5, 0.01, clear=True)
         kept = neg.clone()
         g.invalidate()                     # rebuild from scratch into the same buffer
-        assert torch.equal(kept, neg), it
+        assert torch.equal(kept.view(torch.int32), neg.view(torch.int32)), it
     o, d = ray_batch(rng, 128)
     with_skip = px().render_rays(g, o, d, px().RenderOptions(stop_thresh=0.0))
     from paper_2112_05131_b200 import grid as gmod
-    h = px().SparseGrid(g.links, g.table, g.aabb_min, g.aabb_max)   # fresh: no bitmasks
+    h = px().SparseGrid(g.links, g.table, g.aabb_min, g.aabb_max)   # fresh: no mirror
     old = gmod.USE_CELL_OCC
     gmod.USE_CELL_OCC = False
     try:
