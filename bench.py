@@ -263,22 +263,14 @@ def run_ours(args):
     kernel_events = []
     counts = torch.zeros(args.steps, dtype=torch.int64, device=dev)
 
-    # instrument the three launches of a step with events on the launching stream
-    orig_fused, orig_tv, orig_opt = render.fused_mse_backward_pool, losses.tv_loss, optim.step
-
-    def wrap(fn, name):
-        def inner(*a, **k):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            out = fn(*a, **k)
-            e1.record(stream)
-            kernel_events.append((name, e0, e1))
-            return out
-        return inner
-
-    render.fused_mse_backward_pool = wrap(orig_fused, "render_fused_bwd")
-    losses.tv_loss = wrap(orig_tv, "tv")
-    optim.step = wrap(orig_opt, "opt_step")
+    # per-kernel device times: plx_train_step records 4 events per step on the
+    # launching stream (before render, after render, after TV, after update)
+    ev_sets = []
+    for _ in range(args.steps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        for e in evs:
+            e.record(stream)     # materialise the cudaEvent_t handles
+        ev_sets.append(evs)
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
@@ -287,17 +279,20 @@ def run_ours(args):
     st0 = tr.march_stats.clone()
     t_ev0.record(stream)
     for k in range(args.steps):
+        tr.step_events = ev_sets[k]
         tr.step(args.warmup + k)
         counts[k].copy_(tr.count[0])
     t_ev1.record(stream)
+    tr.step_events = None
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    render.fused_mse_backward_pool, losses.tv_loss, optim.step = orig_fused, orig_tv, orig_opt
     march = ((tr.march_stats - st0).double() / args.steps).cpu().numpy()
     ms = t_ev0.elapsed_time(t_ev1) / args.steps
-    for name, e0, e1 in kernel_events:
-        per_kernel[name].append(e0.elapsed_time(e1))
+    for evs in ev_sets:
+        per_kernel["render_fused_bwd"].append(evs[0].elapsed_time(evs[1]))
+        per_kernel["tv"].append(evs[1].elapsed_time(evs[2]))
+        per_kernel["opt_step"].append(evs[2].elapsed_time(evs[3]))
     U = float(counts.double().mean().item())
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world_size > 1:

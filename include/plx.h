@@ -245,6 +245,30 @@ int plx_build_cell_occ(const plx_grid *g, uint32_t *cell_occ, void *stream);
 int plx_build_sigma_lat(const plx_grid *g, float *sigma_lat, void *stream);
 int plx_build_row_cell(const plx_grid *g, int32_t *row_cell, void *stream);
 
+/* One training step (T:441-486) as one call: zero sums[0..3], fused
+ * render + backward (mse_mode, up_scale), TV on the (start, count) run when
+ * tv_count > 0, and -- when update != 0 (single GPU; on N ranks the
+ * exchange runs in between and the update is separate) -- plx_opt_step with
+ * the fused clear and sums as the divergence guard.  events[0..3] (optional
+ * cudaEvent_t) are recorded before the render, after the render, after TV
+ * and after the update. */
+typedef struct {
+    plx_rays rays;
+    plx_render_opts opts;
+    double up_scale, lam_cauchy;
+    void *scratch;
+    int64_t scratch_bytes;
+    int64_t tv_start, tv_count;
+    double tv_fac[3], tv_eps, tv_f_sigma, tv_f_sh;
+    int32_t update, rmsprop;
+    float *v;
+    double lr_sigma, lr_sh, beta, eps;
+    double *sums;          /* device double[5]: 4 loss sums + sticky halt */
+    int64_t *count;        /* device int64: n_touched (may be NULL)       */
+    void *events[4];
+} plx_step_args;
+int plx_train_step(plx_grid *g, plx_grad *gb, const plx_step_args *a, void *stream);
+
 /* Library identification / self-check. */
 const char *plx_version(void);
 int plx_device_check(void);   /* 0 iff a CUDA device with cc >= 10.0 is present */

@@ -62,6 +62,20 @@ class PlxRays(ctypes.Structure):
                 ("n", ctypes.c_int64)]
 
 
+class PlxStepArgs(ctypes.Structure):
+    _fields_ = [("rays", PlxRays), ("opts", PlxRenderOpts), ("up_scale", ctypes.c_double),
+                ("lam_cauchy", ctypes.c_double), ("scratch", ctypes.c_void_p),
+                ("scratch_bytes", ctypes.c_int64), ("tv_start", ctypes.c_int64),
+                ("tv_count", ctypes.c_int64), ("tv_fac", ctypes.c_double * 3),
+                ("tv_eps", ctypes.c_double), ("tv_f_sigma", ctypes.c_double),
+                ("tv_f_sh", ctypes.c_double), ("update", ctypes.c_int32),
+                ("rmsprop", ctypes.c_int32), ("v", ctypes.c_void_p),
+                ("lr_sigma", ctypes.c_double), ("lr_sh", ctypes.c_double),
+                ("beta", ctypes.c_double), ("eps", ctypes.c_double),
+                ("sums", ctypes.c_void_p), ("count", ctypes.c_void_p),
+                ("events", ctypes.c_void_p * 4)]
+
+
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I32 = ctypes.c_int32
@@ -102,6 +116,8 @@ _SIGS = {
     "plx_build_cell_occ": [ctypes.POINTER(PlxGrid), _P, _P],
     "plx_build_sigma_lat": [ctypes.POINTER(PlxGrid), _P, _P],
     "plx_build_row_cell": [ctypes.POINTER(PlxGrid), _P, _P],
+    "plx_train_step": [ctypes.POINTER(PlxGrid), ctypes.POINTER(PlxGrad),
+                       ctypes.POINTER(PlxStepArgs), _P],
     "plx_version": [],
     "plx_device_check": [],
 }

@@ -853,6 +853,23 @@ extern "C" int plx_tv(const plx_grid *g, const int64_t *cells, int64_t start, in
     return status();
 }
 
+__global__ void count_from_list_kernel(const int64_t *tcnt, int64_t *out) {
+    if (threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long *>(out),
+                                    (unsigned long long)*tcnt);
+}
+
+// Zero the gradient rows of the compacted list (clear_grad, K:593-600):
+// 7 lanes x float4 per row, no loads.
+__global__ void clear_rows_kernel(float *grad, const int32_t *tids, const int64_t *tcnt) {
+    const int64_t n = *tcnt;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * 7;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / 7;
+        reinterpret_cast<float4 *>(grad + (int64_t)tids[j] * PLX_ROW)[t - j * 7] =
+            make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
 template <int UU, int MINB>
 static void launch_rows_t(const OptArgs &a, const int32_t *tids, const int64_t *tcnt,
                           cudaStream_t s) {
@@ -906,15 +923,29 @@ extern "C" int plx_opt_step(plx_grid *g, float *v, plx_grad *gb, double lr_sigma
 
 extern "C" int plx_clear_grad(plx_grad *gb, int64_t rows, int64_t *out_count, void *stream) {
     if (!gb || !gb->grad || !gb->tmask || rows < 0) return PLX_EINVAL;
+    if ((gb->tids == nullptr) != (gb->tcnt == nullptr)) return PLX_EINVAL;
     if (rows == 0) return PLX_OK;
+    constexpr int NT = 256;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (gb->tids) {   // compact + clear the mask, then zero the listed rows
+        if (cudaMemsetAsync(gb->tcnt, 0, sizeof(int64_t), s) != cudaSuccess) return PLX_ECUDA;
+        const int64_t nrange = ((rows + 127) / 128 + kCompactSegs - 1) / kCompactSegs;
+        int64_t nb = (nrange + NT / 32 - 1) / (NT / 32);
+        if (nb > (int64_t)num_sms() * 6) nb = (int64_t)num_sms() * 6;
+        touched_compact_kernel<<<(unsigned)nb, NT, 0, s>>>(gb->tmask, rows, gb->tids, gb->tcnt, 1,
+                                                          nullptr);
+        clear_rows_kernel<<<(unsigned)(num_sms() * 8), NT, 0, s>>>(gb->grad, gb->tids, gb->tcnt);
+        if (out_count)
+            count_from_list_kernel<<<1, 32, 0, s>>>(gb->tcnt, out_count);
+        return status();
+    }
     OptArgs a{nullptr, nullptr, nullptr, gb->grad, nullptr, nullptr, nullptr, gb->tmask, rows, 0.0, 0.0,
               0.0, 0.0, 0, 1, 0,
               reinterpret_cast<unsigned long long *>(out_count)};
-    constexpr int NT = 256;
     const int64_t segs = (rows + 127) / 128;
     int64_t nb = (segs + NT / 32 - 1) / (NT / 32);
     if (nb > (int64_t)num_sms() * opt_blocks_per_sm()) nb = (int64_t)num_sms() * opt_blocks_per_sm();
-    opt_kernel<NT><<<(unsigned)nb, NT, 0, (cudaStream_t)stream>>>(a);
+    opt_kernel<NT><<<(unsigned)nb, NT, 0, s>>>(a);
     return status();
 }
 

@@ -286,12 +286,14 @@ class Trainer:
         # march counters of the fused kernel, accumulated over steps:
         # {positions, samples, chunks, rays} (plx_render_opts.stats)
         self.march_stats = torch.zeros(4, dtype=torch.int64, device=self.device)
-        self._host_sums = [torch.zeros(4, dtype=torch.float64).pin_memory() for _ in range(2)]
-        self._sums_ready = [torch.cuda.Event(), torch.cuda.Event()]
-        self._pending = None
+        # pinned copies of the last steps' loss sums, checked two steps late
+        self._host_sums = [torch.zeros(4, dtype=torch.float64).pin_memory() for _ in range(3)]
+        self._sums_ready = [torch.cuda.Event() for _ in range(3)]
+        self._pending = []
         self.diverged_step = None
         self._peers = None
         self._dp_pack = None
+        self.step_events = None   # optional 4 torch.cuda.Events (plx_step_args.events)
         self._refresh_cache()
 
     def _refresh_cache(self):
@@ -300,6 +302,25 @@ class Trainer:
         self._cgrad = self.grads._c()
         self._kopts = render.kernel_opts(self.grid, self.opts)
         self._kopts.stats = self.march_stats.data_ptr()
+        # the native step descriptor (plx_train_step): static fields here,
+        # per-step fields (batch slice, TV run, learning rates) in step()
+        a = _lib.PlxStepArgs()
+        a.rays = self.pool.rays(None)
+        a.opts = self._kopts
+        a.lam_cauchy = self.cfg.lambda_sparsity
+        B_local = shard_range(self.cfg.batch_size, 0, self.world.size)[1]
+        sp, sn, self._scratch_keep = _lib.render_scratch(self._cgrid, self._kopts, B_local,
+                                                         self.device)
+        a.scratch, a.scratch_bytes = sp, sn
+        dims = self.grid.dims
+        a.tv_fac = (ctypes.c_double * 3)(*(d / 256.0 for d in dims))
+        a.tv_eps = losses.TV_EPS
+        a.rmsprop = int(self.cfg.optimizer == "rmsprop")
+        a.v = self.state.v.data_ptr()
+        a.beta, a.eps = self.state.beta, self.state.eps
+        a.sums = self.sums.data_ptr()
+        a.count = self.count.data_ptr()
+        self._step_args = a
         w = self.world
         if w.active and w.mode == "union":
             R = self.grid.n_rows
@@ -360,37 +381,52 @@ class Trainer:
         cfg = self.cfg
         idx = self.batcher.next_device()
         B = int(idx.numel())
-        jt = None
+        s0, c0 = shard_range(B, self.world.rank, self.world.size)
+        a = self._step_args
+        a.rays.idx = idx.data_ptr() + 8 * s0
+        a.rays.n = c0
+        a.rays.jitter = None
         if self.opts.jitter > 0:
             jt = torch.from_numpy(self.rng.random(B) * self.opts.jitter).to(self.device)
-        s0, c0 = shard_range(B, self.world.rank, self.world.size)
-        self.sums[0:4].zero_()
-        render.fused_mse_backward_pool(
-            self.grid, self.pool, idx[s0:s0 + c0], self.grads, self.opts, n_total=B,
-            lam_cauchy=cfg.lambda_sparsity, sums=self.sums[0:2],
-            jitter=None if jt is None else jt[s0:s0 + c0], kopts=self._kopts, cgrid=self._cgrid,
-            cgrad=self._cgrad)
+            self._jt_keep = jt
+            a.rays.jitter = jt.data_ptr() + 8 * s0
+        a.up_scale = 2.0 / B
         tv_on = (cfg.lambda_tv_sigma > 0 or cfg.lambda_tv_sh > 0) and (
             cfg.tv_until_step < 0 or step < cfg.tv_until_step)
         n_tv = 0
+        a.tv_count = 0
         if tv_on:
             run = losses.sample_tv_cells(self.grid, cfg.tv_sample_frac, self.rng)
             n_tv = run.count
             sub = run.split(self.world.rank, self.world.size)
-            if sub.count:
-                losses.tv_loss(self.grid, sub, cfg.lambda_tv_sigma, cfg.lambda_tv_sh,
-                               self.grads, sums=self.sums[2:4], n_norm=n_tv,
-                               _cgrid=self._cgrid_plain, _cgrad=self._cgrad)
-        slot = step & 1
-        self.exchange_update(step, slot)
+            a.tv_start, a.tv_count = sub.start, sub.count
+            a.tv_f_sigma, a.tv_f_sh = cfg.lambda_tv_sigma / n_tv, cfg.lambda_tv_sh / n_tv
+        a.update = int(not self.world.active)
+        a.lr_sigma = optim.lr_at(cfg.lr_sigma, step)
+        a.lr_sh = optim.lr_at(cfg.lr_sh, step)
+        ev = self.step_events
+        for i in range(4):
+            a.events[i] = ev[i].cuda_event if ev is not None else None
+        L = _lib.lib()
+        _lib.check(L.plx_train_step(ctypes.byref(self._cgrid), ctypes.byref(self._cgrad),
+                                    ctypes.byref(a), _lib.stream_ptr()), "train_step")
+        slot = step % 3
+        if self.world.active:
+            self.exchange_update(step, slot)
+            if ev is not None:
+                ev[3].record()    # "after update" = after the exchange + update
+        else:
+            self._host_sums[slot].copy_(self.sums[0:4], non_blocking=True)
+            self._sums_ready[slot].record()
         rec = {"B": B, "n_tv": n_tv}
         if sync:
             self.check_pending()
             self._sums_ready[slot].synchronize()
             rec.update(self._loss(step, slot, B, n_tv))
         elif check_finite:
-            self.check_pending()
-            self._pending = (step, slot, B, n_tv)
+            self._pending.append((step, slot, B, n_tv))
+            if len(self._pending) > 2:   # the host runs up to two steps ahead
+                self.check_pending(keep=2)
         return rec
 
     def exchange_update(self, step: int, slot: int | None = None) -> None:
@@ -454,11 +490,11 @@ class Trainer:
                                    f"tv=({tv_sig!r}, {tv_sh!r})")
         return {"loss": loss, "mse": loss_mse}
 
-    def check_pending(self) -> None:
-        """Check the loss of the last unchecked step (waits for that step only)."""
-        if self._pending is not None:
-            step, slot, B, n_tv = self._pending
-            self._pending = None
+    def check_pending(self, keep: int = 0) -> None:
+        """Check the losses of unchecked steps, oldest first, leaving the
+        newest `keep` pending (waits for those steps only)."""
+        while len(self._pending) > keep:
+            step, slot, B, n_tv = self._pending.pop(0)
             self._sums_ready[slot].synchronize()
             self._loss(step, slot, B, n_tv)
 

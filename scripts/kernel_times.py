@@ -42,3 +42,19 @@ for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
     tot += sum(v)
     print(f"{sum(v) / steps:9.1f} us/step  n/step={len(v) / steps:4.1f}  {k}")
 print(f"{tot / steps:9.1f} us/step total device time")
+
+# host cost of a step call vs the device step time (no profiler)
+import time  # noqa: E402
+
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda.synchronize()
+host = 0.0
+e0.record()
+for s in range(warm + steps, warm + 2 * steps):
+    h0 = time.perf_counter()
+    tr.step(s)
+    host += time.perf_counter() - h0
+e1.record()
+torch.cuda.synchronize()
+print(f"step {e0.elapsed_time(e1) * 1000 / steps:9.1f} us device-timed, "
+      f"{host * 1e6 / steps:9.1f} us host per tr.step() call")
