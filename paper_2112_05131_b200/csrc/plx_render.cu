@@ -180,22 +180,31 @@ __device__ __forceinline__ void composite_chunk(bool &incl, double att, int lane
 
 __device__ __forceinline__ double relu(double x) { return x > 0.0 ? x : 0.0; }
 
-// Per-warp-slot record list of the backward (SoA; capacity nrec = every
-// march position of the longest chord, R:67-69).  Phase A appends one
-// record per composited sample, B adds the colour, C consumes them.  These
-// replace the reference's per-call s_t / s_dlt / s_sig / s_T / s_w / s_cpre
-// scratch (K:259-264, R:277-278).
+// Record list of the backward (SoA; capacity cap per ray = every march
+// position of the longest chord, R:67-69; a batch is processed in waves of
+// rays so that the records fit a fixed budget).  The march kernel appends
+// one record per composited sample; the colour kernel adds the colour and
+// per-segment sums; the scatter kernel consumes them.  These replace the
+// reference's per-call s_t / s_dlt / s_sig / s_T / s_w / s_cpre scratch
+// (K:259-264, R:277-278).
 struct Scratch {
-    int *counter;      // dynamic ray scheduler (zeroed by the launcher)
-    double *att;       // exp(-sigma delta)                 [slots][nrec]
+    int *counter;      // ray scheduler of the march kernel (zeroed per wave)
+    int64_t cap;       // records per ray
+    int nseg_max;      // segments (32 records) per ray
+    int *ns;           // [rays] composited samples
+    int *seg_first;    // [rays] first segment of the ray (its segments are contiguous)
+    int *seg_ray;      // [segments] ray of each segment
+    int *nseg_total;   // segments allocated so far (zeroed per wave)
+    double *ray_d;     // [rays][3] {T after the march, delta and index of the last position}
+    double *att;       // exp(-sigma delta)                    [rays][cap]
     double *T;         // transmittance before the sample
     double *w;         // compositing weight
-    float4 *c;         // pre-clamp colour (phase B)
+    float4 *c;         // pre-clamp colour (colour kernel)
     int4 *cell;        // {i, j, k, position index}
     float4 *f;         // fractional offsets in the cell
-    int4 *rows;        // 8 stencil rows                     [slots][nrec][2]
+    int4 *rows;        // 8 stencil rows                       [rays][cap][2]
     double *sig;       // sigma (Cauchy term only)
-    int64_t nrec;
+    double *seg_sum;   // [segments][6] {sum w c+ (RGB), sum c+ (bn - bi) (RGB)}
 };
 
 // Per-warp shared staging of one chunk's scatter payload (pass 2).  The
@@ -415,28 +424,48 @@ __global__ void __launch_bounds__(128, 6)
     }
 }
 
-// The fused forward + MSE + backward (K:241-411), phases A / B / C above.
+// ---------------------------------------------------------------------------
+// The fused forward + MSE + backward (K:241-411) as three kernels:
+//   march_bwd_kernel   one warp per ray (dynamic scheduling): the sigma march
+//                      and compositing over positions; every composited
+//                      sample is appended to the ray's record list.
+//   colour_kernel      one warp per 32-record segment of any ray: colours of
+//                      the samples (8 SH rows x 7 float4, f32 FMAs) and the
+//                      segment's sums sum w c+ (and the absolute form's
+//                      sum c+ (bn - bi)).
+//   scatter_kernel     one warp per segment: rgb / upstream from the ray's
+//                      segment sums, the reverse-sweep suffix from the sums
+//                      of the segments before it, dL/dsigma and dL/dc, and
+//                      the lane-distributed scatter accumulator (flushed at
+//                      the segment's end).
+// The colour and scatter work -- ~24 us per 32 samples of dependent gathers
+// and in-order flushes -- is thus spread over all warps instead of being
+// serialised on the warp that marched a long ray (the single-kernel version
+// ran its last half with fewer than half of its warps active).
+// The march kernel allocates each ray's segments (contiguous, one atomic per
+// ray) and finishes the rays that composited nothing.
+
+#ifdef PLX_TIMELINE
+__device__ unsigned long long g_timeline[2 * 8192];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 template <bool ABS, bool NEAREST, int MINB>
 __global__ void __launch_bounds__(128, MINB)
-    bwd_kernel(DGrid G, RayArgs R, KOpts O, Outs out, Scratch S) {
+    march_bwd_kernel(DGrid G, RayArgs R, KOpts O, Outs out, Scratch S) {
     const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int64_t slot = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    double mse_part = 0.0, cau_part = 0.0;
+    double mse_part = 0.0;
+    const int64_t slot = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     unsigned st_pos = 0, st_samp = 0, st_chunks = 0, st_rays = 0;   // warp-uniform
     const unsigned lt_mask = (1u << lane) - 1u;
-    __shared__ SmemChunk smem_all[4];
-    SmemChunk &sc = smem_all[warp];
-    const bool cauchy = out.lam_cauchy > 0.0;
-    double *const r_att = S.att + slot * S.nrec;
-    double *const r_T = S.T + slot * S.nrec;
-    double *const r_w = S.w + slot * S.nrec;
-    float4 *const r_c = S.c + slot * S.nrec;
-    int4 *const r_cell = S.cell + slot * S.nrec;
-    float4 *const r_f = S.f + slot * S.nrec;
-    int4 *const r_rows = S.rows + 2 * slot * S.nrec;
-    double *const r_sig = S.sig + slot * S.nrec;
-
+    const bool cauchy = S.sig != nullptr;
+#ifdef PLX_TIMELINE
+    const unsigned long long t_start = gtimer();
+#endif
     for (;;) {
         int rr = 0;   // dynamic scheduling: rays differ widely in length
         if (lane == 0) rr = atomicAdd(S.counter, 1);
@@ -452,10 +481,9 @@ __global__ void __launch_bounds__(128, MINB)
         }
         const double jit = R.jitter ? R.jitter[ray] : 0.0;
         ray_march_setup(rm, G, O.step, jit);
-
-        // ---------------- A: sigma march + compositing (K:285-323) ----------------
+        const int64_t rb = ray * S.cap;   // this ray's record block
         double T = 1.0, A = 0.0;
-        int ns = 0;   // composited samples (records)
+        int ns = 0;
         bool stopped = false;
         for (int64_t base = 0; base < rm.nsamp && !stopped; base += 32) {
             const int64_t si = base + lane;
@@ -485,108 +513,226 @@ __global__ void __launch_bounds__(128, MINB)
             st_samp += __popc(m);
             if (incl) {
                 if (!rows_ok) load_rows<NEAREST>(G, ijk, rows);
-                const int k = ns + __popc(m & lt_mask);
-                r_att[k] = att;
-                r_T[k] = Ti;
-                r_w[k] = wi;
-                r_cell[k] = make_int4(ijk[0], ijk[1], ijk[2], (int)si);
+                const int64_t k = rb + ns + __popc(m & lt_mask);
+                S.att[k] = att;
+                S.T[k] = Ti;
+                S.w[k] = wi;
+                S.cell[k] = make_int4(ijk[0], ijk[1], ijk[2], (int)si);
                 if (!NEAREST) {
-                    r_f[k] = make_float4((float)fd[0], (float)fd[1], (float)fd[2], 0.f);
-                    r_rows[2 * k] = make_int4(rows[0], rows[1], rows[2], rows[3]);
-                    r_rows[2 * k + 1] = make_int4(rows[4], rows[5], rows[6], rows[7]);
+                    S.f[k] = make_float4((float)fd[0], (float)fd[1], (float)fd[2], 0.f);
+                    S.rows[2 * k] = make_int4(rows[0], rows[1], rows[2], rows[3]);
+                    S.rows[2 * k + 1] = make_int4(rows[4], rows[5], rows[6], rows[7]);
                 } else {
-                    r_rows[2 * k] = make_int4(rows[0], -1, -1, -1);
+                    S.rows[2 * k] = make_int4(rows[0], -1, -1, -1);
                 }
-                if (cauchy) r_sig[k] = sig;
+                if (cauchy) S.sig[k] = sig;
             }
             ns += __popc(m);
         }
-
-        // ---------------- B: colour over the dense sample list (K:305-320) ----------------
-        float bf[9];   // SH basis (K:27-37) in float64, used as f32 by the colour FMAs
-        {
-            double basis[9];
-            sh_basis9(__ldg(R.viewdirs + 3 * src), __ldg(R.viewdirs + 3 * src + 1),
-                      __ldg(R.viewdirs + 3 * src + 2), basis);
-#pragma unroll
-            for (int b = 0; b < 9; ++b) bf[b] = (float)basis[b];
-        }
-        double C0 = 0.0, C1 = 0.0, C2 = 0.0;
-        double Q0 = 0.0, Q1 = 0.0, Q2 = 0.0;   // absolute backward: sum c(bn - bi)
-        __syncwarp();
-        for (int g0 = 0; g0 < ns; g0 += 32) {
-            const int j = g0 + lane;
-            double x0 = 0.0, x1 = 0.0, x2 = 0.0;
-            if (j < ns) {
-                const int4 ra = r_rows[2 * j];
-                const int4 rb = NEAREST ? make_int4(-1, -1, -1, -1) : r_rows[2 * j + 1];
-                const int32_t rows[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-                float4 f4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (!NEAREST) f4 = r_f[j];
-                float c0 = 0.f, c1 = 0.f, c2 = 0.f;
-                constexpr int NQ = NEAREST ? 1 : 8;
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    const int32_t r = rows[q];
-                    if (r < 0) continue;
-                    const float4 *row = reinterpret_cast<const float4 *>(G.table + (int64_t)r * PLX_ROW);
-                    const float4 v0 = __ldg(row + 0), v1 = __ldg(row + 1), v2 = __ldg(row + 2),
-                                 v3 = __ldg(row + 3), v4 = __ldg(row + 4), v5 = __ldg(row + 5),
-                                 v6 = __ldg(row + 6);
-                    // row layout: [-, R0..R8, G0..G8, B0..B8]  (_color_at, K:138-152)
-                    float a0 = bf[0] * v0.y, a1 = bf[0] * v2.z, a2 = bf[0] * v4.w;
-                    a0 = __fmaf_rn(bf[1], v0.z, a0);
-                    a1 = __fmaf_rn(bf[1], v2.w, a1);
-                    a2 = __fmaf_rn(bf[1], v5.x, a2);
-                    a0 = __fmaf_rn(bf[2], v0.w, a0);
-                    a1 = __fmaf_rn(bf[2], v3.x, a1);
-                    a2 = __fmaf_rn(bf[2], v5.y, a2);
-                    a0 = __fmaf_rn(bf[3], v1.x, a0);
-                    a1 = __fmaf_rn(bf[3], v3.y, a1);
-                    a2 = __fmaf_rn(bf[3], v5.z, a2);
-                    a0 = __fmaf_rn(bf[4], v1.y, a0);
-                    a1 = __fmaf_rn(bf[4], v3.z, a1);
-                    a2 = __fmaf_rn(bf[4], v5.w, a2);
-                    a0 = __fmaf_rn(bf[5], v1.z, a0);
-                    a1 = __fmaf_rn(bf[5], v3.w, a1);
-                    a2 = __fmaf_rn(bf[5], v6.x, a2);
-                    a0 = __fmaf_rn(bf[6], v1.w, a0);
-                    a1 = __fmaf_rn(bf[6], v4.x, a1);
-                    a2 = __fmaf_rn(bf[6], v6.y, a2);
-                    a0 = __fmaf_rn(bf[7], v2.x, a0);
-                    a1 = __fmaf_rn(bf[7], v4.y, a1);
-                    a2 = __fmaf_rn(bf[7], v6.z, a2);
-                    a0 = __fmaf_rn(bf[8], v2.y, a0);
-                    a1 = __fmaf_rn(bf[8], v4.z, a1);
-                    a2 = __fmaf_rn(bf[8], v6.w, a2);
-                    float w = 1.f;
-                    if (!NEAREST)
-                        w = ((q & 4) ? f4.x : 1.f - f4.x) * ((q & 2) ? f4.y : 1.f - f4.y) *
-                            ((q & 1) ? f4.z : 1.f - f4.z);
-                    c0 = __fmaf_rn(w, a0, c0);
-                    c1 = __fmaf_rn(w, a1, c1);
-                    c2 = __fmaf_rn(w, a2, c2);
+        // segments of 32 records, contiguous per ray, handed to the colour
+        // and scatter kernels through seg_ray
+        const int nseg = (ns + 31) >> 5;
+        int sbase = 0;
+        if (lane == 0) {
+            S.ns[ray] = ns;
+            S.ray_d[3 * ray] = T;
+            S.ray_d[3 * ray + 1] = rm.L - O.step * (double)(rm.nsamp - 1);   // K:200-205
+            S.ray_d[3 * ray + 2] = (double)(rm.nsamp - 1);
+            if (nseg) sbase = atomicAdd(S.nseg_total, nseg);
+            S.seg_first[ray] = sbase;
+            if (ns == 0) {   // nothing composited: rgb = T bg (K:324-341), no gradient
+                const double c0 = T * O.bg[0], c1 = T * O.bg[1], c2 = T * O.bg[2];
+                if (out.rgb) {
+                    out.rgb[3 * ray] = c0;
+                    out.rgb[3 * ray + 1] = c1;
+                    out.rgb[3 * ray + 2] = c2;
                 }
-                r_c[j] = make_float4(c0, c1, c2, 0.f);
-                const double wi = r_w[j];
-                const double cr0 = relu((double)c0), cr1 = relu((double)c1), cr2 = relu((double)c2);
-                x0 = wi * cr0;
-                x1 = wi * cr1;
-                x2 = wi * cr2;
-                if (ABS) {
-                    const double Ti = r_T[j];
-                    const double bn = (Ti - wi) > 0.0 ? 1.0 : 0.0, bi = Ti > 0.0 ? 1.0 : 0.0;
-                    Q0 += cr0 * (bn - bi);
-                    Q1 += cr1 * (bn - bi);
-                    Q2 += cr2 * (bn - bi);
+                if (out.mse_mode) {
+                    const double e0 = c0 - R.target[3 * src], e1 = c1 - R.target[3 * src + 1],
+                                 e2 = c2 - R.target[3 * src + 2];
+                    mse_part += e0 * e0 + e1 * e1 + e2 * e2;
                 }
             }
-            C0 += warp_sum(x0);
-            C1 += warp_sum(x1);
-            C2 += warp_sum(x2);
         }
-        const double rgb0 = C0 + T * O.bg[0], rgb1 = C1 + T * O.bg[1], rgb2 = C2 + T * O.bg[2];
-        if (lane == 0 && out.rgb) {
+        sbase = __shfl_sync(PLX_FULL_MASK, sbase, 0);
+        for (int k = lane; k < nseg; k += 32) S.seg_ray[sbase + k] = (int)ray;
+    }
+#ifdef PLX_TIMELINE
+    if (lane == 0 && slot < 8192) {
+        g_timeline[2 * slot] = t_start;
+        g_timeline[2 * slot + 1] = gtimer();
+    }
+#endif
+    if (O.stats && lane == 0) {
+        atomicAdd(O.stats + 0, (unsigned long long)st_pos);
+        atomicAdd(O.stats + 1, (unsigned long long)st_samp);
+        atomicAdd(O.stats + 2, (unsigned long long)st_chunks);
+        atomicAdd(O.stats + 3, (unsigned long long)st_rays);
+    }
+    if (lane == 0 && mse_part != 0.0) atomicAdd(out.sums + 0, mse_part);
+}
+
+__device__ __forceinline__ void ray_basis(const RayArgs &R, int64_t src, float *bf) {
+    double basis[9];   // K:27-37 in float64, used as f32 by the colour FMAs
+    sh_basis9(__ldg(R.viewdirs + 3 * src), __ldg(R.viewdirs + 3 * src + 1),
+              __ldg(R.viewdirs + 3 * src + 2), basis);
+#pragma unroll
+    for (int b = 0; b < 9; ++b) bf[b] = (float)basis[b];
+}
+
+template <bool ABS, bool NEAREST, int MINB>
+__global__ void __launch_bounds__(128, MINB)
+    colour_kernel(DGrid G, RayArgs R, Scratch S) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nseg = *S.nseg_total;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t sg = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); sg < nseg;
+         sg += nw) {
+        const int64_t ray = S.seg_ray[sg];
+        const int64_t src = R.idx ? R.idx[ray] : ray;
+        const int j = (int)(sg - S.seg_first[ray]) * 32 + lane;
+        float bf[9];
+        ray_basis(R, src, bf);
+        double x0 = 0.0, x1 = 0.0, x2 = 0.0, q0 = 0.0, q1 = 0.0, q2 = 0.0;
+        if (j < S.ns[ray]) {
+            const int64_t k = ray * S.cap + j;
+            const int4 ra = S.rows[2 * k];
+            const int4 rb = NEAREST ? make_int4(-1, -1, -1, -1) : S.rows[2 * k + 1];
+            const int32_t rows[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+            float4 f4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (!NEAREST) f4 = S.f[k];
+            float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+            constexpr int NQ = NEAREST ? 1 : 8;
+            // Unconditional loads (an empty corner reads row 0 with weight 0):
+            // without the per-corner branch the compiler keeps several
+            // corners' 7 float4 in flight instead of one round trip each.
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int32_t r = rows[q] >= 0 ? rows[q] : 0;
+                const float4 *row = reinterpret_cast<const float4 *>(G.table + (int64_t)r * PLX_ROW);
+                const float4 v0 = __ldg(row + 0), v1 = __ldg(row + 1), v2 = __ldg(row + 2),
+                             v3 = __ldg(row + 3), v4 = __ldg(row + 4), v5 = __ldg(row + 5),
+                             v6 = __ldg(row + 6);
+                // row layout: [-, R0..R8, G0..G8, B0..B8]  (_color_at, K:138-152)
+                float a0 = bf[0] * v0.y, a1 = bf[0] * v2.z, a2 = bf[0] * v4.w;
+                a0 = __fmaf_rn(bf[1], v0.z, a0);
+                a1 = __fmaf_rn(bf[1], v2.w, a1);
+                a2 = __fmaf_rn(bf[1], v5.x, a2);
+                a0 = __fmaf_rn(bf[2], v0.w, a0);
+                a1 = __fmaf_rn(bf[2], v3.x, a1);
+                a2 = __fmaf_rn(bf[2], v5.y, a2);
+                a0 = __fmaf_rn(bf[3], v1.x, a0);
+                a1 = __fmaf_rn(bf[3], v3.y, a1);
+                a2 = __fmaf_rn(bf[3], v5.z, a2);
+                a0 = __fmaf_rn(bf[4], v1.y, a0);
+                a1 = __fmaf_rn(bf[4], v3.z, a1);
+                a2 = __fmaf_rn(bf[4], v5.w, a2);
+                a0 = __fmaf_rn(bf[5], v1.z, a0);
+                a1 = __fmaf_rn(bf[5], v3.w, a1);
+                a2 = __fmaf_rn(bf[5], v6.x, a2);
+                a0 = __fmaf_rn(bf[6], v1.w, a0);
+                a1 = __fmaf_rn(bf[6], v4.x, a1);
+                a2 = __fmaf_rn(bf[6], v6.y, a2);
+                a0 = __fmaf_rn(bf[7], v2.x, a0);
+                a1 = __fmaf_rn(bf[7], v4.y, a1);
+                a2 = __fmaf_rn(bf[7], v6.z, a2);
+                a0 = __fmaf_rn(bf[8], v2.y, a0);
+                a1 = __fmaf_rn(bf[8], v4.z, a1);
+                a2 = __fmaf_rn(bf[8], v6.w, a2);
+                float w = 1.f;
+                if (!NEAREST)
+                    w = ((q & 4) ? f4.x : 1.f - f4.x) * ((q & 2) ? f4.y : 1.f - f4.y) *
+                        ((q & 1) ? f4.z : 1.f - f4.z);
+                if (rows[q] < 0) w = 0.f;   // K:131: empty corners contribute nothing
+                c0 = __fmaf_rn(w, a0, c0);
+                c1 = __fmaf_rn(w, a1, c1);
+                c2 = __fmaf_rn(w, a2, c2);
+            }
+            S.c[k] = make_float4(c0, c1, c2, 0.f);
+            const double wi = S.w[k];
+            const double cr0 = relu((double)c0), cr1 = relu((double)c1), cr2 = relu((double)c2);
+            x0 = wi * cr0;   // K:224-229: only the positive part is accumulated
+            x1 = wi * cr1;
+            x2 = wi * cr2;
+            if (ABS) {
+                const double Ti = S.T[k];
+                const double bn = (Ti - wi) > 0.0 ? 1.0 : 0.0, bi = Ti > 0.0 ? 1.0 : 0.0;
+                q0 = cr0 * (bn - bi);
+                q1 = cr1 * (bn - bi);
+                q2 = cr2 * (bn - bi);
+            }
+        }
+        x0 = warp_sum(x0);
+        x1 = warp_sum(x1);
+        x2 = warp_sum(x2);
+        if (ABS) {
+            q0 = warp_sum(q0);
+            q1 = warp_sum(q1);
+            q2 = warp_sum(q2);
+        }
+        if (lane == 0) {
+            double *o = S.seg_sum + 6 * sg;
+            o[0] = x0;
+            o[1] = x1;
+            o[2] = x2;
+            o[3] = q0;
+            o[4] = q1;
+            o[5] = q2;
+        }
+    }
+}
+
+template <bool ABS, bool NEAREST, int MINB>
+__global__ void __launch_bounds__(128, MINB)
+    scatter_kernel(DGrid G, RayArgs R, KOpts O, Outs out, Scratch S) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const bool cauchy = S.sig != nullptr;
+    __shared__ SmemChunk smem_all[4];
+    SmemChunk &sc = smem_all[warp];
+    double mse_part = 0.0, cau_part = 0.0;
+    const int64_t nseg = *S.nseg_total;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t sg = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; sg < nseg; sg += nw) {
+        const int64_t ray = S.seg_ray[sg];
+        const int64_t src = R.idx ? R.idx[ray] : ray;
+        const int ns_r = S.ns[ray];
+        const int64_t s0 = S.seg_first[ray], s1 = s0 + ((ns_r + 31) >> 5);
+        // ray totals and the prefix of the segments before this one
+        double C0 = 0.0, C1 = 0.0, C2 = 0.0, Q0 = 0.0, Q1 = 0.0, Q2 = 0.0;
+        double B0 = 0.0, B1 = 0.0, B2 = 0.0;
+        for (int64_t t = s0 + lane; t < s1; t += 32) {
+            const double *p = S.seg_sum + 6 * t;
+            C0 += p[0];
+            C1 += p[1];
+            C2 += p[2];
+            if (ABS) {
+                Q0 += p[3];
+                Q1 += p[4];
+                Q2 += p[5];
+            }
+            if (t < sg) {   // before this segment: P (relative) / Q prefix (absolute)
+                B0 += ABS ? p[3] : p[0];
+                B1 += ABS ? p[4] : p[1];
+                B2 += ABS ? p[5] : p[2];
+            }
+        }
+        C0 = warp_sum(C0);
+        C1 = warp_sum(C1);
+        C2 = warp_sum(C2);
+        if (ABS) {
+            Q0 = warp_sum(Q0);
+            Q1 = warp_sum(Q1);
+            Q2 = warp_sum(Q2);
+        }
+        double P0 = warp_sum(B0), P1 = warp_sum(B1), P2 = warp_sum(B2);
+        const double Tfin = S.ray_d[3 * ray], dlt_last = S.ray_d[3 * ray + 1],
+                     last_si = S.ray_d[3 * ray + 2];
+        const double rgb0 = C0 + Tfin * O.bg[0], rgb1 = C1 + Tfin * O.bg[1],
+                     rgb2 = C2 + Tfin * O.bg[2];
+        const bool first = sg == s0;
+        if (first && lane == 0 && out.rgb) {
             out.rgb[3 * ray + 0] = rgb0;
             out.rgb[3 * ray + 1] = rgb1;
             out.rgb[3 * ray + 2] = rgb2;
@@ -597,7 +743,7 @@ __global__ void __launch_bounds__(128, MINB)
             const double e0 = rgb0 - __ldg(R.target + 3 * src + 0);
             const double e1 = rgb1 - __ldg(R.target + 3 * src + 1);
             const double e2 = rgb2 - __ldg(R.target + 3 * src + 2);
-            if (lane == 0) mse_part += e0 * e0 + e1 * e1 + e2 * e2;
+            if (first && lane == 0) mse_part += e0 * e0 + e1 * e1 + e2 * e2;
             up0 = out.up_scale * e0;
             up1 = out.up_scale * e1;
             up2 = out.up_scale * e2;
@@ -606,159 +752,128 @@ __global__ void __launch_bounds__(128, MINB)
             up1 = __ldg(R.target + 3 * src + 1);
             up2 = __ldg(R.target + 3 * src + 2);
         }
-        if (ABS) {
-            Q0 = warp_sum(Q0);
-            Q1 = warp_sum(Q1);
-            Q2 = warp_sum(Q2);
-        }
-
-        // ---------------- C: reverse sweep + scatter (K:343-410) ----------------
+        // ---------------- reverse sweep + scatter (K:343-410) ----------------
         // sf before sample i in the reference's reverse sweep:
         //   relative: T bg + sum_{j>i} w_j c_j = rgb - P_i      (K:351-353, 381-383)
         //   absolute: -bg [T>0] + sum_{j>i} c_j (bn_j - bi_j)   (K:346-349, 374-376)
-        const double bend = T > 0.0 ? 1.0 : 0.0;
-        const double dlt_last = rm.L - O.step * (double)(rm.nsamp - 1);
+        const double bend = Tfin > 0.0 ? 1.0 : 0.0;
+        float bf[9];
+        ray_basis(R, src, bf);
         LaneAcc<NEAREST> ra;
         ra.init(lane, bf);
-        double P0 = 0.0, P1 = 0.0, P2 = 0.0;
-        int pci = 0, pcj = 0, pck = 0;   // carried: previous sample's cell
-        bool pvalid = false;
-        int cflip = 0;                   // carried corner relabelling
-        for (int g0 = 0; g0 < ns; g0 += 32) {
-            const int j = g0 + lane;
-            const bool incl = j < ns;
-            const unsigned mask = __ballot_sync(PLX_FULL_MASK, incl);
-            double att = 1.0, Ti = 0.0, wi = 0.0, sig = 0.0;
-            float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f), f4 = c4;
-            int4 cl = make_int4(0, 0, 0, 0);
-            if (incl) {
-                att = r_att[j];
-                Ti = r_T[j];
-                wi = r_w[j];
-                c4 = r_c[j];
-                cl = r_cell[j];
-                if (!NEAREST) {
-                    f4 = r_f[j];
-                    *reinterpret_cast<int4 *>(&sc.rows[lane][0]) = r_rows[2 * j];
-                    *reinterpret_cast<int4 *>(&sc.rows[lane][4]) = r_rows[2 * j + 1];
-                } else {
-                    sc.rows[lane][0] = r_rows[2 * j].x;
-                }
-                if (cauchy) sig = r_sig[j];
-            }
-            const double dlt = cl.w < rm.nsamp - 1 ? O.step : dlt_last;   // K:200-205
-            const double cc0 = relu((double)c4.x), cc1 = relu((double)c4.y),
-                         cc2 = relu((double)c4.z);
-            double gsig;
-            if (!ABS) {
-                const double y0 = incl ? wi * cc0 : 0.0, y1 = incl ? wi * cc1 : 0.0,
-                             y2 = incl ? wi * cc2 : 0.0;
-                const double i0 = P0 + warp_scan_add(y0, lane), i1 = P1 + warp_scan_add(y1, lane),
-                             i2 = P2 + warp_scan_add(y2, lane);
-                P0 = __shfl_sync(PLX_FULL_MASK, i0, 31);
-                P1 = __shfl_sync(PLX_FULL_MASK, i1, 31);
-                P2 = __shfl_sync(PLX_FULL_MASK, i2, 31);
-                const double sf0 = rgb0 - i0, sf1 = rgb1 - i1, sf2 = rgb2 - i2;
-                gsig = dlt * (up0 * (Ti * att * cc0 - sf0) + up1 * (Ti * att * cc1 - sf1) +
-                              up2 * (Ti * att * cc2 - sf2));
+        const int j = (int)(sg - s0) * 32 + lane;
+        const bool incl = j < ns_r;
+        const unsigned mask = __ballot_sync(PLX_FULL_MASK, incl);
+        double att = 1.0, Ti = 0.0, wi = 0.0, sig = 0.0;
+        float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f), f4 = c4;
+        int4 cl = make_int4(0, 0, 0, 0);
+        if (incl) {
+            const int64_t k = ray * S.cap + j;
+            att = S.att[k];
+            Ti = S.T[k];
+            wi = S.w[k];
+            c4 = S.c[k];
+            cl = S.cell[k];
+            if (!NEAREST) {
+                f4 = S.f[k];
+                *reinterpret_cast<int4 *>(&sc.rows[lane][0]) = S.rows[2 * k];
+                *reinterpret_cast<int4 *>(&sc.rows[lane][4]) = S.rows[2 * k + 1];
             } else {
-                const double Tn = Ti - wi;
-                const double bn = Tn > 0.0 ? 1.0 : 0.0, bi = Ti > 0.0 ? 1.0 : 0.0;
-                const double y0 = incl ? cc0 * (bn - bi) : 0.0, y1 = incl ? cc1 * (bn - bi) : 0.0,
-                             y2 = incl ? cc2 * (bn - bi) : 0.0;
-                const double i0 = P0 + warp_scan_add(y0, lane), i1 = P1 + warp_scan_add(y1, lane),
-                             i2 = P2 + warp_scan_add(y2, lane);
-                P0 = __shfl_sync(PLX_FULL_MASK, i0, 31);
-                P1 = __shfl_sync(PLX_FULL_MASK, i1, 31);
-                P2 = __shfl_sync(PLX_FULL_MASK, i2, 31);
-                const double sf0 = -O.bg[0] * bend + (Q0 - i0);
-                const double sf1 = -O.bg[1] * bend + (Q1 - i1);
-                const double sf2 = -O.bg[2] * bend + (Q2 - i2);
-                const double galpha =
-                    (up0 * (cc0 * bn + sf0) + up1 * (cc1 * bn + sf1) + up2 * (cc2 * bn + sf2));
-                gsig = galpha * dlt * att;
+                sc.rows[lane][0] = S.rows[2 * k].x;
             }
-            if (incl && cauchy) {   // K:384-386
-                cau_part += log(1.0 + 2.0 * sig * sig);
-                gsig += out.lam_cauchy * 4.0 * sig / (1.0 + 2.0 * sig * sig);
-            }
-            // ---- lane-parallel staging of the scatter payload (K:387-410) ----
-            // move code vs the previous sample (this group or carried)
-            const unsigned below = mask & lt_mask;
-            const int pl = below ? lane - 1 : lane;   // the list is dense
-            const int qi = __shfl_sync(PLX_FULL_MASK, cl.x, pl);
-            const int qj = __shfl_sync(PLX_FULL_MASK, cl.y, pl);
-            const int qk = __shfl_sync(PLX_FULL_MASK, cl.z, pl);
-            int mv = 0;
-            if (incl) {
-                const bool hasp = below != 0u || pvalid;
-                const int pi = below ? qi : pci, pj = below ? qj : pcj, pk = below ? qk : pck;
-                if (!hasp) {
-                    mv = MV_FAR;
-                } else {
-                    const int di = cl.x - pi, dj = cl.y - pj, dk = cl.z - pk;
-                    if (di | dj | dk) {
-                        const bool adj = !NEAREST && di >= -1 && di <= 1 && dj >= -1 && dj <= 1 &&
-                                         dk >= -1 && dk <= 1;
-                        mv = adj ? (MV_ADJ | ((di + 1) << 4) | ((dj + 1) << 2) | (dk + 1)) : MV_FAR;
-                    }
-                }
-                sc.mv[lane] = mv;
-            }
-            // flip in effect when sample `lane` is added: carried ^ prefix xor
-            int fx = incl ? axis_bits(mv) : 0;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int y = __shfl_up_sync(PLX_FULL_MASK, fx, off);
-                if (lane >= off) fx ^= y;
-            }
-            const int fl = cflip ^ fx;
-            if (incl) {
-                const float gk[4] = {(float)gsig, c4.x > 0.f ? (float)(up0 * wi) : 0.f,
-                                     c4.y > 0.f ? (float)(up1 * wi) : 0.f,
-                                     c4.z > 0.f ? (float)(up2 * wi) : 0.f};
-                if (NEAREST) {
-#pragma unroll
-                    for (int L = 0; L < 32; ++L) sc.val[L][lane] = L < 4 ? gk[L] : 0.f;
-                } else {
-                    // corner e = q ^ fl of physical slot q: xor-ing a bit of the
-                    // corner index swaps (1 - f, f) on that axis
-                    const float lx = (fl & 4) ? f4.x : 1.f - f4.x, hx = (fl & 4) ? 1.f - f4.x : f4.x;
-                    const float ly = (fl & 2) ? f4.y : 1.f - f4.y, hy = (fl & 2) ? 1.f - f4.y : f4.y;
-                    const float lz = (fl & 1) ? f4.z : 1.f - f4.z, hz = (fl & 1) ? 1.f - f4.z : f4.z;
-#pragma unroll
-                    for (int qs = 0; qs < 8; ++qs) {
-                        const float w = ((qs & 4) ? hx : lx) * ((qs & 2) ? hy : ly) *
-                                        ((qs & 1) ? hz : lz);
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) sc.val[4 * qs + kk][lane] = w * gk[kk];
-                    }
+            if (cauchy) sig = S.sig[k];
+        }
+        // delta of this sample (K:200-205): step, except at the last position
+        const double dl = (double)cl.w == last_si ? dlt_last : O.step;
+        const double cc0 = relu((double)c4.x), cc1 = relu((double)c4.y),
+                     cc2 = relu((double)c4.z);
+        double gsig;
+        if (!ABS) {
+            const double y0 = incl ? wi * cc0 : 0.0, y1 = incl ? wi * cc1 : 0.0,
+                         y2 = incl ? wi * cc2 : 0.0;
+            const double i0 = P0 + warp_scan_add(y0, lane), i1 = P1 + warp_scan_add(y1, lane),
+                         i2 = P2 + warp_scan_add(y2, lane);
+            const double sf0 = rgb0 - i0, sf1 = rgb1 - i1, sf2 = rgb2 - i2;
+            gsig = dl * (up0 * (Ti * att * cc0 - sf0) + up1 * (Ti * att * cc1 - sf1) +
+                         up2 * (Ti * att * cc2 - sf2));
+        } else {
+            const double Tn = Ti - wi;
+            const double bn = Tn > 0.0 ? 1.0 : 0.0, bi = Ti > 0.0 ? 1.0 : 0.0;
+            const double y0 = incl ? cc0 * (bn - bi) : 0.0, y1 = incl ? cc1 * (bn - bi) : 0.0,
+                         y2 = incl ? cc2 * (bn - bi) : 0.0;
+            const double i0 = P0 + warp_scan_add(y0, lane), i1 = P1 + warp_scan_add(y1, lane),
+                         i2 = P2 + warp_scan_add(y2, lane);
+            const double sf0 = -O.bg[0] * bend + (Q0 - i0);
+            const double sf1 = -O.bg[1] * bend + (Q1 - i1);
+            const double sf2 = -O.bg[2] * bend + (Q2 - i2);
+            const double galpha =
+                (up0 * (cc0 * bn + sf0) + up1 * (cc1 * bn + sf1) + up2 * (cc2 * bn + sf2));
+            gsig = galpha * dl * att;
+        }
+        if (incl && cauchy) {   // K:384-386
+            cau_part += log(1.0 + 2.0 * sig * sig);
+            gsig += out.lam_cauchy * 4.0 * sig / (1.0 + 2.0 * sig * sig);
+        }
+        // ---- lane-parallel staging of the scatter payload (K:387-410) ----
+        const unsigned below = mask & lt_mask;
+        const int pl = below ? lane - 1 : lane;   // the list is dense
+        const int qi = __shfl_sync(PLX_FULL_MASK, cl.x, pl);
+        const int qj = __shfl_sync(PLX_FULL_MASK, cl.y, pl);
+        const int qk = __shfl_sync(PLX_FULL_MASK, cl.z, pl);
+        int mv = 0;
+        if (incl) {
+            if (!below) {
+                mv = MV_FAR;   // segment start: nothing carried
+            } else {
+                const int di = cl.x - qi, dj = cl.y - qj, dk = cl.z - qk;
+                if (di | dj | dk) {
+                    const bool adj = !NEAREST && di >= -1 && di <= 1 && dj >= -1 && dj <= 1 &&
+                                     dk >= -1 && dk <= 1;
+                    mv = adj ? (MV_ADJ | ((di + 1) << 4) | ((dj + 1) << 2) | (dk + 1)) : MV_FAR;
                 }
             }
-            // carry to the next group
-            const int hl = 31 - __clz(mask);
-            cflip = __shfl_sync(PLX_FULL_MASK, fl, hl);
-            pci = __shfl_sync(PLX_FULL_MASK, cl.x, hl);
-            pcj = __shfl_sync(PLX_FULL_MASK, cl.y, hl);
-            pck = __shfl_sync(PLX_FULL_MASK, cl.z, hl);
-            pvalid = true;
-            __syncwarp();
-            // ---- serial, in sample order: moves (flushes) + one add ----
-            const int n = __popc(mask);
-            for (int jj = 0; jj < n; ++jj) {
-                const int mvj = sc.mv[jj];
-                if (mvj) ra.move(mvj, sc, jj, out.grad, out.tmask, lane);
-                ra.acc += sc.val[lane][jj];
+            sc.mv[lane] = mv;
+        }
+        // flip in effect when sample `lane` is added: prefix xor of the moves
+        int fx = incl ? axis_bits(mv) : 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(PLX_FULL_MASK, fx, off);
+            if (lane >= off) fx ^= y;
+        }
+        const int fl = fx;
+        if (incl) {
+            const float gk[4] = {(float)gsig, c4.x > 0.f ? (float)(up0 * wi) : 0.f,
+                                 c4.y > 0.f ? (float)(up1 * wi) : 0.f,
+                                 c4.z > 0.f ? (float)(up2 * wi) : 0.f};
+            if (NEAREST) {
+#pragma unroll
+                for (int L = 0; L < 32; ++L) sc.val[L][lane] = L < 4 ? gk[L] : 0.f;
+            } else {
+                // corner e = q ^ fl of physical slot q: xor-ing a bit of the
+                // corner index swaps (1 - f, f) on that axis
+                const float lx = (fl & 4) ? f4.x : 1.f - f4.x, hx = (fl & 4) ? 1.f - f4.x : f4.x;
+                const float ly = (fl & 2) ? f4.y : 1.f - f4.y, hy = (fl & 2) ? 1.f - f4.y : f4.y;
+                const float lz = (fl & 1) ? f4.z : 1.f - f4.z, hz = (fl & 1) ? 1.f - f4.z : f4.z;
+#pragma unroll
+                for (int qs = 0; qs < 8; ++qs) {
+                    const float w = ((qs & 4) ? hx : lx) * ((qs & 2) ? hy : ly) *
+                                    ((qs & 1) ? hz : lz);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) sc.val[4 * qs + kk][lane] = w * gk[kk];
+                }
             }
-            __syncwarp();
+        }
+        __syncwarp();
+        // ---- serial, in sample order: moves (flushes) + one add ----
+        const int n = __popc(mask);
+        for (int jj = 0; jj < n; ++jj) {
+            const int mvj = sc.mv[jj];
+            if (mvj) ra.move(mvj, sc, jj, out.grad, out.tmask, lane);
+            ra.acc += sc.val[lane][jj];
         }
         ra.flush_all(out.grad, out.tmask, lane);
-    }
-    if (O.stats && lane == 0) {
-        atomicAdd(O.stats + 0, (unsigned long long)st_pos);
-        atomicAdd(O.stats + 1, (unsigned long long)st_samp);
-        atomicAdd(O.stats + 2, (unsigned long long)st_chunks);
-        atomicAdd(O.stats + 3, (unsigned long long)st_rays);
+        __syncwarp();
     }
     cau_part = warp_sum(cau_part);   // one pair of f64 atomics per warp
     if (lane == 0) {
@@ -766,7 +881,6 @@ __global__ void __launch_bounds__(128, MINB)
         if (cau_part != 0.0) atomicAdd(out.sums + 1, cau_part);
     }
 }
-
 }  // namespace plx
 
 using namespace plx;
@@ -794,52 +908,40 @@ int num_sms() {
     return n;
 }
 
-// Minimum resident 128-thread blocks per SM the backward is compiled for:
-// 4 / 5 = register budget 128 / 96 per thread (16 / 20 warps per SM);
-// PLX_BWD_MINB selects, default 4.
-int bwd_minb() {
-    static int m = 0;
-    if (!m) {
-        const char *e = getenv("PLX_BWD_MINB");
-        m = (e && atoi(e) == 5) ? 5 : 4;
-    }
-    return m;
-}
+// Kernel variants over (absolute, nearest).
+#define PLX_DISPATCH(o, KERNEL, MINB, GRID, ...)                                           \
+    do {                                                                                  \
+        if ((o)->nearest) {                                                               \
+            if ((o)->absolute) KERNEL<true, true, MINB><<<GRID, kThreads, 0, s>>>(__VA_ARGS__); \
+            else KERNEL<false, true, MINB><<<GRID, kThreads, 0, s>>>(__VA_ARGS__);         \
+        } else {                                                                          \
+            if ((o)->absolute) KERNEL<true, false, MINB><<<GRID, kThreads, 0, s>>>(__VA_ARGS__); \
+            else KERNEL<false, false, MINB><<<GRID, kThreads, 0, s>>>(__VA_ARGS__);        \
+        }                                                                                 \
+    } while (0)
 
 template <bool ABS, bool NEAREST, int MINB>
-int bwd_blocks_per_sm_t() {
+int march_blocks_per_sm() {
     static int nb = 0;
     if (!nb) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bwd_kernel<ABS, NEAREST, MINB>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, march_bwd_kernel<ABS, NEAREST, MINB>,
                                                       kThreads, 0);
         if (nb <= 0) nb = 1;
     }
     return nb;
 }
 
-template <int MINB>
-int bwd_blocks_per_sm_m(const plx_render_opts *o) {
+#ifndef PLX_COLOUR_MINB
+#define PLX_COLOUR_MINB 4
+#endif
+constexpr int kMarchMinB = 6, kColourMinB = PLX_COLOUR_MINB, kScatterMinB = 4;
+
+int march_blocks(const plx_render_opts *o) {
     if (o->nearest)
-        return o->absolute ? bwd_blocks_per_sm_t<true, true, MINB>()
-                           : bwd_blocks_per_sm_t<false, true, MINB>();
-    return o->absolute ? bwd_blocks_per_sm_t<true, false, MINB>()
-                       : bwd_blocks_per_sm_t<false, false, MINB>();
-}
-
-int bwd_blocks_per_sm(const plx_render_opts *o) {
-    return bwd_minb() == 5 ? bwd_blocks_per_sm_m<5>(o) : bwd_blocks_per_sm_m<4>(o);
-}
-
-template <int MINB>
-void launch_bwd(const plx_render_opts *o, dim3 grid, cudaStream_t s, DGrid G, RayArgs R, KOpts K,
-                Outs out, Scratch S) {
-    if (o->nearest) {
-        if (o->absolute) bwd_kernel<true, true, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
-        else bwd_kernel<false, true, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
-    } else {
-        if (o->absolute) bwd_kernel<true, false, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
-        else bwd_kernel<false, false, MINB><<<grid, kThreads, 0, s>>>(G, R, K, out, S);
-    }
+        return o->absolute ? march_blocks_per_sm<true, true, kMarchMinB>()
+                           : march_blocks_per_sm<false, true, kMarchMinB>();
+    return o->absolute ? march_blocks_per_sm<true, false, kMarchMinB>()
+                       : march_blocks_per_sm<false, false, kMarchMinB>();
 }
 
 template <int MODE>
@@ -861,25 +963,37 @@ int64_t max_records(const plx_grid *g, double step) {
     return (int64_t)ceil(sqrt(d2) / step) + 4;
 }
 
+// Records are kept for every march position of the longest chord of every
+// ray of a wave; a batch larger than the budget runs in waves.
+constexpr int64_t kRecordBudget = (int64_t)2 << 30;   // bytes of records per wave
+constexpr int64_t kRecordBytes = 112;                 // att, T, w, c, cell, f, rows, sig
+
 struct ScratchLayout {
-    int64_t slots, nrec, bytes;
-    int64_t off_att, off_T, off_w, off_c, off_cell, off_f, off_rows, off_sig;
+    int64_t wave, cap, bytes;
+    int nseg_max;
+    int64_t off_ns, off_segfirst, off_segray, off_rayd, off_att, off_T, off_w, off_c, off_cell, off_f, off_rows,
+        off_sig, off_segsum;
 };
 
 ScratchLayout layout(const plx_grid *g, const plx_render_opts *o, int64_t n_rays) {
     ScratchLayout L;
-    int64_t blocks = (int64_t)num_sms() * bwd_blocks_per_sm(o);
-    const int64_t need = (n_rays + kWarps - 1) / kWarps;
-    if (n_rays > 0 && need < blocks) blocks = need;
-    L.slots = blocks * kWarps;
-    L.nrec = max_records(g, o->step);
-    const int64_t n = L.slots * L.nrec;
+    L.cap = max_records(g, o->step);
+    L.nseg_max = (int)((L.cap + 31) / 32);
+    int64_t wave = kRecordBudget / (L.cap * kRecordBytes);
+    if (wave < 1024) wave = 1024;
+    if (n_rays > 0 && n_rays < wave) wave = n_rays;
+    L.wave = wave;
+    const int64_t n = wave * L.cap;
     int64_t off = 256;
     auto take = [&](int64_t bytes) {
         const int64_t at = off;
         off = (off + bytes + 255) & ~(int64_t)255;
         return at;
     };
+    L.off_ns = take(wave * 4);
+    L.off_segfirst = take(wave * 4);
+    L.off_segray = take(wave * L.nseg_max * 4);
+    L.off_rayd = take(wave * 24);
     L.off_att = take(n * 8);
     L.off_T = take(n * 8);
     L.off_w = take(n * 8);
@@ -888,6 +1002,7 @@ ScratchLayout layout(const plx_grid *g, const plx_render_opts *o, int64_t n_rays
     L.off_f = take(n * 16);
     L.off_rows = take(n * 32);
     L.off_sig = take(n * 8);
+    L.off_segsum = take(wave * L.nseg_max * 48);
     L.bytes = off;
     return L;
 }
@@ -949,22 +1064,19 @@ extern "C" int plx_render_fused_bwd(const plx_grid *g, const plx_rays *rays,
     if (rays->n == 0) return PLX_OK;
     const ScratchLayout L = layout(g, o, rays->n);
     if (scratch_bytes < L.bytes) return PLX_EINVAL;
-    Outs out{};
-    out.rgb = out_rgb;
-    out.sums = out_sums;
-    out.grad = gb->grad;
-    out.tmask = gb->tmask;
-    out.mse_mode = mse_mode;
-    out.up_scale = up_scale;
-    out.lam_cauchy = lam_cauchy;
     DGrid G = make_dgrid(*g);
-    RayArgs R{rays->origins, rays->dirs, rays->viewdirs, rays->target, rays->jitter, rays->idx,
-              rays->n};
     KOpts K{o->step, o->stop_thresh, {o->bg[0], o->bg[1], o->bg[2]},
             reinterpret_cast<unsigned long long *>(o->stats)};
     char *base = reinterpret_cast<char *>(scratch);
     Scratch S;
     S.counter = reinterpret_cast<int *>(base);
+    S.cap = L.cap;
+    S.nseg_max = L.nseg_max;
+    S.nseg_total = reinterpret_cast<int *>(base) + 1;
+    S.ns = reinterpret_cast<int *>(base + L.off_ns);
+    S.seg_first = reinterpret_cast<int *>(base + L.off_segfirst);
+    S.seg_ray = reinterpret_cast<int *>(base + L.off_segray);
+    S.ray_d = reinterpret_cast<double *>(base + L.off_rayd);
     S.att = reinterpret_cast<double *>(base + L.off_att);
     S.T = reinterpret_cast<double *>(base + L.off_T);
     S.w = reinterpret_cast<double *>(base + L.off_w);
@@ -972,15 +1084,47 @@ extern "C" int plx_render_fused_bwd(const plx_grid *g, const plx_rays *rays,
     S.cell = reinterpret_cast<int4 *>(base + L.off_cell);
     S.f = reinterpret_cast<float4 *>(base + L.off_f);
     S.rows = reinterpret_cast<int4 *>(base + L.off_rows);
-    S.sig = reinterpret_cast<double *>(base + L.off_sig);
-    S.nrec = L.nrec;
+    S.sig = lam_cauchy > 0.0 ? reinterpret_cast<double *>(base + L.off_sig) : nullptr;
+    S.seg_sum = reinterpret_cast<double *>(base + L.off_segsum);
     cudaStream_t s = (cudaStream_t)stream;
-    if (cudaMemsetAsync(S.counter, 0, sizeof(int), s) != cudaSuccess) return PLX_ECUDA;
-    const dim3 grid((unsigned)(L.slots / kWarps));
-    if (bwd_minb() == 5) launch_bwd<5>(o, grid, s, G, R, K, out, S);
-    else launch_bwd<4>(o, grid, s, G, R, K, out, S);
+    const int sms = num_sms();
+    for (int64_t w0 = 0; w0 < rays->n; w0 += L.wave) {
+        const int64_t nw = rays->n - w0 < L.wave ? rays->n - w0 : L.wave;
+        RayArgs R{rays->origins, rays->dirs, rays->viewdirs, rays->target,
+                  rays->jitter ? rays->jitter + w0 : nullptr, rays->idx ? rays->idx + w0 : nullptr,
+                  nw};
+        if (!rays->idx) {   // implicit indices: offset the arrays instead
+            R.origins += 3 * w0;
+            R.dirs += 3 * w0;
+            R.viewdirs += 3 * w0;
+            R.target += 3 * w0;
+        }
+        Outs out{};
+        out.rgb = out_rgb ? out_rgb + 3 * w0 : nullptr;
+        out.sums = out_sums;
+        out.grad = gb->grad;
+        out.tmask = gb->tmask;
+        out.mse_mode = mse_mode;
+        out.up_scale = up_scale;
+        out.lam_cauchy = lam_cauchy;
+        // ray counter + segment counter
+        if (cudaMemsetAsync(S.counter, 0, 2 * sizeof(int), s) != cudaSuccess) return PLX_ECUDA;
+        int64_t mb = (int64_t)sms * march_blocks(o);
+        if (mb > (nw + kWarps - 1) / kWarps) mb = (nw + kWarps - 1) / kWarps;
+        PLX_DISPATCH(o, march_bwd_kernel, kMarchMinB, dim3((unsigned)mb), G, R, K, out, S);
+        const dim3 sg_grid((unsigned)(sms * 8));
+        PLX_DISPATCH(o, colour_kernel, kColourMinB, sg_grid, G, R, S);
+        PLX_DISPATCH(o, scatter_kernel, kScatterMinB, sg_grid, G, R, K, out, S);
+    }
     return cudaPeekAtLastError() == cudaSuccess ? PLX_OK : PLX_ECUDA;
 }
+
+#ifdef PLX_TIMELINE
+extern "C" int plx_debug_timeline(unsigned long long *host, int n) {
+    return cudaMemcpyFromSymbol(host, g_timeline, sizeof(unsigned long long) * 2 * n) == cudaSuccess
+               ? PLX_OK : PLX_ECUDA;
+}
+#endif
 
 extern "C" int plx_max_weight(const plx_grid *g, const plx_rays *rays, const plx_render_opts *o,
                               double *out_w, void *stream) {

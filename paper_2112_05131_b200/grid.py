@@ -310,13 +310,18 @@ class SparseGrid:
         g.hi = (ctypes.c_double * 3)(*self.aabb_max)
         g.scale = (ctypes.c_double * 3)(*self.lattice_scale)
         g.dmax = (ctypes.c_double * 3)(*(np.array(self.dims, dtype=np.float64) - 1.0))
-        g.cell_occ = self.cell_occ().data_ptr() if (with_occ and USE_CELL_OCC) else None
         if with_lat is None:
             with_lat = with_occ and USE_CELL_OCC
         if (with_lat or self._lat is not None) and self.n_rows:
             lat, rc = self.lattice_sigma()
             g.sigma_lat = lat.data_ptr()
             g.row_cell = rc.data_ptr()
+        # the cell-occupancy bitmask skips empty space; a fully occupied
+        # (identity-linked) grid has none, and with the sigma mirror the test
+        # would only add a dependent load to every march position
+        dense = self._lat is not None and self._lat.data_ptr() == self.density.data_ptr()
+        g.cell_occ = (self.cell_occ().data_ptr() if (with_occ and USE_CELL_OCC and not dense)
+                      else None)
         return g
 
     def to_numpy(self):
