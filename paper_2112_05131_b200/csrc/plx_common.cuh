@@ -24,6 +24,7 @@ struct DGrid {
     const float *__restrict__ density;   // sigma per row
     const uint32_t *__restrict__ cell_occ;
     const float *sigma_lat;              // lattice-indexed sigma mirror, NaN = empty (mutable)
+    bool identity;                       // links[c] == c for every point (dense grid)
     int32_t Dx, Dy, Dz;
     double lo[3], hi[3], scale[3], dmax[3];
 };
@@ -35,6 +36,9 @@ inline DGrid make_dgrid(const plx_grid &g) {
     d.density = g.density;
     d.cell_occ = g.cell_occ;
     d.sigma_lat = g.sigma_lat;
+    // the caller aliases the sigma mirror to density exactly when the grid is
+    // identity-linked (SparseGrid.lattice_sigma)
+    d.identity = g.sigma_lat != nullptr && g.sigma_lat == g.density;
     d.Dx = (int32_t)g.dims[0];
     d.Dy = (int32_t)g.dims[1];
     d.Dz = (int32_t)g.dims[2];
@@ -188,7 +192,18 @@ __device__ __forceinline__ int stencil(const DGrid &G, const double *g, int32_t 
 // Stencil rows of a base cell / lattice point (K:84-123), -1 = empty.
 template <bool NEAREST>
 __device__ __forceinline__ void load_rows(const DGrid &G, const int *ijk, int32_t *rows) {
-    const int32_t *base = G.links + flat(G, ijk[0], ijk[1], ijk[2]);
+    const int64_t c = flat(G, ijk[0], ijk[1], ijk[2]);
+    if (G.identity) {   // dense identity-linked grid: row = lattice point
+        const int64_t sy = G.Dz, sx = (int64_t)G.Dy * G.Dz;
+        rows[0] = (int32_t)c;
+        if (!NEAREST) {
+#pragma unroll
+            for (int q = 1; q < 8; ++q)
+                rows[q] = (int32_t)(c + ((q >> 2) & 1) * sx + ((q >> 1) & 1) * sy + (q & 1));
+        }
+        return;
+    }
+    const int32_t *base = G.links + c;
     if (NEAREST) {
         rows[0] = __ldg(base);
         return;

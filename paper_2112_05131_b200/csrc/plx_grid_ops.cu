@@ -82,15 +82,22 @@ __global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
             const uint32_t c32 = (uint32_t)cid, dz = (uint32_t)G.Dz;
             const uint32_t ij = c32 / dz, k = c32 - ij * dz;
             const uint32_t i = ij / (uint32_t)G.Dy, j = ij - i * (uint32_t)G.Dy;
-            r0 = __ldg(G.links + cid);
             int64_t ii = i + 1, jj = j + 1, kk = k + 1;
             bool hx = true, hy = true, hz = true;
             if (ii >= G.Dx) { if (a.wrap[0]) ii = 0; else hx = false; }
             if (jj >= G.Dy) { if (a.wrap[1]) jj = 0; else hy = false; }
             if (kk >= G.Dz) { if (a.wrap[2]) kk = 0; else hz = false; }
-            rx = hx ? __ldg(G.links + flat(G, ii, j, k)) : -1;
-            ry = hy ? __ldg(G.links + flat(G, i, jj, k)) : -1;
-            rz = hz ? __ldg(G.links + flat(G, i, j, kk)) : -1;
+            if (G.identity) {   // dense identity-linked grid: no link gathers
+                r0 = (int32_t)cid;
+                rx = hx ? (int32_t)flat(G, ii, j, k) : -1;
+                ry = hy ? (int32_t)flat(G, i, jj, k) : -1;
+                rz = hz ? (int32_t)flat(G, i, j, kk) : -1;
+            } else {
+                r0 = __ldg(G.links + cid);
+                rx = hx ? __ldg(G.links + flat(G, ii, j, k)) : -1;
+                ry = hy ? __ldg(G.links + flat(G, i, jj, k)) : -1;
+                rz = hz ? __ldg(G.links + flat(G, i, j, kk)) : -1;
+            }
             const bool okx = rx >= 0, oky = ry >= 0, okz = rz >= 0;
             const bool sh_on = r0 >= 0 && (okx || oky || okz);
             float4 v0 = make_float4(0, 0, 0, 0), vx = v0, vy = v0, vz = v0;

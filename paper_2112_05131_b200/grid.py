@@ -245,19 +245,30 @@ class SparseGrid:
     def invalidate(self) -> None:
         """Call after editing `links` or `density` in place: rebuilds the
         derived structures (cell occupancy bitmask, lattice sigma mirror,
-        row -> cell map) in their existing buffers, so descriptors cached by
-        a caller stay valid."""
+        row -> cell map).  Density edits are absorbed in place (cached
+        descriptors stay valid); after a links edit rebuild descriptors too
+        (the mirror may stop or start aliasing `density`)."""
         c = self._c(with_occ=False, with_lat=False)
         L, s = _lib.lib(), _lib.stream_ptr()
         if self._cell_occ is not None:
             _lib.check(L.plx_build_cell_occ(ctypes.byref(c), self._cell_occ.data_ptr(), s),
                        "build_cell_occ")
-        if self._row_cell is not None and self.n_rows:
-            _lib.check(L.plx_build_row_cell(ctypes.byref(c), self._row_cell.data_ptr(), s),
-                       "build_row_cell")
-        if self._lat is not None and self._lat.data_ptr() != self.density.data_ptr():
-            _lib.check(L.plx_build_sigma_lat(ctypes.byref(c), self._lat.data_ptr(), s),
-                       "build_sigma_lat")
+        if self._lat is not None:
+            aliased = self._lat.data_ptr() == self.density.data_ptr()
+            ncell = int(np.prod(self.dims))
+            identity = self.n_rows == ncell and bool(torch.equal(
+                self._links.view(-1), torch.arange(ncell, dtype=torch.int32, device=self.device)))
+            if aliased != identity:
+                self._lat = None
+                self._row_cell = None
+                self.lattice_sigma()
+                return
+            if self._row_cell is not None and self.n_rows and not aliased:
+                _lib.check(L.plx_build_row_cell(ctypes.byref(c), self._row_cell.data_ptr(), s),
+                           "build_row_cell")
+            if not aliased:
+                _lib.check(L.plx_build_sigma_lat(ctypes.byref(c), self._lat.data_ptr(), s),
+                           "build_sigma_lat")
 
     def cell_occ(self) -> torch.Tensor:
         if self._cell_occ is None:
