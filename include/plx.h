@@ -18,7 +18,9 @@
  * [rows x 28] (SH channel-major in columns 1..27, column 0 padding), so the
  * sigma gathers of the march touch a compact 4 B/row array instead of 112-
  * byte rows; the gradient buffer and RMSProp state are float32 (rows x 28,
- * column 0 = sigma).  Arithmetic is float64 except the colour dot products.
+ * column 0 = sigma).  Row arrays (table, grad, v) have a pitch of PLX_STRIDE
+ * = 32 floats: every row is one 128-byte cache line, so row gathers and
+ * read-modify-writes never straddle lines or write partial sectors.  Arithmetic is float64 except the colour dot products.
  * Rays are float64 (N x 3).  The touched-row set of GradientBuffer (G:25-68:
  * touched_mask + insertion-ordered touched_ids + count) is kept as the byte
  * mask alone; the count is produced by plx_opt_step / plx_count_touched.
@@ -32,7 +34,9 @@
 extern "C" {
 #endif
 
-#define PLX_ROW 28
+#define PLX_ROW 28     /* columns of a row: sigma (or padding) + 27 SH        */
+#define PLX_STRIDE 32  /* row pitch in floats: 128-byte rows, one cache line;
+                          columns 28..31 are padding (never read as data)  */
 
 enum {
     PLX_OK = 0,
@@ -45,7 +49,7 @@ enum {
  * (K:174-177, K:242-248, K:415-416, K:457-459) and SparseGrid (G:71-92). */
 typedef struct {
     const int32_t *links;  /* [Dx*Dy*Dz] C-order (z fastest), -1 = empty     */
-    float *table;          /* [rows*28] SH rows: columns 1..27 = the
+    float *table;          /* [rows*PLX_STRIDE] SH rows: columns 1..27 = the
                               reference table's SH columns; column 0 is
                               padding (16-byte rows), never read          */
     float *density;        /* [rows] sigma = the reference table column 0  */
@@ -77,7 +81,7 @@ typedef struct {
  * plx_opt_step compacts the mask into them and updates the list (two-phase);
  * when both are NULL it sweeps the mask in place. */
 typedef struct {
-    float *grad;           /* [rows*28] */
+    float *grad;           /* [rows*PLX_STRIDE] */
     uint8_t *tmask;        /* [rows]    */
     int32_t *tids;         /* [rows] scratch, or NULL (order unspecified)  */
     int64_t *tcnt;         /* [1] length of tids after plx_opt_step, or NULL */
@@ -171,7 +175,8 @@ int plx_clear_grad(plx_grad *gb, int64_t rows, int64_t *out_count, void *stream)
  * MAX of the masks.  scratch: plx_scan_scratch_bytes(rows) bytes. */
 int plx_touched_list(const uint8_t *tmask, int64_t rows, int32_t *ids, int64_t *count,
                      void *scratch, void *stream);
-/* dst[j] = src row ids[j] (28 floats) for j < *count (device); cap bounds
+/* dst[j] = src row ids[j] for j < *count (device): rows of PLX_STRIDE floats
+ * packed at a 28-float pitch (the all-reduce moves no padding); cap bounds
  * the launch (rows). */
 int plx_pack_rows(const float *src, const int32_t *ids, const int64_t *count, int64_t cap,
                   float *dst, void *stream);
@@ -190,7 +195,7 @@ int plx_opt_step_list(plx_grid *g, float *v, plx_grad *gb, const int32_t *ids,
 typedef struct {
     int32_t n, rank;
     int64_t rows;
-    float *grad[PLX_MAX_PEERS];        /* rows x 28 each */
+    float *grad[PLX_MAX_PEERS];        /* rows x PLX_STRIDE each */
     uint8_t *tmask[PLX_MAX_PEERS];
     float *table[PLX_MAX_PEERS];       /* SH rows (column 0 unused) */
     float *density[PLX_MAX_PEERS];

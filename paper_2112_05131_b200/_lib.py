@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("PLX_LIB") or os.path.join(_HERE, "libplx.so")
 
 PLX_OK, PLX_EINVAL, PLX_ECUDA = 0, 1, 2
 ROW = 28
+STRIDE = 32   # row pitch of table / grad / v in floats (128-byte rows, plx.h)
 
 
 class PlxError(RuntimeError):

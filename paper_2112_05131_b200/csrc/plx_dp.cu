@@ -31,8 +31,8 @@ __global__ void pack_rows_kernel(const float *src, const int32_t *ids, const int
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = t / 7;
         const int q = (int)(t - j * 7);
-        reinterpret_cast<float4 *>(dst + j * PLX_ROW)[q] =
-            __ldg(reinterpret_cast<const float4 *>(src + (int64_t)ids[j] * PLX_ROW) + q);
+        reinterpret_cast<float4 *>(dst + j * PLX_ROW)[q] =   // packed: 28-float pitch
+            __ldg(reinterpret_cast<const float4 *>(src + (int64_t)ids[j] * PLX_STRIDE) + q);
     }
 }
 
@@ -68,9 +68,9 @@ __global__ void __launch_bounds__(256, 2) opt_list_kernel(ListArgs a) {
         if (lane >= 28 || j >= n) continue;
         const int64_t r = a.ids[j];
         float4 g4 = a.gpack ? reinterpret_cast<const float4 *>(a.gpack + j * PLX_ROW)[quad]
-                            : reinterpret_cast<const float4 *>(a.grad + r * PLX_ROW)[quad];
-        float4 t4 = reinterpret_cast<const float4 *>(a.table + r * PLX_ROW)[quad];
-        float4 v4 = a.h.rmsprop ? reinterpret_cast<const float4 *>(a.v + r * PLX_ROW)[quad]
+                            : reinterpret_cast<const float4 *>(a.grad + r * PLX_STRIDE)[quad];
+        float4 t4 = reinterpret_cast<const float4 *>(a.table + r * PLX_STRIDE)[quad];
+        float4 v4 = a.h.rmsprop ? reinterpret_cast<const float4 *>(a.v + r * PLX_STRIDE)[quad]
                                 : make_float4(0.f, 0.f, 0.f, 0.f);
         float den = 0.f;
         int32_t cell = 0;
@@ -86,10 +86,10 @@ __global__ void __launch_bounds__(256, 2) opt_list_kernel(ListArgs a) {
             t4.x = 0.f;
             if (a.clear) a.tmask[r] = 0;
         }
-        reinterpret_cast<float4 *>(a.table + r * PLX_ROW)[quad] = t4;
-        if (a.h.rmsprop) reinterpret_cast<float4 *>(a.v + r * PLX_ROW)[quad] = v4;
+        reinterpret_cast<float4 *>(a.table + r * PLX_STRIDE)[quad] = t4;
+        if (a.h.rmsprop) reinterpret_cast<float4 *>(a.v + r * PLX_STRIDE)[quad] = v4;
         if (a.clear)
-            reinterpret_cast<float4 *>(a.grad + r * PLX_ROW)[quad] = make_float4(0.f, 0.f, 0.f, 0.f);
+            reinterpret_cast<float4 *>(a.grad + r * PLX_STRIDE)[quad] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
 
@@ -164,14 +164,14 @@ __global__ void __launch_bounds__(256) dp_owner_update_kernel(DpArgs a) {
                 const int64_t r = seg * 128 + list[wib][j];
                 float4 g4 = make_float4(0.f, 0.f, 0.f, 0.f);
                 for (int k = 0; k < a.n; ++k) {
-                    const float4 x = reinterpret_cast<const float4 *>(a.grad[k] + r * PLX_ROW)[quad];
+                    const float4 x = reinterpret_cast<const float4 *>(a.grad[k] + r * PLX_STRIDE)[quad];
                     g4.x += x.x;
                     g4.y += x.y;
                     g4.z += x.z;
                     g4.w += x.w;
                 }
-                float4 t4 = reinterpret_cast<const float4 *>(a.table[a.rank] + r * PLX_ROW)[quad];
-                float4 v4 = a.h.rmsprop ? reinterpret_cast<const float4 *>(a.v + r * PLX_ROW)[quad]
+                float4 t4 = reinterpret_cast<const float4 *>(a.table[a.rank] + r * PLX_STRIDE)[quad];
+                float4 v4 = a.h.rmsprop ? reinterpret_cast<const float4 *>(a.v + r * PLX_STRIDE)[quad]
                                         : make_float4(0.f, 0.f, 0.f, 0.f);
                 int32_t cell = 0;
                 if (quad == 0) {
@@ -179,11 +179,11 @@ __global__ void __launch_bounds__(256) dp_owner_update_kernel(DpArgs a) {
                     if (a.row_cell) cell = a.row_cell[r];
                 }
                 opt_apply4(a.h, quad, g4, t4, v4);
-                if (a.h.rmsprop) reinterpret_cast<float4 *>(a.v + r * PLX_ROW)[quad] = v4;
+                if (a.h.rmsprop) reinterpret_cast<float4 *>(a.v + r * PLX_STRIDE)[quad] = v4;
                 const float sig = t4.x;
                 if (quad == 0) t4.x = 0.f;
                 for (int k = 0; k < a.n; ++k) {
-                    reinterpret_cast<float4 *>(a.table[k] + r * PLX_ROW)[quad] = t4;
+                    reinterpret_cast<float4 *>(a.table[k] + r * PLX_STRIDE)[quad] = t4;
                     if (quad == 0) {
                         a.density[k][r] = sig;
                         if (a.lat[k]) a.lat[k][cell] = sig;

@@ -102,10 +102,10 @@ __global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
             const bool sh_on = r0 >= 0 && (okx || oky || okz);
             float4 v0 = make_float4(0, 0, 0, 0), vx = v0, vy = v0, vz = v0;
             if (sh_on) {
-                v0 = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)r0 * PLX_ROW) + quad);
-                if (okx) vx = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)rx * PLX_ROW) + quad);
-                if (oky) vy = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)ry * PLX_ROW) + quad);
-                if (okz) vz = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)rz * PLX_ROW) + quad);
+                v0 = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)r0 * PLX_STRIDE) + quad);
+                if (okx) vx = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)rx * PLX_STRIDE) + quad);
+                if (oky) vy = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)ry * PLX_STRIDE) + quad);
+                if (okz) vz = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)rz * PLX_STRIDE) + quad);
             }
             if (quad == 0) {
                 // opacity term (K:505-532): missing neighbours read as 0
@@ -158,13 +158,13 @@ __global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
             }
             if (a.with_grad) {
                 if (rx >= 0 && (gx[0] != 0.f || gx[1] != 0.f || gx[2] != 0.f || gx[3] != 0.f))
-                    red_add_v4(a.grad + (int64_t)rx * PLX_ROW + 4 * quad, gx[0], gx[1], gx[2], gx[3]);
+                    red_add_v4(a.grad + (int64_t)rx * PLX_STRIDE + 4 * quad, gx[0], gx[1], gx[2], gx[3]);
                 if (ry >= 0 && (gy[0] != 0.f || gy[1] != 0.f || gy[2] != 0.f || gy[3] != 0.f))
-                    red_add_v4(a.grad + (int64_t)ry * PLX_ROW + 4 * quad, gy[0], gy[1], gy[2], gy[3]);
+                    red_add_v4(a.grad + (int64_t)ry * PLX_STRIDE + 4 * quad, gy[0], gy[1], gy[2], gy[3]);
                 if (rz >= 0 && (gz[0] != 0.f || gz[1] != 0.f || gz[2] != 0.f || gz[3] != 0.f))
-                    red_add_v4(a.grad + (int64_t)rz * PLX_ROW + 4 * quad, gz[0], gz[1], gz[2], gz[3]);
+                    red_add_v4(a.grad + (int64_t)rz * PLX_STRIDE + 4 * quad, gz[0], gz[1], gz[2], gz[3]);
                 if (r0 >= 0 && (g0v[0] != 0.f || g0v[1] != 0.f || g0v[2] != 0.f || g0v[3] != 0.f))
-                    red_add_v4(a.grad + (int64_t)r0 * PLX_ROW + 4 * quad, g0v[0], g0v[1], g0v[2], g0v[3]);
+                    red_add_v4(a.grad + (int64_t)r0 * PLX_STRIDE + 4 * quad, g0v[0], g0v[1], g0v[2], g0v[3]);
             }
         }
         if (a.with_grad) {   // _touch (K:155-160): a row is touched if any column got a value
@@ -285,12 +285,12 @@ __global__ void __launch_bounds__(NT) opt_kernel(OptArgs a) {
                 act[u] = lane < 28 && j < total;
                 rw[u] = act[u] ? seg * 128 + list[wib][j] : 0;
                 if (act[u]) {
-                    g4[u] = reinterpret_cast<const float4 *>(a.grad + rw[u] * PLX_ROW)[quad];
+                    g4[u] = reinterpret_cast<const float4 *>(a.grad + rw[u] * PLX_STRIDE)[quad];
                     if (a.update) {
-                        t4[u] = reinterpret_cast<const float4 *>(a.table + rw[u] * PLX_ROW)[quad];
+                        t4[u] = reinterpret_cast<const float4 *>(a.table + rw[u] * PLX_STRIDE)[quad];
                         if (quad == 0) den[u] = a.density[rw[u]];
                         if (a.rmsprop)
-                            v4[u] = reinterpret_cast<const float4 *>(a.v + rw[u] * PLX_ROW)[quad];
+                            v4[u] = reinterpret_cast<const float4 *>(a.v + rw[u] * PLX_STRIDE)[quad];
                     }
                 }
             }
@@ -305,11 +305,11 @@ __global__ void __launch_bounds__(NT) opt_kernel(OptArgs a) {
                         if (a.sigma_lat) lat_update(a, a.row_cell[rw[u]], t4[u].x);
                         t4[u].x = 0.f;
                     }
-                    reinterpret_cast<float4 *>(a.table + rw[u] * PLX_ROW)[quad] = t4[u];
-                    if (a.rmsprop) reinterpret_cast<float4 *>(a.v + rw[u] * PLX_ROW)[quad] = v4[u];
+                    reinterpret_cast<float4 *>(a.table + rw[u] * PLX_STRIDE)[quad] = t4[u];
+                    if (a.rmsprop) reinterpret_cast<float4 *>(a.v + rw[u] * PLX_STRIDE)[quad] = v4[u];
                 }
                 if (a.clear)
-                    reinterpret_cast<float4 *>(a.grad + rw[u] * PLX_ROW)[quad] =
+                    reinterpret_cast<float4 *>(a.grad + rw[u] * PLX_STRIDE)[quad] =
                         make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
@@ -468,13 +468,13 @@ __global__ void __launch_bounds__(256, MINB) opt_rows_kernel(OptArgs a, const in
         for (int u = 0; u < kOptU; ++u) {
             if (cur[u] < 0) continue;
             const int64_t r = cur[u];
-            g4[u] = reinterpret_cast<const float4 *>(a.grad + r * PLX_ROW)[quad];
-            t4[u] = reinterpret_cast<const float4 *>(a.table + r * PLX_ROW)[quad];
+            g4[u] = reinterpret_cast<const float4 *>(a.grad + r * PLX_STRIDE)[quad];
+            t4[u] = reinterpret_cast<const float4 *>(a.table + r * PLX_STRIDE)[quad];
             if (quad == 0) {   // merged after all loads are issued
                 den[u] = a.density[r];
                 cell[u] = a.sigma_lat ? a.row_cell[r] : 0;
             }
-            if (a.rmsprop) v4[u] = reinterpret_cast<const float4 *>(a.v + r * PLX_ROW)[quad];
+            if (a.rmsprop) v4[u] = reinterpret_cast<const float4 *>(a.v + r * PLX_STRIDE)[quad];
         }
         load_ids(g0 + nw * kOptU, nxt);
 #pragma unroll
@@ -488,10 +488,10 @@ __global__ void __launch_bounds__(256, MINB) opt_rows_kernel(OptArgs a, const in
                 lat_update(a, cell[u], t4[u].x);
                 t4[u].x = 0.f;
             }
-            reinterpret_cast<float4 *>(a.table + r * PLX_ROW)[quad] = t4[u];
-            if (a.rmsprop) reinterpret_cast<float4 *>(a.v + r * PLX_ROW)[quad] = v4[u];
+            reinterpret_cast<float4 *>(a.table + r * PLX_STRIDE)[quad] = t4[u];
+            if (a.rmsprop) reinterpret_cast<float4 *>(a.v + r * PLX_STRIDE)[quad] = v4[u];
             if (a.clear)
-                reinterpret_cast<float4 *>(a.grad + r * PLX_ROW)[quad] =
+                reinterpret_cast<float4 *>(a.grad + r * PLX_STRIDE)[quad] =
                     make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
@@ -589,8 +589,8 @@ __global__ void prune_apply_kernel(DGrid G, const int32_t *new_links, int64_t nc
         new_density[id] = G.density[old];
         return;
     }
-    reinterpret_cast<float4 *>(new_table + (int64_t)id * PLX_ROW)[part] =
-        reinterpret_cast<const float4 *>(G.table + (int64_t)old * PLX_ROW)[part];
+    reinterpret_cast<float4 *>(new_table + (int64_t)id * PLX_STRIDE)[part] =
+        reinterpret_cast<const float4 *>(G.table + (int64_t)old * PLX_STRIDE)[part];
 }
 
 // -------------------------------------------------------- upsample --------
@@ -665,7 +665,7 @@ __global__ void upsample_apply_kernel(DGrid G, UpArgs u, const int32_t *new_link
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         if (rows[q] < 0) continue;   // empty corners read 0, no renormalisation
-        float4 v = __ldg(reinterpret_cast<const float4 *>(G.table + (int64_t)rows[q] * PLX_ROW) + part);
+        float4 v = __ldg(reinterpret_cast<const float4 *>(G.table + (int64_t)rows[q] * PLX_STRIDE) + part);
         if (part == 0) v.x = __ldg(G.density + rows[q]);
         acc[0] += ws[q] * (double)v.x;
         acc[1] += ws[q] * (double)v.y;
@@ -676,7 +676,7 @@ __global__ void upsample_apply_kernel(DGrid G, UpArgs u, const int32_t *new_link
         new_density[id] = (float)acc[0];
         acc[0] = 0.0;
     }
-    reinterpret_cast<float4 *>(new_table + (int64_t)id * PLX_ROW)[part] =
+    reinterpret_cast<float4 *>(new_table + (int64_t)id * PLX_STRIDE)[part] =
         make_float4((float)acc[0], (float)acc[1], (float)acc[2], (float)acc[3]);
 }
 
@@ -872,7 +872,7 @@ __global__ void clear_rows_kernel(float *grad, const int32_t *tids, const int64_
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * 7;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = t / 7;
-        reinterpret_cast<float4 *>(grad + (int64_t)tids[j] * PLX_ROW)[t - j * 7] =
+        reinterpret_cast<float4 *>(grad + (int64_t)tids[j] * PLX_STRIDE)[t - j * 7] =
             make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }

@@ -98,7 +98,7 @@ __device__ __forceinline__ void eval_sample(const DGrid &G, const RayMarch &rm, 
     for (int q = 0; q < NQ; ++q) {
         int32_t r = s.rows[q];
         if (r < 0) continue;
-        const float4 *row = reinterpret_cast<const float4 *>(G.table + (int64_t)r * PLX_ROW);
+        const float4 *row = reinterpret_cast<const float4 *>(G.table + (int64_t)r * PLX_STRIDE);
         float4 v0 = __ldg(row + 0), v1 = __ldg(row + 1), v2 = __ldg(row + 2), v3 = __ldg(row + 3);
         float4 v4 = __ldg(row + 4), v5 = __ldg(row + 5), v6 = __ldg(row + 6);
         // row layout: [sig, R0..R8, G0..G8, B0..B8]
@@ -303,7 +303,7 @@ struct LaneAcc {
             const float v3 = ((hisel & 8u) ? ahi : alo) * cb[3];
             if (quad == 0) tmask[r] = 1;
             if (v0 != 0.f || v1 != 0.f || v2 != 0.f || v3 != 0.f)
-                red_add_v4(grad + (int64_t)r * PLX_ROW + 4 * quad, v0, v1, v2, v3);
+                red_add_v4(grad + (int64_t)r * PLX_STRIDE + 4 * quad, v0, v1, v2, v3);
         }
         if (NEAREST || (((q ^ flip) & bit) != 0) == (side != 0)) {
             acc = 0.f;
@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(128, MINB)
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 const int32_t r = rows[q] >= 0 ? rows[q] : 0;
-                const float4 *row = reinterpret_cast<const float4 *>(G.table + (int64_t)r * PLX_ROW);
+                const float4 *row = reinterpret_cast<const float4 *>(G.table + (int64_t)r * PLX_STRIDE);
                 const float4 v0 = __ldg(row + 0), v1 = __ldg(row + 1), v2 = __ldg(row + 2),
                              v3 = __ldg(row + 3), v4 = __ldg(row + 4), v5 = __ldg(row + 5),
                              v6 = __ldg(row + 6);

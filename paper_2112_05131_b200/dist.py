@@ -82,6 +82,8 @@ def reduce_gradients(world: World, grad: torch.Tensor, tmask: torch.Tensor,
     sums <- sum, all in place."""
     if not world.active:
         return
+    if not grad.is_contiguous():   # a 28-column view of the 32-float-pitch rows
+        grad = torch.as_strided(grad, (grad.shape[0], grad.stride(0)), (grad.stride(0), 1))
     dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=world.group)
     dist.all_reduce(tmask, op=dist.ReduceOp.MAX, group=world.group)
     if sums is not None:

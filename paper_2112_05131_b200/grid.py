@@ -20,11 +20,18 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import ROW
+from ._lib import ROW, STRIDE
 from .sh import SH_C0
 
 EMPTY = -1
 ROW_SIZE = ROW
+
+
+def row_array(n_rows: int, device, zero: bool = True) -> torch.Tensor:
+    """(n_rows, 28) float32 view of a (n_rows, 32) allocation: the kernels'
+    128-byte row pitch (plx.h PLX_STRIDE), columns 28..31 padding."""
+    f = torch.zeros if zero else torch.empty
+    return f((int(n_rows), STRIDE), dtype=torch.float32, device=device)[:, :ROW]
 
 # Empty-space skipping through the per-cell occupancy bitmask (an exact
 # shortcut: a cell whose 8 corners are all empty has occ == False, K:126-135).
@@ -44,7 +51,7 @@ class GradientBuffer:
 
     def __init__(self, n_rows: int, device=None):
         dev = _dev(device)
-        self.data = torch.zeros((int(n_rows), ROW), dtype=torch.float32, device=dev)
+        self.data = row_array(n_rows, dev)
         self.touched_mask = torch.zeros(int(n_rows), dtype=torch.uint8, device=dev)
         self._count = torch.zeros(1, dtype=torch.int64, device=dev)
         # touched_ids / _count (G:25-68): filled by the two-phase optimiser step
@@ -142,7 +149,7 @@ class SparseGrid:
         g = cls.__new__(cls)
         g._links = links.to(torch.int32).contiguous()
         g.density = torch.empty(int(n_rows), dtype=torch.float32, device=device)
-        g.sh = torch.empty((int(n_rows), ROW), dtype=torch.float32, device=device)
+        g.sh = row_array(n_rows, device, zero=False)
         g.aabb_min = np.asarray(aabb_min, dtype=np.float64).reshape(3).copy()
         g.aabb_max = np.asarray(aabb_max, dtype=np.float64).reshape(3).copy()
         g._cell_occ = None
@@ -207,7 +214,8 @@ class SparseGrid:
                 self.invalidate()
             return
         self.density = t[:, 0].to(device=dev, dtype=torch.float32).contiguous()
-        self.sh = t.to(device=dev, dtype=torch.float32).clone().contiguous()
+        self.sh = row_array(t.shape[0], dev, zero=False)
+        self.sh.copy_(t)
         self.sh[:, 0] = 0.0
         self._lat = None
         self._row_cell = None
