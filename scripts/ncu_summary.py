@@ -66,6 +66,7 @@ def main():
     traffic_path = "profiles/ncu_traffic.json"
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     lines = [f"# ncu summary `{tag}`", ""]
+    sums = {}
     for rep in reps:
         for rec in raw(rep):
             name = rec.get("Kernel Name", ("", "?"))[1]
@@ -84,13 +85,19 @@ def main():
             try:
                 rd = float(rec["dram__bytes_read.sum"][1]) * UNIT[rec["dram__bytes_read.sum"][0]]
                 wr = float(rec["dram__bytes_write.sum"][1]) * UNIT[rec["dram__bytes_write.sum"][0]]
-                key = ("render_fused_bwd" if "march_kernel<(int)1" in name or "march_kernel<1" in name
-                       else "opt_step" if "opt_kernel" in name
+                # the bench's per-step legs: the backward is three kernels, the
+                # update two (their DRAM bytes add up per launch of the leg)
+                key = ("render_fused_bwd" if any(k in name for k in
+                                                 ("march_bwd_kernel", "colour_kernel",
+                                                  "scatter_kernel"))
+                       else "opt_step" if any(k in name for k in
+                                              ("opt_rows_kernel", "touched_compact"))
                        else "tv" if "tv_kernel" in name else None)
                 if key:
-                    traffic[key] = rd + wr
+                    sums[key] = sums.get(key, 0.0) + rd + wr
             except (KeyError, ValueError):
                 pass
+    traffic.update(sums)
     if launches:
         text = open(launches).read().splitlines()
         start = [i for i, l in enumerate(text) if l.startswith('"ID"')][0]
