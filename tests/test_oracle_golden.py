@@ -163,3 +163,16 @@ def test_plnx_writer_crc_matches_reference_golden(i):
         return
     links, table, lo, hi = artifact_io.read_plnx(f"{GOLDEN}/plnx/{gold['file']}")
     assert artifact_io.plnx_bytes(links, table, lo, hi) == raw
+
+
+def test_to_ndc_matches_reference():
+    """camera.to_ndc (camera.py:103-134) on random rays incl. rays parallel to
+    the image plane, against the reference's own output (ndc.npz)."""
+    from paper_2112_05131_b200.camera import Camera, to_ndc
+    z = load("ndc.npz")
+    w, h = (int(x) for x in z["cam_wh"])
+    cam = Camera(c2w=np.eye(4), focal=float(z["cam_focal"][0]), width=w, height=h)
+    on, dn, valid = to_ndc(z["o"], z["d"], cam, near=1.0)
+    np.testing.assert_array_equal(valid, z["valid"])
+    np.testing.assert_array_equal(on, z["on"])
+    np.testing.assert_array_equal(dn, z["dn"])
