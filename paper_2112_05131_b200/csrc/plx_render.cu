@@ -965,7 +965,7 @@ int64_t max_records(const plx_grid *g, double step) {
 
 // Records are kept for every march position of the longest chord of every
 // ray of a wave; a batch larger than the budget runs in waves.
-constexpr int64_t kRecordBudget = (int64_t)2 << 30;   // bytes of records per wave
+constexpr int64_t kRecordBudget = (int64_t)8 << 30;   // bytes of records per wave
 constexpr int64_t kRecordBytes = 112;                 // att, T, w, c, cell, f, rows, sig
 
 struct ScratchLayout {
