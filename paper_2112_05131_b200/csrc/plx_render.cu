@@ -580,73 +580,146 @@ __device__ __forceinline__ void ray_basis(const RayArgs &R, int64_t src, float *
     for (int b = 0; b < 9; ++b) bf[b] = (float)basis[b];
 }
 
+// Per-warp shared staging of the colour kernel: the rows of the segment's
+// distinct cells and their basis dot products d = (basis . SH_R, . SH_G,
+// . SH_B) (_color_at, K:138-152, factorised: colour = sum_q w_q d_q).
+struct SmemColour {
+    int32_t rows[32][8];
+    float4 d[256];
+};
+
+// Colours of one 32-record segment per warp.  Consecutive samples share
+// cells (two per voxel at half-voxel steps), so the 8 rows of each DISTINCT
+// cell are loaded once, cooperatively and coalesced: 8 lanes per row (7
+// float4 + an idle lane), 4 rows per warp instruction -- 4 cache lines per
+// instruction instead of up to 32 when every lane gathered its own sample's
+// rows (that version ran at 70 % of the L1 throughput limit).  Each row's 3
+// dot products are reduced over its 8 lanes and staged in shared memory;
+// every lane then forms its sample's colour from 8 staged d's.
 template <bool ABS, bool NEAREST, int MINB>
 __global__ void __launch_bounds__(128, MINB)
     colour_kernel(DGrid G, RayArgs R, Scratch S) {
     const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const unsigned le_mask = lane == 31 ? 0xffffffffu : (2u << lane) - 1u;
+    __shared__ SmemColour smem_all[4];
+    SmemColour &sm = smem_all[warp];
+    const int part = lane & 7, sub = lane >> 3;   // row-load role: column quad, row slot
     const int64_t nseg = *S.nseg_total;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t sg = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); sg < nseg;
-         sg += nw) {
+    for (int64_t sg = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; sg < nseg; sg += nw) {
         const int64_t ray = S.seg_ray[sg];
         const int64_t src = R.idx ? R.idx[ray] : ray;
         const int j = (int)(sg - S.seg_first[ray]) * 32 + lane;
+        const bool valid = j < S.ns[ray];
         float bf[9];
         ray_basis(R, src, bf);
-        double x0 = 0.0, x1 = 0.0, x2 = 0.0, q0 = 0.0, q1 = 0.0, q2 = 0.0;
-        if (j < S.ns[ray]) {
-            const int64_t k = ray * S.cap + j;
+        // this lane's 4 columns 4*part .. 4*part+3 -> per-channel coefficients
+        float cR[4], cG[4], cB[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int c = 4 * part + e;   // column 0 = sigma padding; 28..31 pitch padding
+            float coef = 0.f;
+            int ch = -1;
+            if (part < 7 && c >= 1) {
+                ch = (c - 1) / 9;
+                const int b = (c - 1) % 9;
+#pragma unroll
+                for (int bb = 0; bb < 9; ++bb)
+                    if (bb == b) coef = bf[bb];
+            }
+            cR[e] = ch == 0 ? coef : 0.f;
+            cG[e] = ch == 1 ? coef : 0.f;
+            cB[e] = ch == 2 ? coef : 0.f;
+        }
+        const int64_t k = ray * S.cap + j;
+        int4 cl = make_int4(0, 0, 0, 0);
+        float4 f4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        int32_t rows[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+        if (valid) {
+            cl = S.cell[k];
             const int4 ra = S.rows[2 * k];
-            const int4 rb = NEAREST ? make_int4(-1, -1, -1, -1) : S.rows[2 * k + 1];
-            const int32_t rows[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-            float4 f4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (!NEAREST) f4 = S.f[k];
+            rows[0] = ra.x;
+            if (!NEAREST) {
+                const int4 rb = S.rows[2 * k + 1];
+                rows[1] = ra.y;
+                rows[2] = ra.z;
+                rows[3] = ra.w;
+                rows[4] = rb.x;
+                rows[5] = rb.y;
+                rows[6] = rb.z;
+                rows[7] = rb.w;
+                f4 = S.f[k];
+            }
+        }
+        // distinct cells of the segment (samples are in march order)
+        const int pi = __shfl_up_sync(PLX_FULL_MASK, cl.x, 1);
+        const int pj = __shfl_up_sync(PLX_FULL_MASK, cl.y, 1);
+        const int pk = __shfl_up_sync(PLX_FULL_MASK, cl.z, 1);
+        const bool fresh = valid && (lane == 0 || cl.x != pi || cl.y != pj || cl.z != pk);
+        const unsigned fm = __ballot_sync(PLX_FULL_MASK, fresh);
+        const int ci = __popc(fm & le_mask) - 1;   // this sample's distinct-cell index
+        const int ncell = __popc(fm);
+        if (fresh) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sm.rows[ci][q] = rows[q];
+        }
+        __syncwarp();
+        // rows of the distinct cells: 16 rows per pass (4 per warp
+        // instruction), coalesced float4 loads; the next pass's loads are
+        // issued before this pass is reduced (software pipeline)
+        const int nrow = 8 * ncell;
+        auto load_pass = [&](int r0, float4 *v) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int rr = r0 + 4 * u + sub;
+                const int32_t row = rr < nrow ? sm.rows[rr >> 3][rr & 7] : -1;
+                v[u] = (row >= 0 && part < 7)
+                           ? __ldg(reinterpret_cast<const float4 *>(G.table + (int64_t)row * PLX_STRIDE) + part)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        };
+        float4 vc[4], vn[4];
+        load_pass(0, vc);
+        for (int r0 = 0; r0 < nrow; r0 += 16) {
+            if (r0 + 16 < nrow) load_pass(r0 + 16, vn);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float x[4] = {vc[u].x, vc[u].y, vc[u].z, vc[u].w};
+                float pR = 0.f, pG = 0.f, pB = 0.f;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    pR = __fmaf_rn(x[e], cR[e], pR);
+                    pG = __fmaf_rn(x[e], cG[e], pG);
+                    pB = __fmaf_rn(x[e], cB[e], pB);
+                }
+#pragma unroll
+                for (int off = 1; off < 8; off <<= 1) {   // reduce over the row's 8 lanes
+                    pR += __shfl_xor_sync(PLX_FULL_MASK, pR, off);
+                    pG += __shfl_xor_sync(PLX_FULL_MASK, pG, off);
+                    pB += __shfl_xor_sync(PLX_FULL_MASK, pB, off);
+                }
+                const int rr = r0 + 4 * u + sub;
+                if (part == 0 && rr < nrow) sm.d[rr] = make_float4(pR, pG, pB, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) vc[u] = vn[u];
+        }
+        __syncwarp();
+        double x0 = 0.0, x1 = 0.0, x2 = 0.0, q0 = 0.0, q1 = 0.0, q2 = 0.0;
+        if (valid) {
             float c0 = 0.f, c1 = 0.f, c2 = 0.f;
             constexpr int NQ = NEAREST ? 1 : 8;
-            // Unconditional loads (an empty corner reads row 0 with weight 0):
-            // without the per-corner branch the compiler keeps several
-            // corners' 7 float4 in flight instead of one round trip each.
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
-                const int32_t r = rows[q] >= 0 ? rows[q] : 0;
-                const float4 *row = reinterpret_cast<const float4 *>(G.table + (int64_t)r * PLX_STRIDE);
-                const float4 v0 = __ldg(row + 0), v1 = __ldg(row + 1), v2 = __ldg(row + 2),
-                             v3 = __ldg(row + 3), v4 = __ldg(row + 4), v5 = __ldg(row + 5),
-                             v6 = __ldg(row + 6);
-                // row layout: [-, R0..R8, G0..G8, B0..B8]  (_color_at, K:138-152)
-                float a0 = bf[0] * v0.y, a1 = bf[0] * v2.z, a2 = bf[0] * v4.w;
-                a0 = __fmaf_rn(bf[1], v0.z, a0);
-                a1 = __fmaf_rn(bf[1], v2.w, a1);
-                a2 = __fmaf_rn(bf[1], v5.x, a2);
-                a0 = __fmaf_rn(bf[2], v0.w, a0);
-                a1 = __fmaf_rn(bf[2], v3.x, a1);
-                a2 = __fmaf_rn(bf[2], v5.y, a2);
-                a0 = __fmaf_rn(bf[3], v1.x, a0);
-                a1 = __fmaf_rn(bf[3], v3.y, a1);
-                a2 = __fmaf_rn(bf[3], v5.z, a2);
-                a0 = __fmaf_rn(bf[4], v1.y, a0);
-                a1 = __fmaf_rn(bf[4], v3.z, a1);
-                a2 = __fmaf_rn(bf[4], v5.w, a2);
-                a0 = __fmaf_rn(bf[5], v1.z, a0);
-                a1 = __fmaf_rn(bf[5], v3.w, a1);
-                a2 = __fmaf_rn(bf[5], v6.x, a2);
-                a0 = __fmaf_rn(bf[6], v1.w, a0);
-                a1 = __fmaf_rn(bf[6], v4.x, a1);
-                a2 = __fmaf_rn(bf[6], v6.y, a2);
-                a0 = __fmaf_rn(bf[7], v2.x, a0);
-                a1 = __fmaf_rn(bf[7], v4.y, a1);
-                a2 = __fmaf_rn(bf[7], v6.z, a2);
-                a0 = __fmaf_rn(bf[8], v2.y, a0);
-                a1 = __fmaf_rn(bf[8], v4.z, a1);
-                a2 = __fmaf_rn(bf[8], v6.w, a2);
+                const float4 d = sm.d[8 * ci + q];
                 float w = 1.f;
                 if (!NEAREST)
                     w = ((q & 4) ? f4.x : 1.f - f4.x) * ((q & 2) ? f4.y : 1.f - f4.y) *
                         ((q & 1) ? f4.z : 1.f - f4.z);
-                if (rows[q] < 0) w = 0.f;   // K:131: empty corners contribute nothing
-                c0 = __fmaf_rn(w, a0, c0);
-                c1 = __fmaf_rn(w, a1, c1);
-                c2 = __fmaf_rn(w, a2, c2);
+                c0 = __fmaf_rn(w, d.x, c0);
+                c1 = __fmaf_rn(w, d.y, c1);
+                c2 = __fmaf_rn(w, d.z, c2);
             }
             S.c[k] = make_float4(c0, c1, c2, 0.f);
             const double wi = S.w[k];
@@ -679,6 +752,7 @@ __global__ void __launch_bounds__(128, MINB)
             o[4] = q1;
             o[5] = q2;
         }
+        __syncwarp();
     }
 }
 
@@ -932,7 +1006,7 @@ int march_blocks_per_sm() {
 }
 
 #ifndef PLX_COLOUR_MINB
-#define PLX_COLOUR_MINB 4
+#define PLX_COLOUR_MINB 6
 #endif
 constexpr int kMarchMinB = 6, kColourMinB = PLX_COLOUR_MINB, kScatterMinB = 4;
 
