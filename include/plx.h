@@ -271,6 +271,11 @@ typedef struct {
     double *sums;          /* device double[5]: 4 loss sums + sticky halt */
     int64_t *count;        /* device int64: n_touched (may be NULL)       */
     void *events[4];
+    /* optional device copies of the per-step scalars (tv_start; lr_sigma,
+     * lr_sh): when set the kernels read them at run time, so the call can be
+     * captured in a CUDA graph once and replayed with new values */
+    const int64_t *dev_tv_start;
+    const double *dev_lr;
 } plx_step_args;
 int plx_train_step(plx_grid *g, plx_grad *gb, const plx_step_args *a, void *stream);
 

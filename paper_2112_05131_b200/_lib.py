@@ -74,7 +74,8 @@ class PlxStepArgs(ctypes.Structure):
                 ("lr_sigma", ctypes.c_double), ("lr_sh", ctypes.c_double),
                 ("beta", ctypes.c_double), ("eps", ctypes.c_double),
                 ("sums", ctypes.c_void_p), ("count", ctypes.c_void_p),
-                ("events", ctypes.c_void_p * 4)]
+                ("events", ctypes.c_void_p * 4), ("dev_tv_start", ctypes.c_void_p),
+                ("dev_lr", ctypes.c_void_p)]
 
 
 _P = ctypes.c_void_p

@@ -17,6 +17,7 @@ namespace plx {
 // ---------------------------------------------------------------- TV ------
 struct TvArgs {
     const int64_t *cells;
+    const int64_t *start_dev;   // optional device copy of start (CUDA-graph replay)
     int64_t start, count, ncell;
     double fac[3], eps, f_sigma, f_sh;
     int wrap[3];
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
             if (a.cells) {
                 cid = a.cells[ci];
             } else {
-                cid = a.start + ci;
+                cid = (a.start_dev ? *a.start_dev : a.start) + ci;
                 if (cid >= a.ncell) cid %= a.ncell;   // wrapped run (rare branch)
             }
             const uint32_t c32 = (uint32_t)cid, dz = (uint32_t)G.Dz;
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
 // one mask byte; touched rows cost exactly their compulsory 672 B.
 struct OptArgs {
     float *table, *density, *v, *grad;
+    const double *lr_dev;      // optional device {lr_sigma, lr_sh} (CUDA-graph replay)
     double *guard;             // optional divergence guard (see guard_halts)
     float *sigma_lat;          // optional lattice sigma mirror: kept current
     const int32_t *row_cell;   // row -> lattice point (required with sigma_lat)
@@ -224,7 +226,8 @@ __device__ __forceinline__ void lat_update(const OptArgs &a, int32_t c, float si
 // The update of one float4 of one row (K:578-590), float64 arithmetic.
 __device__ __forceinline__ void opt_apply(const OptArgs &a, int quad, float4 &g4, float4 &t4,
                                           float4 &v4) {
-    opt_apply4(OptHyper{a.lr_sigma, a.lr_sh, a.beta, a.eps, a.rmsprop}, quad, g4, t4, v4);
+    const double ls = a.lr_dev ? a.lr_dev[0] : a.lr_sigma, lc = a.lr_dev ? a.lr_dev[1] : a.lr_sh;
+    opt_apply4(OptHyper{ls, lc, a.beta, a.eps, a.rmsprop}, quad, g4, t4, v4);
 }
 
 template <int NT>
@@ -828,15 +831,34 @@ unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 int64_t ncell(const plx_grid *g) { return g->dims[0] * g->dims[1] * g->dims[2]; }
 }  // namespace
 
+namespace plx {
+int opt_step_impl(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, double lr_sh,
+                  const double *lr_dev, double beta, double eps, int32_t rmsprop, int32_t clear,
+                  double *guard, int64_t *out_count, void *stream);
+int tv_impl(const plx_grid *g, const int64_t *cells, int64_t start, const int64_t *start_dev,
+            int64_t count, double fac_x, double fac_y, double fac_z, double eps, double f_sigma,
+            double f_sh, int32_t wrap_x, int32_t wrap_y, int32_t wrap_z, int32_t with_grad,
+            plx_grad *gb, double *out_sums, void *stream);
+}  // namespace plx
+
 extern "C" int plx_tv(const plx_grid *g, const int64_t *cells, int64_t start, int64_t count,
                       double fac_x, double fac_y, double fac_z, double eps, double f_sigma,
                       double f_sh, int32_t wrap_x, int32_t wrap_y, int32_t wrap_z,
                       int32_t with_grad, plx_grad *gb, double *out_sums, void *stream) {
+    return plx::tv_impl(g, cells, start, nullptr, count, fac_x, fac_y, fac_z, eps, f_sigma, f_sh,
+                        wrap_x, wrap_y, wrap_z, with_grad, gb, out_sums, stream);
+}
+
+int plx::tv_impl(const plx_grid *g, const int64_t *cells, int64_t start, const int64_t *start_dev,
+                 int64_t count, double fac_x, double fac_y, double fac_z, double eps,
+                 double f_sigma, double f_sh, int32_t wrap_x, int32_t wrap_y, int32_t wrap_z,
+                 int32_t with_grad, plx_grad *gb, double *out_sums, void *stream) {
     if (!grid_ok(g) || !out_sums || count < 0 || (with_grad && (!gb || !gb->grad || !gb->tmask)))
         return PLX_EINVAL;
     if (count == 0) return PLX_OK;
     TvArgs a;
     a.cells = cells;
+    a.start_dev = start_dev;
     a.start = start;
     a.count = count;
     a.ncell = ncell(g);
@@ -899,6 +921,13 @@ static void launch_opt_rows(const OptArgs &a, const int32_t *tids, const int64_t
 extern "C" int plx_opt_step(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, double lr_sh,
                             double beta, double eps, int32_t rmsprop, int32_t clear,
                             double *guard, int64_t *out_count, void *stream) {
+    return plx::opt_step_impl(g, v, gb, lr_sigma, lr_sh, nullptr, beta, eps, rmsprop, clear, guard,
+                              out_count, stream);
+}
+
+int plx::opt_step_impl(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, double lr_sh,
+                       const double *lr_dev, double beta, double eps, int32_t rmsprop,
+                       int32_t clear, double *guard, int64_t *out_count, void *stream) {
     if (!g || !gb || !gb->grad || !gb->tmask || (rmsprop && !v) ||
         (g->rows > 0 && (!g->table || !g->density)))
         return PLX_EINVAL;
@@ -907,7 +936,7 @@ extern "C" int plx_opt_step(plx_grid *g, float *v, plx_grad *gb, double lr_sigma
     // a mirror aliased to density (identity-linked dense grid) needs no upkeep
     float *lat = g->sigma_lat == g->density ? nullptr : g->sigma_lat;
     if (lat && !g->row_cell) return PLX_EINVAL;
-    OptArgs a{g->table, g->density, v, gb->grad, guard, lat, g->row_cell, gb->tmask, g->rows,
+    OptArgs a{g->table, g->density, v, gb->grad, lr_dev, guard, lat, g->row_cell, gb->tmask, g->rows,
               lr_sigma, lr_sh, beta, eps, rmsprop, clear, 1, reinterpret_cast<unsigned long long *>(out_count)};
     constexpr int NT = 256;
     cudaStream_t s = (cudaStream_t)stream;
@@ -946,7 +975,8 @@ extern "C" int plx_clear_grad(plx_grad *gb, int64_t rows, int64_t *out_count, vo
             count_from_list_kernel<<<1, 32, 0, s>>>(gb->tcnt, out_count);
         return status();
     }
-    OptArgs a{nullptr, nullptr, nullptr, gb->grad, nullptr, nullptr, nullptr, gb->tmask, rows, 0.0, 0.0,
+    OptArgs a{nullptr, nullptr, nullptr, gb->grad, nullptr, nullptr, nullptr, nullptr, gb->tmask, rows,
+              0.0, 0.0,
               0.0, 0.0, 0, 1, 0,
               reinterpret_cast<unsigned long long *>(out_count)};
     const int64_t segs = (rows + 127) / 128;

@@ -1011,7 +1011,10 @@ int march_blocks_per_sm() {
 #ifndef PLX_SCATTER_MINB
 #define PLX_SCATTER_MINB 5
 #endif
-constexpr int kMarchMinB = 6, kColourMinB = PLX_COLOUR_MINB, kScatterMinB = PLX_SCATTER_MINB;
+#ifndef PLX_MARCH_MINB
+#define PLX_MARCH_MINB 6
+#endif
+constexpr int kMarchMinB = PLX_MARCH_MINB, kColourMinB = PLX_COLOUR_MINB, kScatterMinB = PLX_SCATTER_MINB;
 
 int march_blocks(const plx_render_opts *o) {
     if (o->nearest)

@@ -2,11 +2,23 @@
 // call: fused render + backward, TV, and (single GPU) the update with the
 // fused clear and the device divergence guard.  The per-step Python cost of
 // the reference's step body (batch gather, three kernel wrappers, loss
-// check) becomes a descriptor update plus this call, so the host stays ahead
-// of the GPU even at ~0.3 ms steps.
+// check) becomes a descriptor update plus this call.  With the per-step
+// scalars read from device memory (dev_tv_start, dev_lr) and the batch in a
+// fixed buffer, the call's launches are captured once as a CUDA graph and
+// replayed every step (Trainer, graph mode).
 #include <cuda_runtime.h>
 
 #include "../../include/plx.h"
+
+namespace plx {
+int opt_step_impl(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, double lr_sh,
+                  const double *lr_dev, double beta, double eps, int32_t rmsprop, int32_t clear,
+                  double *guard, int64_t *out_count, void *stream);
+int tv_impl(const plx_grid *g, const int64_t *cells, int64_t start, const int64_t *start_dev,
+            int64_t count, double fac_x, double fac_y, double fac_z, double eps, double f_sigma,
+            double f_sh, int32_t wrap_x, int32_t wrap_y, int32_t wrap_z, int32_t with_grad,
+            plx_grad *gb, double *out_sums, void *stream);
+}  // namespace plx
 
 extern "C" int plx_train_step(plx_grid *g, plx_grad *gb, const plx_step_args *a, void *stream) {
     if (!g || !gb || !a || !a->sums) return PLX_EINVAL;
@@ -21,17 +33,17 @@ extern "C" int plx_train_step(plx_grid *g, plx_grad *gb, const plx_step_args *a,
     if (rc != PLX_OK) return rc;
     ev(1);
     if (a->tv_count > 0) {
-        rc = plx_tv(g, nullptr, a->tv_start, a->tv_count, a->tv_fac[0], a->tv_fac[1],
-                    a->tv_fac[2], a->tv_eps, a->tv_f_sigma, a->tv_f_sh, 0, 0, 0, 1, gb,
-                    a->sums + 2, stream);
+        rc = plx::tv_impl(g, nullptr, a->tv_start, a->dev_tv_start, a->tv_count, a->tv_fac[0],
+                          a->tv_fac[1], a->tv_fac[2], a->tv_eps, a->tv_f_sigma, a->tv_f_sh, 0, 0,
+                          0, 1, gb, a->sums + 2, stream);
         if (rc != PLX_OK) return rc;
     }
     ev(2);
     if (a->update) {
         if (a->count && cudaMemsetAsync(a->count, 0, sizeof(int64_t), s) != cudaSuccess)
             return PLX_ECUDA;
-        rc = plx_opt_step(g, a->v, gb, a->lr_sigma, a->lr_sh, a->beta, a->eps, a->rmsprop, 1,
-                          a->sums, a->count, stream);
+        rc = plx::opt_step_impl(g, a->v, gb, a->lr_sigma, a->lr_sh, a->dev_lr, a->beta, a->eps,
+                                a->rmsprop, 1, a->sums, a->count, stream);
         if (rc != PLX_OK) return rc;
     }
     ev(3);

@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import dataclasses
 import math
+import os
 import time
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -294,6 +295,13 @@ class Trainer:
         self._peers = None
         self._dp_pack = None
         self.step_events = None   # optional 4 torch.cuda.Events (plx_step_args.events)
+        # single-GPU steps replay a captured CUDA graph (PLX_GRAPH=0 disables)
+        self.use_graph = os.environ.get("PLX_GRAPH", "1") != "0"
+        self._bidx = torch.zeros(cfg.batch_size, dtype=torch.int64, device=self.device)
+        self._dparams = torch.zeros(3, dtype=torch.int64, device=self.device)
+        self._hparams = [torch.zeros(3, dtype=torch.int64).pin_memory() for _ in range(3)]
+        self._graphs, self._graph_args = {}, {}
+        self._eager_done = False
         self._refresh_cache()
 
     def _refresh_cache(self):
@@ -321,6 +329,7 @@ class Trainer:
         a.sums = self.sums.data_ptr()
         a.count = self.count.data_ptr()
         self._step_args = a
+        self._graphs, self._graph_args = {}, {}   # descriptors changed: re-capture
         w = self.world
         if w.active and w.mode == "union":
             R = self.grid.n_rows
@@ -383,33 +392,48 @@ class Trainer:
         B = int(idx.numel())
         s0, c0 = shard_range(B, self.world.rank, self.world.size)
         a = self._step_args
-        a.rays.idx = idx.data_ptr() + 8 * s0
-        a.rays.n = c0
-        a.rays.jitter = None
-        if self.opts.jitter > 0:
-            jt = torch.from_numpy(self.rng.random(B) * self.opts.jitter).to(self.device)
-            self._jt_keep = jt
-            a.rays.jitter = jt.data_ptr() + 8 * s0
-        a.up_scale = 2.0 / B
         tv_on = (cfg.lambda_tv_sigma > 0 or cfg.lambda_tv_sh > 0) and (
             cfg.tv_until_step < 0 or step < cfg.tv_until_step)
         n_tv = 0
-        a.tv_count = 0
+        tv_start = 0
         if tv_on:
             run = losses.sample_tv_cells(self.grid, cfg.tv_sample_frac, self.rng)
             n_tv = run.count
             sub = run.split(self.world.rank, self.world.size)
-            a.tv_start, a.tv_count = sub.start, sub.count
-            a.tv_f_sigma, a.tv_f_sh = cfg.lambda_tv_sigma / n_tv, cfg.lambda_tv_sh / n_tv
-        a.update = int(not self.world.active)
-        a.lr_sigma = optim.lr_at(cfg.lr_sigma, step)
-        a.lr_sh = optim.lr_at(cfg.lr_sh, step)
+            tv_start = sub.start
+        lr_s, lr_c = optim.lr_at(cfg.lr_sigma, step), optim.lr_at(cfg.lr_sh, step)
         ev = self.step_events
-        for i in range(4):
-            a.events[i] = ev[i].cuda_event if ev is not None else None
-        L = _lib.lib()
-        _lib.check(L.plx_train_step(ctypes.byref(self._cgrid), ctypes.byref(self._cgrad),
-                                    ctypes.byref(a), _lib.stream_ptr()), "train_step")
+        if self._graph_ok(B, ev):
+            # CUDA-graph replay: batch into the fixed buffer, per-step scalars
+            # through device memory, the whole step in one launch
+            self._bidx[:B].copy_(idx, non_blocking=True)
+            hp = self._hparams[step % 3]
+            hp[0] = tv_start
+            hp[1:3].view(torch.float64).copy_(torch.tensor([lr_s, lr_c], dtype=torch.float64))
+            self._dparams.copy_(hp, non_blocking=True)
+            self._replay(tv_on)
+        else:
+            a.rays.idx = idx.data_ptr() + 8 * s0
+            a.rays.n = c0
+            a.rays.jitter = None
+            if self.opts.jitter > 0:
+                jt = torch.from_numpy(self.rng.random(B) * self.opts.jitter).to(self.device)
+                self._jt_keep = jt
+                a.rays.jitter = jt.data_ptr() + 8 * s0
+            a.up_scale = 2.0 / B
+            a.tv_count = 0
+            if tv_on:
+                a.tv_start, a.tv_count = sub.start, sub.count
+                a.tv_f_sigma, a.tv_f_sh = cfg.lambda_tv_sigma / n_tv, cfg.lambda_tv_sh / n_tv
+            a.update = int(not self.world.active)
+            a.lr_sigma, a.lr_sh = lr_s, lr_c
+            a.dev_tv_start = None
+            a.dev_lr = None
+            for i in range(4):
+                a.events[i] = ev[i].cuda_event if ev is not None else None
+            _lib.check(_lib.lib().plx_train_step(ctypes.byref(self._cgrid),
+                                                 ctypes.byref(self._cgrad), ctypes.byref(a),
+                                                 _lib.stream_ptr()), "train_step")
         slot = step % 3
         if self.world.active:
             self.exchange_update(step, slot)
@@ -476,6 +500,44 @@ class Trainer:
             st), "dp_owner_update")
         dist.all_reduce(self.count, group=w.group)   # orders every owner before any clear
         self.grads.clear()
+
+    # -- CUDA-graph replay of the native step ------------------------------------
+    def _graph_ok(self, B: int, events) -> bool:
+        ok = (self.use_graph and self._eager_done and not self.world.active and events is None
+              and self.opts.jitter == 0 and B == self.cfg.batch_size)
+        self._eager_done = True   # the first step runs eagerly (one-time library queries)
+        return ok
+
+    def _replay(self, tv_on: bool) -> None:
+        """Replay (capturing on first use) the graph of plx_train_step for this
+        grid, batch size and TV on/off.  Batch indices come from _bidx, the
+        TV start and learning rates from _dparams (device memory)."""
+        g = self._graphs.get(tv_on)
+        if g is None:
+            cfg = self.cfg
+            a = _lib.PlxStepArgs()
+            ctypes.pointer(a)[0] = self._step_args   # copy of the static fields
+            a.rays.idx = self._bidx.data_ptr()
+            a.rays.n = cfg.batch_size
+            a.rays.jitter = None
+            a.up_scale = 2.0 / cfg.batch_size
+            a.update = 1
+            n_tv = max(1, int(round(cfg.tv_sample_frac * int(np.prod(self.grid.dims)))))
+            a.tv_count = n_tv if tv_on else 0
+            a.tv_f_sigma, a.tv_f_sh = cfg.lambda_tv_sigma / n_tv, cfg.lambda_tv_sh / n_tv
+            a.dev_tv_start = self._dparams.data_ptr()
+            a.dev_lr = self._dparams.data_ptr() + 8
+            for i in range(4):
+                a.events[i] = None
+            L = _lib.lib()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                _lib.check(L.plx_train_step(ctypes.byref(self._cgrid), ctypes.byref(self._cgrad),
+                                            ctypes.byref(a), _lib.stream_ptr()), "train_step")
+            self._graphs[tv_on] = g
+            self._graph_args[tv_on] = a
+        g.replay()
 
     def _loss(self, step, slot, B, n_tv) -> dict:
         cfg = self.cfg

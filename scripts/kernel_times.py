@@ -37,6 +37,13 @@ agg = defaultdict(list)
 for e in prof.events():
     if e.device_type.name == "CUDA":
         agg[e.name[:70]].append(e.device_time)
+# idle gaps between consecutive device operations (launch latency etc.)
+spans = sorted((e.time_range.start, e.time_range.end) for e in prof.events()
+               if e.device_type.name == "CUDA")
+gaps = [max(0.0, b[0] - a[1]) for a, b in zip(spans, spans[1:])]
+big = [g for g in gaps if g > 50.0]
+print(f"device idle between ops: {sum(g for g in gaps if g <= 50.0) / steps:7.1f} us/step "
+      f"(+ {len(big)} gaps > 50 us totalling {sum(big):.0f} us)")
 tot = 0.0
 for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
     tot += sum(v)
@@ -58,3 +65,12 @@ e1.record()
 torch.cuda.synchronize()
 print(f"step {e0.elapsed_time(e1) * 1000 / steps:9.1f} us device-timed, "
       f"{host * 1e6 / steps:9.1f} us host per tr.step() call")
+
+# pure host cost of enqueueing a step (no divergence checks, GPU runs behind)
+torch.cuda.synchronize()
+h0 = time.perf_counter()
+for s in range(warm + 2 * steps, warm + 3 * steps):
+    tr.step(s, check_finite=False)
+h1 = time.perf_counter()
+torch.cuda.synchronize()
+print(f"host enqueue only: {(h1 - h0) * 1e6 / steps:9.1f} us per tr.step(check_finite=False)")
