@@ -332,110 +332,104 @@ __global__ void __launch_bounds__(NT) opt_kernel(OptArgs a) {
 // Two-phase variant used when the caller provides the touched-id list of
 // GradientBuffer (G:25-68 touched_ids / _count, plx_grad.tids / tcnt):
 //   phase 1 (touched_compact_kernel): the mask -> a compact list of touched
-//            row ids (one atomic per warp per 2048-row range; order within
-//            the list does not matter, every row is updated independently)
+//            row ids (one atomic per 8192-row tile; ids sorted within a tile,
+//            tiles in atomic order -- every row is updated independently)
 //            and the mask clear;
 //   phase 2 (opt_rows_kernel): grid-stride over the list, 4 rows x 7 float4
 //            per warp group, kOptU groups in flight per lane, so every lane
 //            keeps 3*kOptU independent 16-byte loads outstanding -- the sweep
 //            above serialises mask scan -> loads -> update per segment.
-constexpr int kCompactSegs = 16;   // 128-row segments per warp range
-constexpr int kOptU = 4;
+// One block per tile of kTileRows mask bytes: every thread reads 32 bytes
+// (two uint4), the block scans the per-thread counts, takes its slice of the
+// list with ONE atomic, stages the ids in shared memory in row order and
+// writes them out coalesced.  The mask is HBM-streamed once; the kernel
+// costs ~4 instructions per mask word plus ~4 per touched row.
+constexpr int kCompactNT = 256;
+constexpr int kTileRows = kCompactNT * 32;
 
-__global__ void __launch_bounds__(256) touched_compact_kernel(uint8_t *tmask, int64_t rows,
-                                                              int32_t *tids, int64_t *tcnt,
-                                                              int clear, double *guard) {
-    __shared__ int warp_tot[8];
+// bit 8e+7 of the result set <=> byte e of x nonzero
+__device__ __forceinline__ uint32_t nonzero_bytes_hi(uint32_t x) {
+    return (((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u;
+}
+
+__global__ void __launch_bounds__(kCompactNT, 6) touched_compact_kernel(uint8_t *tmask,
+                                                                        int64_t rows,
+                                                                        int32_t *tids,
+                                                                        int64_t *tcnt, int clear,
+                                                                        double *guard) {
+    __shared__ uint16_t sid[kTileRows];   // row offsets within the tile
+    __shared__ int warp_tot[kCompactNT / 32];
     __shared__ unsigned long long blk_base;
     if (guard_halts(guard)) {   // non-finite loss: no update, no clear (T:473-480)
         if (blockIdx.x == 0 && threadIdx.x == 0) guard[4] = 1.0;
         return;
     }
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t nseg = (rows + 127) >> 7;
-    const int64_t nrange = (nseg + kCompactSegs - 1) / kCompactSegs;
-    // block-uniform trip count: one range per warp per iteration, one atomic
-    // per block per iteration (a single global counter serialises at L2)
-    for (int64_t rg0 = (int64_t)blockIdx.x * 8; rg0 < nrange; rg0 += (int64_t)gridDim.x * 8) {
-        const int64_t rg = rg0 + wib;
-        const int64_t s0 = rg * kCompactSegs;
-        const int64_t s1 = rg < nrange ? min(nseg, s0 + kCompactSegs) : s0;
-        uint32_t m[kCompactSegs];
-        int c = 0;
-        if (s1 - s0 == kCompactSegs && s1 * 128 <= rows) {   // interior: 16 loads in flight
-            const uint32_t *p = reinterpret_cast<const uint32_t *>(tmask + s0 * 128) + lane;
+    const int64_t r0 = (int64_t)blockIdx.x * kTileRows + (int64_t)threadIdx.x * 32;
+    uint32_t w[8];
+    if (r0 + 32 <= rows) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(tmask + r0);
+        const uint4 a0 = __ldcs(p), a1 = __ldcs(p + 1);
+        w[0] = a0.x; w[1] = a0.y; w[2] = a0.z; w[3] = a0.w;
+        w[4] = a1.x; w[5] = a1.y; w[6] = a1.z; w[7] = a1.w;
+    } else {
 #pragma unroll
-            for (int i = 0; i < kCompactSegs; ++i) m[i] = __ldcs(p + 32 * i);
-        } else {
-#pragma unroll
-            for (int i = 0; i < kCompactSegs; ++i) {
-                m[i] = 0u;
-                const int64_t r0 = (s0 + i) * 128 + lane * 4;
-                if (s0 + i < s1) {
-                    if (r0 + 3 < rows) {
-                        m[i] = *reinterpret_cast<const uint32_t *>(tmask + r0);
-                    } else {
-                        for (int e = 0; e < 4; ++e)
-                            if (r0 + e < rows && tmask[r0 + e]) m[i] |= 0xffu << (8 * e);
-                    }
-                }
+        for (int i = 0; i < 8; ++i) {
+            w[i] = 0u;
+            for (int e = 0; e < 4; ++e) {
+                const int64_t r = r0 + 4 * i + e;
+                if (r < rows && tmask[r]) w[i] |= 0xffu << (8 * e);
             }
         }
-#pragma unroll
-        for (int i = 0; i < kCompactSegs; ++i) c += nonzero_bytes(m[i]);
-        int incl = c;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int y = __shfl_up_sync(PLX_FULL_MASK, incl, off);
-            if (lane >= off) incl += y;
-        }
-        if (lane == 31) warp_tot[wib] = incl;
-        __syncthreads();
-        int before = 0, total = 0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            const int t = warp_tot[w];
-            before += w < wib ? t : 0;
-            total += t;
-        }
-        if (threadIdx.x == 0)
-            blk_base = total ? atomicAdd(reinterpret_cast<unsigned long long *>(tcnt),
-                                         (unsigned long long)total)
-                             : 0ull;
-        __syncthreads();
-        int64_t pos = (int64_t)blk_base + before + incl - c;
-        // 4 bits per mask word (one per nonzero byte) -> visit set rows only
-        uint64_t bits = 0;
-#pragma unroll
-        for (int i = 0; i < kCompactSegs; ++i) {
-            uint32_t x = m[i];
-            x = (x | (x >> 4)) & 0x0f0f0f0fu;
-            x = (x | (x >> 2)) & 0x03030303u;
-            x = (x | (x >> 1)) & 0x01010101u;                 // bit 8e = byte e nonzero
-            x = (x | (x >> 7)) & 0x00030003u;
-            x = (x | (x >> 14)) & 0xfu;                        // bits 0..3
-            bits |= (uint64_t)x << (4 * i);
-        }
-        while (bits) {
-            const int b = __ffsll((long long)bits) - 1;
-            bits &= bits - 1;
-            tids[pos++] = (int32_t)((s0 + (b >> 2)) * 128 + lane * 4 + (b & 3));
-        }
-#pragma unroll
-        for (int i = 0; i < kCompactSegs; ++i) {
-            if (!m[i]) continue;
-            const int64_t r0 = (s0 + i) * 128 + lane * 4;
-            if (clear) {
-                if (r0 + 3 < rows) {
-                    *reinterpret_cast<uint32_t *>(tmask + r0) = 0u;
-                } else {
-                    for (int e = 0; e < 4; ++e)
-                        if (r0 + e < rows) tmask[r0 + e] = 0;
-                }
-            }
-        }
-        __syncthreads();   // warp_tot / blk_base reuse
     }
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        w[i] = nonzero_bytes_hi(w[i]);
+        c += __popc(w[i]);
+    }
+    int incl = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(PLX_FULL_MASK, incl, off);
+        if (lane >= off) incl += y;
+    }
+    if (lane == 31) warp_tot[wib] = incl;
+    __syncthreads();
+    int before = 0, total = 0;
+#pragma unroll
+    for (int k = 0; k < kCompactNT / 32; ++k) {
+        const int t = warp_tot[k];
+        before += k < wib ? t : 0;
+        total += t;
+    }
+    if (total == 0) return;   // block-uniform
+    if (threadIdx.x == 0)
+        blk_base = atomicAdd(reinterpret_cast<unsigned long long *>(tcnt), (unsigned long long)total);
+    int q = before + incl - c;
+    const int rb = threadIdx.x * 32;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t x = w[i];
+        if (!x) continue;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (x & (0x80u << (8 * e))) sid[q++] = (uint16_t)(rb + 4 * i + e);
+    }
+    if (clear && c) {
+        if (r0 + 32 <= rows) {
+            uint4 *p = reinterpret_cast<uint4 *>(tmask + r0);
+            const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+            p[0] = z;
+            p[1] = z;
+        } else {
+            for (int r = 0; r < 32 && r0 + r < rows; ++r) tmask[r0 + r] = 0;
+        }
+    }
+    __syncthreads();
+    const int64_t base = (int64_t)blk_base;
+    const int32_t tile0 = (int32_t)((int64_t)blockIdx.x * kTileRows);
+    for (int i = threadIdx.x; i < total; i += kCompactNT) tids[base + i] = tile0 + sid[i];
 }
 
 template <int UU, int MINB>
@@ -942,11 +936,9 @@ int plx::opt_step_impl(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, dou
     cudaStream_t s = (cudaStream_t)stream;
     if (gb->tids) {   // two-phase: compact the touched set, then update the list
         if (cudaMemsetAsync(gb->tcnt, 0, sizeof(int64_t), s) != cudaSuccess) return PLX_ECUDA;
-        const int64_t nrange = ((g->rows + 127) / 128 + kCompactSegs - 1) / kCompactSegs;
-        int64_t nb = (nrange + NT / 32 - 1) / (NT / 32);
-        if (nb > (int64_t)num_sms() * 6) nb = (int64_t)num_sms() * 6;
-        touched_compact_kernel<<<(unsigned)nb, NT, 0, s>>>(gb->tmask, g->rows, gb->tids, gb->tcnt,
-                                                          clear, guard);
+        const int64_t nb = (g->rows + kTileRows - 1) / kTileRows;
+        touched_compact_kernel<<<(unsigned)nb, kCompactNT, 0, s>>>(gb->tmask, g->rows, gb->tids,
+                                                                   gb->tcnt, clear, guard);
         launch_opt_rows(a, gb->tids, gb->tcnt, s);
         return status();
     }
@@ -965,11 +957,9 @@ extern "C" int plx_clear_grad(plx_grad *gb, int64_t rows, int64_t *out_count, vo
     cudaStream_t s = (cudaStream_t)stream;
     if (gb->tids) {   // compact + clear the mask, then zero the listed rows
         if (cudaMemsetAsync(gb->tcnt, 0, sizeof(int64_t), s) != cudaSuccess) return PLX_ECUDA;
-        const int64_t nrange = ((rows + 127) / 128 + kCompactSegs - 1) / kCompactSegs;
-        int64_t nb = (nrange + NT / 32 - 1) / (NT / 32);
-        if (nb > (int64_t)num_sms() * 6) nb = (int64_t)num_sms() * 6;
-        touched_compact_kernel<<<(unsigned)nb, NT, 0, s>>>(gb->tmask, rows, gb->tids, gb->tcnt, 1,
-                                                          nullptr);
+        const int64_t nb = (rows + kTileRows - 1) / kTileRows;
+        touched_compact_kernel<<<(unsigned)nb, kCompactNT, 0, s>>>(gb->tmask, rows, gb->tids,
+                                                                   gb->tcnt, 1, nullptr);
         clear_rows_kernel<<<(unsigned)(num_sms() * 8), NT, 0, s>>>(gb->grad, gb->tids, gb->tcnt);
         if (out_count)
             count_from_list_kernel<<<1, 32, 0, s>>>(gb->tcnt, out_count);
