@@ -11,7 +11,7 @@ One JSON line on rank 0 (contract in the task statement):
   value   rays/s of the device-resident step (ray pool in HBM, batch indices
           drawn by the reference's EpochBatcher RNG), K steps timed with CUDA
           events, max over ranks, weak scaling (5000 rays per GPU)
-  e2e     the same step through the public API with the batch arrays in
+  e2e     the same step through the public API (Trainer.step_rays) with the batch arrays in
           pinned HOST memory: H2D of o/d/viewdir/gt + the kernels + D2H of the
           loss sums, every step
   roofline the dominant kernel's algorithmic bytes / its event-timed duration
@@ -339,24 +339,15 @@ def run_ours(args):
         sel = rng.integers(0, o.shape[0], B_local)
         host.append([torch.from_numpy(np.ascontiguousarray(a[sel])).pin_memory()
                      for a in (o, m, v, gt)])
-    dbuf = [torch.empty((B_local, 3), dtype=torch.float64, device=dev) for _ in range(4)]
-    hsums = torch.zeros(4, dtype=torch.float64).pin_memory()
     h2d = 4 * B_local * 3 * 8
     d2h = 4 * 8
 
     def e2e_step(step, hb):
-        for dsti, src in zip(dbuf, hb):
-            dsti.copy_(src, non_blocking=True)
-        tr.sums[0:4].zero_()
-        render.fused_mse_backward(tr.grid, dbuf[0], dbuf[1], dbuf[2], dbuf[3], tr.grads, tr.opts,
-                                  n_total=B_local * world_size, sums=tr.sums[0:2])
-        run = losses.sample_tv_cells(tr.grid, cfg.tv_sample_frac, tr.rng)
-        losses.tv_loss(tr.grid, run.split(rank, world_size), cfg.lambda_tv_sigma,
-                       cfg.lambda_tv_sh, tr.grads, sums=tr.sums[2:4], n_norm=run.count)
-        tr.exchange_update(step)                 # (all-reduce of sums,) exchange, update
-        hsums.copy_(tr.sums[0:4], non_blocking=True)
-        stream.synchronize()                      # the loss reaches the host every step
-        assert np.isfinite(hsums.numpy()).all()
+        # Trainer.step_rays: the 4 pinned host arrays -> the fixed device
+        # batch buffer, the step (one graph replay on 1 GPU; render + TV +
+        # exchange + update on N), the loss sums -> pinned host memory; the
+        # host checks every step's loss, two steps behind the device
+        tr.step_rays(step, hb[0], hb[1], hb[2], hb[3])
 
     for i in range(W2):
         e2e_step(args.warmup - W2 + i, host[i])
@@ -368,6 +359,7 @@ def run_ours(args):
     e0.record(stream)
     for i in range(K2):
         e2e_step(args.warmup + i, host[W2 + i])
+    tr.check_pending()                  # every timed step's loss read on the host
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()

@@ -301,6 +301,7 @@ class Trainer:
         self._dparams = torch.zeros(3, dtype=torch.int64, device=self.device)
         self._hparams = [torch.zeros(3, dtype=torch.int64).pin_memory() for _ in range(3)]
         self._graphs, self._graph_args = {}, {}
+        self._rays_buf = None   # step_rays(): fixed device batch buffer (4, B, 3)
         self._eager_done = False
         self._refresh_cache()
 
@@ -387,10 +388,39 @@ class Trainer:
         never waits for the step it just enqueued and the GPU never idles
         between steps.  sync=True (logging steps) waits for this step's loss
         and returns it in the record."""
-        cfg = self.cfg
         idx = self.batcher.next_device()
-        B = int(idx.numel())
-        s0, c0 = shard_range(B, self.world.rank, self.world.size)
+        return self._step(step, int(idx.numel()), idx, check_finite, sync)
+
+    def step_rays(self, step: int, origins, dirs, viewdirs, target, check_finite: bool = True,
+                  sync: bool = False) -> dict:
+        """One step on a caller-supplied batch instead of the pool (the step
+        body T:441-486 with the batch T:448-453 given): this rank's rays as
+        (B,3) float64 arrays -- host tensors (pinned: asynchronous copy) or
+        device tensors; viewdirs None = dirs.  The arrays are copied into a
+        fixed device buffer, so on one GPU the step replays the same CUDA
+        graph as step().  The global batch is B x world size (each rank
+        passes its own rays)."""
+        B = int(origins.shape[0])
+        buf = self._rays_buf
+        if buf is None or buf.shape[1] != B:
+            buf = self._rays_buf = torch.empty((4, B, 3), dtype=torch.float64, device=self.device)
+            for k in [k for k in self._graphs if k[0] == "rays"]:
+                del self._graphs[k]
+        for k, src in enumerate((origins, dirs, dirs if viewdirs is None else viewdirs, target)):
+            buf[k].copy_(torch.as_tensor(src), non_blocking=True)
+        return self._step(step, B, None, check_finite, sync)
+
+    def _step(self, step: int, B: int, idx, check_finite: bool, sync: bool) -> dict:
+        """step()/step_rays() body: idx = pool rows of the global batch, or
+        None for the rank-local batch in _rays_buf."""
+        cfg = self.cfg
+        pool_mode = idx is not None
+        if pool_mode:
+            s0, c0 = shard_range(B, self.world.rank, self.world.size)
+            n_global = B
+        else:
+            s0, c0 = 0, B
+            n_global = B * self.world.size
         a = self._step_args
         tv_on = (cfg.lambda_tv_sigma > 0 or cfg.lambda_tv_sh > 0) and (
             cfg.tv_until_step < 0 or step < cfg.tv_until_step)
@@ -403,24 +433,30 @@ class Trainer:
             tv_start = sub.start
         lr_s, lr_c = optim.lr_at(cfg.lr_sigma, step), optim.lr_at(cfg.lr_sh, step)
         ev = self.step_events
-        if self._graph_ok(B, ev):
+        if self._graph_ok(B, ev, pool_mode):
             # CUDA-graph replay: batch into the fixed buffer, per-step scalars
             # through device memory, the whole step in one launch
-            self._bidx[:B].copy_(idx, non_blocking=True)
+            if pool_mode:
+                self._bidx[:B].copy_(idx, non_blocking=True)
             hp = self._hparams[step % 3]
             hp[0] = tv_start
             hp[1:3].view(torch.float64).copy_(torch.tensor([lr_s, lr_c], dtype=torch.float64))
             self._dparams.copy_(hp, non_blocking=True)
-            self._replay(tv_on)
+            self._replay(tv_on, pool_mode)
         else:
-            a.rays.idx = idx.data_ptr() + 8 * s0
+            if pool_mode:
+                a.rays = self.pool.rays(None)
+                a.rays.idx = idx.data_ptr() + 8 * s0
+            else:
+                a.rays = self._rays_desc()
             a.rays.n = c0
             a.rays.jitter = None
             if self.opts.jitter > 0:
-                jt = torch.from_numpy(self.rng.random(B) * self.opts.jitter).to(self.device)
+                jt = torch.from_numpy(self.rng.random(n_global if pool_mode else B)
+                                      * self.opts.jitter).to(self.device)
                 self._jt_keep = jt
                 a.rays.jitter = jt.data_ptr() + 8 * s0
-            a.up_scale = 2.0 / B
+            a.up_scale = 2.0 / n_global
             a.tv_count = 0
             if tv_on:
                 a.tv_start, a.tv_count = sub.start, sub.count
@@ -434,6 +470,7 @@ class Trainer:
             _lib.check(_lib.lib().plx_train_step(ctypes.byref(self._cgrid),
                                                  ctypes.byref(self._cgrad), ctypes.byref(a),
                                                  _lib.stream_ptr()), "train_step")
+        B = n_global
         slot = step % 3
         if self.world.active:
             self.exchange_update(step, slot)
@@ -502,25 +539,39 @@ class Trainer:
         self.grads.clear()
 
     # -- CUDA-graph replay of the native step ------------------------------------
-    def _graph_ok(self, B: int, events) -> bool:
+    def _graph_ok(self, B: int, events, pool_mode: bool = True) -> bool:
         ok = (self.use_graph and self._eager_done and not self.world.active and events is None
-              and self.opts.jitter == 0 and B == self.cfg.batch_size)
+              and self.opts.jitter == 0 and (B == self.cfg.batch_size or not pool_mode))
         self._eager_done = True   # the first step runs eagerly (one-time library queries)
         return ok
 
-    def _replay(self, tv_on: bool) -> None:
+    def _rays_desc(self) -> _lib.PlxRays:
+        r = _lib.PlxRays()
+        buf = self._rays_buf
+        r.origins, r.dirs = buf[0].data_ptr(), buf[1].data_ptr()
+        r.viewdirs, r.target = buf[2].data_ptr(), buf[3].data_ptr()
+        r.jitter, r.idx, r.n = None, None, int(buf.shape[1])
+        return r
+
+    def _replay(self, tv_on: bool, pool_mode: bool = True) -> None:
         """Replay (capturing on first use) the graph of plx_train_step for this
-        grid, batch size and TV on/off.  Batch indices come from _bidx, the
-        TV start and learning rates from _dparams (device memory)."""
-        g = self._graphs.get(tv_on)
+        grid, batch source (pool rows in _bidx, or the rays in _rays_buf) and
+        TV on/off.  The TV start and learning rates come from _dparams
+        (device memory)."""
+        key = ("pool" if pool_mode else "rays", tv_on)
+        g = self._graphs.get(key)
         if g is None:
             cfg = self.cfg
             a = _lib.PlxStepArgs()
             ctypes.pointer(a)[0] = self._step_args   # copy of the static fields
-            a.rays.idx = self._bidx.data_ptr()
-            a.rays.n = cfg.batch_size
+            if pool_mode:
+                a.rays = self.pool.rays(None)
+                a.rays.idx = self._bidx.data_ptr()
+                a.rays.n = cfg.batch_size
+            else:
+                a.rays = self._rays_desc()
             a.rays.jitter = None
-            a.up_scale = 2.0 / cfg.batch_size
+            a.up_scale = 2.0 / int(a.rays.n)
             a.update = 1
             n_tv = max(1, int(round(cfg.tv_sample_frac * int(np.prod(self.grid.dims)))))
             a.tv_count = n_tv if tv_on else 0
@@ -535,8 +586,8 @@ class Trainer:
             with torch.cuda.graph(g):
                 _lib.check(L.plx_train_step(ctypes.byref(self._cgrid), ctypes.byref(self._cgrad),
                                             ctypes.byref(a), _lib.stream_ptr()), "train_step")
-            self._graphs[tv_on] = g
-            self._graph_args[tv_on] = a
+            self._graphs[key] = g
+            self._graph_args[key] = a
         g.replay()
 
     def _loss(self, step, slot, B, n_tv) -> dict:
