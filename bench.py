@@ -337,17 +337,17 @@ def run_ours(args):
     host = []
     for _ in range(K2 + W2):
         sel = rng.integers(0, o.shape[0], B_local)
-        host.append([torch.from_numpy(np.ascontiguousarray(a[sel])).pin_memory()
-                     for a in (o, m, v, gt)])
+        host.append(torch.from_numpy(np.stack([a[sel] for a in (o, m, v, gt)])).pin_memory())
     h2d = 4 * B_local * 3 * 8
     d2h = 4 * 8
 
     def e2e_step(step, hb):
-        # Trainer.step_rays: the 4 pinned host arrays -> the fixed device
-        # batch buffer, the step (one graph replay on 1 GPU; render + TV +
-        # exchange + update on N), the loss sums -> pinned host memory; the
-        # host checks every step's loss, two steps behind the device
-        tr.step_rays(step, hb[0], hb[1], hb[2], hb[3])
+        # Trainer.step_rays: the packed pinned host batch (o, d, viewdir, gt)
+        # -> the fixed device batch buffer in one copy, the step (one graph
+        # replay on 1 GPU; render + TV + exchange + update on N), the loss
+        # sums -> pinned host memory; the host checks every step's loss, two
+        # steps behind the device
+        tr.step_rays(step, hb)
 
     for i in range(W2):
         e2e_step(args.warmup - W2 + i, host[i])

@@ -391,23 +391,29 @@ class Trainer:
         idx = self.batcher.next_device()
         return self._step(step, int(idx.numel()), idx, check_finite, sync)
 
-    def step_rays(self, step: int, origins, dirs, viewdirs, target, check_finite: bool = True,
-                  sync: bool = False) -> dict:
+    def step_rays(self, step: int, origins, dirs=None, viewdirs=None, target=None,
+                  check_finite: bool = True, sync: bool = False) -> dict:
         """One step on a caller-supplied batch instead of the pool (the step
         body T:441-486 with the batch T:448-453 given): this rank's rays as
         (B,3) float64 arrays -- host tensors (pinned: asynchronous copy) or
         device tensors; viewdirs None = dirs.  The arrays are copied into a
         fixed device buffer, so on one GPU the step replays the same CUDA
         graph as step().  The global batch is B x world size (each rank
-        passes its own rays)."""
-        B = int(origins.shape[0])
+        passes its own rays).  A packed (4, B, 3) array [origins, dirs,
+        viewdirs, target] as `origins` alone is copied in one transfer."""
+        packed = dirs is None and origins.dim() == 3 and origins.shape[0] == 4
+        B = int(origins.shape[1] if packed else origins.shape[0])
         buf = self._rays_buf
         if buf is None or buf.shape[1] != B:
             buf = self._rays_buf = torch.empty((4, B, 3), dtype=torch.float64, device=self.device)
             for k in [k for k in self._graphs if k[0] == "rays"]:
                 del self._graphs[k]
-        for k, src in enumerate((origins, dirs, dirs if viewdirs is None else viewdirs, target)):
-            buf[k].copy_(torch.as_tensor(src), non_blocking=True)
+        if packed:
+            buf.copy_(torch.as_tensor(origins), non_blocking=True)
+        else:
+            for k, src in enumerate((origins, dirs, dirs if viewdirs is None else viewdirs,
+                                     target)):
+                buf[k].copy_(torch.as_tensor(src), non_blocking=True)
         return self._step(step, B, None, check_finite, sync)
 
     def _step(self, step: int, B: int, idx, check_finite: bool, sync: bool) -> dict:
