@@ -584,9 +584,28 @@ __device__ __forceinline__ void ray_basis(const RayArgs &R, int64_t src, float *
 // distinct cells and their basis dot products d = (basis . SH_R, . SH_G,
 // . SH_B) (_color_at, K:138-152, factorised: colour = sum_q w_q d_q).
 struct SmemColour {
-    int32_t rows[32][8];
-    float4 d[256];
+    int32_t rows[32][8];    // distinct cells' stencil rows (corner order)
+    int4 cell[32];          // distinct cells' lattice coordinates
+    uint16_t uidx[32][8];   // (cell, corner) -> slot in d (kZeroSlot: empty corner)
+    int32_t urow[256];      // the segment's distinct rows, in load order
+    float4 d[257];          // d per distinct row; d[kZeroSlot] = 0
 };
+constexpr int kZeroSlot = 256;
+
+// Lattice corners shared with an earlier distinct cell of the segment.  A
+// ray's samples are monotone along it, so the cells containing a lattice
+// point P form ONE contiguous run of the distinct-cell sequence, at most 4
+// long (the ray crosses each of the 3 planes through P once).  Corner q
+// (offset (q>>2, q>>1, q)&1) of cell L is corner q + ob of cell L-b iff
+// off(q) + (c_L - c_{L-b}) is in {0,1}^3 -- an 8-bit mask per axis.
+__device__ __forceinline__ unsigned shared_corner_mask(int4 c, int4 p, int &ob) {
+    const int dx = c.x - p.x, dy = c.y - p.y, dz = c.z - p.z;
+    const unsigned mx = dx == 0 ? 0xffu : dx == 1 ? 0x0fu : dx == -1 ? 0xf0u : 0u;
+    const unsigned my = dy == 0 ? 0xffu : dy == 1 ? 0x33u : dy == -1 ? 0xccu : 0u;
+    const unsigned mz = dz == 0 ? 0xffu : dz == 1 ? 0x55u : dz == -1 ? 0xaau : 0u;
+    ob = 4 * dx + 2 * dy + dz;
+    return mx & my & mz;
+}
 
 // Colours of one 32-record segment per warp.  Consecutive samples share
 // cells (two per voxel at half-voxel steps), so the 8 rows of each DISTINCT
@@ -663,17 +682,80 @@ __global__ void __launch_bounds__(128, MINB)
         if (fresh) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) sm.rows[ci][q] = rows[q];
+            sm.cell[ci] = cl;
         }
         __syncwarp();
-        // rows of the distinct cells: 16 rows per pass (4 per warp
-        // instruction), coalesced float4 loads; the next pass's loads are
-        // issued before this pass is reduced (software pipeline)
-        const int nrow = 8 * ncell;
+        // distinct rows: lane L < ncell owns cell L's corners not shared
+        // with cells L-1..L-3 (shared_corner_mask); owned corners get
+        // consecutive slots (warp scan), shared ones the slot of their owner
+        int nrow;
+        if (NEAREST) {
+            nrow = ncell;
+            if (lane < ncell) {
+                const int32_t r = sm.rows[lane][0];
+                sm.urow[lane] = r;
+                sm.uidx[lane][0] = r >= 0 ? (uint16_t)lane : (uint16_t)kZeroSlot;
+            }
+        } else {
+            unsigned m[4] = {0u, 0u, 0u, 0u}, rv = 0u;
+            int ob[4] = {0, 0, 0, 0};
+            if (lane < ncell) {
+                const int4 c = sm.cell[lane];
+#pragma unroll
+                for (int b = 1; b <= 3; ++b) {   // runs are contiguous: nest the masks
+                    if (lane - b >= 0) {
+                        m[b] = shared_corner_mask(c, sm.cell[lane - b], ob[b]);
+                        if (b > 1) m[b] &= m[b - 1];
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) rv |= (sm.rows[lane][q] >= 0 ? 1u : 0u) << q;
+            }
+            const unsigned own = lane < ncell ? (~m[1] & rv & 0xffu) : 0u;
+            const int cnt = __popc(own);
+            int incl = cnt;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(PLX_FULL_MASK, incl, off);
+                if (lane >= off) incl += y;
+            }
+            nrow = __shfl_sync(PLX_FULL_MASK, incl, 31);
+            if (lane < ncell) {
+                int u = incl - cnt;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if ((own >> q) & 1u) {
+                        sm.uidx[lane][q] = (uint16_t)u;
+                        sm.urow[u] = sm.rows[lane][q];
+                        ++u;
+                    } else if (!((rv >> q) & 1u)) {
+                        sm.uidx[lane][q] = (uint16_t)kZeroSlot;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane < ncell) {
+                const unsigned sh = m[1] & rv;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if ((sh >> q) & 1u) {
+                        const int b = ((m[3] >> q) & 1u) ? 3 : ((m[2] >> q) & 1u) ? 2 : 1;
+                        const int o = b == 3 ? ob[3] : b == 2 ? ob[2] : ob[1];
+                        sm.uidx[lane][q] = sm.uidx[lane - b][q + o];
+                    }
+                }
+            }
+        }
+        if (lane == 0) sm.d[kZeroSlot] = make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncwarp();
+        // the distinct rows: 16 rows per pass (4 per warp instruction),
+        // coalesced float4 loads; the next pass's loads are issued before
+        // this pass is reduced (software pipeline)
         auto load_pass = [&](int r0, float4 *v) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int rr = r0 + 4 * u + sub;
-                const int32_t row = rr < nrow ? sm.rows[rr >> 3][rr & 7] : -1;
+                const int32_t row = rr < nrow ? sm.urow[rr] : -1;
                 v[u] = (row >= 0 && part < 7)
                            ? __ldg(reinterpret_cast<const float4 *>(G.table + (int64_t)row * PLX_STRIDE) + part)
                            : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -712,7 +794,7 @@ __global__ void __launch_bounds__(128, MINB)
             constexpr int NQ = NEAREST ? 1 : 8;
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
-                const float4 d = sm.d[8 * ci + q];
+                const float4 d = sm.d[sm.uidx[ci][q]];
                 float w = 1.f;
                 if (!NEAREST)
                     w = ((q & 4) ? f4.x : 1.f - f4.x) * ((q & 2) ? f4.y : 1.f - f4.y) *
