@@ -188,7 +188,8 @@ __device__ __forceinline__ double relu(double x) { return x > 0.0 ? x : 0.0; }
 // reference's per-call s_t / s_dlt / s_sig / s_T / s_w / s_cpre scratch
 // (K:259-264, R:277-278).
 struct Scratch {
-    int *counter;      // ray scheduler of the march kernel (zeroed per wave)
+    int *counter;      // ray scheduler of the march kernel (zeroed per wave);
+                       // counter[2]: colour segment scheduler
     int64_t cap;       // records per ray
     int nseg_max;      // segments (32 records) per ray
     int *ns;           // [rays] composited samples
@@ -625,8 +626,17 @@ __global__ void __launch_bounds__(128, MINB)
     SmemColour &sm = smem_all[warp];
     const int part = lane & 7, sub = lane >> 3;   // row-load role: column quad, row slot
     const int64_t nseg = *S.nseg_total;
+    // first segment static (one per warp), the rest claimed dynamically
+    // (segment costs vary with their distinct cells); the next index is
+    // claimed when a segment starts, so the atomic's latency hides behind
+    // the segment's work.  Measured: all-static 66 / 16.4 us (early /
+    // step 2000), all-dynamic 61 / 17.6, dynamic with prefetch 63 / 24.6.
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t sg = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; sg < nseg; sg += nw) {
+    int64_t si_next = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    for (;;) {
+        const int64_t sg = __shfl_sync(PLX_FULL_MASK, si_next, 0);
+        if (sg >= nseg) break;
+        if (lane == 0) si_next = nw + atomicAdd(S.counter + 2, 1);
         const int64_t ray = S.seg_ray[sg];
         const int64_t src = R.idx ? R.idx[ray] : ray;
         const int j = (int)(sg - S.seg_first[ray]) * 32 + lane;
@@ -850,6 +860,9 @@ __global__ void __launch_bounds__(128, MINB)
     double mse_part = 0.0, cau_part = 0.0;
     const int64_t nseg = *S.nseg_total;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    // static interleave: a ray's consecutive segments go to the warps of one
+    // block at the same time (shared rows in one L1); dynamic scheduling
+    // measured 93 -> 129 us
     for (int64_t sg = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; sg < nseg; sg += nw) {
         const int64_t ray = S.seg_ray[sg];
         const int64_t src = R.idx ? R.idx[ray] : ray;
@@ -1098,6 +1111,17 @@ int march_blocks_per_sm() {
 #endif
 constexpr int kMarchMinB = PLX_MARCH_MINB, kColourMinB = PLX_COLOUR_MINB, kScatterMinB = PLX_SCATTER_MINB;
 
+// Resident blocks per SM of any kernel instantiation (cached per kernel).
+template <typename KernelT>
+int resident_blocks(KernelT *k) {
+    static int nb = 0;
+    if (!nb) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kThreads, 0);
+        if (nb <= 0) nb = 1;
+    }
+    return nb;
+}
+
 int march_blocks(const plx_render_opts *o) {
     if (o->nearest)
         return o->absolute ? march_blocks_per_sm<true, true, kMarchMinB>()
@@ -1269,14 +1293,28 @@ extern "C" int plx_render_fused_bwd(const plx_grid *g, const plx_rays *rays,
         out.mse_mode = mse_mode;
         out.up_scale = up_scale;
         out.lam_cauchy = lam_cauchy;
-        // ray counter + segment counter
-        if (cudaMemsetAsync(S.counter, 0, 2 * sizeof(int), s) != cudaSuccess) return PLX_ECUDA;
+        // ray counter, segment counter, colour scheduler
+        if (cudaMemsetAsync(S.counter, 0, 3 * sizeof(int), s) != cudaSuccess) return PLX_ECUDA;
         int64_t mb = (int64_t)sms * march_blocks(o);
         if (mb > (nw + kWarps - 1) / kWarps) mb = (nw + kWarps - 1) / kWarps;
         PLX_DISPATCH(o, march_bwd_kernel, kMarchMinB, dim3((unsigned)mb), G, R, K, out, S);
-        const dim3 sg_grid((unsigned)(sms * 8));
-        PLX_DISPATCH(o, colour_kernel, kColourMinB, sg_grid, G, R, S);
-        PLX_DISPATCH(o, scatter_kernel, kScatterMinB, sg_grid, G, R, K, out, S);
+        // segment kernels: exactly one resident wave, grid-stride over the
+        // segments (8 blocks per SM at 5-6 resident left a partial second
+        // wave that started only after the first had done its share)
+        int cb, sb;
+        if (o->nearest) {
+            cb = o->absolute ? resident_blocks(colour_kernel<true, true, kColourMinB>)
+                             : resident_blocks(colour_kernel<false, true, kColourMinB>);
+            sb = o->absolute ? resident_blocks(scatter_kernel<true, true, kScatterMinB>)
+                             : resident_blocks(scatter_kernel<false, true, kScatterMinB>);
+        } else {
+            cb = o->absolute ? resident_blocks(colour_kernel<true, false, kColourMinB>)
+                             : resident_blocks(colour_kernel<false, false, kColourMinB>);
+            sb = o->absolute ? resident_blocks(scatter_kernel<true, false, kScatterMinB>)
+                             : resident_blocks(scatter_kernel<false, false, kScatterMinB>);
+        }
+        PLX_DISPATCH(o, colour_kernel, kColourMinB, dim3((unsigned)(sms * cb)), G, R, S);
+        PLX_DISPATCH(o, scatter_kernel, kScatterMinB, dim3((unsigned)(sms * sb)), G, R, K, out, S);
     }
     return cudaPeekAtLastError() == cudaSuccess ? PLX_OK : PLX_ECUDA;
 }
