@@ -870,8 +870,14 @@ int plx::tv_impl(const plx_grid *g, const int64_t *cells, int64_t start, const i
     a.tmask = gb ? gb->tmask : nullptr;
     a.sums = out_sums;
     constexpr int NT = 256;
-    int64_t nb = (count + 31) / 32;   // 8 warps x 4 cells per block iteration
-    if (nb > (int64_t)num_sms() * 8) nb = (int64_t)num_sms() * 8;
+    // 8 warps x 4 cells per block iteration, at most one resident wave
+    static int tv_bps = 0;
+    if (!tv_bps) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tv_bps, tv_kernel<NT>, NT, 0);
+        if (tv_bps <= 0) tv_bps = 1;
+    }
+    int64_t nb = (count + 31) / 32;
+    if (nb > (int64_t)num_sms() * tv_bps) nb = (int64_t)num_sms() * tv_bps;
     tv_kernel<NT><<<(unsigned)nb, NT, 0, (cudaStream_t)stream>>>(make_dgrid(*g), a);
     return status();
 }
