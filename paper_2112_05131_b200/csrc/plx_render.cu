@@ -630,17 +630,32 @@ __global__ void __launch_bounds__(128, MINB)
     // (segment costs vary with their distinct cells); the next index is
     // claimed when a segment starts, so the atomic's latency hides behind
     // the segment's work.  Measured: all-static 66 / 16.4 us (early /
-    // step 2000), all-dynamic 61 / 17.6, dynamic with prefetch 63 / 24.6.
+    // step 2000), all-dynamic 61 / 17.6, all-dynamic claiming ahead 63 / 24.6,
+    // static-first claiming ahead 62.7 / 17.1.
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    int64_t si_next = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    // The next segment's descriptor (ray, first segment, samples, source
+    // row) is prefetched in two dependent levels while this segment's rows
+    // load and reduce, so the per-segment chain seg_ray -> ray fields ->
+    // records -> rows pays one round trip less per level.
+    int64_t nx_sg = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    int nx_ray = nx_sg < nseg ? S.seg_ray[nx_sg] : 0;
+    int nx_first = 0, nx_ns = 0;
+    int64_t nx_src = 0;
+    auto fetch2 = [&](int r_) {
+        nx_first = S.seg_first[r_];
+        nx_ns = S.ns[r_];
+        nx_src = R.idx ? R.idx[r_] : r_;
+    };
+    if (nx_sg < nseg) fetch2(nx_ray);
+    int claim = 0;
     for (;;) {
-        const int64_t sg = __shfl_sync(PLX_FULL_MASK, si_next, 0);
+        const int64_t sg = nx_sg;
         if (sg >= nseg) break;
-        if (lane == 0) si_next = nw + atomicAdd(S.counter + 2, 1);
-        const int64_t ray = S.seg_ray[sg];
-        const int64_t src = R.idx ? R.idx[ray] : ray;
-        const int j = (int)(sg - S.seg_first[ray]) * 32 + lane;
-        const bool valid = j < S.ns[ray];
+        if (lane == 0) claim = atomicAdd(S.counter + 2, 1);
+        const int64_t ray = nx_ray;
+        const int64_t src = nx_src;
+        const int j = (int)(sg - nx_first) * 32 + lane;
+        const bool valid = j < nx_ns;
         float bf[9];
         ray_basis(R, src, bf);
         // this lane's 4 columns 4*part .. 4*part+3 -> per-channel coefficients
@@ -773,6 +788,8 @@ __global__ void __launch_bounds__(128, MINB)
         };
         float4 vc[4], vn[4];
         load_pass(0, vc);
+        nx_sg = nw + __shfl_sync(PLX_FULL_MASK, claim, 0);
+        if (nx_sg < nseg) nx_ray = S.seg_ray[nx_sg];
         for (int r0 = 0; r0 < nrow; r0 += 16) {
             if (r0 + 16 < nrow) load_pass(r0 + 16, vn);
 #pragma unroll
@@ -797,6 +814,7 @@ __global__ void __launch_bounds__(128, MINB)
 #pragma unroll
             for (int u = 0; u < 4; ++u) vc[u] = vn[u];
         }
+        if (nx_sg < nseg) fetch2(nx_ray);
         __syncwarp();
         double x0 = 0.0, x1 = 0.0, x2 = 0.0, q0 = 0.0, q1 = 0.0, q2 = 0.0;
         if (valid) {
@@ -863,11 +881,48 @@ __global__ void __launch_bounds__(128, MINB)
     // static interleave: a ray's consecutive segments go to the warps of one
     // block at the same time (shared rows in one L1); dynamic scheduling
     // measured 93 -> 129 us
-    for (int64_t sg = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; sg < nseg; sg += nw) {
-        const int64_t ray = S.seg_ray[sg];
-        const int64_t src = R.idx ? R.idx[ray] : ray;
-        const int ns_r = S.ns[ray];
-        const int64_t s0 = S.seg_first[ray], s1 = s0 + ((ns_r + 31) >> 5);
+    // The next segment's descriptor is prefetched in two dependent levels
+    // (seg_ray, then the ray's fields) during this segment, and this
+    // segment's records are loaded before its prefix sums are reduced.
+    int64_t sg = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    int nx_ray = sg < nseg ? S.seg_ray[sg] : 0;
+    int nx_first = 0, nx_ns = 0;
+    int64_t nx_src = 0;
+    auto fetch2 = [&](int r_) {
+        nx_first = S.seg_first[r_];
+        nx_ns = S.ns[r_];
+        nx_src = R.idx ? R.idx[r_] : r_;
+    };
+    if (sg < nseg) fetch2(nx_ray);
+    for (; sg < nseg; sg += nw) {
+        const int64_t ray = nx_ray;
+        const int64_t src = nx_src;
+        const int ns_r = nx_ns;
+        const int64_t s0 = nx_first, s1 = s0 + ((ns_r + 31) >> 5);
+        const int64_t sgn = sg + nw;
+        if (sgn < nseg) nx_ray = S.seg_ray[sgn];
+        const int j = (int)(sg - s0) * 32 + lane;
+        const bool incl = j < ns_r;
+        const unsigned mask = __ballot_sync(PLX_FULL_MASK, incl);
+        double att = 1.0, Ti = 0.0, wi = 0.0, sig = 0.0;
+        float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f), f4 = c4;
+        int4 cl = make_int4(0, 0, 0, 0);
+        if (incl) {
+            const int64_t k = ray * S.cap + j;
+            att = S.att[k];
+            Ti = S.T[k];
+            wi = S.w[k];
+            c4 = S.c[k];
+            cl = S.cell[k];
+            if (!NEAREST) {
+                f4 = S.f[k];
+                *reinterpret_cast<int4 *>(&sc.rows[lane][0]) = S.rows[2 * k];
+                *reinterpret_cast<int4 *>(&sc.rows[lane][4]) = S.rows[2 * k + 1];
+            } else {
+                sc.rows[lane][0] = S.rows[2 * k].x;
+            }
+            if (cauchy) sig = S.sig[k];
+        }
         // ray totals and the prefix of the segments before this one
         double C0 = 0.0, C1 = 0.0, C2 = 0.0, Q0 = 0.0, Q1 = 0.0, Q2 = 0.0;
         double B0 = 0.0, B1 = 0.0, B2 = 0.0;
@@ -930,28 +985,7 @@ __global__ void __launch_bounds__(128, MINB)
         ray_basis(R, src, bf);
         LaneAcc<NEAREST> ra;
         ra.init(lane, bf);
-        const int j = (int)(sg - s0) * 32 + lane;
-        const bool incl = j < ns_r;
-        const unsigned mask = __ballot_sync(PLX_FULL_MASK, incl);
-        double att = 1.0, Ti = 0.0, wi = 0.0, sig = 0.0;
-        float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f), f4 = c4;
-        int4 cl = make_int4(0, 0, 0, 0);
-        if (incl) {
-            const int64_t k = ray * S.cap + j;
-            att = S.att[k];
-            Ti = S.T[k];
-            wi = S.w[k];
-            c4 = S.c[k];
-            cl = S.cell[k];
-            if (!NEAREST) {
-                f4 = S.f[k];
-                *reinterpret_cast<int4 *>(&sc.rows[lane][0]) = S.rows[2 * k];
-                *reinterpret_cast<int4 *>(&sc.rows[lane][4]) = S.rows[2 * k + 1];
-            } else {
-                sc.rows[lane][0] = S.rows[2 * k].x;
-            }
-            if (cauchy) sig = S.sig[k];
-        }
+        if (sgn < nseg) fetch2(nx_ray);
         // delta of this sample (K:200-205): step, except at the last position
         const double dl = (double)cl.w == last_si ? dlt_last : O.step;
         const double cc0 = relu((double)c4.x), cc1 = relu((double)c4.y),

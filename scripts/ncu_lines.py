@@ -2,7 +2,7 @@
 """Per-CUDA-source-line hot spots of one kernel in an .ncu-rep (needs -lineinfo):
 warp-stall samples and executed warp instructions aggregated by ncu per line.
 
-usage: python scripts/ncu_lines.py <rep> [top_n]"""
+usage: python scripts/ncu_lines.py <rep> [top_n] [kernel-regex]"""
 import csv
 import io
 import subprocess
@@ -10,7 +10,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kf = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True, check=True).stdout
 fname, hdr, rows = None, None, []
 for r in csv.reader(io.StringIO(out)):
