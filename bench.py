@@ -454,8 +454,9 @@ def run_ours(args):
                          "traffic": traffic, "algorithmic_bytes": alg[dom]},
             "cpu_baseline": cpu,
             "clocks": clk,
-            # per step: fused render+backward, TV, touched-set compaction, update
-            "gpu_launches": 4 * args.steps,
+            # per step: march_bwd, colour, scatter (render backward), TV,
+            # touched-set compaction, update (one graph replay launches all 6)
+            "gpu_launches": (5 + (1 if n_tv else 0)) * args.steps,
         }
         print(json.dumps(line), flush=True)
     if world_size > 1:
