@@ -265,7 +265,8 @@ def run_ours(args):
         tr.grid.invalidate()            # density edited in place: rebuild the sigma mirror
         tr.state.v.copy_(snap_v)
         tr.rng.bit_generator.state = snap_host[0]
-        b.perm, b.cursor, b._perm_dev = snap_host[1].copy(), snap_host[2], snap_host[3]
+        b.perm, b.cursor = snap_host[1].copy(), snap_host[2]
+        b._perm_dev = None              # re-upload into the persistent buffer
         tr.grads.clear()
         torch.cuda.synchronize()
 

@@ -276,6 +276,17 @@ typedef struct {
      * captured in a CUDA graph once and replayed with new values */
     const int64_t *dev_tv_start;
     const double *dev_lr;
+    /* optional device int64 added to rays.idx by the kernels: the batch as a
+     * moving slice of a fixed index buffer, so a captured graph replays any
+     * batch of the same size */
+    const int64_t *dev_idx_off;
+    /* optional pinned HOST memory read / written by the step's kernels (so
+     * a captured step has no memcpy nodes): host_params (4 int64) is copied
+     * to dev_params by the step's first kernel; the loss sums (4 doubles)
+     * are written to host_sums by the update's compaction kernel */
+    const int64_t *host_params;
+    int64_t *dev_params;
+    double *host_sums;
 } plx_step_args;
 int plx_train_step(plx_grid *g, plx_grad *gb, const plx_step_args *a, void *stream);
 

@@ -75,7 +75,9 @@ class PlxStepArgs(ctypes.Structure):
                 ("beta", ctypes.c_double), ("eps", ctypes.c_double),
                 ("sums", ctypes.c_void_p), ("count", ctypes.c_void_p),
                 ("events", ctypes.c_void_p * 4), ("dev_tv_start", ctypes.c_void_p),
-                ("dev_lr", ctypes.c_void_p)]
+                ("dev_lr", ctypes.c_void_p), ("dev_idx_off", ctypes.c_void_p),
+                ("host_params", ctypes.c_void_p), ("dev_params", ctypes.c_void_p),
+                ("host_sums", ctypes.c_void_p)]
 
 
 _P = ctypes.c_void_p

@@ -356,10 +356,14 @@ __global__ void __launch_bounds__(kCompactNT, 6) touched_compact_kernel(uint8_t 
                                                                         int64_t rows,
                                                                         int32_t *tids,
                                                                         int64_t *tcnt, int clear,
-                                                                        double *guard) {
+                                                                        double *guard,
+                                                                        double *host_sums) {
     __shared__ uint16_t sid[kTileRows];   // row offsets within the tile
     __shared__ int warp_tot[kCompactNT / 32];
     __shared__ unsigned long long blk_base;
+    // the step's loss sums are final here (render + TV done): hand them to
+    // the host's pinned slot directly (no memcpy node in the step graph)
+    if (host_sums && blockIdx.x == 0 && threadIdx.x < 4) host_sums[threadIdx.x] = guard[threadIdx.x];
     if (guard_halts(guard)) {   // non-finite loss: no update, no clear (T:473-480)
         if (blockIdx.x == 0 && threadIdx.x == 0) guard[4] = 1.0;
         return;
@@ -825,15 +829,7 @@ unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 int64_t ncell(const plx_grid *g) { return g->dims[0] * g->dims[1] * g->dims[2]; }
 }  // namespace
 
-namespace plx {
-int opt_step_impl(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, double lr_sh,
-                  const double *lr_dev, double beta, double eps, int32_t rmsprop, int32_t clear,
-                  double *guard, int64_t *out_count, void *stream);
-int tv_impl(const plx_grid *g, const int64_t *cells, int64_t start, const int64_t *start_dev,
-            int64_t count, double fac_x, double fac_y, double fac_z, double eps, double f_sigma,
-            double f_sh, int32_t wrap_x, int32_t wrap_y, int32_t wrap_z, int32_t with_grad,
-            plx_grad *gb, double *out_sums, void *stream);
-}  // namespace plx
+#include "plx_internal.h"
 
 extern "C" int plx_tv(const plx_grid *g, const int64_t *cells, int64_t start, int64_t count,
                       double fac_x, double fac_y, double fac_z, double eps, double f_sigma,
@@ -922,12 +918,13 @@ extern "C" int plx_opt_step(plx_grid *g, float *v, plx_grad *gb, double lr_sigma
                             double beta, double eps, int32_t rmsprop, int32_t clear,
                             double *guard, int64_t *out_count, void *stream) {
     return plx::opt_step_impl(g, v, gb, lr_sigma, lr_sh, nullptr, beta, eps, rmsprop, clear, guard,
-                              out_count, stream);
+                              out_count, stream, 0, nullptr);
 }
 
 int plx::opt_step_impl(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, double lr_sh,
                        const double *lr_dev, double beta, double eps, int32_t rmsprop,
-                       int32_t clear, double *guard, int64_t *out_count, void *stream) {
+                       int32_t clear, double *guard, int64_t *out_count, void *stream,
+                       int tcnt_ready, double *host_sums) {
     if (!g || !gb || !gb->grad || !gb->tmask || (rmsprop && !v) ||
         (g->rows > 0 && (!g->table || !g->density)))
         return PLX_EINVAL;
@@ -941,10 +938,12 @@ int plx::opt_step_impl(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, dou
     constexpr int NT = 256;
     cudaStream_t s = (cudaStream_t)stream;
     if (gb->tids) {   // two-phase: compact the touched set, then update the list
-        if (cudaMemsetAsync(gb->tcnt, 0, sizeof(int64_t), s) != cudaSuccess) return PLX_ECUDA;
+        if (!tcnt_ready && cudaMemsetAsync(gb->tcnt, 0, sizeof(int64_t), s) != cudaSuccess)
+            return PLX_ECUDA;
         const int64_t nb = (g->rows + kTileRows - 1) / kTileRows;
         touched_compact_kernel<<<(unsigned)nb, kCompactNT, 0, s>>>(gb->tmask, g->rows, gb->tids,
-                                                                   gb->tcnt, clear, guard);
+                                                                   gb->tcnt, clear, guard,
+                                                                   host_sums);
         launch_opt_rows(a, gb->tids, gb->tcnt, s);
         return status();
     }
@@ -965,7 +964,7 @@ extern "C" int plx_clear_grad(plx_grad *gb, int64_t rows, int64_t *out_count, vo
         if (cudaMemsetAsync(gb->tcnt, 0, sizeof(int64_t), s) != cudaSuccess) return PLX_ECUDA;
         const int64_t nb = (rows + kTileRows - 1) / kTileRows;
         touched_compact_kernel<<<(unsigned)nb, kCompactNT, 0, s>>>(gb->tmask, rows, gb->tids,
-                                                                   gb->tcnt, 1, nullptr);
+                                                                   gb->tcnt, 1, nullptr, nullptr);
         clear_rows_kernel<<<(unsigned)(num_sms() * 8), NT, 0, s>>>(gb->grad, gb->tids, gb->tcnt);
         if (out_count)
             count_from_list_kernel<<<1, 32, 0, s>>>(gb->tcnt, out_count);

@@ -26,10 +26,13 @@
 #include <stdlib.h>
 
 #include "plx_common.cuh"
+#include "plx_internal.h"
 
 namespace plx {
 
 enum Mode { FWD = 0, BWD = 1, MAXW = 2 };
+
+
 
 struct RayArgs {
     const double *__restrict__ origins;
@@ -39,7 +42,13 @@ struct RayArgs {
     const double *__restrict__ jitter;
     const int64_t *__restrict__ idx;
     int64_t n;
+    const int64_t *idx_off;   // optional device offset added to idx (graph replay)
 };
+
+// idx + *idx_off: the batch as a device-resident slice of a fixed buffer
+__device__ __forceinline__ const int64_t *ray_index(const RayArgs &R) {
+    return (R.idx && R.idx_off) ? R.idx + *R.idx_off : R.idx;
+}
 
 struct KOpts {
     double step, stop, bg[3];
@@ -458,6 +467,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 template <bool ABS, bool NEAREST, int MINB>
 __global__ void __launch_bounds__(128, MINB)
     march_bwd_kernel(DGrid G, RayArgs R, KOpts O, Outs out, Scratch S) {
+    R.idx = ray_index(R);
     const int lane = threadIdx.x & 31;
     double mse_part = 0.0;
     const int64_t slot = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -619,6 +629,7 @@ __device__ __forceinline__ unsigned shared_corner_mask(int4 c, int4 p, int &ob) 
 template <bool ABS, bool NEAREST, int MINB>
 __global__ void __launch_bounds__(128, MINB)
     colour_kernel(DGrid G, RayArgs R, Scratch S) {
+    R.idx = ray_index(R);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const unsigned le_mask = lane == 31 ? 0xffffffffu : (2u << lane) - 1u;
@@ -869,6 +880,7 @@ __global__ void __launch_bounds__(128, MINB)
 template <bool ABS, bool NEAREST, int MINB>
 __global__ void __launch_bounds__(128, MINB)
     scatter_kernel(DGrid G, RayArgs R, KOpts O, Outs out, Scratch S) {
+    R.idx = ray_index(R);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -1277,6 +1289,18 @@ extern "C" int plx_render_fused_bwd(const plx_grid *g, const plx_rays *rays,
                                     double lam_cauchy, plx_grad *gb, double *out_rgb,
                                     double *out_sums, void *scratch, int64_t scratch_bytes,
                                     void *stream) {
+    return plx::render_fused_bwd_impl(g, rays, nullptr, o, mse_mode, up_scale, lam_cauchy, gb,
+                                      out_rgb, out_sums, scratch, scratch_bytes, stream, 0);
+}
+
+// idx_off: optional device int64 added to rays->idx by the kernels (the
+// native step's graph replays with the batch as a moving slice of a fixed
+// permutation buffer).
+int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const int64_t *idx_off,
+                               const plx_render_opts *o, int32_t mse_mode, double up_scale,
+                               double lam_cauchy, plx_grad *gb, double *out_rgb,
+                               double *out_sums, void *scratch, int64_t scratch_bytes,
+                               void *stream, int counters_ready) {
     if (!gb || !gb->grad || !gb->tmask || !out_sums || !scratch) return PLX_EINVAL;
     const int rc = check_rays(g, rays, o, true);
     if (rc != PLX_OK) return rc;
@@ -1312,7 +1336,7 @@ extern "C" int plx_render_fused_bwd(const plx_grid *g, const plx_rays *rays,
         const int64_t nw = rays->n - w0 < L.wave ? rays->n - w0 : L.wave;
         RayArgs R{rays->origins, rays->dirs, rays->viewdirs, rays->target,
                   rays->jitter ? rays->jitter + w0 : nullptr, rays->idx ? rays->idx + w0 : nullptr,
-                  nw};
+                  nw, rays->idx ? idx_off : nullptr};
         if (!rays->idx) {   // implicit indices: offset the arrays instead
             R.origins += 3 * w0;
             R.dirs += 3 * w0;
@@ -1327,8 +1351,11 @@ extern "C" int plx_render_fused_bwd(const plx_grid *g, const plx_rays *rays,
         out.mse_mode = mse_mode;
         out.up_scale = up_scale;
         out.lam_cauchy = lam_cauchy;
-        // ray counter, segment counter, colour scheduler
-        if (cudaMemsetAsync(S.counter, 0, 3 * sizeof(int), s) != cudaSuccess) return PLX_ECUDA;
+        // ray counter, segment counter, colour scheduler (zeroed by the
+        // native step's prologue kernel for the first wave)
+        if (!(counters_ready && w0 == 0) &&
+            cudaMemsetAsync(S.counter, 0, 3 * sizeof(int), s) != cudaSuccess)
+            return PLX_ECUDA;
         int64_t mb = (int64_t)sms * march_blocks(o);
         if (mb > (nw + kWarps - 1) / kWarps) mb = (nw + kWarps - 1) / kWarps;
         PLX_DISPATCH(o, march_bwd_kernel, kMarchMinB, dim3((unsigned)mb), G, R, K, out, S);

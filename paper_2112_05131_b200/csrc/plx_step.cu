@@ -12,15 +12,7 @@
 
 #include "../../include/plx.h"
 
-namespace plx {
-int opt_step_impl(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, double lr_sh,
-                  const double *lr_dev, double beta, double eps, int32_t rmsprop, int32_t clear,
-                  double *guard, int64_t *out_count, void *stream);
-int tv_impl(const plx_grid *g, const int64_t *cells, int64_t start, const int64_t *start_dev,
-            int64_t count, double fac_x, double fac_y, double fac_z, double eps, double f_sigma,
-            double f_sh, int32_t wrap_x, int32_t wrap_y, int32_t wrap_z, int32_t with_grad,
-            plx_grad *gb, double *out_sums, void *stream);
-}  // namespace plx
+#include "plx_internal.h"
 
 namespace {
 // Per-device side stream for the TV branch.  TV reads only the parameters
@@ -55,13 +47,33 @@ SideStream *side_for_current_device() {
 }
 }  // namespace
 
+// The step's first node: zeroes the loss sums (not the sticky halt flag
+// sums[4]), the render scratch's 3 counters, the touched count and the
+// compaction counter, and copies the per-step scalars from pinned host
+// memory -- one kernel instead of four memsets and a memcpy in the graph.
+__global__ void step_prologue_kernel(double *sums, int *counters, int64_t *count, int64_t *tcnt,
+                                     const int64_t *host_params, int64_t *dev_params) {
+    const int t = threadIdx.x;
+    if (t < 4) sums[t] = 0.0;
+    if (t < 3) counters[t] = 0;
+    if (t == 0) {
+        if (count) *count = 0;
+        if (tcnt) *tcnt = 0;
+    }
+    if (host_params && t < 4) dev_params[t] = host_params[t];
+}
+
 extern "C" int plx_train_step(plx_grid *g, plx_grad *gb, const plx_step_args *a, void *stream) {
     if (!g || !gb || !a || !a->sums) return PLX_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     auto ev = [&](int i) {
         if (a->events[i]) cudaEventRecord((cudaEvent_t)a->events[i], s);
     };
-    if (cudaMemsetAsync(a->sums, 0, 4 * sizeof(double), s) != cudaSuccess) return PLX_ECUDA;
+    if (!a->scratch || (a->host_params && !a->dev_params)) return PLX_EINVAL;
+    step_prologue_kernel<<<1, 32, 0, s>>>(a->sums, reinterpret_cast<int *>(a->scratch),
+                                          a->update ? a->count : nullptr,
+                                          a->update ? gb->tcnt : nullptr, a->host_params,
+                                          a->dev_params);
     ev(0);
     // TV beside the backward unless per-leg events were asked for (timing)
     const bool timed = a->events[0] || a->events[1] || a->events[2] || a->events[3];
@@ -77,8 +89,9 @@ extern "C" int plx_train_step(plx_grid *g, plx_grad *gb, const plx_step_args *a,
         if (rc != PLX_OK) return rc;
         if (cudaEventRecord(side->join, side->s) != cudaSuccess) return PLX_ECUDA;
     }
-    int rc = plx_render_fused_bwd(g, &a->rays, &a->opts, 1, a->up_scale, a->lam_cauchy, gb,
-                                  nullptr, a->sums, a->scratch, a->scratch_bytes, stream);
+    int rc = plx::render_fused_bwd_impl(g, &a->rays, a->dev_idx_off, &a->opts, 1, a->up_scale,
+                                        a->lam_cauchy, gb, nullptr, a->sums, a->scratch,
+                                        a->scratch_bytes, stream, 1);
     if (rc != PLX_OK) return rc;
     ev(1);
     if (side) {
@@ -91,10 +104,8 @@ extern "C" int plx_train_step(plx_grid *g, plx_grad *gb, const plx_step_args *a,
     }
     ev(2);
     if (a->update) {
-        if (a->count && cudaMemsetAsync(a->count, 0, sizeof(int64_t), s) != cudaSuccess)
-            return PLX_ECUDA;
         rc = plx::opt_step_impl(g, a->v, gb, a->lr_sigma, a->lr_sh, a->dev_lr, a->beta, a->eps,
-                                a->rmsprop, 1, a->sums, a->count, stream);
+                                a->rmsprop, 1, a->sums, a->count, stream, 1, a->host_sums);
         if (rc != PLX_OK) return rc;
     }
     ev(3);

@@ -197,8 +197,16 @@ class EpochBatcher:
         self._perm_dev = None
 
     def _dev_perm(self):
+        """The device permutation, in ONE persistent buffer (a captured step
+        graph reads batches as slices of it); a new epoch's permutation is
+        copied in stream order, after every step that read the old one."""
         if self._perm_dev is None:
-            self._perm_dev = torch.from_numpy(self.perm).to(self.device or "cuda")
+            buf = getattr(self, "_perm_buf", None)
+            if buf is None or buf.numel() != self.n:
+                buf = self._perm_buf = torch.empty(self.n, dtype=torch.int64,
+                                                   device=self.device or "cuda")
+            buf.copy_(torch.from_numpy(self.perm))
+            self._perm_dev = buf
         return self._perm_dev
 
     def next(self) -> np.ndarray:
@@ -216,7 +224,13 @@ class EpochBatcher:
         return np.concatenate(chunks) if len(chunks) > 1 else chunks[0]
 
     def next_device(self) -> torch.Tensor:
-        chunks = []
+        return self.next_slice()[0]
+
+    def next_slice(self):
+        """next_device() and, when the batch is ONE slice of the device
+        permutation buffer (it does not cross an epoch), its offset there;
+        None otherwise."""
+        chunks, offs = [], []
         need = self.batch_size
         while need > 0:
             if self.cursor >= self.n:
@@ -225,9 +239,12 @@ class EpochBatcher:
                 self.cursor = 0
             take = min(need, self.n - self.cursor)
             chunks.append(self._dev_perm()[self.cursor:self.cursor + take])
+            offs.append(self.cursor)
             self.cursor += take
             need -= take
-        return torch.cat(chunks) if len(chunks) > 1 else chunks[0]
+        if len(chunks) > 1:
+            return torch.cat(chunks), None
+        return chunks[0], offs[0]
 
 
 @dataclass
@@ -297,9 +314,11 @@ class Trainer:
         self.step_events = None   # optional 4 torch.cuda.Events (plx_step_args.events)
         # single-GPU steps replay a captured CUDA graph (PLX_GRAPH=0 disables)
         self.use_graph = os.environ.get("PLX_GRAPH", "1") != "0"
-        self._bidx = torch.zeros(cfg.batch_size, dtype=torch.int64, device=self.device)
-        self._dparams = torch.zeros(3, dtype=torch.int64, device=self.device)
-        self._hparams = [torch.zeros(3, dtype=torch.int64).pin_memory() for _ in range(3)]
+        # graph mode: per-step scalars {tv_start, lr_sigma, lr_sh (f64 bits),
+        # batch offset} in 3 pinned slots, copied to _dparams by the graph
+        self._dparams = torch.zeros(4, dtype=torch.int64, device=self.device)
+        self._hparams = [torch.zeros(4, dtype=torch.int64).pin_memory() for _ in range(3)]
+        self._hparams_np = [h.numpy() for h in self._hparams]
         self._graphs, self._graph_args = {}, {}
         self._rays_buf = None   # step_rays(): fixed device batch buffer (4, B, 3)
         self._eager_done = False
@@ -388,8 +407,8 @@ class Trainer:
         never waits for the step it just enqueued and the GPU never idles
         between steps.  sync=True (logging steps) waits for this step's loss
         and returns it in the record."""
-        idx = self.batcher.next_device()
-        return self._step(step, int(idx.numel()), idx, check_finite, sync)
+        idx, off = self.batcher.next_slice()
+        return self._step(step, int(idx.numel()), idx, check_finite, sync, off)
 
     def step_rays(self, step: int, origins, dirs=None, viewdirs=None, target=None,
                   check_finite: bool = True, sync: bool = False) -> dict:
@@ -416,9 +435,11 @@ class Trainer:
                 buf[k].copy_(torch.as_tensor(src), non_blocking=True)
         return self._step(step, B, None, check_finite, sync)
 
-    def _step(self, step: int, B: int, idx, check_finite: bool, sync: bool) -> dict:
-        """step()/step_rays() body: idx = pool rows of the global batch, or
-        None for the rank-local batch in _rays_buf."""
+    def _step(self, step: int, B: int, idx, check_finite: bool, sync: bool,
+              idx_off: int | None = None) -> dict:
+        """step()/step_rays() body: idx = pool rows of the global batch (at
+        offset idx_off of the batcher's permutation buffer when it is one
+        slice of it), or None for the rank-local batch in _rays_buf."""
         cfg = self.cfg
         pool_mode = idx is not None
         if pool_mode:
@@ -439,16 +460,20 @@ class Trainer:
             tv_start = sub.start
         lr_s, lr_c = optim.lr_at(cfg.lr_sigma, step), optim.lr_at(cfg.lr_sh, step)
         ev = self.step_events
-        if self._graph_ok(B, ev, pool_mode):
-            # CUDA-graph replay: batch into the fixed buffer, per-step scalars
-            # through device memory, the whole step in one launch
-            if pool_mode:
-                self._bidx[:B].copy_(idx, non_blocking=True)
-            hp = self._hparams[step % 3]
+        slot = step % 3
+        graphed = self._graph_ok(B, ev, pool_mode) and (idx_off is not None or not pool_mode)
+        if graphed:
+            # CUDA-graph replay of the whole step: the graph for this slot
+            # copies the per-step scalars (TV start, learning rates, batch
+            # offset in the permutation buffer) from pinned slot `slot`, runs
+            # the step and copies the loss sums to pinned slot `slot`; the
+            # graph of step-3 used the slot last
+            self._sums_ready[slot].synchronize()
+            hp = self._hparams_np[slot]
             hp[0] = tv_start
-            hp[1:3].view(torch.float64).copy_(torch.tensor([lr_s, lr_c], dtype=torch.float64))
-            self._dparams.copy_(hp, non_blocking=True)
-            self._replay(tv_on, pool_mode)
+            hp[1:3].view(np.float64)[:] = (lr_s, lr_c)
+            hp[3] = idx_off if pool_mode else 0
+            self._replay(tv_on, pool_mode, slot)
         else:
             if pool_mode:
                 a.rays = self.pool.rays(None)
@@ -477,13 +502,13 @@ class Trainer:
                                                  ctypes.byref(self._cgrad), ctypes.byref(a),
                                                  _lib.stream_ptr()), "train_step")
         B = n_global
-        slot = step % 3
         if self.world.active:
             self.exchange_update(step, slot)
             if ev is not None:
                 ev[3].record()    # "after update" = after the exchange + update
         else:
-            self._host_sums[slot].copy_(self.sums[0:4], non_blocking=True)
+            if not graphed:
+                self._host_sums[slot].copy_(self.sums[0:4], non_blocking=True)
             self._sums_ready[slot].record()
         rec = {"B": B, "n_tv": n_tv}
         if sync:
@@ -559,12 +584,14 @@ class Trainer:
         r.jitter, r.idx, r.n = None, None, int(buf.shape[1])
         return r
 
-    def _replay(self, tv_on: bool, pool_mode: bool = True) -> None:
-        """Replay (capturing on first use) the graph of plx_train_step for this
-        grid, batch source (pool rows in _bidx, or the rays in _rays_buf) and
-        TV on/off.  The TV start and learning rates come from _dparams
-        (device memory)."""
-        key = ("pool" if pool_mode else "rays", tv_on)
+    def _replay(self, tv_on: bool, pool_mode: bool, slot: int) -> None:
+        """Replay (capturing on first use) the graph of one whole step for
+        this grid, batch source (a slice of the batcher's permutation buffer
+        at the offset in _dparams[3], or the rays in _rays_buf), TV on/off and
+        pinned slot: plx_train_step's prologue kernel copies the slot's
+        scalars to _dparams, and its compaction kernel writes the loss sums
+        to the slot's pinned sums."""
+        key = ("pool" if pool_mode else "rays", tv_on, slot)
         g = self._graphs.get(key)
         if g is None:
             cfg = self.cfg
@@ -572,10 +599,12 @@ class Trainer:
             ctypes.pointer(a)[0] = self._step_args   # copy of the static fields
             if pool_mode:
                 a.rays = self.pool.rays(None)
-                a.rays.idx = self._bidx.data_ptr()
+                a.rays.idx = self.batcher._dev_perm().data_ptr()
                 a.rays.n = cfg.batch_size
+                a.dev_idx_off = self._dparams.data_ptr() + 24
             else:
                 a.rays = self._rays_desc()
+                a.dev_idx_off = None
             a.rays.jitter = None
             a.up_scale = 2.0 / int(a.rays.n)
             a.update = 1
@@ -584,6 +613,11 @@ class Trainer:
             a.tv_f_sigma, a.tv_f_sh = cfg.lambda_tv_sigma / n_tv, cfg.lambda_tv_sh / n_tv
             a.dev_tv_start = self._dparams.data_ptr()
             a.dev_lr = self._dparams.data_ptr() + 8
+            # the kernels read the slot's scalars from / write the loss sums
+            # to pinned host memory: the graph has kernel nodes only
+            a.host_params = self._hparams[slot].data_ptr()
+            a.dev_params = self._dparams.data_ptr()
+            a.host_sums = self._host_sums[slot].data_ptr()
             for i in range(4):
                 a.events[i] = None
             L = _lib.lib()

@@ -38,10 +38,22 @@ for e in prof.events():
     if e.device_type.name == "CUDA":
         agg[e.name[:70]].append(e.device_time)
 # idle gaps between consecutive device operations (launch latency etc.)
-spans = sorted((e.time_range.start, e.time_range.end) for e in prof.events()
-               if e.device_type.name == "CUDA")
-gaps = [max(0.0, b[0] - a[1]) for a, b in zip(spans, spans[1:])]
+evs = sorted(((e.time_range.start, e.time_range.end, e.name[:40]) for e in prof.events()
+              if e.device_type.name == "CUDA"))
+spans = [(a, b) for a, b, _ in evs]
+gaps, end = [], None     # idle = time covered by no operation (streams overlap)
+for a, b in spans:
+    if end is not None:
+        gaps.append(max(0.0, a - end))
+    end = b if end is None else max(end, b)
 big = [g for g in gaps if g > 50.0]
+if os.environ.get("KT_TIMELINE"):   # the ops of the last two steps, in start order
+    n_last = 2 * max(1, len(evs) // steps)
+    t0, end = evs[-n_last][0], None
+    for a, b, name in evs[-n_last:]:
+        idle = 0.0 if end is None else max(0.0, a - end)
+        end = b if end is None else max(end, b)
+        print(f"  +{a - t0:8.1f} us  {b - a:7.1f} us  idle before {idle:5.1f}  {name}")
 print(f"device idle between ops: {sum(g for g in gaps if g <= 50.0) / steps:7.1f} us/step "
       f"(+ {len(big)} gaps > 50 us totalling {sum(big):.0f} us)")
 tot = 0.0
