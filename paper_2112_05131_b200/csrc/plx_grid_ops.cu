@@ -836,13 +836,13 @@ extern "C" int plx_tv(const plx_grid *g, const int64_t *cells, int64_t start, in
                       double f_sh, int32_t wrap_x, int32_t wrap_y, int32_t wrap_z,
                       int32_t with_grad, plx_grad *gb, double *out_sums, void *stream) {
     return plx::tv_impl(g, cells, start, nullptr, count, fac_x, fac_y, fac_z, eps, f_sigma, f_sh,
-                        wrap_x, wrap_y, wrap_z, with_grad, gb, out_sums, stream);
+                        wrap_x, wrap_y, wrap_z, with_grad, gb, out_sums, stream, 0);
 }
 
 int plx::tv_impl(const plx_grid *g, const int64_t *cells, int64_t start, const int64_t *start_dev,
                  int64_t count, double fac_x, double fac_y, double fac_z, double eps,
                  double f_sigma, double f_sh, int32_t wrap_x, int32_t wrap_y, int32_t wrap_z,
-                 int32_t with_grad, plx_grad *gb, double *out_sums, void *stream) {
+                 int32_t with_grad, plx_grad *gb, double *out_sums, void *stream, int short_blocks) {
     if (!grid_ok(g) || !out_sums || count < 0 || (with_grad && (!gb || !gb->grad || !gb->tmask)))
         return PLX_EINVAL;
     if (count == 0) return PLX_OK;
@@ -873,7 +873,10 @@ int plx::tv_impl(const plx_grid *g, const int64_t *cells, int64_t start, const i
         if (tv_bps <= 0) tv_bps = 1;
     }
     int64_t nb = (count + 31) / 32;
-    if (nb > (int64_t)num_sms() * tv_bps) nb = (int64_t)num_sms() * tv_bps;
+    // short_blocks: one 32-cell iteration per block, so the blocks of a
+    // background TV yield their SM slots quickly to a higher-priority
+    // stream's kernels; else one resident wave
+    if (!short_blocks && nb > (int64_t)num_sms() * tv_bps) nb = (int64_t)num_sms() * tv_bps;
     tv_kernel<NT><<<(unsigned)nb, NT, 0, (cudaStream_t)stream>>>(make_dgrid(*g), a);
     return status();
 }

@@ -10,12 +10,13 @@
 namespace plx {
 // plx_render_fused_bwd plus: idx_off = optional device int64 added to
 // rays->idx; counters_ready = the scratch's 3 counters were zeroed by the
-// caller (first wave only).
+// caller (first wave only); after_march = optional cudaEvent_t recorded once
+// the first wave's march kernel is enqueued.
 int render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const int64_t *idx_off,
                           const plx_render_opts *o, int32_t mse_mode, double up_scale,
                           double lam_cauchy, plx_grad *gb, double *out_rgb, double *out_sums,
                           void *scratch, int64_t scratch_bytes, void *stream,
-                          int counters_ready);
+                          int counters_ready, void *after_march = nullptr);
 // plx_opt_step plus: lr_dev = optional device {lr_sigma, lr_sh};
 // tcnt_ready = gb->tcnt was zeroed by the caller; host_sums = optional
 // pinned host double[4] that receives the guard's loss sums.
@@ -23,9 +24,10 @@ int opt_step_impl(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, double l
                   const double *lr_dev, double beta, double eps, int32_t rmsprop, int32_t clear,
                   double *guard, int64_t *out_count, void *stream, int tcnt_ready,
                   double *host_sums);
-// plx_tv_loss plus start_dev = optional device run start.
+// plx_tv_loss plus start_dev = optional device run start; short_blocks = one
+// 32-cell iteration per block (a background TV on a low-priority stream).
 int tv_impl(const plx_grid *g, const int64_t *cells, int64_t start, const int64_t *start_dev,
             int64_t count, double fac_x, double fac_y, double fac_z, double eps, double f_sigma,
             double f_sh, int32_t wrap_x, int32_t wrap_y, int32_t wrap_z, int32_t with_grad,
-            plx_grad *gb, double *out_sums, void *stream);
+            plx_grad *gb, double *out_sums, void *stream, int short_blocks = 0);
 }  // namespace plx

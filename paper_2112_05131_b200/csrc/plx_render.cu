@@ -1300,7 +1300,7 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
                                const plx_render_opts *o, int32_t mse_mode, double up_scale,
                                double lam_cauchy, plx_grad *gb, double *out_rgb,
                                double *out_sums, void *scratch, int64_t scratch_bytes,
-                               void *stream, int counters_ready) {
+                               void *stream, int counters_ready, void *after_march) {
     if (!gb || !gb->grad || !gb->tmask || !out_sums || !scratch) return PLX_EINVAL;
     const int rc = check_rays(g, rays, o, true);
     if (rc != PLX_OK) return rc;
@@ -1359,6 +1359,9 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
         int64_t mb = (int64_t)sms * march_blocks(o);
         if (mb > (nw + kWarps - 1) / kWarps) mb = (nw + kWarps - 1) / kWarps;
         PLX_DISPATCH(o, march_bwd_kernel, kMarchMinB, dim3((unsigned)mb), G, R, K, out, S);
+        if (after_march && w0 == 0 &&
+            cudaEventRecord((cudaEvent_t)after_march, s) != cudaSuccess)
+            return PLX_ECUDA;
         // segment kernels: exactly one resident wave, grid-stride over the
         // segments (8 blocks per SM at 5-6 resident left a partial second
         // wave that started only after the first had done its share)
