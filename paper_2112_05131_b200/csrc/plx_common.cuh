@@ -316,6 +316,15 @@ __device__ __forceinline__ bool sigma_at(const DGrid &G, const double *g, double
     float s[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) s[q] = base[((q >> 2) & 1) * sx + ((q >> 1) & 1) * sy + (q & 1)];
+    // All 8 corners occupied with sigma < 0 (NaN compares false): every term
+    // w_q sigma_q is <= 0 and the largest weight is >= 1/8, so the f64 sum is
+    // strictly negative and the caller drops the sample (K:293) -- the
+    // weights need not be formed.  Most march positions take this exit.
+    if (s[0] < 0.f && s[1] < 0.f && s[2] < 0.f && s[3] < 0.f && s[4] < 0.f && s[5] < 0.f &&
+        s[6] < 0.f && s[7] < 0.f) {
+        sig = -1.0;
+        return true;
+    }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         if (s[q] != s[q]) continue;   // empty corner (K:131: skipped)
