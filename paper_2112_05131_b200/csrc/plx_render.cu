@@ -45,6 +45,12 @@ struct RayArgs {
     const int64_t *idx_off;   // optional device offset added to idx (graph replay)
 };
 
+// Stencil rows of a recorded cell on an identity-linked grid (row = lattice
+// point): computed, so the march does not store them and the colour and
+// scatter kernels do not load them.
+template <bool NEAREST>
+__device__ __forceinline__ void identity_rows(const DGrid &G, int4 cl, int32_t *rows);
+
 // idx + *idx_off: the batch as a device-resident slice of a fixed buffer
 __device__ __forceinline__ const int64_t *ray_index(const RayArgs &R) {
     return (R.idx && R.idx_off) ? R.idx + *R.idx_off : R.idx;
@@ -523,18 +529,20 @@ __global__ void __launch_bounds__(128, MINB)
             st_pos += stopped ? 32 - __clz(m) : npos;
             st_samp += __popc(m);
             if (incl) {
-                if (!rows_ok) load_rows<NEAREST>(G, ijk, rows);
                 const int64_t k = rb + ns + __popc(m & lt_mask);
                 S.att[k] = att;
                 S.T[k] = Ti;
                 S.w[k] = wi;
                 S.cell[k] = make_int4(ijk[0], ijk[1], ijk[2], (int)si);
-                if (!NEAREST) {
-                    S.f[k] = make_float4((float)fd[0], (float)fd[1], (float)fd[2], 0.f);
-                    S.rows[2 * k] = make_int4(rows[0], rows[1], rows[2], rows[3]);
-                    S.rows[2 * k + 1] = make_int4(rows[4], rows[5], rows[6], rows[7]);
-                } else {
-                    S.rows[2 * k] = make_int4(rows[0], -1, -1, -1);
+                if (!NEAREST) S.f[k] = make_float4((float)fd[0], (float)fd[1], (float)fd[2], 0.f);
+                if (!G.identity) {   // identity grids: rows follow from the cell
+                    if (!rows_ok) load_rows<NEAREST>(G, ijk, rows);
+                    if (!NEAREST) {
+                        S.rows[2 * k] = make_int4(rows[0], rows[1], rows[2], rows[3]);
+                        S.rows[2 * k + 1] = make_int4(rows[4], rows[5], rows[6], rows[7]);
+                    } else {
+                        S.rows[2 * k] = make_int4(rows[0], -1, -1, -1);
+                    }
                 }
                 if (cauchy) S.sig[k] = sig;
             }
@@ -589,6 +597,12 @@ __device__ __forceinline__ void ray_basis(const RayArgs &R, int64_t src, float *
               __ldg(R.viewdirs + 3 * src + 2), basis);
 #pragma unroll
     for (int b = 0; b < 9; ++b) bf[b] = (float)basis[b];
+}
+
+template <bool NEAREST>
+__device__ __forceinline__ void identity_rows(const DGrid &G, int4 cl, int32_t *rows) {
+    const int ijk[3] = {cl.x, cl.y, cl.z};
+    load_rows<NEAREST>(G, ijk, rows);   // identity fast path: no loads
 }
 
 // Per-warp shared staging of the colour kernel: the rows of the segment's
@@ -693,18 +707,22 @@ __global__ void __launch_bounds__(128, MINB)
         int32_t rows[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
         if (valid) {
             cl = S.cell[k];
-            const int4 ra = S.rows[2 * k];
-            rows[0] = ra.x;
-            if (!NEAREST) {
-                const int4 rb = S.rows[2 * k + 1];
-                rows[1] = ra.y;
-                rows[2] = ra.z;
-                rows[3] = ra.w;
-                rows[4] = rb.x;
-                rows[5] = rb.y;
-                rows[6] = rb.z;
-                rows[7] = rb.w;
-                f4 = S.f[k];
+            if (!NEAREST) f4 = S.f[k];
+            if (G.identity) {
+                identity_rows<NEAREST>(G, cl, rows);
+            } else {
+                const int4 ra = S.rows[2 * k];
+                rows[0] = ra.x;
+                if (!NEAREST) {
+                    const int4 rb = S.rows[2 * k + 1];
+                    rows[1] = ra.y;
+                    rows[2] = ra.z;
+                    rows[3] = ra.w;
+                    rows[4] = rb.x;
+                    rows[5] = rb.y;
+                    rows[6] = rb.z;
+                    rows[7] = rb.w;
+                }
             }
         }
         // distinct cells of the segment (samples are in march order)
@@ -926,8 +944,17 @@ __global__ void __launch_bounds__(128, MINB)
             wi = S.w[k];
             c4 = S.c[k];
             cl = S.cell[k];
-            if (!NEAREST) {
-                f4 = S.f[k];
+            if (!NEAREST) f4 = S.f[k];
+            if (G.identity) {
+                int32_t r8[8];
+                identity_rows<NEAREST>(G, cl, r8);
+                if (!NEAREST) {
+                    *reinterpret_cast<int4 *>(&sc.rows[lane][0]) = make_int4(r8[0], r8[1], r8[2], r8[3]);
+                    *reinterpret_cast<int4 *>(&sc.rows[lane][4]) = make_int4(r8[4], r8[5], r8[6], r8[7]);
+                } else {
+                    sc.rows[lane][0] = r8[0];
+                }
+            } else if (!NEAREST) {
                 *reinterpret_cast<int4 *>(&sc.rows[lane][0]) = S.rows[2 * k];
                 *reinterpret_cast<int4 *>(&sc.rows[lane][4]) = S.rows[2 * k + 1];
             } else {
