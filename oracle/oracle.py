@@ -291,3 +291,110 @@ def upsample(grid, new_dims):
     table = np.empty((n, ROW))
     lib().oracle_upsample(*args, _p(table))
     return Grid(new_links, table, grid.aabb_min, grid.aabb_max)
+
+
+# -- multi-sphere-image background (360 scenes): K:603-977, msi.py -----------
+
+def layer_radii(n_layers):
+    """msi.layer_radii (msi.py:63-67): inverse radii linear from 1 to 0."""
+    inv = np.linspace(1.0, 0.0, n_layers)
+    with np.errstate(divide="ignore"):
+        return 1.0 / inv
+
+
+class BgGradBuf:
+    """Twin of msi.BgGradientBuffer (msi.py:111-127): (L*H*W, 4) f64."""
+
+    def __init__(self, n_texels):
+        self.data = np.zeros((n_texels, 4))
+        self.touched_mask = np.zeros(n_texels, dtype=np.uint8)
+        self.touched_ids = np.zeros(max(n_texels, 1), dtype=np.int64)
+        self._count = np.zeros(1, dtype=np.int64)
+
+    @property
+    def n_touched(self):
+        return int(self._count[0])
+
+    def touched_rows(self):
+        return np.sort(self.touched_ids[: self.n_touched])
+
+    def clear(self):
+        lib().oracle_clear_grad(_p(self.data), _p(self.touched_mask),
+                                _p(self.touched_ids), _p(self._count), _i(4))
+
+
+def bg_sample(bgdata, pts):
+    """msi.sample_background (msi.py:75-108): (sigma (n,), rgb (n, 3))."""
+    bgdata = _f64(bgdata)
+    L, H, W, _ = bgdata.shape
+    p = _f64(np.atleast_2d(pts))
+    out = np.empty((p.shape[0], 4))
+    if lib().oracle_bg_sample(_p(bgdata), _i(L), _i(H), _i(W), _p(p), _i(p.shape[0]),
+                              _p(out)) != 0:
+        raise ValueError("background sample inside the unit sphere")
+    return out[:, 0], out[:, 1:]
+
+
+def render_360(grid, bgdata, radii, origins, dirs, step_frac=0.5, stop_thresh=1e-4,
+               interp="trilinear", gt_rgb=None, buf=None, bg_buf=None, n_total=1,
+               lam_cauchy=0.0, lam_beta=0.0, beta_eps=1e-6):
+    """msi.render_rays_with_background (msi.py:130-183) over render_backward_360
+    (K:661-881).  Returns (rgb, trans_fg, trans_final, mse, cauchy_raw, beta_raw)."""
+    bgdata = _f64(bgdata)
+    L, H, W, _ = bgdata.shape
+    o = _f64(np.atleast_2d(origins))
+    d = _f64(np.atleast_2d(dirs))
+    n = o.shape[0]
+    with_grad = buf is not None
+    tg = np.zeros((n, 3)) if gt_rgb is None else _f64(np.atleast_2d(gt_rgb))
+    if not with_grad:
+        buf, bg_buf = GradBuf(0), BgGradBuf(8)
+    step, dmax, scale = _geom(grid, step_frac)
+    nmax = _max_samples(grid, step) + L + 2
+    rgb, tfg, trans = np.empty((n, 3)), np.empty(n), np.empty(n)
+    sums = np.zeros(3)
+    Dx, Dy, Dz = grid.dims
+    lib().oracle_render_360(
+        _p(grid.links), _i(Dx), _i(Dy), _i(Dz), _p(grid.table), _p(grid.aabb_min),
+        _p(grid.aabb_max), _p(scale), _p(dmax), _d(step), _p(bgdata), _i(L), _i(H), _i(W),
+        _p(_f64(radii)), _p(o), _p(d), _i(n), _d(stop_thresh),
+        ctypes.c_int(interp == "nearest"), _p(tg), ctypes.c_int(1),
+        _d(2.0 / max(n_total, 1)), _d(lam_cauchy), _d(lam_beta), _d(beta_eps),
+        _p(buf.data), _p(buf.touched_mask), _p(buf.touched_ids), _p(buf._count),
+        _p(bg_buf.data), _p(bg_buf.touched_mask), _p(bg_buf.touched_ids), _p(bg_buf._count),
+        _p(rgb), _p(tfg), _p(trans), _i(nmax), ctypes.c_int(with_grad), _p(sums))
+    return rgb, tfg, trans, float(sums[0]), float(sums[1]), float(sums[2])
+
+
+def sample_bg_tv_cells(n_texels, fraction, rng):
+    """msi.sample_bg_tv_cells (msi.py:186-190)."""
+    count = max(1, int(round(fraction * n_texels)))
+    start = int(rng.integers(0, n_texels))
+    return ((start + np.arange(count)) % n_texels).astype(np.int64)
+
+
+def tv_bg(bgdata, cells, lam_sigma, lam_rgb, bg_buf=None, eps=1e-6):
+    """msi.bg_tv_loss (msi.py:193-208) over tv_bg (K:884-977)."""
+    cells = np.ascontiguousarray(cells, dtype=np.int64)
+    if cells.size == 0:
+        return 0.0, 0.0
+    bgdata = _f64(bgdata)
+    L, H, W, _ = bgdata.shape
+    n = cells.size
+    b = bg_buf if bg_buf is not None else BgGradBuf(L * H * W)
+    sums = np.zeros(2)
+    lib().oracle_tv_bg(_p(bgdata), _i(L), _i(H), _i(W), _p(cells), _i(n), _d(eps),
+                       _d(lam_sigma / n), _d(lam_rgb / n), _p(b.data), _p(b.touched_mask),
+                       _p(b.touched_ids), _p(b._count), ctypes.c_int(bg_buf is not None),
+                       _p(sums))
+    return lam_sigma * sums[0] / n, lam_rgb * sums[1] / n
+
+
+def step_table(table, grad, touched_ids, n_touched, v, lr_first, lr_rest,
+               method="rmsprop", beta=0.95, eps=1e-8):
+    """optim.step_table (O:100-107): the sparse update of a bare (rows, cols)
+    f64 table (the background), in place."""
+    ncol = table.shape[1]
+    lib().oracle_opt_step(_p(table), _p(v), _p(grad), _p(np.ascontiguousarray(touched_ids)),
+                          _i(n_touched), _i(ncol), _d(lr_first), _d(lr_rest), _d(beta),
+                          _d(eps), ctypes.c_int(method == "rmsprop"))

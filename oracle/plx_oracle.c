@@ -629,3 +629,349 @@ int64_t oracle_upsample(const int32_t *links, int64_t Dx, int64_t Dy, int64_t Dz
             }
     return n_new;
 }
+
+/* ------------------------------------------------------------------------
+ * Multi-sphere-image background (360 scenes): K:603-977 and msi.py.
+ * bg: f64 [L][H][W][4] (sigma, r, g, b); radii: f64[L], increasing, last inf.
+ * ------------------------------------------------------------------------ */
+
+/* K:606-645 (_bg_stencil): bilinear texel stencil within one layer at the
+ * sphere angles of p; texel centres at half texels, phi wraps, theta clamps. */
+static void bg_stencil(int64_t H, int64_t W, double px, double py, double pz,
+                       int64_t *idx4, double *w4) {
+    const double pi = 3.141592653589793;
+    double r = sqrt(px * px + py * py + pz * pz);
+    double phi = atan2(py, px);
+    double ct = pz / r;
+    if (ct > 1.0) ct = 1.0;
+    if (ct < -1.0) ct = -1.0;
+    double theta = acos(ct);
+    double u = (phi + pi) / (2.0 * pi) * (double)W - 0.5;
+    u = u - floor(u / (double)W) * (double)W;
+    double vv = theta / pi * (double)H - 0.5;
+    if (vv < 0.0) vv = 0.0;
+    if (vv > (double)H - 1.0) vv = (double)H - 1.0;
+    int64_t i0 = (int64_t)u;
+    if (i0 > W - 1) i0 = W - 1;
+    double fu = u - (double)i0;
+    int64_t i1 = i0 + 1;
+    if (i1 >= W) i1 = 0;
+    int64_t j0 = (int64_t)vv;
+    if (j0 > H - 2) j0 = H - 2;
+    double fv = vv - (double)j0;
+    idx4[0] = j0 * W + i0;
+    idx4[1] = j0 * W + i1;
+    idx4[2] = (j0 + 1) * W + i0;
+    idx4[3] = (j0 + 1) * W + i1;
+    w4[0] = (1.0 - fu) * (1.0 - fv);
+    w4[1] = fu * (1.0 - fv);
+    w4[2] = (1.0 - fu) * fv;
+    w4[3] = fu * fv;
+}
+
+/* K:648-658 (_bg_fetch) */
+static void bg_fetch(const double *bg, int64_t H, int64_t W, int64_t layer,
+                     const int64_t *idx4, const double *w4, double *out4) {
+    for (int c = 0; c < 4; ++c) out4[c] = 0.0;
+    for (int q = 0; q < 4; ++q) {
+        const double *tx = bg + ((layer * H * W) + idx4[q]) * 4;
+        for (int c = 0; c < 4; ++c) out4[c] += w4[q] * tx[c];
+    }
+}
+
+/* msi.py:75-108 (sample_background): trilinear over (inverse-radius layer
+ * coordinate, theta, phi), terms summed in (layer, theta, phi) order, then
+ * clamped at zero.  Returns -1 if a point lies inside the unit sphere. */
+int oracle_bg_sample(const double *bg, int64_t L, int64_t H, int64_t W,
+                     const double *pts, int64_t n, double *out4) {
+    const double pi = 3.141592653589793;
+    for (int64_t p = 0; p < n; ++p) {
+        const double *q = pts + 3 * p;
+        double r = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2]);
+        if (r < 1.0 - 1e-9) return -1;
+        double phi = atan2(q[1], q[0]);
+        double c = q[2] / r;
+        if (c < -1.0) c = -1.0;
+        if (c > 1.0) c = 1.0;
+        double theta = acos(c);
+        double u = (phi + pi) / (2.0 * pi) * (double)W - 0.5;
+        u = u - floor(u / (double)W) * (double)W;
+        double v = theta / pi * (double)H - 0.5;
+        if (v < 0.0) v = 0.0;
+        if (v > (double)H - 1.0) v = (double)H - 1.0;
+        double lc = (1.0 - 1.0 / r) * (double)(L - 1);
+        if (lc < 0.0) lc = 0.0;
+        if (lc > (double)(L - 1)) lc = (double)(L - 1);
+        int64_t l0 = (int64_t)floor(lc);
+        if (l0 > L - 2) l0 = L - 2;
+        double fl = lc - (double)l0;
+        int64_t i0 = (int64_t)floor(u);
+        if (i0 > W - 1) i0 = W - 1;
+        double fu = u - (double)i0;
+        int64_t i1 = (i0 + 1) % W;
+        int64_t j0 = (int64_t)floor(v);
+        if (j0 > H - 2) j0 = H - 2;
+        double fv = v - (double)j0;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int dl = 0; dl < 2; ++dl) {
+            double wl = dl ? fl : 1.0 - fl;
+            for (int dj = 0; dj < 2; ++dj) {
+                double wv = dj ? fv : 1.0 - fv;
+                for (int di = 0; di < 2; ++di) {
+                    double wu = di ? fu : 1.0 - fu;
+                    int64_t ii = di ? i1 : i0;
+                    const double *tx = bg + (((l0 + dl) * H + (j0 + dj)) * W + ii) * 4;
+                    double w = wl * wv * wu;
+                    for (int k = 0; k < 4; ++k) acc[k] += w * tx[k];
+                }
+            }
+        }
+        for (int k = 0; k < 4; ++k) out4[4 * p + k] = acc[k] > 0.0 ? acc[k] : 0.0;
+    }
+    return 0;
+}
+
+/* K:661-881 (render_backward_360): foreground grid then one background
+ * sample per sphere crossing beyond the foreground exit, composited over
+ * black; with_grad: the reverse sweep over the concatenated samples with the
+ * Cauchy term (foreground) and the beta regulariser on the foreground
+ * transmittance.  out_sums = {mse, cauchy_raw, beta_raw}. */
+void oracle_render_360(const int32_t *links, int64_t Dx, int64_t Dy, int64_t Dz,
+                       const double *table, const double *lo, const double *hi,
+                       const double *scale, const double *dmax, double step,
+                       const double *bg, int64_t L, int64_t H, int64_t W, const double *radii,
+                       const double *origins, const double *dirs, int64_t nray,
+                       double stop_thresh, int nearest, const double *target, int mse_mode,
+                       double up_scale, double lam_cauchy, double lam_beta, double beta_eps,
+                       double *grad, uint8_t *tmask, int64_t *tids, int64_t *tcnt,
+                       double *bg_grad, uint8_t *bg_tmask, int64_t *bg_tids, int64_t *bg_tcnt,
+                       double *out_rgb, double *out_tfg, double *out_trans, int64_t nmax,
+                       int with_grad, double *out_sums) {
+    int64_t rows[8], idx4[4], nx;
+    double ws[8], basis[9], col[3], w4[4], out4[4];
+    double *s_t = malloc(sizeof(double) * nmax), *s_dlt = malloc(sizeof(double) * nmax);
+    double *s_sig = malloc(sizeof(double) * nmax), *s_T = malloc(sizeof(double) * nmax);
+    double *s_w = malloc(sizeof(double) * nmax), *s_cpre = malloc(sizeof(double) * nmax * 3);
+    int64_t *s_layer = malloc(sizeof(int64_t) * nmax);
+    double *xs_t = malloc(sizeof(double) * (L > 0 ? L : 1));
+    int64_t *xs_l = malloc(sizeof(int64_t) * (L > 0 ? L : 1));
+    double mse_sum = 0.0, cauchy_sum = 0.0, beta_sum = 0.0;
+    for (int64_t ri = 0; ri < nray; ++ri) {
+        const double *o = origins + 3 * ri, *d = dirs + 3 * ri;
+        sh_basis9(d[0], d[1], d[2], basis);
+        double t0, t1;
+        ray_aabb(o, d, lo, hi, &t0, &t1);
+        double cr = 0.0, cg = 0.0, cb = 0.0, T = 1.0;
+        int64_t m = 0;
+        double Lf = t1 - t0;
+        if (Lf > 0.0) {
+            int64_t nsamp = (int64_t)ceil(Lf / step - 1e-9);
+            if (nsamp < 1) nsamp = 1;
+            for (int64_t si = 0; si < nsamp; ++si) {
+                double t = t0 + (double)si * step;
+                double dlt = si < nsamp - 1 ? step : Lf - step * (double)(nsamp - 1);
+                double gx = clamp_coord(o[0] + t * d[0], lo[0], scale[0], dmax[0]);
+                double gy = clamp_coord(o[1] + t * d[1], lo[1], scale[1], dmax[1]);
+                double gz = clamp_coord(o[2] + t * d[2], lo[2], scale[2], dmax[2]);
+                int n = stencil(gx, gy, gz, links, Dx, Dy, Dz, nearest, rows, ws);
+                int occ;
+                double sig = sigma_at(table, rows, ws, n, &occ);
+                if (!occ || sig < 0.0) continue;
+                double att = exp(-sig * dlt);
+                double Tn = T * att, w = T - Tn;
+                color_at(table, rows, ws, n, basis, col);
+                if (col[0] > 0.0) cr += w * col[0];
+                if (col[1] > 0.0) cg += w * col[1];
+                if (col[2] > 0.0) cb += w * col[2];
+                s_t[m] = t; s_dlt[m] = dlt; s_sig[m] = sig; s_T[m] = T; s_w[m] = w;
+                s_cpre[3 * m] = col[0]; s_cpre[3 * m + 1] = col[1]; s_cpre[3 * m + 2] = col[2];
+                s_layer[m] = -1;
+                ++m;
+                T = Tn;
+                if (T < stop_thresh) break;
+            }
+        }
+        double tfg = T;
+        out_tfg[ri] = tfg;
+        double t_exit = t1 > 0.0 ? t1 : 0.0;
+        if (T >= stop_thresh) {
+            double bdot = o[0] * d[0] + o[1] * d[1] + o[2] * d[2];
+            double c0n = o[0] * o[0] + o[1] * o[1] + o[2] * o[2];
+            nx = 0;
+            for (int64_t l = 0; l < L - 1; ++l) {
+                double rad = radii[l];
+                double disc = bdot * bdot - c0n + rad * rad;
+                if (disc <= 0.0) continue;
+                double tl = -bdot + sqrt(disc);
+                if (tl < t_exit) continue;
+                xs_t[nx] = tl;
+                xs_l[nx] = l;
+                ++nx;
+            }
+            for (int64_t q = 0; q < nx; ++q) {
+                double dlt;
+                if (q + 1 < nx) dlt = xs_t[q + 1] - xs_t[q];
+                else if (q >= 1) dlt = xs_t[q] - xs_t[q - 1];
+                else dlt = 1.0;
+                double t = xs_t[q];
+                double px = o[0] + t * d[0], py = o[1] + t * d[1], pz = o[2] + t * d[2];
+                bg_stencil(H, W, px, py, pz, idx4, w4);
+                bg_fetch(bg, H, W, xs_l[q], idx4, w4, out4);
+                double sig = out4[0];
+                if (sig < 0.0) continue;
+                double att = exp(-sig * dlt);
+                double Tn = T * att, w = T - Tn;
+                if (out4[1] > 0.0) cr += w * out4[1];
+                if (out4[2] > 0.0) cg += w * out4[2];
+                if (out4[3] > 0.0) cb += w * out4[3];
+                s_t[m] = t; s_dlt[m] = dlt; s_sig[m] = sig; s_T[m] = T; s_w[m] = w;
+                s_cpre[3 * m] = out4[1]; s_cpre[3 * m + 1] = out4[2]; s_cpre[3 * m + 2] = out4[3];
+                s_layer[m] = xs_l[q];
+                ++m;
+                T = Tn;
+                if (T < stop_thresh) break;
+            }
+        }
+        out_rgb[3 * ri] = cr;
+        out_rgb[3 * ri + 1] = cg;
+        out_rgb[3 * ri + 2] = cb;
+        out_trans[ri] = T;
+        double upr, upg, upb;
+        if (mse_mode) {
+            double er = cr - target[3 * ri], eg = cg - target[3 * ri + 1], eb = cb - target[3 * ri + 2];
+            mse_sum += er * er + eg * eg + eb * eb;
+            upr = up_scale * er; upg = up_scale * eg; upb = up_scale * eb;
+        } else {
+            upr = target[3 * ri]; upg = target[3 * ri + 1]; upb = target[3 * ri + 2];
+        }
+        double tc = tfg;
+        if (tc < beta_eps) tc = beta_eps;
+        if (tc > 1.0 - beta_eps) tc = 1.0 - beta_eps;
+        if (lam_beta > 0.0) beta_sum += log(tc) + log(1.0 - tc);
+        double bup = 0.0;
+        if (lam_beta > 0.0 && beta_eps < tfg && tfg < 1.0 - beta_eps)
+            bup = lam_beta * (1.0 / tc - 1.0 / (1.0 - tc));
+        if (!with_grad) continue;
+        double sfr = 0.0, sfg = 0.0, sfb = 0.0;
+        for (int64_t idx = m - 1; idx >= 0; --idx) {
+            double sig = s_sig[idx], dlt = s_dlt[idx], Ti = s_T[idx], w = s_w[idx];
+            double c0 = s_cpre[3 * idx], c1 = s_cpre[3 * idx + 1], c2 = s_cpre[3 * idx + 2];
+            double ccr = c0 > 0.0 ? c0 : 0.0, ccg = c1 > 0.0 ? c1 : 0.0, ccb = c2 > 0.0 ? c2 : 0.0;
+            double att = exp(-sig * dlt);
+            double gsig = dlt * (upr * (Ti * att * ccr - sfr) + upg * (Ti * att * ccg - sfg) +
+                                 upb * (Ti * att * ccb - sfb));
+            sfr += w * ccr;
+            sfg += w * ccg;
+            sfb += w * ccb;
+            int64_t lay = s_layer[idx];
+            double t = s_t[idx];
+            if (lay < 0) {
+                if (lam_cauchy > 0.0) {
+                    cauchy_sum += log(1.0 + 2.0 * sig * sig);
+                    gsig += lam_cauchy * 4.0 * sig / (1.0 + 2.0 * sig * sig);
+                }
+                if (bup != 0.0) gsig += bup * (-dlt * tfg);
+                double gcr = c0 > 0.0 ? upr * w : 0.0;
+                double gcg = c1 > 0.0 ? upg * w : 0.0;
+                double gcb = c2 > 0.0 ? upb * w : 0.0;
+                double gx = clamp_coord(o[0] + t * d[0], lo[0], scale[0], dmax[0]);
+                double gy = clamp_coord(o[1] + t * d[1], lo[1], scale[1], dmax[1]);
+                double gz = clamp_coord(o[2] + t * d[2], lo[2], scale[2], dmax[2]);
+                int n = stencil(gx, gy, gz, links, Dx, Dy, Dz, nearest, rows, ws);
+                for (int q = 0; q < n; ++q) {
+                    int64_t rw = rows[q];
+                    if (rw < 0) continue;
+                    double wq = ws[q];
+                    touch(rw, tmask, tids, tcnt);
+                    double *gr = grad + rw * ROW;
+                    gr[0] += wq * gsig;
+                    if (gcr != 0.0) for (int b = 0; b < 9; ++b) gr[1 + b] += wq * gcr * basis[b];
+                    if (gcg != 0.0) for (int b = 0; b < 9; ++b) gr[10 + b] += wq * gcg * basis[b];
+                    if (gcb != 0.0) for (int b = 0; b < 9; ++b) gr[19 + b] += wq * gcb * basis[b];
+                }
+            } else {
+                double px = o[0] + t * d[0], py = o[1] + t * d[1], pz = o[2] + t * d[2];
+                bg_stencil(H, W, px, py, pz, idx4, w4);
+                for (int q = 0; q < 4; ++q) {
+                    int64_t flat = lay * H * W + idx4[q];
+                    double wq = w4[q];
+                    touch(flat, bg_tmask, bg_tids, bg_tcnt);
+                    double *gb = bg_grad + flat * 4;
+                    gb[0] += wq * gsig;
+                    if (c0 > 0.0) gb[1] += wq * upr * w;
+                    if (c1 > 0.0) gb[2] += wq * upg * w;
+                    if (c2 > 0.0) gb[3] += wq * upb * w;
+                }
+            }
+        }
+    }
+    free(s_t); free(s_dlt); free(s_sig); free(s_T); free(s_w); free(s_cpre); free(s_layer);
+    free(xs_t); free(xs_l);
+    out_sums[0] = mse_sum;
+    out_sums[1] = cauchy_sum;
+    out_sums[2] = beta_sum;
+}
+
+/* K:884-977 (tv_bg): TV over the background axes (layer, theta, phi), phi
+ * wrapping; opacity uses zero-valued edge neighbours, colour equal-valued
+ * ones; per-axis normalisation D/256.  out_sums = raw {sigma, rgb}. */
+void oracle_tv_bg(const double *bg, int64_t L, int64_t H, int64_t W, const int64_t *cells,
+                  int64_t ncell, double eps, double f_sigma, double f_rgb, double *grad,
+                  uint8_t *tmask, int64_t *tids, int64_t *tcnt, int with_grad,
+                  double *out_sums) {
+    double fl = (double)L / 256.0, fh = (double)H / 256.0, fw = (double)W / 256.0;
+    double e2 = eps * eps, sig_sum = 0.0, rgb_sum = 0.0;
+    for (int64_t ci = 0; ci < ncell; ++ci) {
+        int64_t cid = cells[ci];
+        int64_t l = cid / (H * W), rem = cid % (H * W);
+        int64_t j = rem / W, i = rem % W;
+        int hl = l + 1 < L, hj = j + 1 < H;
+        int64_t iw = i + 1 < W ? i + 1 : 0;
+        for (int c = 0; c < 4; ++c) {
+            double v0 = bg[((l * H + j) * W + i) * 4 + c];
+            double fac = c == 0 ? f_sigma : f_rgb;
+            double vl, vj;
+            if (c == 0) {
+                vl = hl ? bg[(((l + 1) * H + j) * W + i) * 4 + c] : 0.0;
+                vj = hj ? bg[((l * H + j + 1) * W + i) * 4 + c] : 0.0;
+            } else {
+                vl = hl ? bg[(((l + 1) * H + j) * W + i) * 4 + c] : v0;
+                vj = hj ? bg[((l * H + j + 1) * W + i) * 4 + c] : v0;
+            }
+            double vi = bg[((l * H + j) * W + iw) * 4 + c];
+            double da = (vl - v0) * fl, db = (vj - v0) * fh, dc = (vi - v0) * fw;
+            double val = sqrt(da * da + db * db + dc * dc + e2);
+            if (c == 0) sig_sum += val; else rgb_sum += val;
+            if (with_grad && val > 0.0) {
+                double inv = fac / val, g0 = 0.0;
+                if (hl) {
+                    int64_t f = (l + 1) * H * W + j * W + i;
+                    touch(f, tmask, tids, tcnt);
+                    grad[f * 4 + c] += da * fl * inv;
+                    g0 -= da * fl * inv;
+                } else if (c == 0) {
+                    g0 -= da * fl * inv;
+                }
+                if (hj) {
+                    int64_t f = l * H * W + (j + 1) * W + i;
+                    touch(f, tmask, tids, tcnt);
+                    grad[f * 4 + c] += db * fh * inv;
+                    g0 -= db * fh * inv;
+                } else if (c == 0) {
+                    g0 -= db * fh * inv;
+                }
+                int64_t f = l * H * W + j * W + iw;
+                touch(f, tmask, tids, tcnt);
+                grad[f * 4 + c] += dc * fw * inv;
+                g0 -= dc * fw * inv;
+                if (g0 != 0.0) {
+                    int64_t f0 = l * H * W + j * W + i;
+                    touch(f0, tmask, tids, tcnt);
+                    grad[f0 * 4 + c] += g0;
+                }
+            }
+        }
+    }
+    out_sums[0] = sig_sum;
+    out_sums[1] = rgb_sum;
+}
