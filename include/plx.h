@@ -290,6 +290,48 @@ typedef struct {
 } plx_step_args;
 int plx_train_step(plx_grid *g, plx_grad *gb, const plx_step_args *a, void *stream);
 
+/* ---- Multi-sphere-image background (unbounded 360 scenes) ----------------
+ * Reference: msi.py (MsiBackground, BgGradientBuffer, render_rays_with_
+ * background, bg_tv_loss), _kernels.py K:603-977 (render_backward_360,
+ * tv_bg), optim.py O:100-107 (step_table).  All background data is f64. */
+typedef struct {
+    const double *data;    /* [L][H][W][4] (sigma, r, g, b), device          */
+    const double *radii;   /* [L] increasing (msi.layer_radii; last may be inf) */
+    int64_t L, H, W;       /* 2 <= L <= 257, H >= 2, W >= 1                   */
+} plx_msi;
+typedef struct {
+    double *grad;          /* [L*H*W][4] f64 accumulator                     */
+    uint8_t *tmask;        /* [L*H*W] touched texels                         */
+    int32_t *tids;         /* [L*H*W] compacted list (plx_msi_opt_step)      */
+    int64_t *tcnt;         /* device int64                                    */
+} plx_msi_grad;
+/* Scratch for plx_msi_render (per-ray records; rays are processed in waves
+ * that fit the scratch).  -1 on bad arguments. */
+int64_t plx_msi_scratch_bytes(const plx_grid *g, const plx_msi *bg, const plx_render_opts *o,
+                              int64_t n_rays);
+/* msi.render_rays_with_background (msi.py:130-183 -> K:661-881): rays.
+ * origins / dirs (world; the SH basis uses dirs) and rays.target (gt for
+ * mse_mode, else the upstream dL/drgb); opts: step, stop_thresh, nearest.
+ * gb == NULL: forward only.  out_sums (device double[3], accumulated):
+ * {mse, cauchy_raw, beta_raw}; out_rgb (N,3), out_tfg / out_trans (N). */
+int plx_msi_render(const plx_grid *g, const plx_msi *bg, const plx_rays *rays,
+                   const plx_render_opts *o, int32_t mse_mode, double up_scale,
+                   double lam_cauchy, double lam_beta, double beta_eps, plx_grad *gb,
+                   plx_msi_grad *bgb, double *out_rgb, double *out_tfg, double *out_trans,
+                   double *out_sums, void *scratch, int64_t scratch_bytes, void *stream);
+/* msi.bg_tv_loss raw sums (K:884-977): cells (device int64, or NULL for the
+ * run start..start+count wrapping mod L*H*W); bgb NULL = value only;
+ * out_sums (device double[2], accumulated): {sigma, rgb}. */
+int plx_msi_tv(const plx_msi *bg, const int64_t *cells, int64_t start, int64_t count,
+               double eps, double f_sigma, double f_rgb, plx_msi_grad *bgb, double *out_sums,
+               void *stream);
+/* optim.step_table on the background (O:100-107, K:572-590) over the
+ * texels marked in bgb->tmask, then (clear) the clear of K:593-600.
+ * table = bg->data viewed as [L*H*W][4]; v likewise (RMSProp). */
+int plx_msi_opt_step(double *table, double *v, plx_msi_grad *bgb, int64_t n_texels,
+                     double lr_sigma, double lr_rgb, double beta, double eps, int32_t rmsprop,
+                     int32_t clear, int64_t *out_count, void *stream);
+
 /* Library identification / self-check. */
 const char *plx_version(void);
 int plx_device_check(void);   /* 0 iff a CUDA device with cc >= 10.0 is present */

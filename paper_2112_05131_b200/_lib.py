@@ -80,6 +80,16 @@ class PlxStepArgs(ctypes.Structure):
                 ("host_sums", ctypes.c_void_p)]
 
 
+class PlxMsi(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("radii", ctypes.c_void_p), ("L", ctypes.c_int64),
+                ("H", ctypes.c_int64), ("W", ctypes.c_int64)]
+
+
+class PlxMsiGrad(ctypes.Structure):
+    _fields_ = [("grad", ctypes.c_void_p), ("tmask", ctypes.c_void_p), ("tids", ctypes.c_void_p),
+                ("tcnt", ctypes.c_void_p)]
+
+
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I32 = ctypes.c_int32
@@ -122,10 +132,21 @@ _SIGS = {
     "plx_build_row_cell": [ctypes.POINTER(PlxGrid), _P, _P],
     "plx_train_step": [ctypes.POINTER(PlxGrid), ctypes.POINTER(PlxGrad),
                        ctypes.POINTER(PlxStepArgs), _P],
+    "plx_msi_scratch_bytes": [ctypes.POINTER(PlxGrid), ctypes.POINTER(PlxMsi),
+                              ctypes.POINTER(PlxRenderOpts), _I64],
+    "plx_msi_render": [ctypes.POINTER(PlxGrid), ctypes.POINTER(PlxMsi), ctypes.POINTER(PlxRays),
+                       ctypes.POINTER(PlxRenderOpts), _I32, _D, _D, _D, _D,
+                       ctypes.POINTER(PlxGrad), ctypes.POINTER(PlxMsiGrad), _P, _P, _P, _P, _P,
+                       _I64, _P],
+    "plx_msi_tv": [ctypes.POINTER(PlxMsi), _P, _I64, _I64, _D, _D, _D,
+                   ctypes.POINTER(PlxMsiGrad), _P, _P],
+    "plx_msi_opt_step": [_P, _P, ctypes.POINTER(PlxMsiGrad), _I64, _D, _D, _D, _D, _I32, _I32,
+                         _P, _P],
     "plx_version": [],
     "plx_device_check": [],
 }
 _RESTYPE = {"plx_scan_scratch_bytes": _I64, "plx_render_scratch_bytes": _I64, "plx_cell_occ_words": _I64,
+            "plx_msi_scratch_bytes": _I64,
             "plx_version": ctypes.c_char_p}
 
 EXPORTS = tuple(_SIGS)

@@ -249,6 +249,47 @@ __device__ __forceinline__ double warp_scan_mul(double x, int lane) {
 }
 
 // Vectorised fire-and-forget f32 reduction (sm_90+ PTX; SASS REDG.E.ADD.F32x4).
+// Composite one chunk (K:213-233).  In: carry (T for relative, asum for
+// absolute), incl flags and att per lane.  Out: per-lane T_i and w_i (valid
+// on included lanes; included lanes past the early stop are dropped),
+// updated carry, `stopped` (warp-uniform).  Deterministic: pass 2 replays it
+// on the recorded (att, incl) and reproduces pass 1 bit-for-bit.
+template <bool ABS>
+__device__ __forceinline__ void composite_chunk(bool &incl, double att, int lane, double stop,
+                                                double &Tcarry, double &Acarry, double &Ti,
+                                                double &wi, bool &stopped) {
+    double Tn;
+    if (!ABS) {
+        double a = incl ? att : 1.0;
+        double pinc = warp_scan_mul(a, lane);
+        double pexc = __shfl_up_sync(PLX_FULL_MASK, pinc, 1);
+        if (lane == 0) pexc = 1.0;
+        Ti = Tcarry * pexc;
+        Tn = Tcarry * pinc;
+    } else {
+        double v = incl ? 1.0 - att : 0.0;
+        double sinc = warp_scan_add(v, lane);
+        double sexc = __shfl_up_sync(PLX_FULL_MASK, sinc, 1);
+        if (lane == 0) sexc = 0.0;
+        double before = Acarry + sexc;
+        Ti = 1.0 - before;
+        if (Ti < 0.0) Ti = 0.0;
+        Tn = 1.0 - (before + v);
+        if (Tn < 0.0) Tn = 0.0;
+        Acarry = before + v;   // lane-local; broadcast below
+    }
+    wi = Ti - Tn;
+    unsigned stopm = __ballot_sync(PLX_FULL_MASK, incl && Tn < stop);
+    int last = 31;
+    if (stopm) {
+        last = __ffs(stopm) - 1;
+        stopped = true;
+        if (lane > last) incl = false;
+    }
+    Tcarry = __shfl_sync(PLX_FULL_MASK, Tn, last);
+    if (ABS) Acarry = __shfl_sync(PLX_FULL_MASK, Acarry, last);
+}
+
 __device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float c, float d) {
     asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
                  "f"(d)
@@ -262,6 +303,56 @@ __device__ __forceinline__ void red_add_f32(float *addr, float a) {
 }  // namespace plx
 
 namespace plx {
+
+// _color_at (K:138-152) in f32 FMAs: per corner the 3 SH dots with the
+// basis, then the corner weight; c = pre-clamp colour (empty rows skipped).
+template <bool NEAREST>
+__device__ __forceinline__ void colour_at_f32(const DGrid &G, const int32_t *rows, const double *f,
+                                              const float *bf, float *c) {
+    constexpr int NQ = NEAREST ? 1 : 8;
+    float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        int32_t r = rows[q];
+        if (r < 0) continue;
+        const float4 *row = reinterpret_cast<const float4 *>(G.table + (int64_t)r * PLX_STRIDE);
+        float4 v0 = __ldg(row + 0), v1 = __ldg(row + 1), v2 = __ldg(row + 2), v3 = __ldg(row + 3);
+        float4 v4 = __ldg(row + 4), v5 = __ldg(row + 5), v6 = __ldg(row + 6);
+        // row layout: [sig, R0..R8, G0..G8, B0..B8]
+        float a0 = bf[0] * v0.y, a1 = bf[0] * v2.z, a2 = bf[0] * v4.w;
+        a0 = __fmaf_rn(bf[1], v0.z, a0);
+        a1 = __fmaf_rn(bf[1], v2.w, a1);
+        a2 = __fmaf_rn(bf[1], v5.x, a2);
+        a0 = __fmaf_rn(bf[2], v0.w, a0);
+        a1 = __fmaf_rn(bf[2], v3.x, a1);
+        a2 = __fmaf_rn(bf[2], v5.y, a2);
+        a0 = __fmaf_rn(bf[3], v1.x, a0);
+        a1 = __fmaf_rn(bf[3], v3.y, a1);
+        a2 = __fmaf_rn(bf[3], v5.z, a2);
+        a0 = __fmaf_rn(bf[4], v1.y, a0);
+        a1 = __fmaf_rn(bf[4], v3.z, a1);
+        a2 = __fmaf_rn(bf[4], v5.w, a2);
+        a0 = __fmaf_rn(bf[5], v1.z, a0);
+        a1 = __fmaf_rn(bf[5], v3.w, a1);
+        a2 = __fmaf_rn(bf[5], v6.x, a2);
+        a0 = __fmaf_rn(bf[6], v1.w, a0);
+        a1 = __fmaf_rn(bf[6], v4.x, a1);
+        a2 = __fmaf_rn(bf[6], v6.y, a2);
+        a0 = __fmaf_rn(bf[7], v2.x, a0);
+        a1 = __fmaf_rn(bf[7], v4.y, a1);
+        a2 = __fmaf_rn(bf[7], v6.z, a2);
+        a0 = __fmaf_rn(bf[8], v2.y, a0);
+        a1 = __fmaf_rn(bf[8], v4.z, a1);
+        a2 = __fmaf_rn(bf[8], v6.w, a2);
+        const float w = (float)stencil_w<NEAREST>(f, q);
+        c0 = __fmaf_rn(w, a0, c0);
+        c1 = __fmaf_rn(w, a1, c1);
+        c2 = __fmaf_rn(w, a2, c2);
+    }
+    c[0] = c0;
+    c[1] = c1;
+    c[2] = c2;
+}
 
 // _sigma_at (K:126-135) of the stencil at lattice coordinates g: float64 sum
 // over occupied corners in corner order; occ = any corner occupied.  With the
