@@ -109,6 +109,18 @@ def main():
                     p + "opt_v": state.v, p + "opt_table": table})
     np.savez_compressed(OUT / "msi.npz", n=len(cases), **out)
     print("wrote", OUT / "msi.npz")
+    # a grid + background container and its state sidecar written by the
+    # reference's artifact_io (artifact_io.py:42-62, 138-156)
+    from plenoxel import artifact_io
+    g = random_grid(rng, dims=(3, 4, 5), aabb=0.5, holes=0.3)
+    bg = msi.MsiBackground.create(3, 4, 6)
+    bg.data[:] = rng.uniform(-1, 2, bg.data.shape).astype(np.float32)
+    st = optim.OptimState(g.n_rows)
+    st.v[:] = rng.uniform(0, 1, st.v.shape).astype(np.float32)
+    bst = optim.OptimState(bg.n_layers * bg.height * bg.width, 4)
+    bst.v[:] = rng.uniform(0, 1, bst.v.shape).astype(np.float32)
+    artifact_io.save_checkpoint(OUT / "msi_grid.plnx", g, st, 1234, bg, bst)
+    print("wrote", OUT / "msi_grid.plnx")
 
 
 if __name__ == "__main__":
