@@ -1,6 +1,6 @@
-"""End-to-end optimisation on the B200 (drop-in for pkg/src/plenoxel/trainer.py,
-bounded and forward-facing-NDC scenes; the 360° MSI background is out of
-scope).
+"""End-to-end optimisation on the B200 (drop-in for pkg/src/plenoxel/trainer.py:
+bounded, forward-facing-NDC and unbounded-360 scenes; the 360 scenes add the
+multi-sphere-image background of msi.py, stepped by Trainer._step_360).
 
 The step body (T:411-492) keeps the reference's order and RNG consumption --
 EpochBatcher permutations and sample_tv_cells draws come from the same
@@ -94,6 +94,16 @@ class TrainConfig:
     checkpoint_every: int = 0
     jitter: float = 0.0
     ndc_z_pad: float = 0.0
+    # unbounded_360 only (T:77-86)
+    bg_layers: int = 64
+    bg_height: int = 1024
+    bg_width: int = 2048
+    bg_lambda_tv: float = 1e-3
+    bg_lr_sigma: optim.LrSchedule = field(default_factory=lambda: optim.LrSchedule(
+        kind="exponential", lr_init=30.0, lr_final=0.05, total_steps=250000))
+    bg_lr_rgb: optim.LrSchedule = field(default_factory=lambda: optim.LrSchedule(
+        kind="exponential", lr_init=0.01, lr_final=5e-6, total_steps=250000))
+    scene_margin: float = 1.1
 
     def __post_init__(self):
         if self.scene_type not in SCENE_TYPES:
@@ -127,7 +137,15 @@ def default_config(scene_type: str) -> TrainConfig:
                            lambda_tv_sigma=5e-4, lambda_tv_sh=5e-3, lambda_sparsity=1e-12,
                            background=(0.0, 0.0, 0.0))
     if scene_type == "unbounded_360":
-        raise NotImplementedError("unbounded_360 (MSI background) is out of scope, SURVEY §8(f)-4")
+        return TrainConfig(scene_type="unbounded_360", aabb=(-1.0, -1.0, -1.0, 1.0, 1.0, 1.0),
+                           ladder=[LadderRung(0, (128, 128, 128)),
+                                   LadderRung(25600, (256, 256, 256)),
+                                   LadderRung(51200, (512, 512, 512)),
+                                   LadderRung(76800, (640, 640, 640))],
+                           total_steps=102400, prune_criterion="weight", prune_threshold=1.28,
+                           lambda_tv_sigma=5e-5, lambda_tv_sh=5e-3, lambda_sparsity=1e-11,
+                           lambda_beta=1e-5, bg_layers=64, bg_height=1024, bg_width=2048,
+                           bg_lambda_tv=1e-3, background=(0.0, 0.0, 0.0))
     raise ValueError(f"unknown scene type {scene_type!r}")
 
 
@@ -252,6 +270,8 @@ class TrainResult:
     grid: SparseGrid
     metrics: list
     config: TrainConfig
+    background: object = None      # msi.MsiBackground (360 scenes)
+    scene_scale: float = 1.0
 
 
 def _grid_aabb(cfg: TrainConfig, dims):
@@ -262,6 +282,20 @@ def _grid_aabb(cfg: TrainConfig, dims):
         lo[2] -= pad
         hi[2] += pad
     return lo, hi
+
+
+def _scale_from_positions(pos: np.ndarray, margin: float) -> float:
+    """T:282-287: 1 / (margin * max camera distance from the centroid)."""
+    centroid = pos.mean(axis=0)
+    maxdist = float(np.max(np.linalg.norm(pos - centroid, axis=1)))
+    if maxdist <= 0:
+        return 1.0
+    return 1.0 / (margin * maxdist)
+
+
+def _scene_scale_360(dataset, margin: float) -> float:
+    """T:278-279: the 360 camera pre-scale from the training cameras."""
+    return _scale_from_positions(np.stack([c.position for c in dataset.cameras]), margin)
 
 
 def _estimate_table_bytes(dims) -> int:
@@ -277,13 +311,16 @@ class Trainer:
 
     def __init__(self, train_ds, config: TrainConfig, device=None, world: World | None = None):
         cfg = config
-        if cfg.scene_type == "unbounded_360":
-            raise NotImplementedError("unbounded_360 is out of scope (SURVEY §8(f)-4)")
         self.cfg = cfg
         self.world = world or World()
         self.device = torch.device(device or "cuda")
         self.rng = np.random.default_rng(cfg.seed)
         o, m, v, gt = all_rays(train_ds.images, train_ds.cameras, train_ds.scene_type)
+        self.scene_scale = 1.0
+        self.is_360 = cfg.scene_type == "unbounded_360"
+        if self.is_360:   # T:375-377: cameras pre-scaled into the unit sphere
+            self.scene_scale = _scene_scale_360(train_ds, cfg.scene_margin)
+            o = o * self.scene_scale
         self.pool = render.RayPool(o, m, v, gt, device=self.device)
         dims0 = cfg.ladder[0].dims
         lo, hi = _grid_aabb(cfg, dims0)
@@ -293,8 +330,20 @@ class Trainer:
                                       device=self.device)
         self.grads = GradientBuffer(self.grid.n_rows, device=self.device)
         self.opts = render.RenderOptions(step_frac=cfg.step_frac, stop_thresh=cfg.stop_thresh,
-                                         background=tuple(cfg.background), interp=cfg.interp,
+                                         background=(0.0, 0.0, 0.0) if self.is_360
+                                         else tuple(cfg.background), interp=cfg.interp,
                                          formula=cfg.formula, jitter=cfg.jitter)
+        # the MSI background of 360 scenes (T:386-397)
+        self.background = self.bg_state = self.bg_grads = None
+        if self.is_360:
+            from . import msi
+            self.background = msi.MsiBackground.create(cfg.bg_layers, cfg.bg_height,
+                                                       cfg.bg_width, device=self.device)
+            self.background.data[..., 0] = cfg.init_sigma
+            self.background.data[..., 1:] = cfg.init_rgb
+            self.bg_state = msi.BgOptimState(self.background, beta=cfg.rms_beta,
+                                             eps=cfg.rms_eps)
+            self.bg_grads = msi.BgGradientBuffer(self.background)
         self.batcher = EpochBatcher(self.pool.n, cfg.batch_size, self.rng, self.device)
         self.rung_events = {r.step: tuple(r.dims) for r in cfg.ladder[1:]}
         # {mse_sum, cauchy_sum, tv_sigma_sum, tv_sh_sum, halt}: the loss sums of
@@ -312,8 +361,9 @@ class Trainer:
         self._peers = None
         self._dp_pack = None
         self.step_events = None   # optional 4 torch.cuda.Events (plx_step_args.events)
-        # single-GPU steps replay a captured CUDA graph (PLX_GRAPH=0 disables)
-        self.use_graph = os.environ.get("PLX_GRAPH", "1") != "0"
+        # single-GPU steps replay a captured CUDA graph (PLX_GRAPH=0 disables);
+        # 360 scenes step through the public msi API instead
+        self.use_graph = os.environ.get("PLX_GRAPH", "1") != "0" and not self.is_360
         # graph mode: per-step scalars {tv_start, lr_sigma, lr_sh (f64 bits),
         # batch offset} in 3 pinned slots, copied to _dparams by the graph
         self._dparams = torch.zeros(4, dtype=torch.int64, device=self.device)
@@ -384,7 +434,8 @@ class Trainer:
         self._refresh_cache()
         if out_dir is not None:
             artifact_io.save_checkpoint(Path(out_dir) / f"checkpoint_{step:07d}.plnx",
-                                        self.grid, self.state, step)
+                                        self.grid, self.state, step, self.background,
+                                        self.bg_state)
 
     def max_weights(self) -> torch.Tensor:
         """Max-weight over all training rays, sharded over ranks + max-reduce."""
@@ -407,6 +458,8 @@ class Trainer:
         never waits for the step it just enqueued and the GPU never idles
         between steps.  sync=True (logging steps) waits for this step's loss
         and returns it in the record."""
+        if self.is_360:
+            return self._step_360(step)
         idx, off = self.batcher.next_slice()
         return self._step(step, int(idx.numel()), idx, check_finite, sync, off)
 
@@ -520,6 +573,52 @@ class Trainer:
             if len(self._pending) > 2:   # the host runs up to two steps ahead
                 self.check_pending(keep=2)
         return rec
+
+    def _step_360(self, step: int) -> dict:
+        """The 360 step body (T:441-492 with the background): fused render of
+        grid + sphere layers with the MSE, Cauchy and beta terms
+        (msi.render_rays_with_background), grid TV then background TV (the
+        reference's RNG order), the divergence check, the grid update with
+        its fused clear and the background's step_table + clear.  Single GPU;
+        the loss is read every step (the reference's order)."""
+        from . import msi
+
+        cfg = self.cfg
+        if self.world.active:
+            raise NotImplementedError("unbounded_360 runs on one GPU")
+        idx = self.batcher.next_device()
+        B = int(idx.numel())
+        P = self.pool
+        _, _, _, mse_sum, cauchy_raw, beta_raw = msi.render_rays_with_background(
+            self.grid, self.background, P.origins[idx], P.dirs[idx], self.opts,
+            gt_rgb=P.rgb[idx], grads=self.grads, bg_grads=self.bg_grads, n_total=B,
+            lam_cauchy=cfg.lambda_sparsity, lam_beta=cfg.lambda_beta)
+        loss_mse = mse_sum / B
+        tv_on = (cfg.lambda_tv_sigma > 0 or cfg.lambda_tv_sh > 0) and (
+            cfg.tv_until_step < 0 or step < cfg.tv_until_step)
+        tv_sig = tv_sh = 0.0
+        if tv_on:
+            run = losses.sample_tv_cells(self.grid, cfg.tv_sample_frac, self.rng)
+            tv_sig, tv_sh = losses.tv_loss(self.grid, run, cfg.lambda_tv_sigma, cfg.lambda_tv_sh,
+                                           self.grads)
+            if cfg.bg_lambda_tv > 0:
+                bcells = msi.sample_bg_tv_cells(self.background, cfg.tv_sample_frac, self.rng)
+                msi.bg_tv_loss(self.background, bcells, cfg.bg_lambda_tv, cfg.bg_lambda_tv,
+                               self.bg_grads)
+        loss = (loss_mse + tv_sig + tv_sh + cfg.lambda_sparsity * cauchy_raw
+                + cfg.lambda_beta * beta_raw)
+        if not math.isfinite(loss):
+            self.diverged_step = step
+            raise TrainingDiverged(f"non-finite loss at step {step}: mse={loss_mse!r} "
+                                   f"tv=({tv_sig!r}, {tv_sh!r})")
+        lr_s, lr_c = optim.lr_at(cfg.lr_sigma, step), optim.lr_at(cfg.lr_sh, step)
+        self.count.zero_()
+        optim.step(self.grid, self.grads, self.state, lr_s, lr_c, cfg.optimizer, clear=True,
+                   count_out=self.count, _cgrid=self._cgrid, _cgrad=self._cgrad)
+        msi.step_table(self.background, self.bg_grads, self.bg_state,
+                       optim.lr_at(cfg.bg_lr_sigma, step), optim.lr_at(cfg.bg_lr_rgb, step),
+                       cfg.optimizer)
+        return {"B": B, "loss": loss, "mse": loss_mse}
 
     def exchange_update(self, step: int, slot: int | None = None) -> None:
         """After the ranks' renders + TV: reduce the loss sums, exchange the
@@ -657,11 +756,13 @@ class Trainer:
 
     # -- evaluation (T:309-347) -------------------------------------------------
     def evaluate(self, dataset, chunk: int = 1 << 20):
-        return evaluate(self.grid, dataset, self.opts, chunk)
+        return evaluate(self.grid, dataset, self.opts, chunk, self.background, self.scene_scale)
 
 
-def evaluate(grid: SparseGrid, dataset, opts: render.RenderOptions, chunk: int = 1 << 20):
-    """Mean PSNR/SSIM over a dataset's views (T:309-347), device renders."""
+def evaluate(grid: SparseGrid, dataset, opts: render.RenderOptions, chunk: int = 1 << 20,
+             background=None, scene_scale: float = 1.0):
+    """Mean PSNR/SSIM over a dataset's views (T:309-347), device renders; 360
+    scenes: origins pre-scaled, grid + background composite."""
     from .camera import generate_rays, to_ndc
 
     rows = []
@@ -671,13 +772,20 @@ def evaluate(grid: SparseGrid, dataset, opts: render.RenderOptions, chunk: int =
         if dataset.scene_type == "forward_facing_ndc":
             v = d
             o, d, _ = to_ndc(o, d, cam)
-        ot = torch.from_numpy(o).to(grid.device)
+        if dataset.scene_type == "unbounded_360":
+            o = o * scene_scale
+        ot = torch.from_numpy(np.ascontiguousarray(o)).to(grid.device)
         dt = torch.from_numpy(np.ascontiguousarray(d)).to(grid.device)
         vt = torch.from_numpy(np.ascontiguousarray(v)).to(grid.device) if v is not None else None
         pred = torch.empty((o.shape[0], 3), dtype=torch.float64, device=grid.device)
         for s in range(0, o.shape[0], chunk):
-            rgb, _, _ = render.render_rays(grid, ot[s:s + chunk], dt[s:s + chunk], opts,
-                                           viewdirs=None if vt is None else vt[s:s + chunk])
+            if dataset.scene_type == "unbounded_360":
+                from . import msi
+                rgb = msi.render_rays_with_background(grid, background, ot[s:s + chunk],
+                                                      dt[s:s + chunk], opts)[0]
+            else:
+                rgb, _, _ = render.render_rays(grid, ot[s:s + chunk], dt[s:s + chunk], opts,
+                                               viewdirs=None if vt is None else vt[s:s + chunk])
             pred[s:s + chunk] = rgb
         pred = pred.cpu().numpy().reshape(np.asarray(img).shape)
         gt = np.asarray(img, dtype=np.float64)
@@ -688,7 +796,7 @@ def evaluate(grid: SparseGrid, dataset, opts: render.RenderOptions, chunk: int =
 
 def train(train_ds, config: TrainConfig, test_ds=None, out_dir=None, metrics_sink=None,
           device=None, world: World | None = None) -> TrainResult:
-    """T:350-518 on the device (bounded / forward-facing scenes)."""
+    """T:350-518 on the device (bounded, forward-facing and 360 scenes)."""
     cfg = config
     tr = Trainer(train_ds, cfg, device=device, world=world)
     out_dir = Path(out_dir) if out_dir is not None else None
@@ -713,7 +821,7 @@ def train(train_ds, config: TrainConfig, test_ds=None, out_dir=None, metrics_sin
                 tr.check_pending()
         except TrainingDiverged:
             if out_dir is not None:   # the device guard kept the pre-update grid
-                artifact_io.save_grid(tr.grid, out_dir / "diverged.plnx")
+                artifact_io.save_grid(tr.grid, out_dir / "diverged.plnx", tr.background)
             raise
         if log_now:
             emit({"step": step, "loss": rec["loss"], "mse": rec["mse"],
@@ -725,11 +833,13 @@ def train(train_ds, config: TrainConfig, test_ds=None, out_dir=None, metrics_sin
                   "wall_time_s": time.perf_counter() - t_start})
         if cfg.checkpoint_every > 0 and out_dir is not None and (step + 1) % cfg.checkpoint_every == 0:
             artifact_io.save_checkpoint(out_dir / f"checkpoint_{step + 1:07d}.plnx", tr.grid,
-                                        tr.state, step + 1)
+                                        tr.state, step + 1, tr.background, tr.bg_state)
     if test_ds is not None and last_eval != cfg.total_steps:
         p, s, _ = tr.evaluate(test_ds)
         emit({"step": cfg.total_steps, "psnr": p, "ssim": s,
               "wall_time_s": time.perf_counter() - t_start})
     if out_dir is not None:
-        artifact_io.save_checkpoint(out_dir / "final.plnx", tr.grid, tr.state, cfg.total_steps)
-    return TrainResult(grid=tr.grid, metrics=metrics, config=cfg)
+        artifact_io.save_checkpoint(out_dir / "final.plnx", tr.grid, tr.state, cfg.total_steps,
+                                    tr.background, tr.bg_state)
+    return TrainResult(grid=tr.grid, metrics=metrics, config=cfg, background=tr.background,
+                       scene_scale=tr.scene_scale)

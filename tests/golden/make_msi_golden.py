@@ -123,5 +123,42 @@ def main():
     print("wrote", OUT / "msi_grid.plnx")
 
 
+def make_trainer_360():
+    """A 20-step 360 run of the reference's trainer.train (T:350-518 with
+    the MSI background) on the tiny toy set loaded as unbounded_360."""
+    import dataclasses
+    import tempfile
+
+    from make_golden import _dataset_arrays
+
+    with tempfile.TemporaryDirectory() as td:
+        px.make_toy_dataset(Path(td) / "t", n_views=4, res=32, n_test=2, grid_dim=16)
+        train = px.load_nerf_dataset(Path(td) / "t", "unbounded_360", "train",
+                                     background=(0.0, 0.0, 0.0))
+        test = px.load_nerf_dataset(Path(td) / "t", "unbounded_360", "test",
+                                    background=(0.0, 0.0, 0.0))
+    cfg = dataclasses.replace(
+        px.toy_config(grid_dim=8, total_steps=20, batch_size=64), scene_type="unbounded_360",
+        aabb=(-1.0, -1.0, -1.0, 1.0, 1.0, 1.0), bg_layers=4, bg_height=8, bg_width=16,
+        lambda_beta=1e-3, lambda_sparsity=1e-6, background=(0.0, 0.0, 0.0))
+    cfg.eval_every = 0
+    cfg.log_every = 1
+    cfg.seed = 7
+    res = px.train(train, cfg, test_ds=test)
+    loss = np.array([m["loss"] for m in res.metrics if "loss" in m])
+    mse = np.array([m["mse"] for m in res.metrics if "mse" in m])
+    nnz = np.array([m["nnz_fraction"] for m in res.metrics if "nnz_fraction" in m])
+    psnr = [m["psnr"] for m in res.metrics if "psnr" in m][-1]
+    imgs, c2w, focal = _dataset_arrays(train)
+    timgs, tc2w, tfocal = _dataset_arrays(test)
+    np.savez_compressed(OUT / "trainer_360.npz", imgs=imgs, c2w=c2w, focal=focal,
+                        test_imgs=timgs, test_c2w=tc2w, test_focal=tfocal, loss=loss, mse=mse,
+                        nnz=nnz, psnr=np.array([psnr]), table=res.grid.table,
+                        links=res.grid.links, bg=res.background.data,
+                        scene_scale=np.array([res.scene_scale]))
+    print("wrote", OUT / "trainer_360.npz", "psnr", psnr, "loss", loss[:3], loss[-1])
+
+
 if __name__ == "__main__":
     main()
+    make_trainer_360()
