@@ -957,6 +957,18 @@ int plx::opt_step_impl(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, dou
     return status();
 }
 
+int plx::compact_mask_impl(uint8_t *tmask, int64_t rows, int32_t *tids, int64_t *tcnt,
+                           int clear, void *stream) {
+    if (!tmask || !tids || !tcnt || rows < 0) return PLX_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemsetAsync(tcnt, 0, sizeof(int64_t), s) != cudaSuccess) return PLX_ECUDA;
+    if (rows == 0) return PLX_OK;
+    const int64_t nb = (rows + kTileRows - 1) / kTileRows;
+    touched_compact_kernel<<<(unsigned)nb, kCompactNT, 0, s>>>(tmask, rows, tids, tcnt, clear,
+                                                               nullptr, nullptr);
+    return status();
+}
+
 extern "C" int plx_clear_grad(plx_grad *gb, int64_t rows, int64_t *out_count, void *stream) {
     if (!gb || !gb->grad || !gb->tmask || rows < 0) return PLX_EINVAL;
     if ((gb->tids == nullptr) != (gb->tcnt == nullptr)) return PLX_EINVAL;

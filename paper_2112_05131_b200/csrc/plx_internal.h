@@ -30,4 +30,8 @@ int tv_impl(const plx_grid *g, const int64_t *cells, int64_t start, const int64_
             int64_t count, double fac_x, double fac_y, double fac_z, double eps, double f_sigma,
             double f_sh, int32_t wrap_x, int32_t wrap_y, int32_t wrap_z, int32_t with_grad,
             plx_grad *gb, double *out_sums, void *stream, int short_blocks = 0);
+// Byte mask -> compact int32 list of its nonzero rows (tile compaction of the
+// update, order within 8192-row tiles), optionally clearing the mask.
+int compact_mask_impl(uint8_t *tmask, int64_t rows, int32_t *tids, int64_t *tcnt, int clear,
+                      void *stream);
 }  // namespace plx

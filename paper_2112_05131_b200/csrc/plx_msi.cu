@@ -513,33 +513,6 @@ __global__ void msi_opt_kernel(double *table, double *v, double *grad, const int
     }
 }
 
-__global__ void msi_mask_list_kernel(uint8_t *tmask, int64_t n, int32_t *tids, int64_t *tcnt,
-                                     int clear) {
-    // order-free compaction of the background mask (block-aggregated atomics)
-    __shared__ int blk_n;
-    __shared__ unsigned long long blk_base;
-    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < n;
-         b0 += (int64_t)gridDim.x * blockDim.x) {
-        if (threadIdx.x == 0) blk_n = 0;
-        __syncthreads();
-        const int64_t i = b0 + threadIdx.x;
-        const bool on = i < n && tmask[i];
-        int slot = -1;
-        if (on) slot = atomicAdd(&blk_n, 1);
-        __syncthreads();
-        if (threadIdx.x == 0)
-            blk_base = blk_n ? atomicAdd(reinterpret_cast<unsigned long long *>(tcnt),
-                                         (unsigned long long)blk_n)
-                             : 0ull;
-        __syncthreads();
-        if (on) {
-            tids[blk_base + slot] = (int32_t)i;
-            if (clear) tmask[i] = 0;
-        }
-        __syncthreads();
-    }
-}
-
 constexpr int64_t kRecBytes = 5 * 8 + 32 + 4;   // t, delta, sigma, T, w; colour; layer
 constexpr int64_t kRecHeader = 256 + 64;          // counter + alignment slack
 
@@ -665,11 +638,10 @@ extern "C" int plx_msi_opt_step(double *table, double *v, plx_msi_grad *bgb, int
         return PLX_EINVAL;
     if (n_texels == 0) return PLX_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    if (cudaMemsetAsync(bgb->tcnt, 0, sizeof(int64_t), s) != cudaSuccess) return PLX_ECUDA;
-    int64_t nb = (n_texels + 255) / 256;
-    if (nb > (int64_t)num_sms_msi() * 16) nb = (int64_t)num_sms_msi() * 16;
-    msi_mask_list_kernel<<<(unsigned)nb, 256, 0, s>>>(bgb->tmask, n_texels, bgb->tids, bgb->tcnt,
-                                                      clear);
+    if (n_texels > INT32_MAX) return PLX_EINVAL;
+    const int rc = plx::compact_mask_impl(bgb->tmask, n_texels, bgb->tids, bgb->tcnt, clear,
+                                          stream);
+    if (rc != PLX_OK) return rc;
     int64_t nb2 = (n_texels * 4 + 255) / 256;
     if (nb2 > (int64_t)num_sms_msi() * 16) nb2 = (int64_t)num_sms_msi() * 16;
     msi_opt_kernel<<<(unsigned)nb2, 256, 0, s>>>(table, v, bgb->grad, bgb->tids, bgb->tcnt,

@@ -220,27 +220,50 @@ def render_rays_with_background(grid: SparseGrid, bg: MsiBackground, origins, di
     return rgb, tfg, trans, float(s[0]), float(s[1]), float(s[2])
 
 
-def sample_bg_tv_cells(bg: MsiBackground, fraction: float, rng) -> np.ndarray:
+class BgCellRun:
+    """The texel run of sample_bg_tv_cells as (start, count) -- the kernel
+    walks it on the device; np.asarray(run) gives the reference's int64
+    array (msi.py:190)."""
+
+    def __init__(self, start: int, count: int, n_cells: int):
+        self.start, self.count, self.n_cells = int(start), int(count), int(n_cells)
+
+    def __array__(self, dtype=None, copy=None):
+        a = ((self.start + np.arange(self.count)) % self.n_cells).astype(np.int64)
+        return a if dtype is None else a.astype(dtype)
+
+    def __len__(self) -> int:
+        return self.count
+
+    @property
+    def size(self) -> int:
+        return self.count
+
+
+def sample_bg_tv_cells(bg: MsiBackground, fraction: float, rng) -> BgCellRun:
     """msi.py:186-190 (same RNG draws): a contiguous run of texels."""
     n_cells = bg.n_texels
     count = max(1, int(round(fraction * n_cells)))
     start = int(rng.integers(0, n_cells))
-    return ((start + np.arange(count)) % n_cells).astype(np.int64)
+    return BgCellRun(start, count, n_cells)
 
 
 def bg_tv_loss(bg: MsiBackground, cells, lam_sigma: float, lam_rgb: float,
                bg_grads: BgGradientBuffer | None = None, eps: float = 1e-6):
     """msi.py:193-208 -> tv_bg (K:884-977): TV over (layer, theta, phi), phi
     wrapping.  Returns the lambda-scaled (tv_sigma, tv_rgb) means."""
-    cells = np.ascontiguousarray(cells, dtype=np.int64)
-    if cells.size == 0:
-        return 0.0, 0.0
-    n = int(cells.size)
     dev = bg.device
-    ct = torch.from_numpy(cells).to(dev)
+    if isinstance(cells, BgCellRun):   # a run: walked on the device, no upload
+        n, start, ct = cells.count, cells.start, None
+    else:
+        cells = np.ascontiguousarray(cells, dtype=np.int64)
+        n, start = int(cells.size), 0
+        ct = torch.from_numpy(cells).to(dev)
+    if n == 0:
+        return 0.0, 0.0
     sums = torch.zeros(2, dtype=torch.float64, device=dev)
     cbg = bg_grads._c() if bg_grads is not None else None
-    _lib.check(_lib.lib().plx_msi_tv(ctypes.byref(bg._c()), ct.data_ptr(), 0, n, float(eps),
+    _lib.check(_lib.lib().plx_msi_tv(ctypes.byref(bg._c()), _lib.ptr(ct), start, n, float(eps),
                                      lam_sigma / n, lam_rgb / n,
                                      ctypes.byref(cbg) if cbg is not None else None,
                                      sums.data_ptr(), _lib.stream_ptr()), "msi_tv")
