@@ -49,7 +49,7 @@ def main():
     peak, _ = bench.load_peaks()
     out = {"grid": "toy GT upsampled to 512^3", "rows": g512.n_rows, "upsample_64_to_512_ms": up_ms,
            "rays_in_pool": views * res * res, "sweep": []}
-    for logb in range(14, 21):
+    for logb in range(int(os.environ.get("LOGB0", 14)), int(os.environ.get("LOGB1", 21))):
         B = 1 << logb
         cfg.batch_size = B
         tr = trainer.Trainer(ds, cfg, device=dev)
@@ -61,6 +61,7 @@ def main():
             tr.step(s)
         torch.cuda.synchronize()
         counts = []
+        st0 = tr.march_stats.clone()
         t0.record()
         for s in range(steps):
             tr.step(warm + s)
@@ -70,7 +71,9 @@ def main():
         ms = t0.elapsed_time(t1) / steps
         U = float(torch.stack(counts).double().mean())
         step_bytes = 60 * B + U * (4 + 112 + 224 + 672)
+        mst = ((tr.march_stats - st0).double() / steps).cpu().numpy()
         rec = {"B": B, "ms_per_step": ms, "rays_per_s": B / (ms / 1e3), "U": U,
+               "march_positions": float(mst[0]), "samples": float(mst[1]), "chunks": float(mst[2]),
                "U_frac": U / tr.grid.n_rows, "step_bytes": step_bytes,
                "hbm_roofline_rays_per_s": B * peak * 1e9 / step_bytes,
                "frac_of_roofline": (B / (ms / 1e3)) / (B * peak * 1e9 / step_bytes)}
