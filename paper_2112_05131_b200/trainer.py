@@ -370,7 +370,10 @@ class Trainer:
         self._hparams = [torch.zeros(4, dtype=torch.int64).pin_memory() for _ in range(3)]
         self._hparams_np = [h.numpy() for h in self._hparams]
         self._graphs, self._graph_args = {}, {}
-        self._rays_buf = None   # step_rays(): fixed device batch buffer (4, B, 3)
+        self._rays_buf = None   # step_rays(): two device batch slots (4, 2B, 3)
+        self._rays_idx = None
+        self._rays_slot = 0
+        self._copy_stream = None
         self._eager_done = False
         self._refresh_cache()
 
@@ -476,17 +479,38 @@ class Trainer:
         packed = dirs is None and origins.dim() == 3 and origins.shape[0] == 4
         B = int(origins.shape[1] if packed else origins.shape[0])
         buf = self._rays_buf
-        if buf is None or buf.shape[1] != B:
-            buf = self._rays_buf = torch.empty((4, B, 3), dtype=torch.float64, device=self.device)
+        if buf is None or buf.shape[1] != 2 * B:
+            # two batch slots (4, 2B, 3) + the identity index the graph
+            # offsets into (batch p = rows [pB, (p+1)B))
+            torch.cuda.synchronize()
+            buf = self._rays_buf = torch.empty((4, 2 * B, 3), dtype=torch.float64,
+                                               device=self.device)
+            self._rays_idx = torch.arange(2 * B, dtype=torch.int64, device=self.device)
+            self._rays_free = [torch.cuda.Event(), torch.cuda.Event()]
+            self._rays_copied = [torch.cuda.Event(), torch.cuda.Event()]
+            if self._copy_stream is None:
+                self._copy_stream = torch.cuda.Stream(device=self.device)
             for k in [k for k in self._graphs if k[0] == "rays"]:
                 del self._graphs[k]
-        if packed:
-            buf.copy_(torch.as_tensor(origins), non_blocking=True)
-        else:
-            for k, src in enumerate((origins, dirs, dirs if viewdirs is None else viewdirs,
-                                     target)):
-                buf[k].copy_(torch.as_tensor(src), non_blocking=True)
-        return self._step(step, B, None, check_finite, sync)
+        p = step % 2
+        dst = buf[:, p * B:(p + 1) * B]
+        # the H2D of this batch runs on a copy stream, overlapping the step
+        # still in flight; it waits for the step that last read slot p
+        cs, main = self._copy_stream, torch.cuda.current_stream(self.device)
+        cs.wait_event(self._rays_free[p])
+        with torch.cuda.stream(cs):
+            if packed:
+                dst.copy_(torch.as_tensor(origins), non_blocking=True)
+            else:
+                for k, src in enumerate((origins, dirs, dirs if viewdirs is None else viewdirs,
+                                         target)):
+                    dst[k].copy_(torch.as_tensor(src), non_blocking=True)
+            self._rays_copied[p].record(cs)
+        main.wait_event(self._rays_copied[p])
+        self._rays_slot = p
+        rec = self._step(step, B, None, check_finite, sync)
+        self._rays_free[p].record(main)
+        return rec
 
     def _step(self, step: int, B: int, idx, check_finite: bool, sync: bool,
               idx_off: int | None = None) -> dict:
@@ -525,14 +549,14 @@ class Trainer:
             hp = self._hparams_np[slot]
             hp[0] = tv_start
             hp[1:3].view(np.float64)[:] = (lr_s, lr_c)
-            hp[3] = idx_off if pool_mode else 0
+            hp[3] = idx_off if pool_mode else self._rays_slot * B
             self._replay(tv_on, pool_mode, slot)
         else:
             if pool_mode:
                 a.rays = self.pool.rays(None)
                 a.rays.idx = idx.data_ptr() + 8 * s0
             else:
-                a.rays = self._rays_desc()
+                a.rays = self._rays_desc(self._rays_slot)
             a.rays.n = c0
             a.rays.jitter = None
             if self.opts.jitter > 0:
@@ -675,12 +699,18 @@ class Trainer:
         self._eager_done = True   # the first step runs eagerly (one-time library queries)
         return ok
 
-    def _rays_desc(self) -> _lib.PlxRays:
+    def _rays_desc(self, slot: int | None = None) -> _lib.PlxRays:
+        """Descriptor of the step_rays batch buffer: slot p's rays directly
+        (eager), or slot None: both slots through the identity index, the
+        graph adding the slot's row offset (dev_idx_off)."""
         r = _lib.PlxRays()
         buf = self._rays_buf
-        r.origins, r.dirs = buf[0].data_ptr(), buf[1].data_ptr()
-        r.viewdirs, r.target = buf[2].data_ptr(), buf[3].data_ptr()
-        r.jitter, r.idx, r.n = None, None, int(buf.shape[1])
+        B = int(buf.shape[1]) // 2
+        off = 0 if slot is None else slot * B
+        r.origins, r.dirs = buf[0, off:].data_ptr(), buf[1, off:].data_ptr()
+        r.viewdirs, r.target = buf[2, off:].data_ptr(), buf[3, off:].data_ptr()
+        r.jitter, r.n = None, B
+        r.idx = self._rays_idx.data_ptr() if slot is None else None
         return r
 
     def _replay(self, tv_on: bool, pool_mode: bool, slot: int) -> None:
@@ -702,8 +732,8 @@ class Trainer:
                 a.rays.n = cfg.batch_size
                 a.dev_idx_off = self._dparams.data_ptr() + 24
             else:
-                a.rays = self._rays_desc()
-                a.dev_idx_off = None
+                a.rays = self._rays_desc(None)
+                a.dev_idx_off = self._dparams.data_ptr() + 24
             a.rays.jitter = None
             a.up_scale = 2.0 / int(a.rays.n)
             a.update = 1
