@@ -370,7 +370,7 @@ class Trainer:
         self._hparams = [torch.zeros(4, dtype=torch.int64).pin_memory() for _ in range(3)]
         self._hparams_np = [h.numpy() for h in self._hparams]
         self._graphs, self._graph_args = {}, {}
-        self._rays_buf = None   # step_rays(): two device batch slots (4, 2B, 3)
+        self._rays_buf = None   # step_rays(): two device batch slots (2, 4, B, 3)
         self._rays_idx = None
         self._rays_slot = 0
         self._copy_stream = None
@@ -479,13 +479,14 @@ class Trainer:
         packed = dirs is None and origins.dim() == 3 and origins.shape[0] == 4
         B = int(origins.shape[1] if packed else origins.shape[0])
         buf = self._rays_buf
-        if buf is None or buf.shape[1] != 2 * B:
-            # two batch slots (4, 2B, 3) + the identity index the graph
-            # offsets into (batch p = rows [pB, (p+1)B))
+        if buf is None or buf.shape[2] != B:
+            # two contiguous batch slots (2, 4, B, 3): slot p's arrays sit 4B
+            # rows after slot 0's, so the graph reads slot p as rows
+            # [4pB, 4pB + B) through the identity index + offset 4pB
             torch.cuda.synchronize()
-            buf = self._rays_buf = torch.empty((4, 2 * B, 3), dtype=torch.float64,
+            buf = self._rays_buf = torch.empty((2, 4, B, 3), dtype=torch.float64,
                                                device=self.device)
-            self._rays_idx = torch.arange(2 * B, dtype=torch.int64, device=self.device)
+            self._rays_idx = torch.arange(5 * B, dtype=torch.int64, device=self.device)
             self._rays_free = [torch.cuda.Event(), torch.cuda.Event()]
             self._rays_copied = [torch.cuda.Event(), torch.cuda.Event()]
             if self._copy_stream is None:
@@ -493,7 +494,7 @@ class Trainer:
             for k in [k for k in self._graphs if k[0] == "rays"]:
                 del self._graphs[k]
         p = step % 2
-        dst = buf[:, p * B:(p + 1) * B]
+        dst = buf[p]
         # the H2D of this batch runs on a copy stream, overlapping the step
         # still in flight; it waits for the step that last read slot p
         cs, main = self._copy_stream, torch.cuda.current_stream(self.device)
@@ -549,7 +550,7 @@ class Trainer:
             hp = self._hparams_np[slot]
             hp[0] = tv_start
             hp[1:3].view(np.float64)[:] = (lr_s, lr_c)
-            hp[3] = idx_off if pool_mode else self._rays_slot * B
+            hp[3] = idx_off if pool_mode else self._rays_slot * 4 * B
             self._replay(tv_on, pool_mode, slot)
         else:
             if pool_mode:
@@ -701,15 +702,13 @@ class Trainer:
 
     def _rays_desc(self, slot: int | None = None) -> _lib.PlxRays:
         """Descriptor of the step_rays batch buffer: slot p's rays directly
-        (eager), or slot None: both slots through the identity index, the
-        graph adding the slot's row offset (dev_idx_off)."""
+        (eager), or slot None: slot 0's arrays through the identity index,
+        the graph adding the slot's row offset 4pB (dev_idx_off)."""
         r = _lib.PlxRays()
-        buf = self._rays_buf
-        B = int(buf.shape[1]) // 2
-        off = 0 if slot is None else slot * B
-        r.origins, r.dirs = buf[0, off:].data_ptr(), buf[1, off:].data_ptr()
-        r.viewdirs, r.target = buf[2, off:].data_ptr(), buf[3, off:].data_ptr()
-        r.jitter, r.n = None, B
+        sb = self._rays_buf[0 if slot is None else slot]
+        r.origins, r.dirs = sb[0].data_ptr(), sb[1].data_ptr()
+        r.viewdirs, r.target = sb[2].data_ptr(), sb[3].data_ptr()
+        r.jitter, r.n = None, int(sb.shape[1])
         r.idx = self._rays_idx.data_ptr() if slot is None else None
         return r
 
