@@ -6,7 +6,7 @@ set -e
 NAME=$1; DEFS=$2
 D=$(cd "$(dirname "$0")/../paper_2112_05131_b200/csrc" && pwd)
 T=$(mktemp -d)
-for f in plx_render plx_grid_ops plx_dp plx_step; do
+for f in $(sed -n "s/^SRCS := //p" "$D/Makefile" | sed "s/\.cu//g"); do
   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -fmad=false \
        -Xcompiler -fPIC -Xptxas -v $DEFS -c "$D/$f.cu" -o "$T/$f.o" 2> "$T/$f.log" || { cat "$T/$f.log"; exit 1; }
 done
