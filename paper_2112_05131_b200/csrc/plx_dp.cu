@@ -122,6 +122,7 @@ __device__ __forceinline__ int nz_bytes(uint32_t m) {
 // and the new rows stored into every rank's grid.
 __global__ void __launch_bounds__(256) dp_owner_update_kernel(DpArgs a) {
     __shared__ uint8_t list[8][128];
+    __shared__ uint8_t ranks[8][128];   // per listed row: bit k = rank k touched it
     if (guard_halts(a.guard)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) a.guard[4] = 1.0;
         return;
@@ -133,15 +134,20 @@ __global__ void __launch_bounds__(256) dp_owner_update_kernel(DpArgs a) {
     unsigned long long cnt = 0;
     for (int64_t seg = seg0 + (int64_t)blockIdx.x * 8 + wib; seg < seg1; seg += nw) {
         const int64_t r0 = seg * 128 + lane * 4;
-        uint32_t m = 0;
+        uint32_t m = 0, rk = 0;   // rk: byte e = ranks that touched row r0 + e
         for (int k = 0; k < a.n; ++k) {
+            uint32_t mk = 0;
             if (r0 + 3 < a.hi) {
-                m |= *reinterpret_cast<const volatile uint32_t *>(a.tmask[k] + r0);
+                mk = *reinterpret_cast<const volatile uint32_t *>(a.tmask[k] + r0);
             } else {
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
-                    if (r0 + e < a.hi && a.tmask[k][r0 + e]) m |= 0xffu << (8 * e);
+                    if (r0 + e < a.hi && a.tmask[k][r0 + e]) mk |= 0xffu << (8 * e);
             }
+            m |= mk;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if ((mk >> (8 * e)) & 0xffu) rk |= (1u << k) << (8 * e);
         }
         const int c = nz_bytes(m);
         int incl = c;
@@ -155,15 +161,23 @@ __global__ void __launch_bounds__(256) dp_owner_update_kernel(DpArgs a) {
         int pos = incl - c;
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-            if ((m >> (8 * e)) & 0xffu) list[wib][pos++] = (uint8_t)(lane * 4 + e);
+            if ((m >> (8 * e)) & 0xffu) {
+                ranks[wib][pos] = (uint8_t)((rk >> (8 * e)) & 0xffu);
+                list[wib][pos++] = (uint8_t)(lane * 4 + e);
+            }
         __syncwarp();
         cnt += (unsigned long long)total;
         for (int gi = 0; gi < total; gi += 4) {
             const int j = gi + sub;
             if (lane < 28 && j < total) {
                 const int64_t r = seg * 128 + list[wib][j];
+                const unsigned rb = ranks[wib][j];
                 float4 g4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                // only the ranks that touched the row hold a nonzero gradient
+                // row: skip the others' peer reads (adding their zeros is the
+                // identity, so the rank-order sum is unchanged)
                 for (int k = 0; k < a.n; ++k) {
+                    if (!((rb >> k) & 1u)) continue;
                     const float4 x = reinterpret_cast<const float4 *>(a.grad[k] + r * PLX_STRIDE)[quad];
                     g4.x += x.x;
                     g4.y += x.y;
