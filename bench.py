@@ -142,7 +142,7 @@ def bench_config(args):
 
 
 # ------------------------------------------------------------ CPU oracle --
-def oracle_steps(args, n_steps, ds, time_budget_s=None):
+def oracle_steps(args, n_steps, ds, time_budget_s=None, warmup=1):
     """The reference's step body (T:455-486: fused_mse_backward + tv_loss +
     optim.step + grads.clear) through the f64 C port, on one host core.
     Returns (rays_per_s, steps_timed, sample description)."""
@@ -161,7 +161,7 @@ def oracle_steps(args, n_steps, ds, time_budget_s=None):
     perm = rng.permutation(o.shape[0])
     times = []
     t_start = time.perf_counter()
-    for step in range(n_steps + 1):
+    for step in range(n_steps + warmup):
         idx = perm[(step * B) % len(perm):][:B]
         t0 = time.perf_counter()
         orc.fused_mse_backward(g, o[idx], m[idx], v[idx], gt[idx], buf, B,
@@ -172,11 +172,11 @@ def oracle_steps(args, n_steps, ds, time_budget_s=None):
         orc.opt_step(g, buf, v_state, popt.lr_at(cfg.lr_sigma, step), popt.lr_at(cfg.lr_sh, step))
         buf.clear()
         dt = time.perf_counter() - t0
-        if step > 0:     # discard the first step (first-touch page faults)
+        if step >= warmup:   # discard the warm-up steps (first-touch page faults)
             times.append(dt)
         if time_budget_s and time.perf_counter() - t_start > time_budget_s and times:
             break
-    sample = (f"{len(times)} timed step(s) of {B} rays (+1 discarded), dense {args.dims}^3 f64 "
+    sample = (f"{len(times)} timed step(s) of {B} rays (+{warmup} discarded), dense {args.dims}^3 f64 "
               f"grid, TV 1% cells, RMSProp; sequential C port of K:173-600, 1 thread")
     return B / float(np.mean(times)), len(times), sample
 
@@ -209,9 +209,11 @@ def run_reference(args):
     # the scene is rendered by the oracle itself: nothing of ours on this arm
     n_views = max(1, min(args.views, -(-(args.steps + 1) * args.batch // (args.res ** 2))))
     ds = oracle_scene(n_views, args.res)
-    rps, k, sample = oracle_steps(args, max(1, args.steps), ds, time_budget_s=budget)
+    warm = max(1, args.warmup)
+    rps, k, sample = oracle_steps(args, max(1, args.steps), ds, time_budget_s=budget, warmup=warm)
     line = {"impl": "reference", "metric": METRIC, "value": rps, "unit": "rays/s",
-            "n_gpus": args.gpus, "steps": k, "warmup": 1, "ms_per_step": 1000.0 * args.batch / rps,
+            "n_gpus": args.gpus, "steps": k, "warmup": warm,
+            "ms_per_step": 1000.0 * args.batch / rps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": WORKLOAD, "grid": f"{args.dims}^3",
                                             "rays_per_step": args.batch},
