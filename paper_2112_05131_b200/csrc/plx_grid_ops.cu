@@ -352,7 +352,28 @@ __device__ __forceinline__ uint32_t nonzero_bytes_hi(uint32_t x) {
     return (((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u;
 }
 
-__global__ void __launch_bounds__(kCompactNT, 6) touched_compact_kernel(uint8_t *tmask,
+__device__ __forceinline__ void load_mask_words(const uint8_t *tmask, int64_t rows, int64_t r0,
+                                                uint32_t *w) {
+    if (r0 + 32 <= rows) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(tmask + r0);
+        const uint4 a0 = __ldcs(p), a1 = __ldcs(p + 1);
+        w[0] = a0.x; w[1] = a0.y; w[2] = a0.z; w[3] = a0.w;
+        w[4] = a1.x; w[5] = a1.y; w[6] = a1.z; w[7] = a1.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            w[i] = 0u;
+            for (int e = 0; e < 4; ++e) {
+                const int64_t r = r0 + 4 * i + e;
+                if (r < rows && tmask[r]) w[i] |= 0xffu << (8 * e);
+            }
+        }
+    }
+}
+
+// Persistent over the tiles (one resident wave), the next tile's mask words
+// loaded while the current one is compacted.
+__global__ void __launch_bounds__(kCompactNT, 4) touched_compact_kernel(uint8_t *tmask,
                                                                         int64_t rows,
                                                                         int32_t *tids,
                                                                         int64_t *tcnt, int clear,
@@ -369,71 +390,82 @@ __global__ void __launch_bounds__(kCompactNT, 6) touched_compact_kernel(uint8_t 
         return;
     }
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t r0 = (int64_t)blockIdx.x * kTileRows + (int64_t)threadIdx.x * 32;
-    uint32_t w[8];
-    if (r0 + 32 <= rows) {
-        const uint4 *p = reinterpret_cast<const uint4 *>(tmask + r0);
-        const uint4 a0 = __ldcs(p), a1 = __ldcs(p + 1);
-        w[0] = a0.x; w[1] = a0.y; w[2] = a0.z; w[3] = a0.w;
-        w[4] = a1.x; w[5] = a1.y; w[6] = a1.z; w[7] = a1.w;
-    } else {
+    const int64_t ntiles = (rows + kTileRows - 1) / kTileRows;
+    uint32_t w[8], wn[8];
+    int64_t t = blockIdx.x;
+    if (t < ntiles) load_mask_words(tmask, rows, t * kTileRows + (int64_t)threadIdx.x * 32, w);
+    for (; t < ntiles; t += gridDim.x) {
+        const int64_t r0 = t * kTileRows + (int64_t)threadIdx.x * 32;
+        const int64_t tn = t + gridDim.x;
+        if (tn < ntiles) load_mask_words(tmask, rows, tn * kTileRows + (int64_t)threadIdx.x * 32, wn);
+        int c = 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            w[i] = 0u;
-            for (int e = 0; e < 4; ++e) {
-                const int64_t r = r0 + 4 * i + e;
-                if (r < rows && tmask[r]) w[i] |= 0xffu << (8 * e);
+            w[i] = nonzero_bytes_hi(w[i]);
+            c += __popc(w[i]);
+        }
+        int incl = c;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(PLX_FULL_MASK, incl, off);
+            if (lane >= off) incl += y;
+        }
+        if (lane == 31) warp_tot[wib] = incl;
+        __syncthreads();
+        int before = 0, total = 0;
+#pragma unroll
+        for (int k = 0; k < kCompactNT / 32; ++k) {
+            const int tt = warp_tot[k];
+            before += k < wib ? tt : 0;
+            total += tt;
+        }
+        if (total != 0) {   // block-uniform
+            if (threadIdx.x == 0)
+                blk_base = atomicAdd(reinterpret_cast<unsigned long long *>(tcnt),
+                                     (unsigned long long)total);
+            int q = before + incl - c;
+            const int rb = threadIdx.x * 32;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t x = w[i];
+                if (!x) continue;
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (x & (0x80u << (8 * e))) sid[q++] = (uint16_t)(rb + 4 * i + e);
             }
+            if (clear && c) {
+                if (r0 + 32 <= rows) {
+                    uint4 *p = reinterpret_cast<uint4 *>(tmask + r0);
+                    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+                    p[0] = z;
+                    p[1] = z;
+                } else {
+                    for (int r = 0; r < 32 && r0 + r < rows; ++r) tmask[r0 + r] = 0;
+                }
+            }
+            __syncthreads();
+            const int64_t base = (int64_t)blk_base;
+            const int32_t tile0 = (int32_t)(t * kTileRows);
+            for (int i = threadIdx.x; i < total; i += kCompactNT) tids[base + i] = tile0 + sid[i];
         }
-    }
-    int c = 0;
+        __syncthreads();   // smem reuse by the next tile
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        w[i] = nonzero_bytes_hi(w[i]);
-        c += __popc(w[i]);
+        for (int i = 0; i < 8; ++i) w[i] = wn[i];
     }
-    int incl = c;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const int y = __shfl_up_sync(PLX_FULL_MASK, incl, off);
-        if (lane >= off) incl += y;
+}
+
+static int compact_grid(int64_t rows) {
+    static int bps = 0;
+    if (!bps) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, touched_compact_kernel, kCompactNT, 0);
+        if (bps <= 0) bps = 1;
     }
-    if (lane == 31) warp_tot[wib] = incl;
-    __syncthreads();
-    int before = 0, total = 0;
-#pragma unroll
-    for (int k = 0; k < kCompactNT / 32; ++k) {
-        const int t = warp_tot[k];
-        before += k < wib ? t : 0;
-        total += t;
-    }
-    if (total == 0) return;   // block-uniform
-    if (threadIdx.x == 0)
-        blk_base = atomicAdd(reinterpret_cast<unsigned long long *>(tcnt), (unsigned long long)total);
-    int q = before + incl - c;
-    const int rb = threadIdx.x * 32;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const uint32_t x = w[i];
-        if (!x) continue;
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-            if (x & (0x80u << (8 * e))) sid[q++] = (uint16_t)(rb + 4 * i + e);
-    }
-    if (clear && c) {
-        if (r0 + 32 <= rows) {
-            uint4 *p = reinterpret_cast<uint4 *>(tmask + r0);
-            const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-            p[0] = z;
-            p[1] = z;
-        } else {
-            for (int r = 0; r < 32 && r0 + r < rows; ++r) tmask[r0 + r] = 0;
-        }
-    }
-    __syncthreads();
-    const int64_t base = (int64_t)blk_base;
-    const int32_t tile0 = (int32_t)((int64_t)blockIdx.x * kTileRows);
-    for (int i = threadIdx.x; i < total; i += kCompactNT) tids[base + i] = tile0 + sid[i];
+    const int64_t ntiles = (rows + kTileRows - 1) / kTileRows;
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t cap = (int64_t)(sms > 0 ? sms : 148) * bps;
+    return (int)(ntiles < cap ? (ntiles > 0 ? ntiles : 1) : cap);
 }
 
 template <int UU, int MINB>
@@ -943,7 +975,7 @@ int plx::opt_step_impl(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, dou
     if (gb->tids) {   // two-phase: compact the touched set, then update the list
         if (!tcnt_ready && cudaMemsetAsync(gb->tcnt, 0, sizeof(int64_t), s) != cudaSuccess)
             return PLX_ECUDA;
-        const int64_t nb = (g->rows + kTileRows - 1) / kTileRows;
+        const int64_t nb = compact_grid(g->rows);
         touched_compact_kernel<<<(unsigned)nb, kCompactNT, 0, s>>>(gb->tmask, g->rows, gb->tids,
                                                                    gb->tcnt, clear, guard,
                                                                    host_sums);
@@ -963,7 +995,7 @@ int plx::compact_mask_impl(uint8_t *tmask, int64_t rows, int32_t *tids, int64_t 
     cudaStream_t s = (cudaStream_t)stream;
     if (cudaMemsetAsync(tcnt, 0, sizeof(int64_t), s) != cudaSuccess) return PLX_ECUDA;
     if (rows == 0) return PLX_OK;
-    const int64_t nb = (rows + kTileRows - 1) / kTileRows;
+    const int64_t nb = compact_grid(rows);
     touched_compact_kernel<<<(unsigned)nb, kCompactNT, 0, s>>>(tmask, rows, tids, tcnt, clear,
                                                                nullptr, nullptr);
     return status();
@@ -977,7 +1009,7 @@ extern "C" int plx_clear_grad(plx_grad *gb, int64_t rows, int64_t *out_count, vo
     cudaStream_t s = (cudaStream_t)stream;
     if (gb->tids) {   // compact + clear the mask, then zero the listed rows
         if (cudaMemsetAsync(gb->tcnt, 0, sizeof(int64_t), s) != cudaSuccess) return PLX_ECUDA;
-        const int64_t nb = (rows + kTileRows - 1) / kTileRows;
+        const int64_t nb = compact_grid(rows);
         touched_compact_kernel<<<(unsigned)nb, kCompactNT, 0, s>>>(gb->tmask, rows, gb->tids,
                                                                    gb->tcnt, 1, nullptr, nullptr);
         clear_rows_kernel<<<(unsigned)(num_sms() * 8), NT, 0, s>>>(gb->grad, gb->tids, gb->tcnt);
