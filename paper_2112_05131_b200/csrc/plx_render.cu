@@ -599,23 +599,27 @@ __global__ void __launch_bounds__(128, MINB)
         const bool valid = j < nx_ns;
         float bf[9];
         ray_basis(R, src, bf);
-        // this lane's 4 columns 4*part .. 4*part+3 -> per-channel coefficients
-        float cR[4], cG[4], cB[4];
+        // this lane's 4 columns 4*part .. 4*part+3 span at most two colour
+        // channels: cA feeds the first (chA), cB the second.  Per row the
+        // part-0 lane then gathers R = a0+a1+a2, G = b2+a3+a4, B = b4+a5+a6.
+        float cA[4], cB[4];
+        {
+            const int chA = part < 7 ? ((part == 0 ? 1 : 4 * part) - 1) / 9 : -1;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int c = 4 * part + e;   // column 0 = sigma padding; 28..31 pitch padding
-            float coef = 0.f;
-            int ch = -1;
-            if (part < 7 && c >= 1) {
-                ch = (c - 1) / 9;
-                const int b = (c - 1) % 9;
+            for (int e = 0; e < 4; ++e) {
+                const int c = 4 * part + e;   // column 0 = sigma padding; 28..31 pitch padding
+                float coef = 0.f;
+                int ch = -1;
+                if (part < 7 && c >= 1) {
+                    ch = (c - 1) / 9;
+                    const int b = (c - 1) % 9;
 #pragma unroll
-                for (int bb = 0; bb < 9; ++bb)
-                    if (bb == b) coef = bf[bb];
+                    for (int bb = 0; bb < 9; ++bb)
+                        if (bb == b) coef = bf[bb];
+                }
+                cA[e] = ch >= 0 && ch == chA ? coef : 0.f;
+                cB[e] = ch >= 0 && ch != chA ? coef : 0.f;
             }
-            cR[e] = ch == 0 ? coef : 0.f;
-            cG[e] = ch == 1 ? coef : 0.f;
-            cB[e] = ch == 2 ? coef : 0.f;
         }
         const int64_t k = ray * S.cap + j;
         int4 cl = make_int4(0, 0, 0, 0);
@@ -740,19 +744,22 @@ __global__ void __launch_bounds__(128, MINB)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const float x[4] = {vc[u].x, vc[u].y, vc[u].z, vc[u].w};
-                float pR = 0.f, pG = 0.f, pB = 0.f;
+                float pa = 0.f, pb = 0.f;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    pR = __fmaf_rn(x[e], cR[e], pR);
-                    pG = __fmaf_rn(x[e], cG[e], pG);
-                    pB = __fmaf_rn(x[e], cB[e], pB);
+                    pa = __fmaf_rn(x[e], cA[e], pa);
+                    pb = __fmaf_rn(x[e], cB[e], pb);
                 }
-#pragma unroll
-                for (int off = 1; off < 8; off <<= 1) {   // reduce over the row's 8 lanes
-                    pR += __shfl_xor_sync(PLX_FULL_MASK, pR, off);
-                    pG += __shfl_xor_sync(PLX_FULL_MASK, pG, off);
-                    pB += __shfl_xor_sync(PLX_FULL_MASK, pB, off);
-                }
+                // gather the row's channel sums at its part-0 lane
+                const float a1 = __shfl_down_sync(PLX_FULL_MASK, pa, 1);
+                const float a2 = __shfl_down_sync(PLX_FULL_MASK, pa, 2);
+                const float b2 = __shfl_down_sync(PLX_FULL_MASK, pb, 2);
+                const float a3 = __shfl_down_sync(PLX_FULL_MASK, pa, 3);
+                const float a4 = __shfl_down_sync(PLX_FULL_MASK, pa, 4);
+                const float b4 = __shfl_down_sync(PLX_FULL_MASK, pb, 4);
+                const float a5 = __shfl_down_sync(PLX_FULL_MASK, pa, 5);
+                const float a6 = __shfl_down_sync(PLX_FULL_MASK, pa, 6);
+                const float pR = (pa + a1) + a2, pG = (b2 + a3) + a4, pB = (b4 + a5) + a6;
                 const int rr = r0 + 4 * u + sub;
                 if (part == 0 && rr < nrow) sm.d[rr] = make_float4(pR, pG, pB, 0.f);
             }
