@@ -39,7 +39,9 @@ __device__ __forceinline__ void root_and_rinv(double s, double &root, double &ri
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
     const double hs = 0.5 * s;
-    y = y * fma(-hs * y, y, 1.5);
+    // two Newton steps take the hardware estimate to ~2^-44 -- ample for
+    // rinv, which only feeds f32-rounded gradients; the root gets a final
+    // Newton step of its own (~2^-88 before rounding: the sums stay f64-exact)
     y = y * fma(-hs * y, y, 1.5);
     y = y * fma(-hs * y, y, 1.5);
     double r = s * y;
