@@ -489,27 +489,50 @@ __global__ void msi_tv_kernel(MsiDev B, const int64_t *cells, int64_t start, int
 }
 
 // O:100-107 / K:572-590 on the f64 background table over the compacted
-// touched list, then the clear of K:593-600: one thread per (row, column).
-__global__ void msi_opt_kernel(double *table, double *v, double *grad, const int32_t *tids,
-                               const int64_t *tcnt, double lr_first, double lr_rest, double beta,
-                               double eps, int rmsprop, int clear) {
+// touched list (sorted within each 8192-texel tile), then the clear of
+// K:593-600: one thread per texel, its three 32-B sectors (grad, v, table)
+// loaded together.  The background's touched texels are scattered over GBs
+// of f64 state, so this is a random-sector RMW; a (texel, channel) thread map
+// chained the loads behind the grad clear's store and ran 4-6x slower
+// (scripts/probes/texel_rmw.cu), and a mask sweep in address order (lane = 4
+// texels) serialised the touched texels per lane and was slower still.
+__device__ __forceinline__ double rms_apply(double &t, double &vv, double g, double lr,
+                                            double beta, double eps, int rmsprop) {
+    if (g == 0.0) return t;
+    if (rmsprop) {
+        vv = beta * vv + (1.0 - beta) * g * g;
+        t -= lr * g / (sqrt(vv) + eps);
+    } else {
+        t -= lr * g;
+    }
+    return t;
+}
+
+__global__ void __launch_bounds__(256) msi_opt_kernel(double *__restrict__ table,
+                                                      double *__restrict__ v,
+                                                      double *__restrict__ grad,
+                                                      const int32_t *__restrict__ tids,
+                                                      const int64_t *tcnt, double lr_first,
+                                                      double lr_rest, double beta, double eps,
+                                                      int rmsprop, int clear) {
     const int64_t n = *tcnt;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * 4;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
          t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = tids[t >> 2];
-        const int c = (int)(t & 3);
-        const int64_t e = 4 * r + c;
-        const double g = grad[e];
-        if (clear) grad[e] = 0.0;
-        if (g == 0.0) continue;
-        const double lr = c == 0 ? lr_first : lr_rest;
-        if (rmsprop) {
-            const double nv = beta * v[e] + (1.0 - beta) * g * g;
-            v[e] = nv;
-            table[e] -= lr * g / (sqrt(nv) + eps);
-        } else {
-            table[e] -= lr * g;
-        }
+        const int64_t r = tids[t];
+        double2 *gp = reinterpret_cast<double2 *>(grad + 4 * r);
+        double2 *tp = reinterpret_cast<double2 *>(table + 4 * r);
+        double2 *vp = reinterpret_cast<double2 *>(v + 4 * r);
+        const double2 g0 = gp[0], g1 = gp[1];
+        double2 t0 = tp[0], t1 = tp[1];
+        double2 v0 = make_double2(0.0, 0.0), v1 = v0;
+        if (rmsprop) { v0 = vp[0]; v1 = vp[1]; }
+        if (clear) { gp[0] = make_double2(0.0, 0.0); gp[1] = gp[0]; }
+        rms_apply(t0.x, v0.x, g0.x, lr_first, beta, eps, rmsprop);
+        rms_apply(t0.y, v0.y, g0.y, lr_rest, beta, eps, rmsprop);
+        rms_apply(t1.x, v1.x, g1.x, lr_rest, beta, eps, rmsprop);
+        rms_apply(t1.y, v1.y, g1.y, lr_rest, beta, eps, rmsprop);
+        tp[0] = t0; tp[1] = t1;
+        if (rmsprop) { vp[0] = v0; vp[1] = v1; }
     }
 }
 
@@ -642,10 +665,10 @@ extern "C" int plx_msi_opt_step(double *table, double *v, plx_msi_grad *bgb, int
     const int rc = plx::compact_mask_impl(bgb->tmask, n_texels, bgb->tids, bgb->tcnt, clear,
                                           stream);
     if (rc != PLX_OK) return rc;
-    int64_t nb2 = (n_texels * 4 + 255) / 256;
-    if (nb2 > (int64_t)num_sms_msi() * 16) nb2 = (int64_t)num_sms_msi() * 16;
-    msi_opt_kernel<<<(unsigned)nb2, 256, 0, s>>>(table, v, bgb->grad, bgb->tids, bgb->tcnt,
-                                                 lr_sigma, lr_rgb, beta, eps, rmsprop, clear);
+    int64_t nb = (n_texels + 255) / 256;
+    if (nb > (int64_t)num_sms_msi() * 8) nb = (int64_t)num_sms_msi() * 8;
+    msi_opt_kernel<<<(unsigned)nb, 256, 0, s>>>(table, v, bgb->grad, bgb->tids, bgb->tcnt,
+                                                lr_sigma, lr_rgb, beta, eps, rmsprop, clear);
     if (out_count && cudaMemcpyAsync(out_count, bgb->tcnt, sizeof(int64_t),
                                      cudaMemcpyDeviceToDevice, s) != cudaSuccess)
         return PLX_ECUDA;
