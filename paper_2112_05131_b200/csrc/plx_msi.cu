@@ -416,69 +416,76 @@ __global__ void __launch_bounds__(kMsiThreads)
     }
 }
 
-// K:884-977 (tv_bg): one thread per (cell, channel); f64; phi wraps.
-__global__ void msi_tv_kernel(MsiDev B, const int64_t *cells, int64_t start, int64_t count,
-                              double eps, double f_sigma, double f_rgb, double *grad,
-                              uint8_t *tmask, double *sums) {
+// K:884-977 (tv_bg): one thread per texel, its four neighbour sectors (self,
+// l+1, j+1, i+1 with the phi wrap) loaded together, then the per-channel
+// terms of the reference; f64.
+__device__ __forceinline__ void ld_texel(const double *D, int64_t f, double (&o)[4]) {
+    const double2 *p = reinterpret_cast<const double2 *>(D + 4 * f);
+    const double2 a = __ldg(p), b = __ldg(p + 1);
+    o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+}
+
+__global__ void __launch_bounds__(256) msi_tv_kernel(MsiDev B, const int64_t *cells,
+                                                     int64_t start, int64_t count, double eps,
+                                                     double f_sigma, double f_rgb, double *grad,
+                                                     uint8_t *tmask, double *sums) {
     const int64_t n = (int64_t)B.L * B.H * B.W;
     const double fl = (double)B.L / 256.0, fh = (double)B.H / 256.0, fw = (double)B.W / 256.0;
     const double e2 = eps * eps;
+    const int64_t HW = (int64_t)B.H * B.W;
     double s_sig = 0.0, s_rgb = 0.0;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count * 4;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t ci = t >> 2;
-        const int c = (int)(t & 3);
+    for (int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ci < count;
+         ci += (int64_t)gridDim.x * blockDim.x) {
         int64_t cid = cells ? cells[ci] : start + ci;
         if (!cells && cid >= n) cid %= n;
-        const int64_t HW = (int64_t)B.H * B.W;
         const int64_t l = cid / HW, rem = cid - l * HW;
         const int64_t j = rem / B.W, i = rem - j * B.W;
         const bool hl = l + 1 < B.L, hj = j + 1 < B.H;
         const int64_t iw = i + 1 < B.W ? i + 1 : 0;
-        const double *D = B.data;
-        const double v0 = D[((l * B.H + j) * B.W + i) * 4 + c];
-        const double fac = c == 0 ? f_sigma : f_rgb;
-        double vl, vj;
-        if (c == 0) {
-            vl = hl ? D[(((l + 1) * B.H + j) * B.W + i) * 4] : 0.0;
-            vj = hj ? D[((l * B.H + j + 1) * B.W + i) * 4] : 0.0;
-        } else {
-            vl = hl ? D[(((l + 1) * B.H + j) * B.W + i) * 4 + c] : v0;
-            vj = hj ? D[((l * B.H + j + 1) * B.W + i) * 4 + c] : v0;
-        }
-        const double vi = D[((l * B.H + j) * B.W + iw) * 4 + c];
-        const double da = (vl - v0) * fl, db = (vj - v0) * fh, dc = (vi - v0) * fw;
-        const double val = sqrt(da * da + db * db + dc * dc + e2);
-        if (c == 0) s_sig += val; else s_rgb += val;
-        if (grad && val > 0.0) {
-            const double inv = fac / val;
+        const int64_t f0 = cid, fL = cid + HW, fJ = cid + B.W, fI = l * HW + j * B.W + iw;
+        double v0[4], vl[4], vj[4], vi[4];
+        ld_texel(B.data, f0, v0);
+        ld_texel(B.data, fI, vi);
+        if (hl) ld_texel(B.data, fL, vl);
+        else { vl[0] = 0.0; vl[1] = v0[1]; vl[2] = v0[2]; vl[3] = v0[3]; }
+        if (hj) ld_texel(B.data, fJ, vj);
+        else { vj[0] = 0.0; vj[1] = v0[1]; vj[2] = v0[2]; vj[3] = v0[3]; }
+        bool mark_l = false, mark_j = false, mark_i = false, mark_0 = false;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const double da = (vl[c] - v0[c]) * fl, db = (vj[c] - v0[c]) * fh,
+                         dc = (vi[c] - v0[c]) * fw;
+            const double val = sqrt(da * da + db * db + dc * dc + e2);
+            if (c == 0) s_sig += val; else s_rgb += val;
+            if (!grad || !(val > 0.0)) continue;
+            const double inv = (c == 0 ? f_sigma : f_rgb) / val;
             double g0 = 0.0;
             if (hl) {
-                const int64_t f = (l + 1) * HW + j * B.W + i;
-                tmask[f] = 1;
-                atomicAdd(grad + 4 * f + c, da * fl * inv);
+                mark_l = true;
+                atomicAdd(grad + 4 * fL + c, da * fl * inv);
                 g0 -= da * fl * inv;
             } else if (c == 0) {
                 g0 -= da * fl * inv;
             }
             if (hj) {
-                const int64_t f = l * HW + (j + 1) * B.W + i;
-                tmask[f] = 1;
-                atomicAdd(grad + 4 * f + c, db * fh * inv);
+                mark_j = true;
+                atomicAdd(grad + 4 * fJ + c, db * fh * inv);
                 g0 -= db * fh * inv;
             } else if (c == 0) {
                 g0 -= db * fh * inv;
             }
-            const int64_t f = l * HW + j * B.W + iw;
-            tmask[f] = 1;
-            atomicAdd(grad + 4 * f + c, dc * fw * inv);
+            mark_i = true;
+            atomicAdd(grad + 4 * fI + c, dc * fw * inv);
             g0 -= dc * fw * inv;
             if (g0 != 0.0) {
-                const int64_t f0 = l * HW + j * B.W + i;
-                tmask[f0] = 1;
+                mark_0 = true;
                 atomicAdd(grad + 4 * f0 + c, g0);
             }
         }
+        if (mark_l) tmask[fL] = 1;
+        if (mark_j) tmask[fJ] = 1;
+        if (mark_i) tmask[fI] = 1;
+        if (mark_0) tmask[f0] = 1;
     }
     s_sig = warp_sum(s_sig);
     s_rgb = warp_sum(s_rgb);
@@ -644,8 +651,8 @@ extern "C" int plx_msi_tv(const plx_msi *bg, const int64_t *cells, int64_t start
     if (bgb && (!bgb->grad || !bgb->tmask)) return PLX_EINVAL;
     if (count == 0) return PLX_OK;
     MsiDev B{bg->data, bg->radii, (int)bg->L, (int)bg->H, (int)bg->W};
-    int64_t nb = (count * 4 + 255) / 256;
-    if (nb > (int64_t)num_sms_msi() * 16) nb = (int64_t)num_sms_msi() * 16;
+    int64_t nb = (count + 255) / 256;
+    if (nb > (int64_t)num_sms_msi() * 8) nb = (int64_t)num_sms_msi() * 8;
     msi_tv_kernel<<<(unsigned)nb, 256, 0, (cudaStream_t)stream>>>(
         B, cells, start, count, eps, f_sigma, f_rgb, bgb ? bgb->grad : nullptr,
         bgb ? bgb->tmask : nullptr, out_sums);
