@@ -144,8 +144,11 @@ __device__ __forceinline__ void stencil_rows(const DGrid &G, const double *g, in
 // reverse chunks, the suffix sums S_i = sum_{j>i} w_j ReLU(c_j) per chunk by
 // a warp scan plus the carry (K:780-800), the grid scatter with red.v4 and
 // the texel scatter with f64 atomics.
+#ifndef MSI_MINB
+#define MSI_MINB 4
+#endif
 template <bool NEAREST>
-__global__ void __launch_bounds__(kMsiThreads)
+__global__ void __launch_bounds__(kMsiThreads, MSI_MINB)
     msi_render_kernel(DGrid G, MsiDev B, MsiRays R, MsiOpts O, MsiOut out, MsiRec S) {
     __shared__ double xs_t_all[kMsiWarps][kMaxCross];
     __shared__ int xs_l_all[kMsiWarps][kMaxCross];
@@ -595,12 +598,12 @@ extern "C" int plx_msi_render(const plx_grid *g, const plx_msi *bg, const plx_ra
                               plx_msi_grad *bgb, double *out_rgb, double *out_tfg,
                               double *out_trans, double *out_sums, void *scratch,
                               int64_t scratch_bytes, void *stream) {
-    if (!g || !bg || !rays || !o || !out_rgb || !out_tfg || !out_trans || !out_sums || !scratch)
-        return PLX_EINVAL;
+    if (!g || !bg || !rays || !o || !out_sums) return PLX_EINVAL;
+    if (rays->n > 0 && (!out_rgb || !out_tfg || !out_trans || !scratch)) return PLX_EINVAL;
     if (!bg->data || !bg->radii || bg->L < 2 || bg->H < 2 || bg->W < 1 || bg->L - 1 > kMaxCross)
         return PLX_EINVAL;
-    if (!rays->origins || !rays->dirs || !rays->target || rays->n < 0 || o->step <= 0.0)
-        return PLX_EINVAL;
+    if (rays->n < 0 || o->step <= 0.0) return PLX_EINVAL;
+    if (rays->n > 0 && (!rays->origins || !rays->dirs || !rays->target)) return PLX_EINVAL;
     if (gb && (!gb->grad || !gb->tmask || !bgb || !bgb->grad || !bgb->tmask)) return PLX_EINVAL;
     if (rays->n == 0) return PLX_OK;
     const MsiLayout L = msi_layout(g, bg, o, rays->n);

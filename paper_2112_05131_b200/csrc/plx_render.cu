@@ -1190,9 +1190,11 @@ ScratchLayout layout(const plx_grid *g, const plx_render_opts *o, int64_t n_rays
 }
 
 int check_rays(const plx_grid *g, const plx_rays *rays, const plx_render_opts *o, bool views) {
-    if (!grid_ok(g) || !rays || !o || rays->n < 0 || !rays->origins || !rays->dirs) return PLX_EINVAL;
+    if (!grid_ok(g) || !rays || !o || rays->n < 0) return PLX_EINVAL;
     if (rays->n >= (int64_t)1 << 31) return PLX_EINVAL;
-    if (views && !rays->viewdirs) return PLX_EINVAL;
+    // an empty batch is a no-op: its (zero-length) buffers may be null
+    if (rays->n > 0 && (!rays->origins || !rays->dirs || (views && !rays->viewdirs)))
+        return PLX_EINVAL;
     if (!(o->step > 0.0)) return PLX_EINVAL;
     return PLX_OK;
 }
@@ -1220,7 +1222,7 @@ int launch_march(const plx_grid *g, const plx_rays *rays, const plx_render_opts 
 
 extern "C" int plx_render_fwd(const plx_grid *g, const plx_rays *rays, const plx_render_opts *o,
                               double *out_rgb, double *out_trans, double *out_wsum, void *stream) {
-    if (!out_rgb) return PLX_EINVAL;
+    if (!out_rgb && rays && rays->n > 0) return PLX_EINVAL;
     Outs out{};
     out.rgb = out_rgb;
     out.trans = out_trans;
@@ -1251,11 +1253,11 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
                                double lam_cauchy, plx_grad *gb, double *out_rgb,
                                double *out_sums, void *scratch, int64_t scratch_bytes,
                                void *stream, int counters_ready, void *after_march) {
-    if (!gb || !gb->grad || !gb->tmask || !out_sums || !scratch) return PLX_EINVAL;
+    if (!gb || !gb->grad || !gb->tmask || !out_sums) return PLX_EINVAL;
     const int rc = check_rays(g, rays, o, true);
     if (rc != PLX_OK) return rc;
-    if (!rays->target) return PLX_EINVAL;
     if (rays->n == 0) return PLX_OK;
+    if (!rays->target || !scratch) return PLX_EINVAL;
     const ScratchLayout L = layout(g, o, rays->n);
     if (scratch_bytes < L.bytes) return PLX_EINVAL;
     DGrid G = make_dgrid(*g);
