@@ -121,6 +121,24 @@ def main():
         t_step += e[2].elapsed_time(e[3])
     ms_render, ms_step = t_render / args.steps, t_step / args.steps
 
+    # Roofline of the fused render/backward on its compulsory bytes: every
+    # distinct grid row it touches read once (112 B of the 128-B row) and its
+    # gradient row read + written once (the red.add lines), every distinct
+    # background texel the same at 32 B, plus the ray inputs / outputs; the
+    # per-sample record scratch is this design's, not compulsory.
+    grads.clear()
+    bgg.clear()
+    render()
+    torch.cuda.synchronize()
+    rows, texels = grads.n_touched, bgg.n_touched
+    grads.clear()
+    bgg.clear()
+    alg = rows * 3 * 112 + texels * 3 * 32 + n * (9 + 3 + 3 + 2) * 8
+    peaks = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                         "MEASURED_PEAKS.json")
+    peak = json.load(open(peaks))["hbm_gbs"] if os.path.exists(peaks) else 7700.0
+    achieved = alg / (ms_render * 1e-3) / 1e9
+
     # CPU oracle on a bounded sample of the same rays (1 core)
     from oracle import oracle as orc
     og = orc.Grid.dense((D,) * 3, (-1.0,) * 3, (1.0,) * 3, sigma=0.1, rgb=0.1)
@@ -140,6 +158,11 @@ def main():
                    f"{args.width} f64 texels", "rays": n, "steps": args.steps},
         "render_bwd_ms": ms_render, "render_bwd_rays_per_s": n / (ms_render / 1e3),
         "step_ms": ms_step, "step_rays_per_s": n / (ms_step / 1e3), "step_legs_ms": legs,
+        "roofline": {"kernel": "msi_render (fused render/backward)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "algorithmic_bytes": alg,
+                     "touched_rows": rows, "touched_texels": texels,
+                     "model": "rows*3*112 + texels*3*32 + rays*17*8"},
         "step_note": "render+backward, background TV (1% texels), background update + clear, "
                      "grid gradient clear",
         "cpu_oracle": {"rays_per_s": k / cpu_s, "rays": k, "cores": 1,
