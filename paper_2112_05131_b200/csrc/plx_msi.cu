@@ -152,7 +152,16 @@ __global__ void __launch_bounds__(kMsiThreads, MSI_MINB)
     msi_render_kernel(DGrid G, MsiDev B, MsiRays R, MsiOpts O, MsiOut out, MsiRec S) {
     __shared__ double xs_t_all[kMsiWarps][kMaxCross];
     __shared__ int xs_l_all[kMsiWarps][kMaxCross];
+    // backward staging of the foreground scatter: per fg sample (dense slot)
+    // and corner, the row and (w gsig, w gc_r, w gc_g, w gc_b) in f64
+    constexpr int NQS = NEAREST ? 1 : 8;
+    __shared__ int32_t st_row_all[kMsiWarps][32 * NQS];
+    __shared__ double4 st_val_all[kMsiWarps][32 * NQS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t *st_row = st_row_all[warp];
+    double4 *st_val = st_val_all[warp];
+    // this lane's float4 of a 28-float row in the cooperative scatter
+    const int su = lane % 7, spair = lane / 7;
     double *xs_t = xs_t_all[warp];
     int *xs_l = xs_l_all[warp];
     const unsigned lt = (1u << lane) - 1u;
@@ -174,6 +183,20 @@ __global__ void __launch_bounds__(kMsiThreads, MSI_MINB)
         float bf[9];
 #pragma unroll
         for (int b = 0; b < 9; ++b) bf[b] = (float)basis[b];
+        // coefficient e = 4 su + j of the row: 0 sigma, 1-9 R, 10-18 G, 19-27 B
+        double sb[4];
+        int sk[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int e = 4 * su + j;
+            sk[j] = e == 0 ? 0 : 1 + (e - 1) / 9;
+            const int bi = e == 0 ? 0 : (e - 1) % 9;
+            double bv = basis[0];
+#pragma unroll
+            for (int b = 1; b < 9; ++b)
+                if (bi == b) bv = basis[b];
+            sb[j] = bv;
+        }
         double t0a, t1a;
         ray_aabb(rm.o, rm.d, G.lo, G.hi, t0a, t1a);
         ray_march_setup(rm, G, O.step, 0.0);
@@ -349,64 +372,78 @@ __global__ void __launch_bounds__(kMsiThreads, MSI_MINB)
             sf0 += tot0;
             sf1 += tot1;
             sf2 += tot2;
-            if (!valid) continue;
-            const double att = exp(-sig * dlt);
-            double gsig = dlt * (up0 * (Ti * att * cc0 - s0) + up1 * (Ti * att * cc1 - s1) +
-                                 up2 * (Ti * att * cc2 - s2));
-            if (lay < 0) {
-                if (O.lam_cauchy > 0.0) {
-                    cau_part += log(1.0 + 2.0 * sig * sig);
-                    gsig += O.lam_cauchy * 4.0 * sig / (1.0 + 2.0 * sig * sig);
-                }
-                if (bup != 0.0) gsig += bup * (-dlt * tfg);
-                const double gc0 = c.x > 0.0 ? up0 * w : 0.0, gc1 = c.y > 0.0 ? up1 * w : 0.0,
-                             gc2 = c.z > 0.0 ? up2 * w : 0.0;
-                double g[3], f[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-                for (int a = 0; a < 3; ++a)
-                    g[a] = clamp_coord(rm.o[a] + t * rm.d[a], G.lo[a], G.scale[a], G.dmax[a]);
-                int32_t rows[8];
-                stencil_rows<NEAREST>(G, g, rows, f);
-                constexpr int NQ = NEAREST ? 1 : 8;
-#pragma unroll 1
-                for (int q = 0; q < NQ; ++q) {
-                    const int32_t r = rows[q];
-                    if (r < 0) continue;
-                    const double wq = stencil_w<NEAREST>(f, q);
-                    out.tmask[r] = 1;
-                    float v[28];
-                    v[0] = (float)(wq * gsig);
-#pragma unroll
-                    for (int b = 0; b < 9; ++b) {
-                        v[1 + b] = gc0 != 0.0 ? (float)(wq * gc0 * basis[b]) : 0.f;
-                        v[10 + b] = gc1 != 0.0 ? (float)(wq * gc1 * basis[b]) : 0.f;
-                        v[19 + b] = gc2 != 0.0 ? (float)(wq * gc2 * basis[b]) : 0.f;
+            const bool fg = valid && lay < 0;
+            const unsigned fgm = __ballot_sync(PLX_FULL_MASK, fg);
+            if (valid) {
+                const double att = exp(-sig * dlt);
+                double gsig = dlt * (up0 * (Ti * att * cc0 - s0) + up1 * (Ti * att * cc1 - s1) +
+                                     up2 * (Ti * att * cc2 - s2));
+                if (fg) {
+                    if (O.lam_cauchy > 0.0) {
+                        cau_part += log(1.0 + 2.0 * sig * sig);
+                        gsig += O.lam_cauchy * 4.0 * sig / (1.0 + 2.0 * sig * sig);
                     }
-                    float *row = out.grad + (int64_t)r * PLX_STRIDE;
+                    if (bup != 0.0) gsig += bup * (-dlt * tfg);
+                    const double gc0 = c.x > 0.0 ? up0 * w : 0.0,
+                                 gc1 = c.y > 0.0 ? up1 * w : 0.0,
+                                 gc2 = c.z > 0.0 ? up2 * w : 0.0;
+                    double g[3], f[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-                    for (int u = 0; u < 7; ++u)
-                        if (v[4 * u] != 0.f || v[4 * u + 1] != 0.f || v[4 * u + 2] != 0.f ||
-                            v[4 * u + 3] != 0.f)
-                            red_add_v4(row + 4 * u, v[4 * u], v[4 * u + 1], v[4 * u + 2],
-                                       v[4 * u + 3]);
-                }
-            } else {
-                int idx4[4];
-                double w4[4];
-                bg_stencil(B.H, B.W, rm.o[0] + t * rm.d[0], rm.o[1] + t * rm.d[1],
-                           rm.o[2] + t * rm.d[2], idx4, w4);
+                    for (int a = 0; a < 3; ++a)
+                        g[a] = clamp_coord(rm.o[a] + t * rm.d[a], G.lo[a], G.scale[a],
+                                           G.dmax[a]);
+                    int32_t rows[8];
+                    stencil_rows<NEAREST>(G, g, rows, f);
+                    const int slot = __popc(fgm & lt) * NQS;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int64_t flat = (int64_t)lay * B.H * B.W + idx4[q];
-                    const double wq = w4[q];
-                    out.bg_tmask[flat] = 1;
-                    double *gb = out.bg_grad + 4 * flat;
-                    atomicAdd(gb, wq * gsig);
-                    if (c.x > 0.0) atomicAdd(gb + 1, wq * up0 * w);
-                    if (c.y > 0.0) atomicAdd(gb + 2, wq * up1 * w);
-                    if (c.z > 0.0) atomicAdd(gb + 3, wq * up2 * w);
+                    for (int q = 0; q < NQS; ++q) {
+                        const int32_t r = rows[q];
+                        st_row[slot + q] = r;
+                        if (r < 0) continue;
+                        const double wq = stencil_w<NEAREST>(f, q);
+                        out.tmask[r] = 1;
+                        st_val[slot + q] = make_double4(wq * gsig, wq * gc0, wq * gc1, wq * gc2);
+                    }
+                } else {
+                    int idx4[4];
+                    double w4[4];
+                    bg_stencil(B.H, B.W, rm.o[0] + t * rm.d[0], rm.o[1] + t * rm.d[1],
+                               rm.o[2] + t * rm.d[2], idx4, w4);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int64_t flat = (int64_t)lay * B.H * B.W + idx4[q];
+                        const double wq = w4[q];
+                        out.bg_tmask[flat] = 1;
+                        double *gb = out.bg_grad + 4 * flat;
+                        atomicAdd(gb, wq * gsig);
+                        if (c.x > 0.0) atomicAdd(gb + 1, wq * up0 * w);
+                        if (c.y > 0.0) atomicAdd(gb + 2, wq * up1 * w);
+                        if (c.z > 0.0) atomicAdd(gb + 3, wq * up2 * w);
+                    }
                 }
             }
+            __syncwarp();
+            // warp-cooperative scatter: 4 (sample, corner) rows per pass, lane
+            // = one float4 of a row, so each red.v4 instruction covers whole
+            // 112-B rows instead of 32 scattered 16-B pieces
+            const int npairs = __popc(fgm) * NQS;
+            if (lane < 28) {
+                for (int pidx = spair; pidx < npairs; pidx += 4) {
+                    const int32_t r = st_row[pidx];
+                    if (r < 0) continue;
+                    const double4 sv = st_val[pidx];
+                    float v[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const double a = sk[j] == 0 ? sv.x : sk[j] == 1 ? sv.y : sk[j] == 2 ? sv.z : sv.w;
+                        v[j] = sk[j] == 0 ? (float)a : (float)(a * sb[j]);
+                    }
+                    if (v[0] != 0.f || v[1] != 0.f || v[2] != 0.f || v[3] != 0.f)
+                        red_add_v4(out.grad + (int64_t)r * PLX_STRIDE + 4 * su, v[0], v[1], v[2],
+                                   v[3]);
+                }
+            }
+            __syncwarp();
         }
     }
     mse_part = warp_sum(mse_part);

@@ -79,6 +79,13 @@ def main():
                                     tfg.data_ptr(), trans.data_ptr(), sums.data_ptr(),
                                     scratch.data_ptr(), need, stream), "msi_render")
 
+    def render_fwd():
+        _lib.check(L.plx_msi_render(ctypes.byref(cg), ctypes.byref(cb), ctypes.byref(r),
+                                    ctypes.byref(ko), 1, 2.0 / n, 1e-11, 1e-5, 1e-6,
+                                    None, None, rgb.data_ptr(), tfg.data_ptr(),
+                                    trans.data_ptr(), sums.data_ptr(), scratch.data_ptr(),
+                                    need, stream), "msi_render_fwd")
+
     legs = {"render_bwd": 0.0, "bg_tv": 0.0, "bg_update": 0.0, "grid_clear": 0.0}
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
 
@@ -120,6 +127,14 @@ def main():
         torch.cuda.synchronize()
         t_step += e[2].elapsed_time(e[3])
     ms_render, ms_step = t_render / args.steps, t_step / args.steps
+    t_fwd = 0.0
+    for _ in range(args.steps):
+        e[0].record()
+        render_fwd()
+        e[1].record()
+        torch.cuda.synchronize()
+        t_fwd += e[0].elapsed_time(e[1])
+    ms_fwd = t_fwd / args.steps
 
     # Roofline of the fused render/backward on its compulsory bytes: every
     # distinct grid row it touches read once (112 B of the 128-B row) and its
@@ -156,7 +171,7 @@ def main():
         "metric": "360 train rays/sec (grid + MSI background fused render/backward)",
         "config": {"grid": f"{D}^3 dense", "background": f"{args.layers}x{args.height}x"
                    f"{args.width} f64 texels", "rays": n, "steps": args.steps},
-        "render_bwd_ms": ms_render, "render_bwd_rays_per_s": n / (ms_render / 1e3),
+        "render_bwd_ms": ms_render, "render_fwd_only_ms": ms_fwd, "render_bwd_rays_per_s": n / (ms_render / 1e3),
         "step_ms": ms_step, "step_rays_per_s": n / (ms_step / 1e3), "step_legs_ms": legs,
         "roofline": {"kernel": "msi_render (fused render/backward)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
