@@ -224,6 +224,7 @@ def load_checkpoint(path, device="cuda"):
     v, step, beta, eps, bg_v = read_state_full(str(path) + ".state")
     state = OptimState(grid.n_rows, beta=beta, eps=eps, device=device)
     state.v[:, :v.shape[1]].copy_(torch.from_numpy(v))
+    state.step_count = step
     bg_state = None
     if bg_v is not None and background is not None:
         from .msi import BgOptimState

@@ -76,6 +76,23 @@ def owner_slice(rows: int, rank: int, size: int) -> tuple[int, int]:
     return s0 * 128, min(s1 * 128, int(rows))
 
 
+def gather_owned_rows(world: World, v: torch.Tensor) -> torch.Tensor:
+    """p2p mode keeps each row's RMSProp state current only on the row's
+    owner (owner_slice): a copy of `v` whose every owner slice comes from
+    its owner rank (checkpoints, T:435-439 / T:501-510)."""
+    out = v.clone()
+    if not world.active:
+        return out
+    for r in range(world.size):
+        lo, hi = owner_slice(v.shape[0], r, world.size)
+        if hi <= lo:
+            continue
+        part = out[lo:hi].contiguous()
+        dist.broadcast(part, src=r, group=world.group)
+        out[lo:hi] = part
+    return out
+
+
 def reduce_gradients(world: World, grad: torch.Tensor, tmask: torch.Tensor,
                      sums: torch.Tensor | None = None) -> None:
     """Mode "dense": grad <- sum over ranks, tmask <- max (logical OR),

@@ -255,6 +255,9 @@ class EpochBatcher:
                 self.perm = self.rng.permutation(self.n)
                 self._perm_dev = None
                 self.cursor = 0
+                # the old epoch's tail is a view of the permutation buffer the
+                # new epoch's permutation is about to be copied into
+                chunks = [c.clone() for c in chunks]
             take = min(need, self.n - self.cursor)
             chunks.append(self._dev_perm()[self.cursor:self.cursor + take])
             offs.append(self.cursor)
@@ -436,8 +439,28 @@ class Trainer:
         self.grads = GradientBuffer(self.grid.n_rows, device=self.device)
         self._refresh_cache()
         if out_dir is not None:
-            artifact_io.save_checkpoint(Path(out_dir) / f"checkpoint_{step:07d}.plnx",
-                                        self.grid, self.state, step, self.background,
+            self.save_checkpoint(Path(out_dir) / f"checkpoint_{step:07d}.plnx", step)
+
+    def full_state(self) -> optim.OptimState:
+        """The RMSProp state of every row.  In p2p mode each rank updates
+        only the rows it owns (dist.owner_slice), so the other ranks' slices
+        of `v` are gathered from their owners."""
+        w = self.world
+        if not (w.active and w.mode == "p2p"):
+            return self.state
+        from .dist import gather_owned_rows
+        v = gather_owned_rows(w, self.state.v)
+        st = optim.OptimState.__new__(optim.OptimState)
+        st.__dict__.update(self.state.__dict__)
+        st.v = v
+        return st
+
+    def save_checkpoint(self, path, step: int) -> None:
+        """artifact_io.save_checkpoint of the whole run (rank 0 writes; the
+        p2p state slices are gathered on every rank first)."""
+        st = self.full_state()
+        if self.world.rank == 0:
+            artifact_io.save_checkpoint(path, self.grid, st, step, self.background,
                                         self.bg_state)
 
     def max_weights(self) -> torch.Tensor:
@@ -529,6 +552,12 @@ class Trainer:
         a = self._step_args
         tv_on = (cfg.lambda_tv_sigma > 0 or cfg.lambda_tv_sh > 0) and (
             cfg.tv_until_step < 0 or step < cfg.tv_until_step)
+        jt = None
+        if self.opts.jitter > 0:
+            # R:106-111 draws the jitter inside fused_mse_backward (T:453-457),
+            # before sample_tv_cells (T:463)
+            jt = torch.from_numpy(self.rng.random(n_global if pool_mode else B)
+                                  * self.opts.jitter).to(self.device)
         n_tv = 0
         tv_start = 0
         if tv_on:
@@ -560,9 +589,7 @@ class Trainer:
                 a.rays = self._rays_desc(self._rays_slot)
             a.rays.n = c0
             a.rays.jitter = None
-            if self.opts.jitter > 0:
-                jt = torch.from_numpy(self.rng.random(n_global if pool_mode else B)
-                                      * self.opts.jitter).to(self.device)
+            if jt is not None:
                 self._jt_keep = jt
                 a.rays.jitter = jt.data_ptr() + 8 * s0
             a.up_scale = 2.0 / n_global
@@ -823,6 +850,17 @@ def evaluate(grid: SparseGrid, dataset, opts: render.RenderOptions, chunk: int =
             rows)
 
 
+def _checked(tr: Trainer, out_dir) -> None:
+    """Check every step still unchecked (the host runs two steps ahead of
+    the device's loss sums) before the grid is used outside the step loop."""
+    try:
+        tr.check_pending()
+    except TrainingDiverged:
+        if out_dir is not None and tr.world.rank == 0:
+            artifact_io.save_grid(tr.grid, Path(out_dir) / "diverged.plnx", tr.background)
+        raise
+
+
 def train(train_ds, config: TrainConfig, test_ds=None, out_dir=None, metrics_sink=None,
           device=None, world: World | None = None) -> TrainResult:
     """T:350-518 on the device (bounded, forward-facing and 360 scenes)."""
@@ -842,6 +880,7 @@ def train(train_ds, config: TrainConfig, test_ds=None, out_dir=None, metrics_sin
     last_eval = -1
     for step in range(cfg.total_steps):
         if step in tr.rung_events:
+            _checked(tr, out_dir)     # the reference raises before any rung event
             tr.rung_event(tr.rung_events[step], out_dir, step)
         log_now = cfg.log_every > 0 and step % cfg.log_every == 0
         try:
@@ -849,26 +888,26 @@ def train(train_ds, config: TrainConfig, test_ds=None, out_dir=None, metrics_sin
             if step == cfg.total_steps - 1:
                 tr.check_pending()
         except TrainingDiverged:
-            if out_dir is not None:   # the device guard kept the pre-update grid
+            if out_dir is not None and tr.world.rank == 0:   # the device guard kept the pre-update grid
                 artifact_io.save_grid(tr.grid, out_dir / "diverged.plnx", tr.background)
             raise
         if log_now:
             emit({"step": step, "loss": rec["loss"], "mse": rec["mse"],
                   "nnz_fraction": tr.nnz_fraction()})
         if test_ds is not None and cfg.eval_every > 0 and (step + 1) % cfg.eval_every == 0:
+            _checked(tr, out_dir)
             p, s, _ = tr.evaluate(test_ds)
             last_eval = step + 1
             emit({"step": step + 1, "psnr": p, "ssim": s,
                   "wall_time_s": time.perf_counter() - t_start})
         if cfg.checkpoint_every > 0 and out_dir is not None and (step + 1) % cfg.checkpoint_every == 0:
-            artifact_io.save_checkpoint(out_dir / f"checkpoint_{step + 1:07d}.plnx", tr.grid,
-                                        tr.state, step + 1, tr.background, tr.bg_state)
+            _checked(tr, out_dir)
+            tr.save_checkpoint(out_dir / f"checkpoint_{step + 1:07d}.plnx", step + 1)
     if test_ds is not None and last_eval != cfg.total_steps:
         p, s, _ = tr.evaluate(test_ds)
         emit({"step": cfg.total_steps, "psnr": p, "ssim": s,
               "wall_time_s": time.perf_counter() - t_start})
     if out_dir is not None:
-        artifact_io.save_checkpoint(out_dir / "final.plnx", tr.grid, tr.state, cfg.total_steps,
-                                    tr.background, tr.bg_state)
+        tr.save_checkpoint(out_dir / "final.plnx", cfg.total_steps)
     return TrainResult(grid=tr.grid, metrics=metrics, config=cfg, background=tr.background,
                        scene_scale=tr.scene_scale)

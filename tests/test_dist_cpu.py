@@ -102,3 +102,39 @@ def test_owner_slices_tile_the_rows():
             assert spans[0][0] == 0 and spans[-1][1] == rows
             for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
                 assert a1 == b0 and a0 % 128 == 0
+
+
+def _gather_worker(rank, size, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    from paper_2112_05131_b200.dist import World, gather_owned_rows, owner_slice
+
+    rows = 1000
+    v = torch.full((rows, 32), -1.0)          # stale everywhere ...
+    lo, hi = owner_slice(rows, rank, size)
+    v[lo:hi] = torch.arange(lo, hi, dtype=torch.float32)[:, None] + 0.5   # ... but the owned slice
+    full = gather_owned_rows(World(rank, size, mode="p2p"), v)
+    out.put((rank, full.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_p2p_checkpoint_state_gathers_owner_slices():
+    """in p2p mode only a row's owner holds its current RMSProp
+    state; a checkpoint must gather every owner's slice (identical on all
+    ranks)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + (os.getpid() + 7) % 1000
+    size = 3
+    ps = [ctx.Process(target=_gather_worker, args=(r, size, port, q)) for r in range(size)]
+    for p in ps:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(size))
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    want = np.broadcast_to(np.arange(1000, dtype=np.float32)[:, None] + 0.5, (1000, 32))
+    for r in range(size):
+        np.testing.assert_array_equal(got[r], want)
