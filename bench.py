@@ -52,7 +52,10 @@ def parse():
     p.add_argument("--views", type=int, default=100)
     p.add_argument("--res", type=int, default=200)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--cpu-budget", type=float, default=30.0,
+                   help="seconds of timed oracle steps in the CPU legs (after the warm-up)")
+    p.add_argument("--dry-run", action="store_true",
+                   help="launcher / collective check only: no kernels (runs on CPU, gloo)")
     p.add_argument("--steady-step", type=int, default=2000,
                    help="also time K steps after training to this step (0 = off)")
     return p.parse_args()
@@ -130,6 +133,19 @@ def toy_scene(n_views, res, device):
     return train
 
 
+# The C2 step's hyperparameters: default_config("bounded") (T:102-154) with a
+# 256^3 rung; shared by both arms (tests/test_bench_cpu.py checks them against
+# trainer.default_config).
+C2 = dict(aabb=(-1.5, -1.5, -1.5, 1.5, 1.5, 1.5), init_sigma=0.1, init_rgb=0.1, step_frac=0.5,
+          stop_thresh=1e-4, background=(1.0, 1.0, 1.0), lambda_tv_sigma=1e-5,
+          lambda_tv_sh=1e-3, tv_sample_frac=0.01, tv_until_step=38400, rms_beta=0.95,
+          rms_eps=1e-8, seed=0,
+          lr_sigma=("delayed_exponential", 30.0, 0.05, 250000, 15000, 0.01),
+          lr_sh=("exponential", 0.01, 5e-6, 250000, 0, 0.01))
+DTYPE = ("f32 grid storage; f64 march/sigma/compositing/update arithmetic; "
+         "f32 colour FMAs and f32 gradient reductions")
+
+
 def bench_config(args):
     from paper_2112_05131_b200 import trainer
 
@@ -141,84 +157,129 @@ def bench_config(args):
     return cfg
 
 
-# ------------------------------------------------------------ CPU oracle --
-def oracle_steps(args, n_steps, ds, time_budget_s=None, warmup=1):
-    """The reference's step body (T:455-486: fused_mse_backward + tv_loss +
-    optim.step + grads.clear) through the f64 C port, on one host core.
-    Returns (rays_per_s, steps_timed, sample description)."""
-    from oracle import oracle as orc
-    from paper_2112_05131_b200 import optim as popt
-    from paper_2112_05131_b200.camera import all_rays
+def workload_config(args, n_gpus):
+    """The `config` object of BOTH arms' lines (the workload, nothing measured)."""
+    R = args.dims ** 3
+    return {"workload": WORKLOAD, "grid": f"{args.dims}^3 dense init",
+            "rays_per_gpu": args.batch, "global_batch": args.batch * n_gpus,
+            "views": args.views, "res": args.res, "ray_pool": args.views * args.res ** 2,
+            "batcher": "EpochBatcher (T:233-255), trainer rng seed 0",
+            "timed_steps": f"{args.warmup}..{args.warmup + args.steps - 1} from the dense init",
+            "parallelism": f"dp{n_gpus}",
+            "l2": "inputs_larger_than_l2 (sh+density+grad+v = %.2f GB)" % (R * (3 * 112 + 4) / 1e9)}
 
-    o, m, v, gt = all_rays(ds.images, ds.cameras)
-    cfg = bench_config(args)
-    B = args.batch
-    lo, hi = np.array(cfg.aabb[:3]), np.array(cfg.aabb[3:])
-    g = orc.Grid.dense((args.dims,) * 3, lo, hi, sigma=cfg.init_sigma, rgb=cfg.init_rgb)
+
+def host_info():
+    """nproc and the CPU model of this host."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+# ------------------------------------------------------------ CPU oracle --
+def oracle_train(args, rays_for, n_pool, B, warmup, steps, budget_s):
+    """The reference's step body (T:441-492: EpochBatcher draw, fused_mse_
+    backward + tv_loss + optim.step + grads.clear) through the f64 C port on
+    one host core, from the dense init: `warmup` untimed steps, then up to
+    `steps` timed ones (stopping after budget_s of timed work, >= 3 steps).
+    rays_for(idx) -> (o, m, v, gt) of pool rows idx.  Returns (rays/s, steps
+    timed, sample description)."""
+    from oracle import oracle as orc
+
+    c = C2
+    lo, hi = np.array(c["aabb"][:3]), np.array(c["aabb"][3:])
+    g = orc.Grid.dense((args.dims,) * 3, lo, hi, sigma=c["init_sigma"], rgb=c["init_rgb"])
     v_state = np.zeros_like(g.table)
     buf = orc.GradBuf(g.n_rows)
-    rng = np.random.default_rng(cfg.seed)
-    perm = rng.permutation(o.shape[0])
+    rng = np.random.default_rng(c["seed"])
+    batcher = orc.EpochBatcher(n_pool, B, rng)
+    ks, kh = c["lr_sigma"], c["lr_sh"]
     times = []
-    t_start = time.perf_counter()
-    for step in range(n_steps + warmup):
-        idx = perm[(step * B) % len(perm):][:B]
+    for step in range(warmup + steps):
+        idx = batcher.next()
+        o, m, v, gt = rays_for(idx)
         t0 = time.perf_counter()
-        orc.fused_mse_backward(g, o[idx], m[idx], v[idx], gt[idx], buf, B,
-                               step_frac=cfg.step_frac, stop_thresh=cfg.stop_thresh,
-                               background=cfg.background)
-        cells = orc.sample_tv_cells(g.dims, cfg.tv_sample_frac, rng)
-        orc.tv_loss(g, cells, cfg.lambda_tv_sigma, cfg.lambda_tv_sh, buf)
-        orc.opt_step(g, buf, v_state, popt.lr_at(cfg.lr_sigma, step), popt.lr_at(cfg.lr_sh, step))
+        orc.fused_mse_backward(g, o, m, v, gt, buf, B, step_frac=c["step_frac"],
+                               stop_thresh=c["stop_thresh"], background=c["background"])
+        if step < c["tv_until_step"]:
+            cells = orc.sample_tv_cells(g.dims, c["tv_sample_frac"], rng)
+            orc.tv_loss(g, cells, c["lambda_tv_sigma"], c["lambda_tv_sh"], buf)
+        orc.opt_step(g, buf, v_state, orc.lr_at(ks[0], *ks[1:4], step, ks[4], ks[5]),
+                     orc.lr_at(kh[0], *kh[1:4], step, kh[4], kh[5]),
+                     beta=c["rms_beta"], eps=c["rms_eps"])
         buf.clear()
         dt = time.perf_counter() - t0
-        if step >= warmup:   # discard the warm-up steps (first-touch page faults)
+        if step >= warmup:
             times.append(dt)
-        if time_budget_s and time.perf_counter() - t_start > time_budget_s and times:
-            break
-    sample = (f"{len(times)} timed step(s) of {B} rays (+{warmup} discarded), dense {args.dims}^3 f64 "
-              f"grid, TV 1% cells, RMSProp; sequential C port of K:173-600, 1 thread")
+            if sum(times) > budget_s and len(times) >= 3:
+                break
+    sample = (f"steps {warmup}..{warmup + len(times) - 1} timed ({warmup} untimed from the "
+              f"dense init) of {B} rays, same pool and EpochBatcher draws, dense {args.dims}^3 "
+              f"f64 grid, TV 1% cells, RMSProp; sequential C port of K:173-600, 1 thread")
     return B / float(np.mean(times)), len(times), sample
 
 
-def oracle_scene(n_views, res):
-    """Scene for a box without a GPU (not used on the B200 box)."""
+def oracle_pool(args):
+    """The C2 ray pool for the reference arm without a GPU: the same toy scene
+    and hemisphere cameras as scenes.make_toy_dataset (toy.py:129-162), with
+    rays generated by the C restatement of camera.py:91-100 and the ground
+    truth rendered by the oracle (and 8-bit quantised like the PNG round
+    trip) only for the rows a batch draws."""
+    import math
+
     from oracle import oracle as orc
     from paper_2112_05131_b200 import scenes
-    from paper_2112_05131_b200.camera import generate_rays
 
     table, shape = scenes.toy_grid_arrays(64)
+    table = table.astype(np.float32).astype(np.float64)   # the device scene's f32 table
     g = orc.Grid(np.arange(table.shape[0], dtype=np.int32).reshape(shape), table,
-                 (-1.1,) * 3, (1.1,) * 3)
+                 (-scenes.TOY_AABB,) * 3, (scenes.TOY_AABB,) * 3)
     g, _ = orc.prune(g, "density", 1e-6)
-    cams, _ = scenes.hemisphere_cameras(n_views, res, phase=1.0)
-    imgs = []
-    for cam in cams:
-        o, d = generate_rays(cam)
+    phase = float(np.random.default_rng(0).uniform(0, 2 * math.pi))
+    cams, _ = scenes.hemisphere_cameras(args.views, args.res, phase=phase)
+    ppv = args.res * args.res
+
+    def rays_for(idx):
+        idx = np.asarray(idx)
+        o, d = np.empty((len(idx), 3)), np.empty((len(idx), 3))
+        views = idx // ppv
+        for vi in np.unique(views):
+            sel = np.nonzero(views == vi)[0]
+            c = cams[int(vi)]
+            o[sel], d[sel] = orc.generate_rays(c.c2w, c.focal, c.width, c.height, idx[sel] % ppv)
         rgb, _, _ = orc.render_rays(g, o, d)
-        imgs.append((np.rint(np.clip(rgb, 0, 1) * 255) / 255.0).astype(np.float32)
-                    .reshape(res, res, 3))
-    return scenes.Dataset(np.stack(imgs), cams)
+        gt = (np.rint(np.clip(rgb, 0.0, 1.0) * 255.0) / 255.0).astype(np.float32)
+        return o, d, d, gt.astype(np.float64)
+
+    return rays_for, len(cams) * ppv
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    budget = 150.0
-    # the scene is rendered by the oracle itself: nothing of ours on this arm
-    n_views = max(1, min(args.views, -(-(args.steps + 1) * args.batch // (args.res ** 2))))
-    ds = oracle_scene(n_views, args.res)
-    warm = max(1, args.warmup)
-    rps, k, sample = oracle_steps(args, max(1, args.steps), ds, time_budget_s=budget, warmup=warm)
+    n_gpus = args.gpus
+    B = args.batch * n_gpus
+    rays_for, n_pool = oracle_pool(args)
+    budget = 120.0
+    rps, k, sample = oracle_train(args, rays_for, n_pool, B, args.warmup, max(1, args.steps),
+                                  budget)
     line = {"impl": "reference", "metric": METRIC, "value": rps, "unit": "rays/s",
-            "n_gpus": args.gpus, "steps": k, "warmup": warm,
-            "ms_per_step": 1000.0 * args.batch / rps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "grid": f"{args.dims}^3",
-                                            "rays_per_step": args.batch},
+            "n_gpus": n_gpus, "steps": k, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * B / rps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 (the reference's numba kernels, restated in C)",
+            "data": "synthetic (reference toy scene; rays and ground truth generated on the host)",
+            "config": workload_config(args, n_gpus),
             "cpu_baseline": {"value": rps, "unit": "rays/s", "cores": 1, "kind": "port",
-                             "sample": sample},
+                             "sample": sample, "host": host_info()},
             "e2e": {"value": rps, "unit": "rays/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -240,7 +301,9 @@ def run_ours(args):
     from paper_2112_05131_b200.dist import World, shard_range
 
     world = World(rank, world_size) if world_size > 1 else World()
-    assert args.gpus == world_size, "--gpus must match the launched world size"
+    if world_size > 1 and rank == 0:
+        print(f"bench: {world_size} ranks, NCCL {'.'.join(map(str, torch.cuda.nccl.version()))}, "
+              f"exchange mode {world.mode}", file=sys.stderr, flush=True)
 
     ds = toy_scene(args.views, args.res, dev)
     cfg = bench_config(args)
@@ -425,31 +488,41 @@ def run_ours(args):
         except Exception:
             traffic = None
     step_bytes = 60 * args.batch + 8 * n_tv + U * (4 + 112 + 224 + 672)
+    # our kernels per timed step: prologue, march_bwd, colour, scatter, TV,
+    # touched compaction, update (1 GPU, one graph replay); N ranks: the
+    # exchange replaces compaction + update (p2p: owner update + clear)
+    launches = (6 + (1 if n_tv else 0)) * args.steps
 
     cpu = None
     if rank == 0 and world_size == 1 and not args.no_cpu_baseline:
-        rps, k, sample = oracle_steps(args, args.cpu_steps, ds)
-        cpu = {"value": rps, "unit": "rays/s", "cores": 1, "kind": "port", "sample": sample}
+        # the same pool, batcher draws and step window as `value`, on one core
+        def rays_for(ix):
+            return o[ix], m[ix], v[ix], gt[ix]
+
+        rps, k, sample = oracle_train(args, rays_for, o.shape[0], args.batch, args.warmup,
+                                      args.steps, args.cpu_budget)
+        cpu = {"value": rps, "unit": "rays/s", "cores": 1, "kind": "port", "sample": sample,
+               "host": host_info()}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world_size,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPE,
             "data": "synthetic (reference toy scene rendered on device, 8-bit)",
-            "config": {"workload": WORKLOAD, "grid": f"{args.dims}^3 dense init",
-                       "rays_per_gpu": args.batch, "global_batch": args.batch * world_size,
-                       "views": args.views, "res": args.res, "parallelism": f"dp{world_size}" + (f"-{world.mode}" if world_size > 1 else ""),
-                       "l2": "inputs_larger_than_l2 (sh+density+grad+v = %.2f GB)" % (R * (3 * 112 + 4) / 1e9),
-                       "touched_rows_U": U, "touched_rows_render": U_render, "tv_cells": n_tv,
-                       "march_positions_per_step": float(march[0]),
-                       "samples_per_step": float(march[1]),
-                       "chunks_per_step": float(march[2]),
-                       "step_bytes_model": step_bytes,
-                       "steady_state": steady,
-                       "step_hbm_frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
-                       "kernel_ms": avg,
-                       "kernel_ms_note": "the timed steps replay one CUDA graph each; kernel_ms re-runs the same K steps from a snapshot with eager launches"},
+            "config": workload_config(args, world_size),
+            "stats": {"dp_mode": world.mode if world_size > 1 else None,
+                      "touched_rows_U": U, "touched_rows_render": U_render, "tv_cells": n_tv,
+                      "march_positions_per_step": float(march[0]),
+                      "samples_per_step": float(march[1]),
+                      "chunks_per_step": float(march[2]),
+                      "step_bytes_model": step_bytes,
+                      "step_hbm_frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
+                      "steady_state": steady,
+                      "kernel_ms": avg,
+                      "kernel_ms_note": "the timed steps replay one CUDA graph each; kernel_ms "
+                                        "re-runs the same K steps from a snapshot with eager "
+                                        "launches"},
             "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
@@ -459,17 +532,73 @@ def run_ours(args):
             "clocks": clk,
             # per step: march_bwd, colour, scatter (render backward), TV,
             # touched-set compaction, update (one graph replay launches all 6)
-            "gpu_launches": (5 + (1 if n_tv else 0)) * args.steps,
+            "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
     if world_size > 1:
         dist.destroy_process_group()
 
 
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(args) -> int:
+    """`python bench.py --gpus N` without torchrun: re-launch this script as N
+    ranks exactly the way the driver does (torch.distributed.run, one process
+    per GPU, rendezvous on 127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_dry(args):
+    """The launcher / timing-collective path without kernels: every rank
+    joins the process group (NCCL with GPUs, else gloo), times a barrier,
+    takes the max over ranks, and rank 0 prints a JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    world_size = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world_size > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    t0 = time.perf_counter()
+    if world_size > 1:
+        dist.barrier()
+    ms = torch.tensor([1000.0 * (time.perf_counter() - t0)], dtype=torch.float64)
+    if world_size > 1:
+        if torch.cuda.is_available():
+            ms = ms.cuda(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world_size,
+                          "ranks_joined": world_size, "barrier_ms_max": float(ms.item()),
+                          "config": workload_config(args, world_size)}), flush=True)
+    if world_size > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    launched = "WORLD_SIZE" in os.environ
     if args.impl == "reference":
-        run_reference(args)
+        run_reference(args)      # rank 0 only; no ranks need launching
+        return
+    if args.gpus > 1 and not launched:
+        sys.exit(launch_ranks(args))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={ws}; using the launched world size",
+              file=sys.stderr, flush=True)
+        args.gpus = ws
+    if args.dry_run:
+        run_dry(args)
         return
     run_ours(args)
 

@@ -398,3 +398,67 @@ def step_table(table, grad, touched_ids, n_touched, v, lr_first, lr_rest,
     lib().oracle_opt_step(_p(table), _p(v), _p(grad), _p(np.ascontiguousarray(touched_ids)),
                           _i(n_touched), _i(ncol), _d(lr_first), _d(lr_rest), _d(beta),
                           _d(eps), ctypes.c_int(method == "rmsprop"))
+
+
+# ---------------------------------------------------------------- cameras --
+def camera_array(c2w, focal, width, height):
+    """{c2w[:3, :4] row-major, focal, width, height} as the C restatement's
+    float64[15] camera record."""
+    c = np.zeros(15)
+    c[:12] = np.asarray(c2w, dtype=np.float64)[:3, :4].reshape(-1)
+    c[12:] = (float(focal), float(width), float(height))
+    return c
+
+
+def generate_rays(c2w, focal, width, height, pixels=None):
+    """camera.py:91-100 (all pixels, row-major, or the given pixel ids)."""
+    cam = camera_array(c2w, focal, width, height)
+    pix = None if pixels is None else np.ascontiguousarray(pixels, dtype=np.int64)
+    n = int(width) * int(height) if pix is None else len(pix)
+    o, d = np.empty((n, 3)), np.empty((n, 3))
+    lib().oracle_generate_rays(_p(cam), None if pix is None else _p(pix), _i(n), _p(o), _p(d))
+    return o, d
+
+
+def to_ndc(origins, dirs, focal, width, height, near=0.0):
+    """camera.py:103-134 -> (o_ndc, d_ndc, valid)."""
+    o, d = _f64(np.atleast_2d(origins)).copy(), _f64(np.atleast_2d(dirs)).copy()
+    valid = np.zeros(len(o), dtype=np.uint8)
+    lib().oracle_to_ndc(_p(o), _p(d), _i(len(o)), _d(focal), _d(width), _d(height), _d(near),
+                        _p(valid))
+    return o, d, valid.astype(bool)
+
+
+# ------------------------------------------------- trainer host logic --
+class EpochBatcher:
+    """trainer.py:233-255: without-replacement batches, one rng.permutation
+    per epoch from the trainer's rng."""
+
+    def __init__(self, n, batch_size, rng):
+        self.n, self.batch_size, self.rng = n, batch_size, rng
+        self.perm = rng.permutation(n)
+        self.cursor = 0
+
+    def next(self):
+        chunks, need = [], self.batch_size
+        while need > 0:
+            if self.cursor >= self.n:
+                self.perm = self.rng.permutation(self.n)
+                self.cursor = 0
+            take = min(need, self.n - self.cursor)
+            chunks.append(self.perm[self.cursor:self.cursor + take])
+            self.cursor += take
+            need -= take
+        return np.concatenate(chunks) if len(chunks) > 1 else chunks[0]
+
+
+def lr_at(kind, lr_init, lr_final, total_steps, step, delay_steps=0, delay_mult=0.01):
+    """optim.py:42-55 (same op order)."""
+    if kind == "constant":
+        return lr_init
+    t = min(max(step / total_steps, 0.0), 1.0)
+    lr = lr_init * (lr_final / lr_init) ** t
+    if kind == "delayed_exponential" and delay_steps > 0:
+        p = min(max(step / delay_steps, 0.0), 1.0)
+        lr *= delay_mult + (1.0 - delay_mult) * math.sin(0.5 * math.pi * p)
+    return lr

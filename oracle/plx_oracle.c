@@ -975,3 +975,59 @@ void oracle_tv_bg(const double *bg, int64_t L, int64_t H, int64_t W, const int64
     out_sums[0] = sig_sum;
     out_sums[1] = rgb_sum;
 }
+
+/*
+ * camera.py:91-100 generate_rays for a subset of pixels of one view, and the
+ * NDC warp camera.py:103-134 (the reference's numpy op order).
+ *   cam = {c2w row-major 3x4 (12), focal, width, height}
+ *   xs = (i + 0.5 - W/2) / f;   ys = -(j + 0.5 - H/2) / f
+ *   d  = d_cam @ R^T with d_cam = (x, y, -1): numpy's matmul runs OpenBLAS
+ *        dgemm, whose k-loop accumulates with FMAs from zero
+ *        (fma(x2, r2, fma(x1, r1, x0 r0))) -- checked bit-exact against
+ *        numpy on this machine by tests/test_oracle_golden.py;
+ *   d /= sqrt((d0 d0 + d1 d1) + d2 d2)    (np.linalg.norm, axis=-1)
+ */
+void oracle_generate_rays(const double *cam, const int64_t *pix, int64_t n, double *o, double *d) {
+    const double f = cam[12];
+    const int64_t W = (int64_t)cam[13], H = (int64_t)cam[14];
+    (void)H;
+    for (int64_t r = 0; r < n; ++r) {
+        const int64_t p = pix ? pix[r] : r;
+        const int64_t i = p % W, j = p / W;
+        const double x = (((double)i + 0.5) - (double)W / 2.0) / f;
+        const double y = (-(((double)j + 0.5) - cam[14] / 2.0)) / f;
+        const double dc[3] = {x, y, -1.0};
+        double v[3];
+        for (int a = 0; a < 3; ++a) {
+            const double *row = cam + 4 * a;   /* R[a, :] */
+            v[a] = fma(dc[2], row[2], fma(dc[1], row[1], dc[0] * row[0]));
+        }
+        const double nrm = sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+        for (int a = 0; a < 3; ++a) {
+            d[3 * r + a] = v[a] / nrm;
+            o[3 * r + a] = cam[4 * a + 3];
+        }
+    }
+}
+
+/* camera.py:103-134: o, d in place -> NDC; valid[r] = |d_z| > 1e-10 */
+void oracle_to_ndc(double *o, double *d, int64_t n, double focal, double W, double H,
+                   double near, uint8_t *valid) {
+    if (near <= 0.0) near = 1.0;
+    const double fx = focal / (W / 2.0), fy = focal / (H / 2.0);
+    for (int64_t r = 0; r < n; ++r) {
+        double *oo = o + 3 * r, *dd = d + 3 * r;
+        const int ok = fabs(dd[2]) > 1e-10;
+        const double dz = ok ? dd[2] : 1.0;
+        const double t = -(near + oo[2]) / dz;
+        const double p0 = oo[0] + t * dd[0], p1 = oo[1] + t * dd[1], p2 = oo[2] + t * dd[2];
+        const double oz = fabs(p2) > 1e-12 ? p2 : -1e-12;
+        const double on0 = -fx * p0 / oz, on1 = -fy * p1 / oz, on2 = 1.0 + 2.0 * near / oz;
+        const double dn0 = -fx * (dd[0] / dz - p0 / oz);
+        const double dn1 = -fy * (dd[1] / dz - p1 / oz);
+        const double dn2 = -2.0 * near / oz;
+        oo[0] = on0; oo[1] = on1; oo[2] = on2;
+        dd[0] = dn0; dd[1] = dn1; dd[2] = dn2;
+        if (valid) valid[r] = (uint8_t)ok;
+    }
+}

@@ -176,3 +176,37 @@ def test_to_ndc_matches_reference():
     np.testing.assert_array_equal(valid, z["valid"])
     np.testing.assert_array_equal(on, z["on"])
     np.testing.assert_array_equal(dn, z["dn"])
+
+
+def test_generate_rays_matches_reference():
+    """camera.py:91-100 restated (oracle_generate_rays) bit-for-bit, all
+    pixels and a scattered pixel subset."""
+    z = load("camera.npz")
+    k = 0
+    while f"cam{k}_c2w" in z:
+        w, h = (int(x) for x in z[f"cam{k}_wh"])
+        c2w, f = z[f"cam{k}_c2w"], float(z[f"cam{k}_focal"])
+        o, d = orc.generate_rays(c2w, f, w, h)
+        np.testing.assert_array_equal(d, z[f"cam{k}_d"])
+        assert np.all(o == c2w[:3, 3])
+        pix = np.random.default_rng(k).integers(0, w * h, 97)
+        _, ds = orc.generate_rays(c2w, f, w, h, pixels=pix)
+        np.testing.assert_array_equal(ds, z[f"cam{k}_d"][pix])
+        k += 1
+    assert k >= 6
+
+
+def test_to_ndc_matches_reference():
+    """camera.py:103-134 restated (oracle_to_ndc) bit-for-bit, incl. all_rays'
+    forward-facing pool (camera.py:292-314)."""
+    z = load("camera.npz")
+    for k in range(3):
+        w, h = (int(x) for x in z[f"ndc{k}_wh"])
+        c2w, f = z[f"ndc{k}_c2w"], float(z[f"ndc{k}_focal"])
+        o, d = orc.generate_rays(c2w, f, w, h)
+        on, dn, valid = orc.to_ndc(o, d, f, w, h, float(z[f"ndc{k}_near"]))
+        np.testing.assert_array_equal(on, z[f"ndc{k}_o"])
+        np.testing.assert_array_equal(dn, z[f"ndc{k}_d"])
+        np.testing.assert_array_equal(valid, z[f"ndc{k}_valid"])
+    np.testing.assert_array_equal(z["ff_o"], z["ndc0_o"])
+    np.testing.assert_array_equal(z["ff_d"], z["ndc0_d"])
