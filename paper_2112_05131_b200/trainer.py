@@ -579,8 +579,8 @@ class Trainer:
             hp = self._hparams_np[slot]
             hp[0] = tv_start
             hp[1:3].view(np.float64)[:] = (lr_s, lr_c)
-            hp[3] = idx_off if pool_mode else self._rays_slot * 4 * B
-            self._replay(tv_on, pool_mode, slot)
+            hp[3] = idx_off + s0 if pool_mode else self._rays_slot * 4 * B
+            self._replay(tv_on, pool_mode, slot, c0, sub.count if tv_on else 0, n_tv)
         else:
             if pool_mode:
                 a.rays = self.pool.rays(None)
@@ -722,7 +722,7 @@ class Trainer:
 
     # -- CUDA-graph replay of the native step ------------------------------------
     def _graph_ok(self, B: int, events, pool_mode: bool = True) -> bool:
-        ok = (self.use_graph and self._eager_done and not self.world.active and events is None
+        ok = (self.use_graph and self._eager_done and events is None
               and self.opts.jitter == 0 and (B == self.cfg.batch_size or not pool_mode))
         self._eager_done = True   # the first step runs eagerly (one-time library queries)
         return ok
@@ -739,13 +739,16 @@ class Trainer:
         r.idx = self._rays_idx.data_ptr() if slot is None else None
         return r
 
-    def _replay(self, tv_on: bool, pool_mode: bool, slot: int) -> None:
+    def _replay(self, tv_on: bool, pool_mode: bool, slot: int, n_local: int, tv_local: int,
+                n_tv: int) -> None:
         """Replay (capturing on first use) the graph of one whole step for
         this grid, batch source (a slice of the batcher's permutation buffer
         at the offset in _dparams[3], or the rays in _rays_buf), TV on/off and
         pinned slot: plx_train_step's prologue kernel copies the slot's
         scalars to _dparams, and its compaction kernel writes the loss sums
-        to the slot's pinned sums."""
+        to the slot's pinned sums.  With N ranks the graph holds this rank's
+        render (n_local rays) and TV sub-run (tv_local of the n_tv cells);
+        the exchange and update follow eagerly (exchange_update)."""
         key = ("pool" if pool_mode else "rays", tv_on, slot)
         g = self._graphs.get(key)
         if g is None:
@@ -755,17 +758,18 @@ class Trainer:
             if pool_mode:
                 a.rays = self.pool.rays(None)
                 a.rays.idx = self.batcher._dev_perm().data_ptr()
-                a.rays.n = cfg.batch_size
-                a.dev_idx_off = self._dparams.data_ptr() + 24
+                n_global = cfg.batch_size
             else:
                 a.rays = self._rays_desc(None)
-                a.dev_idx_off = self._dparams.data_ptr() + 24
+                n_global = n_local * self.world.size
+            a.rays.n = n_local
+            a.dev_idx_off = self._dparams.data_ptr() + 24
             a.rays.jitter = None
-            a.up_scale = 2.0 / int(a.rays.n)
-            a.update = 1
-            n_tv = max(1, int(round(cfg.tv_sample_frac * int(np.prod(self.grid.dims)))))
-            a.tv_count = n_tv if tv_on else 0
-            a.tv_f_sigma, a.tv_f_sh = cfg.lambda_tv_sigma / n_tv, cfg.lambda_tv_sh / n_tv
+            a.up_scale = 2.0 / n_global
+            a.update = int(not self.world.active)
+            a.tv_count = tv_local if tv_on else 0
+            nt = max(n_tv, 1)
+            a.tv_f_sigma, a.tv_f_sh = cfg.lambda_tv_sigma / nt, cfg.lambda_tv_sh / nt
             a.dev_tv_start = self._dparams.data_ptr()
             a.dev_lr = self._dparams.data_ptr() + 8
             # the kernels read the slot's scalars from / write the loss sums

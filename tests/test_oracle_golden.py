@@ -178,7 +178,7 @@ def test_to_ndc_matches_reference():
     np.testing.assert_array_equal(dn, z["dn"])
 
 
-def test_generate_rays_matches_reference():
+def test_oracle_generate_rays_matches_reference():
     """camera.py:91-100 restated (oracle_generate_rays) bit-for-bit, all
     pixels and a scattered pixel subset."""
     z = load("camera.npz")
@@ -196,7 +196,7 @@ def test_generate_rays_matches_reference():
     assert k >= 6
 
 
-def test_to_ndc_matches_reference():
+def test_oracle_to_ndc_matches_reference():
     """camera.py:103-134 restated (oracle_to_ndc) bit-for-bit, incl. all_rays'
     forward-facing pool (camera.py:292-314)."""
     z = load("camera.npz")
