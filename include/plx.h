@@ -100,9 +100,33 @@ typedef struct {
                               position chunks, rays}; NULL = off          */
 } plx_render_opts;
 
+/* A camera ray pool: replaces the reference's host-built
+ * ray arrays (camera.py:91-134 generate_rays / to_ndc, camera.py:292-314
+ * all_rays; 96 B of float64 per ray) by the views' camera records and the
+ * float32 ground-truth colours (12 B per ray).  Kernels regenerate a ray
+ * from its pool row, bit-identical to the reference's arrays.  Pool row p is
+ * global pixel pixel[p] (or p when pixel == NULL) = view * W*H + y * W + x,
+ * row-major pixels as all_rays orders them. */
+#define PLX_CAM 16   /* doubles per camera record */
+typedef struct {
+    const double *cams;      /* [n_views][PLX_CAM]: c2w[:3,:4] row-major (12),
+                                focal, width, height, near (camera.py:27-48) */
+    const float *rgb;        /* [rows][3] gt colours (the image float32
+                                values, camera.py:193), or NULL           */
+    const int64_t *pixel;    /* optional [rows] global pixel id per pool row
+                                (forward-facing pools drop invalid rays)   */
+    int64_t n_views, width, height;
+    int32_t ndc;             /* forward-facing: march rays warped to NDC
+                                (camera.py:103-134); SH uses the world dir */
+    int32_t reserved;
+    double scale;            /* origin pre-scale (360 scenes, T:375-377), 1 */
+} plx_cameras;
+
 /* A ray batch.  If idx != NULL ray r of the batch is pool row idx[r] of
  * origins/dirs/viewdirs/target (device-resident ray pool);
- * outputs are always indexed by batch position r. */
+ * outputs are always indexed by batch position r.  With cams != NULL the
+ * pool is that camera pool instead: origins/dirs/viewdirs are ignored and
+ * target defaults to cams->rgb (used when target == NULL). */
 typedef struct {
     const double *origins;   /* [*,3]                                        */
     const double *dirs;      /* [*,3] march directions                       */
@@ -111,7 +135,33 @@ typedef struct {
     const double *jitter;    /* [n] start offsets in steps, or NULL (= 0)    */
     const int64_t *idx;      /* [n] pool indices, or NULL                    */
     int64_t n;
+    const plx_cameras *cams; /* HOST pointer to a camera pool, or NULL      */
 } plx_rays;
+
+/* Materialise pool rows idx[0..n) (or rows 0..n-1 when idx == NULL) of a
+ * camera pool as float64 (n,3) arrays: march origins / directions, view
+ * directions and gt colours (any output may be NULL) -- all_rays
+ * (camera.py:292-314) on the device. */
+int plx_generate_rays(const plx_cameras *cams, const int64_t *idx, int64_t n, double *origins,
+                      double *dirs, double *viewdirs, double *rgb, void *stream);
+/* to_ndc (camera.py:103-134) of n device rays in place, for the camera
+ * record `cam` (HOST double[PLX_CAM]); valid[n] (uint8, may be NULL) =
+ * |d_z| > 1e-10. */
+int plx_to_ndc(const double *cam, double *origins, double *dirs, uint8_t *valid, int64_t n,
+               void *stream);
+
+/* Image metrics of evaluate (T:309-347): losses.psnr / losses.ssim
+ * (losses.py:110-165) of one view on the device.  a, b: (h, w, c) float64;
+ * window: HOST double[11], the normalised Gaussian of losses.py:124-128.
+ * out_sums (device double[2], ACCUMULATED) += {sum of (a-b)^2 over all
+ * values, sum of the SSIM map over the valid interior [5:-5, 5:-5] of every
+ * channel}; psnr = -10 log10(out[0] / (h w c)), ssim = out[1] / ((h-10)
+ * (w-10) c).  scratch: plx_image_metrics_scratch_bytes(h, w, c) bytes.
+ * window == NULL: only the squared-error sum (psnr alone, any image size). */
+int64_t plx_image_metrics_scratch_bytes(int64_t h, int64_t w, int64_t c);
+int plx_image_metrics(const double *a, const double *b, int64_t h, int64_t w, int64_t c,
+                      const double *window, double k1, double k2, double *out_sums,
+                      void *scratch, int64_t scratch_bytes, void *stream);
 
 /* render_forward (K:173-238) via render_rays (R:114-140).
  * out_trans / out_wsum may be NULL. */

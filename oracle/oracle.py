@@ -462,3 +462,39 @@ def lr_at(kind, lr_init, lr_final, total_steps, step, delay_steps=0, delay_mult=
         p = min(max(step / delay_steps, 0.0), 1.0)
         lr *= delay_mult + (1.0 - delay_mult) * math.sin(0.5 * math.pi * p)
     return lr
+
+
+# ---------------------------------------------------------------- metrics --
+def psnr(a, b):
+    """losses.py:110-119."""
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    mse = float(np.mean((a - b) ** 2))
+    return math.inf if mse == 0.0 else -10.0 * math.log10(mse)
+
+
+def ssim(a, b, k1=0.01, k2=0.03):
+    """losses.py:122-165 (scipy correlate1d, zero padding, valid interior)."""
+    from scipy.ndimage import correlate1d
+
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    if a.ndim == 2:
+        a, b = a[..., None], b[..., None]
+    r = 5
+    x = np.arange(-r, r + 1, dtype=np.float64)
+    win = np.exp(-(x * x) / (2.0 * 1.5 * 1.5))
+    win = win / win.sum()
+    c1, c2 = k1 * k1, k2 * k2
+
+    def filt(img):
+        out = correlate1d(img, win, axis=0, mode="constant")
+        out = correlate1d(out, win, axis=1, mode="constant")
+        return out[r:-r, r:-r]
+
+    vals = []
+    for ch in range(a.shape[2]):
+        x_, y_ = a[..., ch], b[..., ch]
+        mx, my = filt(x_), filt(y_)
+        vx, vy, cov = filt(x_ * x_) - mx * mx, filt(y_ * y_) - my * my, filt(x_ * y_) - mx * my
+        vals.append(np.mean((2 * mx * my + c1) * (2 * cov + c2) /
+                            ((mx * mx + my * my + c1) * (vx + vy + c2))))
+    return float(np.mean(vals))

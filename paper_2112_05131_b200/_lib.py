@@ -56,11 +56,21 @@ class PlxRenderOpts(ctypes.Structure):
                 ("absolute", ctypes.c_int32), ("stats", ctypes.c_void_p)]
 
 
+CAM = 16   # doubles per camera record (PLX_CAM)
+
+
+class PlxCameras(ctypes.Structure):
+    _fields_ = [("cams", ctypes.c_void_p), ("rgb", ctypes.c_void_p), ("pixel", ctypes.c_void_p),
+                ("n_views", ctypes.c_int64), ("width", ctypes.c_int64),
+                ("height", ctypes.c_int64), ("ndc", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("scale", ctypes.c_double)]
+
+
 class PlxRays(ctypes.Structure):
     _fields_ = [("origins", ctypes.c_void_p), ("dirs", ctypes.c_void_p),
                 ("viewdirs", ctypes.c_void_p), ("target", ctypes.c_void_p),
                 ("jitter", ctypes.c_void_p), ("idx", ctypes.c_void_p),
-                ("n", ctypes.c_int64)]
+                ("n", ctypes.c_int64), ("cams", ctypes.POINTER(PlxCameras))]
 
 
 class PlxStepArgs(ctypes.Structure):
@@ -142,11 +152,15 @@ _SIGS = {
                    ctypes.POINTER(PlxMsiGrad), _P, _P],
     "plx_msi_opt_step": [_P, _P, ctypes.POINTER(PlxMsiGrad), _I64, _D, _D, _D, _D, _I32, _I32,
                          _P, _P],
+    "plx_generate_rays": [ctypes.POINTER(PlxCameras), _P, _I64, _P, _P, _P, _P, _P],
+    "plx_to_ndc": [_P, _P, _P, _P, _I64, _P],
+    "plx_image_metrics_scratch_bytes": [_I64, _I64, _I64],
+    "plx_image_metrics": [_P, _P, _I64, _I64, _I64, _P, _D, _D, _P, _P, _I64, _P],
     "plx_version": [],
     "plx_device_check": [],
 }
 _RESTYPE = {"plx_scan_scratch_bytes": _I64, "plx_render_scratch_bytes": _I64, "plx_cell_occ_words": _I64,
-            "plx_msi_scratch_bytes": _I64,
+            "plx_msi_scratch_bytes": _I64, "plx_image_metrics_scratch_bytes": _I64,
             "plx_version": ctypes.c_char_p}
 
 EXPORTS = tuple(_SIGS)

@@ -1,13 +1,23 @@
-"""Pinhole ray generation and the NDC warp (host side, float64), restating
-pkg/src/plenoxel/camera.py:27-134 and 292-314.  These feed the device ray
-pool once per dataset; they are not on the per-step hot path."""
+"""Cameras and rays (drop-in for pkg/src/plenoxel/camera.py:27-134, 292-314).
+
+The reference builds every training ray on the host (generate_rays, to_ndc,
+all_rays: 96 bytes of float64 per ray).  Here rays are generated on the
+device from (view, pixel) ids by libplx.so (plx_generate_rays / plx_to_ndc,
+csrc/plx_camera.cuh), bit-identical to the reference's float64 arrays; the
+trainer never materialises them at all (render.CameraPool feeds the kernels
+the camera records).  The functions below keep the reference's API and
+return numpy arrays like it does.
+"""
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
 import numpy as np
+
+from . import _lib
 
 
 @dataclass
@@ -36,57 +46,50 @@ class Camera:
         return self.c2w[:3, 3]
 
 
-def generate_rays(cam: Camera):
-    """All pixel-centre rays, row-major (camera.py:91-100)."""
-    xs = (np.arange(cam.width) + 0.5 - cam.width / 2) / cam.focal
-    ys = -(np.arange(cam.height) + 0.5 - cam.height / 2) / cam.focal
-    gx, gy = np.meshgrid(xs, ys)
-    d_cam = np.stack([gx, gy, -np.ones_like(gx)], axis=-1).reshape(-1, 3)
-    d = d_cam @ cam.c2w[:3, :3].T
-    d /= np.linalg.norm(d, axis=-1, keepdims=True)
-    o = np.broadcast_to(cam.position, d.shape).copy()
-    return o, np.ascontiguousarray(d)
+def camera_record(cam: Camera) -> np.ndarray:
+    """The PLX_CAM-double record of plx_cameras: c2w[:3, :4] row-major,
+    focal, width, height, near."""
+    r = np.zeros(_lib.CAM)
+    r[:12] = cam.c2w[:3, :4].reshape(-1)
+    r[12:] = (float(cam.focal), float(cam.width), float(cam.height), float(cam.near))
+    return r
 
 
-def to_ndc(origins, dirs, cam: Camera, near: float | None = None):
-    """Forward-facing NDC warp (camera.py:103-134)."""
-    near = cam.near if near is None else near
-    if near <= 0:
-        near = 1.0
-    o = np.atleast_2d(np.asarray(origins, dtype=np.float64)).copy()
-    d = np.atleast_2d(np.asarray(dirs, dtype=np.float64)).copy()
-    valid = np.abs(d[:, 2]) > 1e-10
-    dz = np.where(valid, d[:, 2], 1.0)
-    t = -(near + o[:, 2]) / dz
-    o = o + t[:, None] * d
-    oz = np.where(np.abs(o[:, 2]) > 1e-12, o[:, 2], -1e-12)
-    fx = cam.focal / (cam.width / 2.0)
-    fy = cam.focal / (cam.height / 2.0)
-    o_ndc = np.stack([-fx * o[:, 0] / oz, -fy * o[:, 1] / oz, 1.0 + 2.0 * near / oz], -1)
-    d_ndc = np.stack([-fx * (d[:, 0] / dz - o[:, 0] / oz),
-                      -fy * (d[:, 1] / dz - o[:, 1] / oz),
-                      -2.0 * near / oz], axis=-1)
-    return o_ndc, d_ndc, valid
+def generate_rays(cam: Camera, device=None):
+    """All pixel-centre rays of a view, row-major (camera.py:91-100) ->
+    (origins, dirs) float64 (H*W, 3) numpy arrays, generated on the device."""
+    from .render import CameraPool
+
+    pool = CameraPool([cam], None, device=device)
+    o, d, _, _ = pool.materialize(None, rgb=False)
+    return o.cpu().numpy(), d.cpu().numpy()
 
 
-def all_rays(images, cameras, scene_type: str = "bounded"):
+def to_ndc(origins, dirs, cam: Camera, near: float | None = None, device=None):
+    """Forward-facing NDC warp (camera.py:103-134) on the device ->
+    (o_ndc, d_ndc, valid) numpy arrays."""
+    import torch
+
+    rec = camera_record(cam)
+    if near is not None:
+        rec[15] = float(near)
+    dev = torch.device(device or "cuda")
+    o = torch.from_numpy(np.ascontiguousarray(np.atleast_2d(origins), dtype=np.float64)).to(dev)
+    d = torch.from_numpy(np.ascontiguousarray(np.atleast_2d(dirs), dtype=np.float64)).to(dev)
+    valid = torch.empty(o.shape[0], dtype=torch.uint8, device=dev)
+    _lib.check(_lib.lib().plx_to_ndc(rec.ctypes.data_as(ctypes.c_void_p), o.data_ptr(),
+                                     d.data_ptr(), valid.data_ptr(), o.shape[0],
+                                     _lib.stream_ptr()), "to_ndc")
+    return o.cpu().numpy(), d.cpu().numpy(), valid.cpu().numpy().astype(bool)
+
+
+def all_rays(images, cameras, scene_type: str = "bounded", device=None):
     """Flatten every pixel of every view (camera.py:292-314) ->
-    (origins, march_dirs, view_dirs, rgb), each (N, 3) float64.
+    (origins, march_dirs, view_dirs, rgb), each (N, 3) float64 numpy, with
+    forward-facing rays that are parallel to the image plane dropped.  The
+    arrays are generated on the device (render.CameraPool); the trainer uses
+    the pool directly and never calls this."""
+    from .render import CameraPool
 
-    `images` are float arrays in [0, 1]; the reference stores them as float32
-    (camera.py:193) and widens to float64 here, so we do the same."""
-    origins, mdirs, vdirs, rgb = [], [], [], []
-    for img, cam in zip(images, cameras):
-        o, d = generate_rays(cam)
-        v = d
-        img = np.asarray(img, dtype=np.float32).reshape(-1, 3)
-        if scene_type == "forward_facing_ndc":
-            o, d, valid = to_ndc(o, d, cam)
-            if not np.all(valid):
-                o, d, v, img = o[valid], d[valid], v[valid], img[valid]
-        origins.append(o)
-        mdirs.append(d)
-        vdirs.append(v)
-        rgb.append(np.asarray(img, dtype=np.float64))
-    return (np.concatenate(origins), np.concatenate(mdirs), np.concatenate(vdirs),
-            np.concatenate(rgb))
+    pool = CameraPool(cameras, images, ndc=scene_type == "forward_facing_ndc", device=device)
+    return tuple(t.cpu().numpy() for t in pool.materialize(None))

@@ -675,6 +675,7 @@ extern "C" int plx_msi_render(const plx_grid *g, const plx_msi *bg, const plx_ra
     if (!bg->data || !bg->radii || bg->L < 2 || bg->H < 2 || bg->W < 1 || bg->L - 1 > kMaxCross)
         return PLX_EINVAL;
     if (rays->n < 0 || o->step <= 0.0) return PLX_EINVAL;
+    if (rays->cams) return PLX_EINVAL;   // array rays only (plx_generate_rays materialises a pool)
     if (rays->n > 0 && (!rays->origins || !rays->dirs || !rays->target)) return PLX_EINVAL;
     if (gb && (!gb->grad || !gb->tmask || !bgb || !bgb->grad || !bgb->tmask)) return PLX_EINVAL;
     if (rays->n == 0) return PLX_OK;

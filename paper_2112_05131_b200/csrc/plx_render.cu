@@ -25,6 +25,7 @@
 // grids, so B and C iterate over samples, not positions.
 #include <stdlib.h>
 
+#include "plx_camera.cuh"
 #include "plx_common.cuh"
 #include "plx_internal.h"
 
@@ -43,7 +44,44 @@ struct RayArgs {
     const int64_t *__restrict__ idx;
     int64_t n;
     const int64_t *idx_off;   // optional device offset added to idx (graph replay)
+    CamPool C;                // camera pool (C.cams != nullptr): rays generated
+    int64_t base;             // pool row of batch ray 0 when idx == nullptr
 };
+
+// Pool row of batch ray `ray`.
+__device__ __forceinline__ int64_t ray_src(const RayArgs &R, int64_t ray) {
+    return R.idx ? R.idx[ray] : R.base + ray;
+}
+
+// March origin / direction of pool row src: the arrays, or the camera pool
+// (camera.py:91-134, 292-314 on the device, plx_camera.cuh).
+__device__ __forceinline__ void ray_od(const RayArgs &R, int64_t src, double *o, double *d) {
+    if (R.C.cams) {
+        cam_march_ray(R.C, src, o, d);
+        return;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        o[a] = __ldg(R.origins + 3 * src + a);
+        d[a] = __ldg(R.dirs + 3 * src + a);
+    }
+}
+
+// Unit view (SH) direction of pool row src.
+__device__ __forceinline__ void ray_vd(const RayArgs &R, int64_t src, double *v) {
+    if (R.C.cams) {
+        cam_view_dir(R.C, src, v);
+        return;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) v[a] = __ldg(R.viewdirs + 3 * src + a);
+}
+
+// Target (gt colour, or the upstream dL/dC) of pool row src, channel c.
+__device__ __forceinline__ double ray_tgt(const RayArgs &R, int64_t src, int c) {
+    if (R.C.cams && !R.target) return (double)__ldg(R.C.rgb + 3 * src + c);
+    return __ldg(R.target + 3 * src + c);
+}
 
 // Stencil rows of a recorded cell on an identity-linked grid (row = lattice
 // point): computed, so the march does not store them and the colour and
@@ -280,18 +318,14 @@ __global__ void __launch_bounds__(128, 6)
     unsigned st_pos = 0, st_samp = 0, st_chunks = 0, st_rays = 0;   // warp-uniform
     for (int64_t ray = slot; ray < R.n; ray += nslots) {
         ++st_rays;
-        const int64_t src = R.idx ? R.idx[ray] : ray;
+        const int64_t src = ray_src(R, ray);
         RayMarch rm;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            rm.o[a] = __ldg(R.origins + 3 * src + a);
-            rm.d[a] = __ldg(R.dirs + 3 * src + a);
-        }
+        ray_od(R, src, rm.o, rm.d);
         float bf[9];
         if (MODE == FWD) {
-            double basis[9];
-            sh_basis9(__ldg(R.viewdirs + 3 * src), __ldg(R.viewdirs + 3 * src + 1),
-                      __ldg(R.viewdirs + 3 * src + 2), basis);
+            double basis[9], vd[3];
+            ray_vd(R, src, vd);
+            sh_basis9(vd[0], vd[1], vd[2], basis);
 #pragma unroll
             for (int b = 0; b < 9; ++b) bf[b] = (float)basis[b];
         }
@@ -405,13 +439,9 @@ __global__ void __launch_bounds__(128, MINB)
         const int64_t ray = __shfl_sync(PLX_FULL_MASK, rr, 0);
         if (ray >= R.n) break;
         ++st_rays;
-        const int64_t src = R.idx ? R.idx[ray] : ray;
+        const int64_t src = ray_src(R, ray);
         RayMarch rm;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            rm.o[a] = __ldg(R.origins + 3 * src + a);
-            rm.d[a] = __ldg(R.dirs + 3 * src + a);
-        }
+        ray_od(R, src, rm.o, rm.d);
         const double jit = R.jitter ? R.jitter[ray] : 0.0;
         ray_march_setup(rm, G, O.step, jit);
         const int64_t rb = ray * S.cap;   // this ray's record block
@@ -483,8 +513,8 @@ __global__ void __launch_bounds__(128, MINB)
                     out.rgb[3 * ray + 2] = c2;
                 }
                 if (out.mse_mode) {
-                    const double e0 = c0 - R.target[3 * src], e1 = c1 - R.target[3 * src + 1],
-                                 e2 = c2 - R.target[3 * src + 2];
+                    const double e0 = c0 - ray_tgt(R, src, 0), e1 = c1 - ray_tgt(R, src, 1),
+                                 e2 = c2 - ray_tgt(R, src, 2);
                     mse_part += e0 * e0 + e1 * e1 + e2 * e2;
                 }
             }
@@ -508,9 +538,9 @@ __global__ void __launch_bounds__(128, MINB)
 }
 
 __device__ __forceinline__ void ray_basis(const RayArgs &R, int64_t src, float *bf) {
-    double basis[9];   // K:27-37 in float64, used as f32 by the colour FMAs
-    sh_basis9(__ldg(R.viewdirs + 3 * src), __ldg(R.viewdirs + 3 * src + 1),
-              __ldg(R.viewdirs + 3 * src + 2), basis);
+    double basis[9], vd[3];   // K:27-37 in float64, used as f32 by the colour FMAs
+    ray_vd(R, src, vd);
+    sh_basis9(vd[0], vd[1], vd[2], basis);
 #pragma unroll
     for (int b = 0; b < 9; ++b) bf[b] = (float)basis[b];
 }
@@ -585,7 +615,7 @@ __global__ void __launch_bounds__(128, MINB)
     auto fetch2 = [&](int r_) {
         nx_first = S.seg_first[r_];
         nx_ns = S.ns[r_];
-        nx_src = R.idx ? R.idx[r_] : r_;
+        nx_src = ray_src(R, r_);
     };
     if (nx_sg < nseg) fetch2(nx_ray);
     int claim = 0;
@@ -844,7 +874,7 @@ __global__ void __launch_bounds__(128, MINB)
     auto fetch2 = [&](int r_) {
         nx_first = S.seg_first[r_];
         nx_ns = S.ns[r_];
-        nx_src = R.idx ? R.idx[r_] : r_;
+        nx_src = ray_src(R, r_);
     };
     if (sg < nseg) fetch2(nx_ray);
     for (; sg < nseg; sg += nw) {
@@ -926,17 +956,17 @@ __global__ void __launch_bounds__(128, MINB)
         // ---------------- upstream (K:330-341) ----------------
         double up0, up1, up2;
         if (out.mse_mode) {
-            const double e0 = rgb0 - __ldg(R.target + 3 * src + 0);
-            const double e1 = rgb1 - __ldg(R.target + 3 * src + 1);
-            const double e2 = rgb2 - __ldg(R.target + 3 * src + 2);
+            const double e0 = rgb0 - ray_tgt(R, src, 0);
+            const double e1 = rgb1 - ray_tgt(R, src, 1);
+            const double e2 = rgb2 - ray_tgt(R, src, 2);
             if (first && lane == 0) mse_part += e0 * e0 + e1 * e1 + e2 * e2;
             up0 = out.up_scale * e0;
             up1 = out.up_scale * e1;
             up2 = out.up_scale * e2;
         } else {
-            up0 = __ldg(R.target + 3 * src + 0);
-            up1 = __ldg(R.target + 3 * src + 1);
-            up2 = __ldg(R.target + 3 * src + 2);
+            up0 = ray_tgt(R, src, 0);
+            up1 = ray_tgt(R, src, 1);
+            up2 = ray_tgt(R, src, 2);
         }
         // ---------------- reverse sweep + scatter (K:343-410) ----------------
         // sf before sample i in the reference's reverse sweep:
@@ -1192,6 +1222,11 @@ ScratchLayout layout(const plx_grid *g, const plx_render_opts *o, int64_t n_rays
 int check_rays(const plx_grid *g, const plx_rays *rays, const plx_render_opts *o, bool views) {
     if (!grid_ok(g) || !rays || !o || rays->n < 0) return PLX_EINVAL;
     if (rays->n >= (int64_t)1 << 31) return PLX_EINVAL;
+    if (rays->cams) {
+        const plx_cameras *c = rays->cams;
+        if (!c->cams || c->n_views < 1 || c->width < 1 || c->height < 1) return PLX_EINVAL;
+        return (o->step > 0.0) ? PLX_OK : PLX_EINVAL;
+    }
     // an empty batch is a no-op: its (zero-length) buffers may be null
     if (rays->n > 0 && (!rays->origins || !rays->dirs || (views && !rays->viewdirs)))
         return PLX_EINVAL;
@@ -1207,7 +1242,7 @@ int launch_march(const plx_grid *g, const plx_rays *rays, const plx_render_opts 
     if (rays->n == 0) return PLX_OK;
     DGrid G = make_dgrid(*g);
     RayArgs R{rays->origins, rays->dirs, rays->viewdirs, rays->target, rays->jitter, rays->idx,
-              rays->n};
+              rays->n, nullptr, make_campool(rays->cams), 0};
     KOpts K{o->step, o->stop_thresh, {o->bg[0], o->bg[1], o->bg[2]},
             reinterpret_cast<unsigned long long *>(o->stats)};
     int64_t blocks = (rays->n + kWarps - 1) / kWarps;   // static grid-stride over rays
@@ -1257,7 +1292,8 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
     const int rc = check_rays(g, rays, o, true);
     if (rc != PLX_OK) return rc;
     if (rays->n == 0) return PLX_OK;
-    if (!rays->target || !scratch) return PLX_EINVAL;
+    if ((!rays->target && !(rays->cams && rays->cams->rgb && mse_mode)) || !scratch)
+        return PLX_EINVAL;
     const ScratchLayout L = layout(g, o, rays->n);
     if (scratch_bytes < L.bytes) return PLX_EINVAL;
     DGrid G = make_dgrid(*g);
@@ -1288,8 +1324,10 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
         const int64_t nw = rays->n - w0 < L.wave ? rays->n - w0 : L.wave;
         RayArgs R{rays->origins, rays->dirs, rays->viewdirs, rays->target,
                   rays->jitter ? rays->jitter + w0 : nullptr, rays->idx ? rays->idx + w0 : nullptr,
-                  nw, rays->idx ? idx_off : nullptr};
-        if (!rays->idx) {   // implicit indices: offset the arrays instead
+                  nw, rays->idx ? idx_off : nullptr, make_campool(rays->cams), 0};
+        if (!rays->idx && rays->cams) {
+            R.base = w0;   // camera pool rows w0 + r
+        } else if (!rays->idx) {   // implicit indices: offset the arrays instead
             R.origins += 3 * w0;
             R.dirs += 3 * w0;
             R.viewdirs += 3 * w0;
@@ -1348,4 +1386,71 @@ extern "C" int plx_max_weight(const plx_grid *g, const plx_rays *rays, const plx
     Outs out{};
     out.maxw = out_w;
     return launch_march<MAXW>(g, rays, o, out, stream);
+}
+
+// all_rays (camera.py:292-314) of pool rows on the device: one thread per ray.
+__global__ void generate_rays_kernel(CamPool C, const int64_t *idx, int64_t n, double *o,
+                                     double *d, double *v, double *rgb) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t src = idx ? idx[r] : r;
+        double oo[3], dd[3];
+        if (o || d) {
+            cam_march_ray(C, src, oo, dd);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                if (o) o[3 * r + a] = oo[a];
+                if (d) d[3 * r + a] = dd[a];
+            }
+        }
+        if (v) {
+            cam_view_dir(C, src, dd);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) v[3 * r + a] = dd[a];
+        }
+        if (rgb) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) rgb[3 * r + a] = (double)C.rgb[3 * src + a];
+        }
+    }
+}
+
+extern "C" int plx_generate_rays(const plx_cameras *cams, const int64_t *idx, int64_t n,
+                                 double *origins, double *dirs, double *viewdirs, double *rgb,
+                                 void *stream) {
+    if (!cams || !cams->cams || n < 0 || cams->width < 1 || cams->height < 1) return PLX_EINVAL;
+    if (rgb && !cams->rgb) return PLX_EINVAL;
+    if (n == 0) return PLX_OK;
+    int64_t blocks = (n + 255) / 256;
+    const int64_t cap = (int64_t)num_sms() * 16;
+    if (blocks > cap) blocks = cap;
+    generate_rays_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        make_campool(cams), idx, n, origins, dirs, viewdirs, rgb);
+    return cudaPeekAtLastError() == cudaSuccess ? PLX_OK : PLX_ECUDA;
+}
+
+namespace {
+struct CamRecord {
+    double v[PLX_CAM];
+};
+__global__ void to_ndc_kernel(CamRecord cam, double *o, double *d, uint8_t *valid, int64_t n) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const bool ok = cam_to_ndc(cam.v, o + 3 * r, d + 3 * r);
+        if (valid) valid[r] = ok ? 1 : 0;
+    }
+}
+}  // namespace
+
+extern "C" int plx_to_ndc(const double *cam, double *origins, double *dirs, uint8_t *valid,
+                          int64_t n, void *stream) {
+    if (!cam || n < 0 || (n > 0 && (!origins || !dirs))) return PLX_EINVAL;
+    if (n == 0) return PLX_OK;
+    CamRecord c;
+    for (int k = 0; k < PLX_CAM; ++k) c.v[k] = cam[k];
+    int64_t blocks = (n + 255) / 256;
+    const int64_t cap = (int64_t)num_sms() * 16;
+    if (blocks > cap) blocks = cap;
+    to_ndc_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(c, origins, dirs, valid, n);
+    return cudaPeekAtLastError() == cudaSuccess ? PLX_OK : PLX_ECUDA;
 }

@@ -447,6 +447,25 @@ class SparseGrid:
                                         out.data_ptr(), _lib.stream_ptr()), "max_weight")
         return out.cpu().numpy() if as_np else out
 
+    def max_weight_accumulate_pool(self, pool, first: int = 0, count: int | None = None,
+                                   step_frac: float = 0.5, stop_thresh: float = 1e-4,
+                                   interp: str = "trilinear", chunk: int = 1 << 22):
+        """max_weight_accumulate (G:287-302) over the rays of camera-pool rows
+        [first, first + count), generated in the kernel.  -> device float64."""
+        count = pool.n - first if count is None else int(count)
+        out = torch.zeros(self.n_rows, dtype=torch.float64, device=self.device)
+        step = step_frac * float(np.min(self.voxel_size))
+        opts = _lib.make_opts(step, stop_thresh, (0, 0, 0), interp == "nearest", False)
+        c = self._c()
+        L = _lib.lib()
+        for s0 in range(first, first + count, chunk):
+            n = min(chunk, first + count - s0)
+            idx = torch.arange(s0, s0 + n, dtype=torch.int64, device=self.device)
+            r = pool.rays(idx)
+            _lib.check(L.plx_max_weight(ctypes.byref(c), ctypes.byref(r), ctypes.byref(opts),
+                                        out.data_ptr(), _lib.stream_ptr()), "max_weight")
+        return out
+
     # -- consistency --------------------------------------------------------
     def validate(self) -> None:
         """G:306-316: links/table bijection and finite values."""

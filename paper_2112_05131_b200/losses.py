@@ -2,8 +2,9 @@
 
 tv_loss (L:50-77) runs the sm_100a TV kernel; sample_tv_cells (L:41-47)
 draws the same contiguous wrapped run from the same numpy RNG call but hands
-the kernel (start, count) instead of materialising the id array.  MSE /
-Cauchy / PSNR / SSIM are host-side helpers with the reference's semantics.
+the kernel (start, count) instead of materialising the id array.  PSNR /
+SSIM (L:110-165) run on the device (plx_image_metrics); MSE / Cauchy are
+host-side helpers with the reference's semantics.
 """
 
 from __future__ import annotations
@@ -109,53 +110,63 @@ def cauchy_sparsity_loss(sigmas, lam: float):
     return lam * float(np.sum(np.log1p(2.0 * s * s))), lam * 4.0 * s / (1.0 + 2.0 * s * s)
 
 
-def psnr(a, b) -> float:
-    """L:110-119."""
-    a = np.asarray(a, dtype=np.float64)
-    b = np.asarray(b, dtype=np.float64)
-    if a.shape != b.shape:
-        raise ValueError("image dimension mismatch")
-    mse = float(np.mean((a - b) ** 2))
-    if mse == 0.0:
-        return math.inf
-    return -10.0 * math.log10(mse)
-
-
 def _gaussian_window(radius: int = 5, sigma: float = 1.5) -> np.ndarray:
+    """L:124-128."""
     x = np.arange(-radius, radius + 1, dtype=np.float64)
     w = np.exp(-(x * x) / (2.0 * sigma * sigma))
     return w / w.sum()
 
 
-def ssim(a, b, k1: float = 0.01, k2: float = 0.03) -> float:
-    """L:128-165 (11x11 Gaussian, sigma 1.5, valid interior)."""
-    from scipy.ndimage import correlate1d
+_WINDOW = _gaussian_window(5)
 
-    a = np.asarray(a, dtype=np.float64)
-    b = np.asarray(b, dtype=np.float64)
-    if a.shape != b.shape:
+
+def _image_tensor(x, device):
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=torch.float64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(device)
+
+
+def image_metrics(a, b, with_ssim: bool = True, k1: float = 0.01, k2: float = 0.03,
+                  device=None):
+    """(psnr, ssim) of two images in [0, 1] (L:110-165) computed on the device
+    (plx_image_metrics): one (H, W[, C]) pair -> two scalars, no image leaves
+    the device.  ssim is None when with_ssim is False."""
+    dev = torch.device(device) if device is not None else (
+        a.device if isinstance(a, torch.Tensor) and a.is_cuda else torch.device("cuda"))
+    ta, tb = _image_tensor(a, dev), _image_tensor(b, dev)
+    if ta.shape != tb.shape:
         raise ValueError("image dimension mismatch")
-    if a.ndim == 2:
-        a, b = a[..., None], b[..., None]
+    if ta.dim() == 2:
+        ta, tb = ta[..., None], tb[..., None]
+    if ta.dim() != 3:
+        raise ValueError("images must be (H, W) or (H, W, C)")
+    h, w, c = (int(x) for x in ta.shape)
     radius = 5
-    win = _gaussian_window(radius)
-    if a.shape[0] <= 2 * radius or a.shape[1] <= 2 * radius:
+    if with_ssim and (h <= 2 * radius or w <= 2 * radius):
         raise ValueError("image smaller than the SSIM window")
-    c1, c2 = k1 * k1, k2 * k2
+    L = _lib.lib()
+    sums = torch.zeros(2, dtype=torch.float64, device=dev)
+    scratch, nb = None, 0
+    if with_ssim:
+        nb = int(L.plx_image_metrics_scratch_bytes(h, w, c))
+        scratch = torch.empty(nb, dtype=torch.uint8, device=dev)
+    _lib.check(L.plx_image_metrics(
+        ta.data_ptr(), tb.data_ptr(), h, w, c,
+        _WINDOW.ctypes.data_as(ctypes.c_void_p) if with_ssim else None, k1, k2,
+        sums.data_ptr(), _lib.ptr(scratch), nb, _lib.stream_ptr()), "image_metrics")
+    sq, ss = (float(x) for x in sums.cpu())
+    mse = sq / (h * w * c)
+    p = math.inf if mse == 0.0 else -10.0 * math.log10(mse)
+    s = ss / ((h - 2 * radius) * (w - 2 * radius) * c) if with_ssim else None
+    return p, s
 
-    def filt(img):
-        out = correlate1d(img, win, axis=0, mode="constant")
-        out = correlate1d(out, win, axis=1, mode="constant")
-        return out[radius:-radius, radius:-radius]
 
-    vals = []
-    for ch in range(a.shape[2]):
-        x, y = a[..., ch], b[..., ch]
-        mx, my = filt(x), filt(y)
-        vx = filt(x * x) - mx * mx
-        vy = filt(y * y) - my * my
-        cov = filt(x * y) - mx * my
-        num = (2 * mx * my + c1) * (2 * cov + c2)
-        den = (mx * mx + my * my + c1) * (vx + vy + c2)
-        vals.append(np.mean(num / den))
-    return float(np.mean(vals))
+def psnr(a, b) -> float:
+    """L:110-119 on the device: inf if the images are equal."""
+    return image_metrics(a, b, with_ssim=False)[0]
+
+
+def ssim(a, b, k1: float = 0.01, k2: float = 0.03) -> float:
+    """L:128-165 on the device: 11x11 Gaussian window (sigma 1.5), statistics
+    over the valid interior, averaged over colour channels."""
+    return image_metrics(a, b, True, k1, k2)[1]

@@ -265,6 +265,83 @@ class RayPool:
         return r
 
 
+class CameraPool:
+    """Device ray pool of a set of calibrated views: the
+    camera records and the float32 ground-truth colours (12 B per ray instead
+    of the reference's 96 B of host-built float64 rays, camera.py:292-314).
+    Pool row p is pixel p of the views in all_rays order (view-major,
+    row-major pixels); the kernels regenerate its ray in the reference's
+    float64 operation order (plx_camera.cuh).  Forward-facing pools (ndc)
+    march NDC-warped rays and drop the rays parallel to the image plane as
+    all_rays does (camera.py:303-307); `scale` pre-scales origins (360
+    scenes, T:375-377)."""
+
+    def __init__(self, cameras, images=None, ndc: bool = False, scale: float = 1.0,
+                 drop_invalid: bool = True, device=None):
+        from .camera import camera_record
+
+        dev = torch.device(device or "cuda")
+        cams = list(cameras)
+        if not cams:
+            raise ValueError("dataset needs at least one view")
+        W, H = int(cams[0].width), int(cams[0].height)
+        if any((int(c.width), int(c.height)) != (W, H) for c in cams):
+            raise ValueError("images have mixed resolutions")      # camera.py:196-198
+        self.device = dev
+        self.width, self.height, self.n_views = W, H, len(cams)
+        self.cams = torch.from_numpy(np.stack([camera_record(c) for c in cams])).to(dev)
+        self.rgb = None
+        if images is not None:
+            img = np.ascontiguousarray(np.asarray(images, dtype=np.float32).reshape(-1, 3))
+            if img.shape[0] != len(cams) * W * H:
+                raise ValueError("image/camera count mismatch")
+            self.rgb = torch.from_numpy(img).to(dev)
+        self.pixel = None
+        self.ndc, self.scale = bool(ndc), float(scale)
+        self.n = len(cams) * W * H
+        self._sync()
+        if self.ndc and drop_invalid:
+            _, _, v, _ = self.materialize(None, origins=False, dirs=False, rgb=False)
+            valid = v[:, 2].abs() > 1e-10
+            if not bool(valid.all()):
+                self.pixel = torch.nonzero(valid).flatten().to(torch.int64).contiguous()
+                if self.rgb is not None:
+                    self.rgb = self.rgb[valid].contiguous()
+                self.n = int(self.pixel.numel())
+                self._sync()
+
+    def _sync(self) -> None:
+        c = _lib.PlxCameras()
+        c.cams = self.cams.data_ptr()
+        c.rgb = _lib.ptr(self.rgb)
+        c.pixel = _lib.ptr(self.pixel)
+        c.n_views, c.width, c.height = self.n_views, self.width, self.height
+        c.ndc = int(self.ndc)
+        c.scale = self.scale
+        self._c = c
+
+    def rays(self, idx: torch.Tensor | None, n: int | None = None) -> _lib.PlxRays:
+        r = _lib.PlxRays()
+        r.cams = ctypes.pointer(self._c)
+        r.jitter = None
+        r.idx = _lib.ptr(idx)
+        r.n = int(idx.numel()) if idx is not None else int(n if n is not None else self.n)
+        return r
+
+    def materialize(self, idx: torch.Tensor | None, origins: bool = True, dirs: bool = True,
+                    viewdirs: bool = True, rgb: bool = True):
+        """Pool rows idx (all rows if None) as float64 (n, 3) device tensors
+        (origins, march dirs, view dirs, gt) -- None where not requested."""
+        n = int(idx.numel()) if idx is not None else self.n
+        mk = lambda want: (torch.empty((n, 3), dtype=torch.float64, device=self.device)  # noqa: E731
+                           if want else None)
+        out = (mk(origins), mk(dirs), mk(viewdirs), mk(rgb and self.rgb is not None))
+        _lib.check(_lib.lib().plx_generate_rays(
+            ctypes.byref(self._c), _lib.ptr(idx), n, *(_lib.ptr(t) for t in out),
+            _lib.stream_ptr()), "generate_rays")
+        return out
+
+
 def fused_mse_backward_pool(grid: SparseGrid, pool: RayPool, idx: torch.Tensor,
                             grads: GradientBuffer, opts: RenderOptions, n_total: int,
                             lam_cauchy: float, sums: torch.Tensor, jitter=None,
@@ -285,15 +362,27 @@ def fused_mse_backward_pool(grid: SparseGrid, pool: RayPool, idx: torch.Tensor,
         ctypes.byref(gb), None, sums.data_ptr(), sp, sn, _lib.stream_ptr()), "render_fused_bwd")
 
 
+def render_pool(grid: SparseGrid, pool: CameraPool, opts: RenderOptions, first: int = 0,
+                count: int | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """render_forward (K:173-238) of pool rows [first, first + count) with the
+    rays generated in the kernel -> (count, 3) float64 device tensor."""
+    count = pool.n - first if count is None else int(count)
+    out = out if out is not None else torch.empty((count, 3), dtype=torch.float64,
+                                                  device=grid.device)
+    idx = torch.arange(first, first + count, dtype=torch.int64, device=grid.device)
+    r = pool.rays(idx)
+    c = grid._c(with_occ=opts.interp == "trilinear")
+    ko = kernel_opts(grid, opts)
+    _lib.check(_lib.lib().plx_render_fwd(ctypes.byref(c), ctypes.byref(r), ctypes.byref(ko),
+                                         out.data_ptr(), None, None, _lib.stream_ptr()),
+               "render_fwd")
+    return out
+
+
 def render_image(grid: SparseGrid, camera, opts: RenderOptions | None = None,
                  chunk: int = 1 << 20) -> np.ndarray:
-    """R:282-293: full camera view -> (H, W, 3) float64 image."""
-    from .camera import generate_rays
-
+    """R:282-293: full camera view -> (H, W, 3) float64 image, rays generated
+    on the device."""
     opts = opts or RenderOptions()
-    origins, dirs = generate_rays(camera)
-    out = np.empty((camera.height * camera.width, 3))
-    for s in range(0, origins.shape[0], chunk):
-        rgb, _, _ = render_rays(grid, origins[s:s + chunk], dirs[s:s + chunk], opts)
-        out[s:s + chunk] = rgb
-    return out.reshape(camera.height, camera.width, 3)
+    pool = CameraPool([camera], None, device=grid.device)
+    return render_pool(grid, pool, opts).cpu().numpy().reshape(camera.height, camera.width, 3)

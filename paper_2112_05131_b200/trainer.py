@@ -31,7 +31,6 @@ import torch
 import yaml
 
 from . import _lib, artifact_io, losses, optim, render
-from .camera import all_rays
 import ctypes
 
 import torch.distributed as dist
@@ -318,13 +317,15 @@ class Trainer:
         self.world = world or World()
         self.device = torch.device(device or "cuda")
         self.rng = np.random.default_rng(cfg.seed)
-        o, m, v, gt = all_rays(train_ds.images, train_ds.cameras, train_ds.scene_type)
         self.scene_scale = 1.0
         self.is_360 = cfg.scene_type == "unbounded_360"
         if self.is_360:   # T:375-377: cameras pre-scaled into the unit sphere
             self.scene_scale = _scene_scale_360(train_ds, cfg.scene_margin)
-            o = o * self.scene_scale
-        self.pool = render.RayPool(o, m, v, gt, device=self.device)
+        # the training rays (T:372, all_rays) as a device camera pool: the
+        # kernels generate each ray from its (view, pixel) row
+        self.pool = render.CameraPool(train_ds.cameras, train_ds.images,
+                                      ndc=train_ds.scene_type == "forward_facing_ndc",
+                                      scale=self.scene_scale, device=self.device)
         dims0 = cfg.ladder[0].dims
         lo, hi = _grid_aabb(cfg, dims0)
         self.grid = SparseGrid.dense(dims0, lo, hi, sigma=cfg.init_sigma, rgb=cfg.init_rgb,
@@ -466,9 +467,8 @@ class Trainer:
     def max_weights(self) -> torch.Tensor:
         """Max-weight over all training rays, sharded over ranks + max-reduce."""
         s, c = shard_range(self.pool.n, self.world.rank, self.world.size)
-        w = self.grid.max_weight_accumulate(self.pool.origins[s:s + c], self.pool.dirs[s:s + c],
-                                            self.cfg.step_frac, self.cfg.stop_thresh,
-                                            self.cfg.interp)
+        w = self.grid.max_weight_accumulate_pool(self.pool, s, c, self.cfg.step_frac,
+                                                 self.cfg.stop_thresh, self.cfg.interp)
         max_reduce(self.world, w)
         return w
 
@@ -640,10 +640,10 @@ class Trainer:
             raise NotImplementedError("unbounded_360 runs on one GPU")
         idx = self.batcher.next_device()
         B = int(idx.numel())
-        P = self.pool
+        o, d, _, gt = self.pool.materialize(idx, viewdirs=False)
         _, _, _, mse_sum, cauchy_raw, beta_raw = msi.render_rays_with_background(
-            self.grid, self.background, P.origins[idx], P.dirs[idx], self.opts,
-            gt_rgb=P.rgb[idx], grads=self.grads, bg_grads=self.bg_grads, n_total=B,
+            self.grid, self.background, o, d, self.opts,
+            gt_rgb=gt, grads=self.grads, bg_grads=self.bg_grads, n_total=B,
             lam_cauchy=cfg.lambda_sparsity, lam_beta=cfg.lambda_beta)
         loss_mse = mse_sum / B
         tv_on = (cfg.lambda_tv_sigma > 0 or cfg.lambda_tv_sh > 0) and (
@@ -821,35 +821,35 @@ class Trainer:
 
 def evaluate(grid: SparseGrid, dataset, opts: render.RenderOptions, chunk: int = 1 << 20,
              background=None, scene_scale: float = 1.0):
-    """Mean PSNR/SSIM over a dataset's views (T:309-347), device renders; 360
-    scenes: origins pre-scaled, grid + background composite."""
-    from .camera import generate_rays, to_ndc
-
+    """Mean PSNR/SSIM over a dataset's views (T:309-347) on the device: each
+    view's rays are generated and rendered by the kernels (evaluation keeps
+    every pixel: forward-facing rays are warped without dropping, as
+    T:316-319 does), the metrics are computed on the device
+    (plx_image_metrics) and only two scalars per view come back."""
+    pool = render.CameraPool(dataset.cameras, dataset.images,
+                             ndc=dataset.scene_type == "forward_facing_ndc",
+                             scale=scene_scale if dataset.scene_type == "unbounded_360" else 1.0,
+                             drop_invalid=False, device=grid.device)
+    ppv = pool.width * pool.height
+    pred = torch.empty((ppv, 3), dtype=torch.float64, device=grid.device)
     rows = []
-    for vi, (img, cam) in enumerate(zip(dataset.images, dataset.cameras)):
-        o, d = generate_rays(cam)
-        v = None
-        if dataset.scene_type == "forward_facing_ndc":
-            v = d
-            o, d, _ = to_ndc(o, d, cam)
+    for vi in range(pool.n_views):
+        first = vi * ppv
         if dataset.scene_type == "unbounded_360":
-            o = o * scene_scale
-        ot = torch.from_numpy(np.ascontiguousarray(o)).to(grid.device)
-        dt = torch.from_numpy(np.ascontiguousarray(d)).to(grid.device)
-        vt = torch.from_numpy(np.ascontiguousarray(v)).to(grid.device) if v is not None else None
-        pred = torch.empty((o.shape[0], 3), dtype=torch.float64, device=grid.device)
-        for s in range(0, o.shape[0], chunk):
-            if dataset.scene_type == "unbounded_360":
-                from . import msi
-                rgb = msi.render_rays_with_background(grid, background, ot[s:s + chunk],
-                                                      dt[s:s + chunk], opts)[0]
-            else:
-                rgb, _, _ = render.render_rays(grid, ot[s:s + chunk], dt[s:s + chunk], opts,
-                                               viewdirs=None if vt is None else vt[s:s + chunk])
-            pred[s:s + chunk] = rgb
-        pred = pred.cpu().numpy().reshape(np.asarray(img).shape)
-        gt = np.asarray(img, dtype=np.float64)
-        rows.append({"view": vi, "psnr": losses.psnr(pred, gt), "ssim": losses.ssim(pred, gt)})
+            from . import msi
+            idx = torch.arange(first, first + ppv, dtype=torch.int64, device=grid.device)
+            o, d, _, _ = pool.materialize(idx, viewdirs=False, rgb=False)
+            for s in range(0, ppv, chunk):
+                pred[s:s + chunk] = msi.render_rays_with_background(
+                    grid, background, o[s:s + chunk], d[s:s + chunk], opts)[0]
+        else:
+            for s in range(0, ppv, chunk):
+                render.render_pool(grid, pool, opts, first + s, min(chunk, ppv - s),
+                                   out=pred[s:s + chunk])
+        gt = pool.rgb[first:first + ppv].double()
+        shape = (pool.height, pool.width, 3)
+        p, ss = losses.image_metrics(pred.view(shape), gt.view(shape))
+        rows.append({"view": vi, "psnr": p, "ssim": ss})
     return (float(np.mean([r["psnr"] for r in rows])), float(np.mean([r["ssim"] for r in rows])),
             rows)
 

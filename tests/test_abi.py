@@ -53,7 +53,8 @@ def test_struct_layouts_match_header(tmp_path):
     structs = {"plx_grid": _lib.PlxGrid, "plx_grad": _lib.PlxGrad,
                "plx_render_opts": _lib.PlxRenderOpts, "plx_rays": _lib.PlxRays,
                "plx_dp_peers": _lib.PlxDpPeers, "plx_step_args": _lib.PlxStepArgs,
-               "plx_msi": _lib.PlxMsi, "plx_msi_grad": _lib.PlxMsiGrad}
+               "plx_msi": _lib.PlxMsi, "plx_msi_grad": _lib.PlxMsiGrad,
+               "plx_cameras": _lib.PlxCameras}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "plx.h"', "int main(void) {"]
     for cname, py in structs.items():
         lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')

@@ -46,8 +46,8 @@ def test_reference_arm_pool_is_the_same_pool():
     import math
 
     import bench
+    from oracle import oracle as orc
     from paper_2112_05131_b200 import scenes
-    from paper_2112_05131_b200.camera import generate_rays
 
     class A:
         views, res, dims = 100, 200, 256
@@ -59,7 +59,8 @@ def test_reference_arm_pool_is_the_same_pool():
     idx = np.array([0, 1, 39999, 40000, 123457, 3999999])
     o, d, v, gt = rays_for(idx)
     for r, i in enumerate(idx):
-        oo, dd = generate_rays(cams[i // 40000])
+        c = cams[i // 40000]
+        oo, dd = orc.generate_rays(c.c2w, c.focal, c.width, c.height)
         np.testing.assert_array_equal(o[r], oo[i % 40000])
         np.testing.assert_array_equal(d[r], dd[i % 40000])
     assert np.all((gt >= 0) & (gt <= 1))
