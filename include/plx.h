@@ -7,7 +7,10 @@
  * L1 wrappers call into numba.  Conventions follow the
  * reference's:
  *   - the caller owns and allocates every buffer (outputs, gradients, scratch);
- *     entry points never allocate persistent state;
+ *     entry points never allocate persistent state -- with ONE exception:
+ *     plx_train_step creates, on its first call per device, a side stream, a
+ *     high-priority stream and four events (TV runs beside the backward) and
+ *     keeps them for the process; plx_release_streams() destroys them;
  *   - kernels never fail on data; argument validation returns PLX_EINVAL;
  *   - all pointers are DEVICE pointers unless stated; work is enqueued on
  *     `stream` (a cudaStream_t, NULL = legacy default stream) and is
@@ -171,7 +174,10 @@ int plx_render_fwd(const plx_grid *g, const plx_rays *rays, const plx_render_opt
 /* render_backward (K:241-411) via fused_mse_backward (R:253-279, mse_mode=1,
  * up_scale = 2/n_total) and render_rays_backward (R:205-239, mse_mode=0,
  * target = upstream dL/dC).  Gradients are ADDED into gb->grad with f32
- * reductions; every occupied stencil row of every recorded sample is marked
+ * reductions (red.global.add.f32: the hardware flushes subnormal operands
+ * and results to zero, so contributions below 1.18e-38 in magnitude are
+ * dropped -- the reference's f64 accumulator keeps them; K:581 then skips
+ * only exact zeros); every occupied stencil row of every recorded sample is marked
  * in gb->tmask.  out_sums (device double[2]) is ACCUMULATED with
  * {mse_sum, cauchy_sum}; out_rgb may be NULL.  `scratch` is a device
  * workspace of at least plx_render_scratch_bytes(g, o, rays->n) bytes (it
@@ -339,6 +345,9 @@ typedef struct {
     double *host_sums;
 } plx_step_args;
 int plx_train_step(plx_grid *g, plx_grad *gb, const plx_step_args *a, void *stream);
+/* Destroy the per-device streams / events plx_train_step created (call with
+ * no step in flight, e.g. at shutdown). */
+int plx_release_streams(void);
 
 /* ---- Multi-sphere-image background (unbounded 360 scenes) ----------------
  * Reference: msi.py (MsiBackground, BgGradientBuffer, render_rays_with_

@@ -156,6 +156,7 @@ _SIGS = {
     "plx_to_ndc": [_P, _P, _P, _P, _I64, _P],
     "plx_image_metrics_scratch_bytes": [_I64, _I64, _I64],
     "plx_image_metrics": [_P, _P, _I64, _I64, _I64, _P, _D, _D, _P, _P, _I64, _P],
+    "plx_release_streams": [],
     "plx_version": [],
     "plx_device_check": [],
 }
@@ -180,6 +181,8 @@ def load(path: str = LIB_PATH):
             "there is no CPU fallback")
     lib = ctypes.CDLL(path)
     for name, argtypes in _SIGS.items():
+        if os.environ.get("PLX_LIB") and not hasattr(lib, name):
+            continue   # an older variant build (A/B) may lack newer entry points
         fn = getattr(lib, name)
         fn.argtypes = argtypes
         fn.restype = _RESTYPE.get(name, ctypes.c_int)

@@ -67,6 +67,29 @@ __device__ __forceinline__ void ray_od(const RayArgs &R, int64_t src, double *o,
     }
 }
 
+// March origin / direction and the unit view (SH) direction of pool row src
+// in one go (the camera ray is generated once).
+__device__ __forceinline__ void ray_od_vd(const RayArgs &R, int64_t src, double *o, double *d,
+                                          double *v) {
+    if (R.C.cams) {
+        const double *cam = cam_pixel_ray(R.C, src, o, v);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) d[a] = v[a];
+        if (R.C.scale != 1.0) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) o[a] = o[a] * R.C.scale;
+        }
+        if (R.C.ndc) cam_to_ndc(cam, o, d);
+        return;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        o[a] = __ldg(R.origins + 3 * src + a);
+        d[a] = __ldg(R.dirs + 3 * src + a);
+        v[a] = __ldg(R.viewdirs + 3 * src + a);
+    }
+}
+
 // Unit view (SH) direction of pool row src.
 __device__ __forceinline__ void ray_vd(const RayArgs &R, int64_t src, double *v) {
     if (R.C.cams) {
@@ -166,6 +189,7 @@ struct Scratch {
     int *seg_ray;      // [segments] ray of each segment
     int *nseg_total;   // segments allocated so far (zeroed per wave)
     double *ray_d;     // [rays][3] {T after the march, delta and index of the last position}
+    float4 *basis;     // [rays][3] the ray's 9 SH basis values (K:27-37, f32) + 3 pad
     double *att;       // exp(-sigma delta)                    [rays][cap]
     double *T;         // transmittance before the sample
     double *w;         // compositing weight
@@ -175,7 +199,25 @@ struct Scratch {
     int4 *rows;        // 8 stencil rows                       [rays][cap][2]
     double *sig;       // sigma (Cauchy term only)
     double *seg_sum;   // [segments][6] {sum w c+ (RGB), sum c+ (bn - bi) (RGB)}
+    // spatial processing order of the segments (seg_order_*): ord[q] =
+    // {segment, ray} of the q-th segment the colour / scatter kernels take;
+    // nullptr = allocation order
+    int2 *ord;
+    int *seg_key;      // [segments] spatial bucket of each segment
+    int *bucket;       // [kBuckets] counts, then (scan) cursors; zeroed by the march
 };
+
+// The q-th segment of the processing order and its ray.
+__device__ __forceinline__ void seg_at(const Scratch &S, int64_t q, int64_t &sg, int &ray) {
+    if (S.ord) {
+        const int2 e = S.ord[q];
+        sg = e.x;
+        ray = e.y;
+    } else {
+        sg = q;
+        ray = S.seg_ray[q];
+    }
+}
 
 // Per-warp shared staging of one chunk's scatter payload (pass 2).  The
 // lane-parallel phase writes, per included sample j: its stencil rows, its
@@ -420,6 +462,87 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
+// ---------------------------------------------------------------------------
+// Spatial order of the segments.  A 5000-ray random batch touches each SH /
+// gradient row from several rays at unrelated times, and the step's row
+// working set exceeds L2, so the colour kernel's row gathers and the
+// scatter's red.add row fills mostly miss L2 when segments are taken in
+// allocation (ray) order.  Processing segments bucketed by the 3-D location
+// of their first sample (a 16^3 Morton grid over the lattice) keeps the
+// segments in flight spatially compact: rows shared by crossing rays are
+// gathered / reduced while still in L2.  Counting sort, three small kernels
+// between the march and the colour kernel; the order within a bucket is
+// arbitrary (results do not depend on it beyond f32 atomic order).
+constexpr int kBucketBits = 4;
+constexpr int kBuckets = 1 << (3 * kBucketBits);
+
+__device__ __forceinline__ int spread3(int v) {
+    int r = 0;
+#pragma unroll
+    for (int b = 0; b < kBucketBits; ++b) r |= ((v >> b) & 1) << (3 * b);
+    return r;
+}
+
+__global__ void seg_key_kernel(Scratch S, int shx, int shy, int shz) {
+    const int64_t nseg = *S.nseg_total;
+    for (int64_t sg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sg < nseg;
+         sg += (int64_t)gridDim.x * blockDim.x) {
+        const int ray = S.seg_ray[sg];
+        const int64_t j0 = (sg - S.seg_first[ray]) * 32;
+        const int4 c = S.cell[(int64_t)ray * S.cap + j0];
+        const int key =
+            (spread3(c.x >> shx) << 2) | (spread3(c.y >> shy) << 1) | spread3(c.z >> shz);
+        S.seg_key[sg] = key;
+        atomicAdd(S.bucket + key, 1);
+    }
+}
+
+// exclusive scan of the kBuckets counts in place (one block of 1024 threads)
+__global__ void __launch_bounds__(1024) seg_scan_kernel(Scratch S) {
+    constexpr int PER = kBuckets / 1024;
+    __shared__ int warp_tot[32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    int v[PER], sum = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        v[i] = S.bucket[PER * t + i];
+        sum += v[i];
+    }
+    int x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(PLX_FULL_MASK, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int y = warp_tot[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int z = __shfl_up_sync(PLX_FULL_MASK, y, o);
+            if (lane >= o) y += z;
+        }
+        warp_tot[lane] = y;
+    }
+    __syncthreads();
+    int excl = x - sum + (w ? warp_tot[w - 1] : 0);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        S.bucket[PER * t + i] = excl;
+        excl += v[i];
+    }
+}
+
+__global__ void seg_place_kernel(Scratch S) {
+    const int64_t nseg = *S.nseg_total;
+    for (int64_t sg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sg < nseg;
+         sg += (int64_t)gridDim.x * blockDim.x) {
+        const int pos = atomicAdd(S.bucket + S.seg_key[sg], 1);
+        S.ord[pos] = make_int2((int)sg, S.seg_ray[sg]);
+    }
+}
+
 template <bool ABS, bool NEAREST, int MINB>
 __global__ void __launch_bounds__(128, MINB)
     march_bwd_kernel(DGrid G, RayArgs R, KOpts O, Outs out, Scratch S) {
@@ -430,6 +553,8 @@ __global__ void __launch_bounds__(128, MINB)
     unsigned st_pos = 0, st_samp = 0, st_chunks = 0, st_rays = 0;   // warp-uniform
     const unsigned lt_mask = (1u << lane) - 1u;
     const bool cauchy = S.sig != nullptr;
+    if (S.bucket && blockIdx.x == 0)   // counts of seg_key_kernel (runs after this kernel)
+        for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) S.bucket[i] = 0;
 #ifdef PLX_TIMELINE
     const unsigned long long t_start = gtimer();
 #endif
@@ -441,7 +566,20 @@ __global__ void __launch_bounds__(128, MINB)
         ++st_rays;
         const int64_t src = ray_src(R, ray);
         RayMarch rm;
-        ray_od(R, src, rm.o, rm.d);
+        {
+            // the ray's SH basis (K:27-37, f64 -> f32 for the colour FMAs),
+            // stored once for the colour and scatter kernels
+            double vd[3], basis[9];
+            ray_od_vd(R, src, rm.o, rm.d, vd);
+            sh_basis9(vd[0], vd[1], vd[2], basis);
+            float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < 3; ++k)   // static indices: basis stays in registers
+                if (lane == k)
+                    b4 = make_float4((float)basis[3 * k], (float)basis[3 * k + 1],
+                                     (float)basis[3 * k + 2], 0.f);
+            if (lane < 3) S.basis[3 * ray + lane] = b4;
+        }
         const double jit = R.jitter ? R.jitter[ray] : 0.0;
         ray_march_setup(rm, G, O.step, jit);
         const int64_t rb = ray * S.cap;   // this ray's record block
@@ -537,13 +675,17 @@ __global__ void __launch_bounds__(128, MINB)
     if (lane == 0 && mse_part != 0.0) atomicAdd(out.sums + 0, mse_part);
 }
 
-__device__ __forceinline__ void ray_basis(const RayArgs &R, int64_t src, float *bf) {
-    double basis[9], vd[3];   // K:27-37 in float64, used as f32 by the colour FMAs
-    ray_vd(R, src, vd);
-    sh_basis9(vd[0], vd[1], vd[2], basis);
+// The ray's basis as stored by the march kernel.
+__device__ __forceinline__ void ray_basis_rec(const Scratch &S, int64_t ray, float *bf) {
 #pragma unroll
-    for (int b = 0; b < 9; ++b) bf[b] = (float)basis[b];
+    for (int k = 0; k < 3; ++k) {
+        const float4 b = S.basis[3 * ray + k];
+        bf[3 * k] = b.x;
+        bf[3 * k + 1] = b.y;
+        bf[3 * k + 2] = b.z;
+    }
 }
+
 
 template <bool NEAREST>
 __device__ __forceinline__ void identity_rows(const DGrid &G, int4 cl, int32_t *rows) {
@@ -608,8 +750,10 @@ __global__ void __launch_bounds__(128, MINB)
     // row) is prefetched in two dependent levels while this segment's rows
     // load and reduce, so the per-segment chain seg_ray -> ray fields ->
     // records -> rows pays one round trip less per level.
-    int64_t nx_sg = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    int nx_ray = nx_sg < nseg ? S.seg_ray[nx_sg] : 0;
+    int64_t nx_q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    int64_t nx_sg = 0;
+    int nx_ray = 0;
+    if (nx_q < nseg) seg_at(S, nx_q, nx_sg, nx_ray);
     int nx_first = 0, nx_ns = 0;
     int64_t nx_src = 0;
     auto fetch2 = [&](int r_) {
@@ -617,18 +761,18 @@ __global__ void __launch_bounds__(128, MINB)
         nx_ns = S.ns[r_];
         nx_src = ray_src(R, r_);
     };
-    if (nx_sg < nseg) fetch2(nx_ray);
+    if (nx_q < nseg) fetch2(nx_ray);
     int claim = 0;
     for (;;) {
+        if (nx_q >= nseg) break;
         const int64_t sg = nx_sg;
-        if (sg >= nseg) break;
         if (lane == 0) claim = atomicAdd(S.counter + 2, 1);
         const int64_t ray = nx_ray;
         const int64_t src = nx_src;
         const int j = (int)(sg - nx_first) * 32 + lane;
         const bool valid = j < nx_ns;
         float bf[9];
-        ray_basis(R, src, bf);
+        ray_basis_rec(S, ray, bf);
         // this lane's 4 columns 4*part .. 4*part+3 span at most two colour
         // channels: cA feeds the first (chA), cB the second.  Per row the
         // part-0 lane then gathers R = a0+a1+a2, G = b2+a3+a4, B = b4+a5+a6.
@@ -767,8 +911,8 @@ __global__ void __launch_bounds__(128, MINB)
         };
         float4 vc[4], vn[4];
         load_pass(0, vc);
-        nx_sg = nw + __shfl_sync(PLX_FULL_MASK, claim, 0);
-        if (nx_sg < nseg) nx_ray = S.seg_ray[nx_sg];
+        nx_q = nw + __shfl_sync(PLX_FULL_MASK, claim, 0);
+        if (nx_q < nseg) seg_at(S, nx_q, nx_sg, nx_ray);
         for (int r0 = 0; r0 < nrow; r0 += 16) {
             if (r0 + 16 < nrow) load_pass(r0 + 16, vn);
 #pragma unroll
@@ -796,7 +940,7 @@ __global__ void __launch_bounds__(128, MINB)
 #pragma unroll
             for (int u = 0; u < 4; ++u) vc[u] = vn[u];
         }
-        if (nx_sg < nseg) fetch2(nx_ray);
+        if (nx_q < nseg) fetch2(nx_ray);
         __syncwarp();
         double x0 = 0.0, x1 = 0.0, x2 = 0.0, q0 = 0.0, q1 = 0.0, q2 = 0.0;
         if (valid) {
@@ -867,8 +1011,10 @@ __global__ void __launch_bounds__(128, MINB)
     // The next segment's descriptor is prefetched in two dependent levels
     // (seg_ray, then the ray's fields) during this segment, and this
     // segment's records are loaded before its prefix sums are reduced.
-    int64_t sg = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    int nx_ray = sg < nseg ? S.seg_ray[sg] : 0;
+    int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    int64_t nx_sg = 0;
+    int nx_ray = 0;
+    if (q < nseg) seg_at(S, q, nx_sg, nx_ray);
     int nx_first = 0, nx_ns = 0;
     int64_t nx_src = 0;
     auto fetch2 = [&](int r_) {
@@ -876,14 +1022,15 @@ __global__ void __launch_bounds__(128, MINB)
         nx_ns = S.ns[r_];
         nx_src = ray_src(R, r_);
     };
-    if (sg < nseg) fetch2(nx_ray);
-    for (; sg < nseg; sg += nw) {
+    if (q < nseg) fetch2(nx_ray);
+    for (; q < nseg; q += nw) {
+        const int64_t sg = nx_sg;
         const int64_t ray = nx_ray;
         const int64_t src = nx_src;
         const int ns_r = nx_ns;
         const int64_t s0 = nx_first, s1 = s0 + ((ns_r + 31) >> 5);
-        const int64_t sgn = sg + nw;
-        if (sgn < nseg) nx_ray = S.seg_ray[sgn];
+        const int64_t qn = q + nw;
+        if (qn < nseg) seg_at(S, qn, nx_sg, nx_ray);
         const int j = (int)(sg - s0) * 32 + lane;
         const bool incl = j < ns_r;
         const unsigned mask = __ballot_sync(PLX_FULL_MASK, incl);
@@ -918,7 +1065,13 @@ __global__ void __launch_bounds__(128, MINB)
         // ray totals and the prefix of the segments before this one
         double C0 = 0.0, C1 = 0.0, C2 = 0.0, Q0 = 0.0, Q1 = 0.0, Q2 = 0.0;
         double B0 = 0.0, B1 = 0.0, B2 = 0.0;
-        for (int64_t t = s0 + lane; t < s1; t += 32) {
+        // short rays (<= 4 segments: nearly all of them) -- every lane sums
+        // the few segment sums itself in segment order (broadcast loads, no
+        // shuffles); long rays -- lane-strided partial sums + warp reduction.
+        // The path depends only on the ray, so all of a ray's segments see
+        // bit-identical totals.
+        const bool few = s1 - s0 <= 4;
+        for (int64_t t = few ? s0 : s0 + lane; t < s1; t += few ? 1 : 32) {
             const double *p = S.seg_sum + 6 * t;
             C0 += p[0];
             C1 += p[1];
@@ -934,15 +1087,20 @@ __global__ void __launch_bounds__(128, MINB)
                 B2 += ABS ? p[5] : p[2];
             }
         }
-        C0 = warp_sum(C0);
-        C1 = warp_sum(C1);
-        C2 = warp_sum(C2);
-        if (ABS) {
-            Q0 = warp_sum(Q0);
-            Q1 = warp_sum(Q1);
-            Q2 = warp_sum(Q2);
+        if (!few) {
+            C0 = warp_sum(C0);
+            C1 = warp_sum(C1);
+            C2 = warp_sum(C2);
+            if (ABS) {
+                Q0 = warp_sum(Q0);
+                Q1 = warp_sum(Q1);
+                Q2 = warp_sum(Q2);
+            }
+            B0 = warp_sum(B0);
+            B1 = warp_sum(B1);
+            B2 = warp_sum(B2);
         }
-        double P0 = warp_sum(B0), P1 = warp_sum(B1), P2 = warp_sum(B2);
+        double P0 = B0, P1 = B1, P2 = B2;
         const double Tfin = S.ray_d[3 * ray], dlt_last = S.ray_d[3 * ray + 1],
                      last_si = S.ray_d[3 * ray + 2];
         const double rgb0 = C0 + Tfin * O.bg[0], rgb1 = C1 + Tfin * O.bg[1],
@@ -974,10 +1132,10 @@ __global__ void __launch_bounds__(128, MINB)
         //   absolute: -bg [T>0] + sum_{j>i} c_j (bn_j - bi_j)   (K:346-349, 374-376)
         const double bend = Tfin > 0.0 ? 1.0 : 0.0;
         float bf[9];
-        ray_basis(R, src, bf);
+        ray_basis_rec(S, ray, bf);
         LaneAcc<NEAREST> ra;
         ra.init(lane, bf);
-        if (sgn < nseg) fetch2(nx_ray);
+        if (qn < nseg) fetch2(nx_ray);
         // delta of this sample (K:200-205): step, except at the last position
         const double dl = (double)cl.w == last_si ? dlt_last : O.step;
         const double cc0 = relu((double)c4.x), cc1 = relu((double)c4.y),
@@ -1183,8 +1341,8 @@ constexpr int64_t kRecordBytes = 112;                 // att, T, w, c, cell, f, 
 struct ScratchLayout {
     int64_t wave, cap, bytes;
     int nseg_max;
-    int64_t off_ns, off_segfirst, off_segray, off_rayd, off_att, off_T, off_w, off_c, off_cell, off_f, off_rows,
-        off_sig, off_segsum;
+    int64_t off_ns, off_segfirst, off_segray, off_rayd, off_basis, off_att, off_T, off_w, off_c, off_cell, off_f, off_rows,
+        off_sig, off_segsum, off_segkey, off_ord, off_bucket;
 };
 
 ScratchLayout layout(const plx_grid *g, const plx_render_opts *o, int64_t n_rays) {
@@ -1206,6 +1364,7 @@ ScratchLayout layout(const plx_grid *g, const plx_render_opts *o, int64_t n_rays
     L.off_segfirst = take(wave * 4);
     L.off_segray = take(wave * L.nseg_max * 4);
     L.off_rayd = take(wave * 24);
+    L.off_basis = take(wave * 48);
     L.off_att = take(n * 8);
     L.off_T = take(n * 8);
     L.off_w = take(n * 8);
@@ -1215,6 +1374,9 @@ ScratchLayout layout(const plx_grid *g, const plx_render_opts *o, int64_t n_rays
     L.off_rows = take(n * 32);
     L.off_sig = take(n * 8);
     L.off_segsum = take(wave * L.nseg_max * 48);
+    L.off_segkey = take(wave * L.nseg_max * 4);
+    L.off_ord = take(wave * L.nseg_max * 8);
+    L.off_bucket = take(kBuckets * 4);
     L.bytes = off;
     return L;
 }
@@ -1309,6 +1471,7 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
     S.seg_first = reinterpret_cast<int *>(base + L.off_segfirst);
     S.seg_ray = reinterpret_cast<int *>(base + L.off_segray);
     S.ray_d = reinterpret_cast<double *>(base + L.off_rayd);
+    S.basis = reinterpret_cast<float4 *>(base + L.off_basis);
     S.att = reinterpret_cast<double *>(base + L.off_att);
     S.T = reinterpret_cast<double *>(base + L.off_T);
     S.w = reinterpret_cast<double *>(base + L.off_w);
@@ -1318,6 +1481,19 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
     S.rows = reinterpret_cast<int4 *>(base + L.off_rows);
     S.sig = lam_cauchy > 0.0 ? reinterpret_cast<double *>(base + L.off_sig) : nullptr;
     S.seg_sum = reinterpret_cast<double *>(base + L.off_segsum);
+    static const bool order_off = [] {
+        const char *e = getenv("PLX_SEG_ORDER");
+        return e && e[0] == '0';
+    }();
+    S.seg_key = reinterpret_cast<int *>(base + L.off_segkey);
+    S.ord = order_off ? nullptr : reinterpret_cast<int2 *>(base + L.off_ord);
+    S.bucket = order_off ? nullptr : reinterpret_cast<int *>(base + L.off_bucket);
+    int shift[3];
+    for (int a = 0; a < 3; ++a) {   // 16 buckets per axis over the base cells
+        int bits = 0;
+        while (((g->dims[a] - 2) >> bits) > 0) ++bits;
+        shift[a] = bits > kBucketBits ? bits - kBucketBits : 0;
+    }
     cudaStream_t s = (cudaStream_t)stream;
     const int sms = num_sms();
     for (int64_t w0 = 0; w0 < rays->n; w0 += L.wave) {
@@ -1366,6 +1542,11 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
                              : resident_blocks(colour_kernel<false, false, kColourMinB>);
             sb = o->absolute ? resident_blocks(scatter_kernel<true, false, kScatterMinB>)
                              : resident_blocks(scatter_kernel<false, false, kScatterMinB>);
+        }
+        if (S.ord) {
+            seg_key_kernel<<<sms * 2, 256, 0, s>>>(S, shift[0], shift[1], shift[2]);
+            seg_scan_kernel<<<1, 1024, 0, s>>>(S);
+            seg_place_kernel<<<sms * 2, 256, 0, s>>>(S);
         }
         PLX_DISPATCH(o, colour_kernel, kColourMinB, dim3((unsigned)(sms * cb)), G, R, S);
         PLX_DISPATCH(o, scatter_kernel, kScatterMinB, dim3((unsigned)(sms * sb)), G, R, K, out, S);

@@ -152,3 +152,24 @@ extern "C" int plx_train_step(plx_grid *g, plx_grad *gb, const plx_step_args *a,
     ev(3);
     return cudaPeekAtLastError() == cudaSuccess ? PLX_OK : PLX_ECUDA;
 }
+
+extern "C" int plx_release_streams(void) {
+    int dev0 = 0;
+    cudaGetDevice(&dev0);
+    for (int d = 0; d < 64; ++d) {
+        SideStream &ss = g_side[d];
+        if (!ss.s) continue;
+        cudaSetDevice(d);
+        cudaStreamSynchronize(ss.s);
+        cudaStreamSynchronize(ss.hp);
+        cudaEventDestroy(ss.fork);
+        cudaEventDestroy(ss.join);
+        cudaEventDestroy(ss.in);
+        cudaEventDestroy(ss.out);
+        cudaStreamDestroy(ss.s);
+        cudaStreamDestroy(ss.hp);
+        ss = SideStream();
+    }
+    cudaSetDevice(dev0);
+    return cudaPeekAtLastError() == cudaSuccess ? PLX_OK : PLX_ECUDA;
+}
