@@ -11,9 +11,9 @@ timeout 900 $NCU -k "regex:march_bwd|colour_kernel|scatter_kernel|opt_rows|tv_ke
   > gpurun_out/prof_c2_r2.log 2>&1
 # C5 at 2^18 (6 waves/step) and 2^20: render kernels of the first wave after 3 warm-up steps
 STEPS=1 WARM=3 LOGB0=18 LOGB1=19 timeout 900 $NCU -k "regex:march_bwd|colour_kernel|scatter_kernel" \
-  -s 54 -c 3 -o gpurun_out/prof_c5_18_r2 python scripts/sweep_c5.py > gpurun_out/prof_c5_18_r2.log 2>&1
-STEPS=1 WARM=2 LOGB0=20 LOGB1=21 timeout 900 $NCU -k "regex:march_bwd|colour_kernel|scatter_kernel|opt_rows" \
-  -s 150 -c 4 -o gpurun_out/prof_c5_20_r2 python scripts/sweep_c5.py > gpurun_out/prof_c5_20_r2.log 2>&1
+  -s 63 -c 3 -o gpurun_out/prof_c5_18_r2 python scripts/sweep_c5.py > gpurun_out/prof_c5_18_r2.log 2>&1
+STEPS=1 WARM=2 LOGB0=20 LOGB1=21 timeout 900 $NCU -k "regex:march_bwd|colour_kernel|scatter_kernel" \
+  -s 150 -c 3 -o gpurun_out/prof_c5_20_r2 python scripts/sweep_c5.py > gpurun_out/prof_c5_20_r2.log 2>&1
 # launch list of the default bench command (per-launch durations, serialised)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/launches_r2.csv python bench.py --steps 3 --warmup 5 --no-cpu-baseline \

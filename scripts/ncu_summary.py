@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Summarise ncu captures (.ncu-rep) and launch lists (.csv) into profiles/.
 
-usage: python scripts/ncu_summary.py <tag> <rep> [<rep> ...] [--launches csv]
+usage: python scripts/ncu_summary.py <tag> <rep> [<rep> ...] [--launches csv] [--no-traffic]
 Writes profiles/<tag>_ncu.md and merges per-kernel DRAM bytes into
 profiles/ncu_traffic.json (read by bench.py for roofline.traffic)."""
 
@@ -97,7 +97,8 @@ def main():
                     sums[key] = sums.get(key, 0.0) + rd + wr
             except (KeyError, ValueError):
                 pass
-    traffic.update(sums)
+    if "--no-traffic" not in sys.argv:
+        traffic.update(sums)
     if launches:
         text = open(launches).read().splitlines()
         start = [i for i, l in enumerate(text) if l.startswith('"ID"')][0]
