@@ -931,27 +931,6 @@ __global__ void __launch_bounds__(128, MINB)
         nx_src = ray_src(R, r_);
     };
     if (q < nseg) fetch2(nx_ray);
-#ifndef PLX_SCATTER_NO_PREFETCH
-    // the next segment's records, loaded one iteration ahead (their loads
-    // overlap this segment's staging and in-order loop instead of stalling
-    // the next iteration's preamble)
-    double p_att = 1.0, p_T = 0.0, p_w = 0.0;
-    float4 p_c4 = make_float4(0.f, 0.f, 0.f, 0.f), p_f4 = p_c4;
-    int4 p_cl = make_int4(0, 0, 0, 0);
-    auto fetch_rec = [&](int64_t sg_, int64_t ray_, int first_, int ns_) {
-        const int jj = (int)(sg_ - first_) * 32 + lane;
-        if (jj < ns_) {
-            const int64_t kk = ray_ * S.cap + jj;
-            p_att = S.att[kk];
-            p_T = S.T[kk];
-            p_w = S.w[kk];
-            p_c4 = S.c[kk];
-            p_cl = S.cell[kk];
-            if (!NEAREST) p_f4 = S.f[kk];
-        }
-    };
-    if (q < nseg) fetch_rec(nx_sg, nx_ray, nx_first, nx_ns);
-#endif
     for (; q < nseg; q += nw) {
         const int64_t sg = nx_sg;
         const int64_t ray = nx_ray;
@@ -968,21 +947,12 @@ __global__ void __launch_bounds__(128, MINB)
         int4 cl = make_int4(0, 0, 0, 0);
         if (incl) {
             const int64_t k = ray * S.cap + j;
-#ifndef PLX_SCATTER_NO_PREFETCH
-            att = p_att;
-            Ti = p_T;
-            wi = p_w;
-            c4 = p_c4;
-            cl = p_cl;
-            f4 = p_f4;
-#else
             att = S.att[k];
             Ti = S.T[k];
             wi = S.w[k];
             c4 = S.c[k];
             cl = S.cell[k];
             if (!NEAREST) f4 = S.f[k];
-#endif
             if (G.identity) {
                 int32_t r8[8];
                 identity_rows<NEAREST>(G, cl, r8);
@@ -1074,9 +1044,6 @@ __global__ void __launch_bounds__(128, MINB)
         LaneAcc<NEAREST> ra;
         ra.init(lane, bf);
         if (qn < nseg) fetch2(nx_ray);
-#ifndef PLX_SCATTER_NO_PREFETCH
-        if (qn < nseg) fetch_rec(nx_sg, nx_ray, nx_first, nx_ns);
-#endif
         // delta of this sample (K:200-205): step, except at the last position
         const double dl = (double)cl.w == last_si ? dlt_last : O.step;
         const double cc0 = relu((double)c4.x), cc1 = relu((double)c4.y),
