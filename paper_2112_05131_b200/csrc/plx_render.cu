@@ -1260,6 +1260,13 @@ ScratchLayout layout(const plx_grid *g, const plx_render_opts *o, int64_t n_rays
     int64_t wave = kRecordBudget / (L.cap * kRecordBytes);
     if (wave < 1024) wave = 1024;
     if (n_rays > 0 && n_rays < wave) wave = n_rays;
+    // equal waves: a fixed-size wave left a small last wave (2^18 rays at
+    // 512^3: six waves of 43 K rays + one of 2.9 K) whose launches ran the
+    // kernels mostly as tails
+    if (n_rays > wave) {
+        const int64_t nw = (n_rays + wave - 1) / wave;
+        wave = (n_rays + nw - 1) / nw;
+    }
     L.wave = wave;
     const int64_t n = wave * L.cap;
     int64_t off = 256;
