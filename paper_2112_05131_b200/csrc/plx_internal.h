@@ -8,6 +8,17 @@
 #include "../../include/plx.h"
 
 namespace plx {
+// The 360 backward's background stage (plx_msi_render with gradients):
+// render_fused_bwd_impl runs msi_bg_kernel between the colour and scatter
+// kernels and the bounded kernels leave rgb / mse to it.
+struct MsiHook {
+    const double *data, *radii;   // background [L][H][W][4], radii [L]
+    int64_t L, H, W;
+    double lam_beta, beta_eps;
+    double *out_tfg, *out_trans;  // (N)
+    double *bg_grad;              // [L*H*W][4]
+    uint8_t *bg_tmask;
+};
 // plx_render_fused_bwd plus: idx_off = optional device int64 added to
 // rays->idx; counters_ready = the scratch's 3 counters were zeroed by the
 // caller (first wave only); after_march = optional cudaEvent_t recorded once
@@ -16,7 +27,8 @@ int render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const int64_t
                           const plx_render_opts *o, int32_t mse_mode, double up_scale,
                           double lam_cauchy, plx_grad *gb, double *out_rgb, double *out_sums,
                           void *scratch, int64_t scratch_bytes, void *stream,
-                          int counters_ready, void *after_march = nullptr);
+                          int counters_ready, void *after_march = nullptr,
+                          const MsiHook *msi = nullptr);
 // plx_opt_step plus: lr_dev = optional device {lr_sigma, lr_sh};
 // tcnt_ready = gb->tcnt was zeroed by the caller; host_sums = optional
 // pinned host double[4] that receives the guard's loss sums.

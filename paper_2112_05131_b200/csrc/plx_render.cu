@@ -28,6 +28,7 @@
 #include "plx_camera.cuh"
 #include "plx_common.cuh"
 #include "plx_internal.h"
+#include "plx_msi.cuh"
 
 namespace plx {
 
@@ -130,6 +131,7 @@ struct Outs {
     uint8_t *tmask;
     int mse_mode;
     double up_scale, lam_cauchy;
+    int bgmode;   // 360 backward: msi_bg_kernel owns rgb / mse and the background terms
 };
 
 // One march position evaluated by one lane.
@@ -199,7 +201,30 @@ struct Scratch {
     int4 *rows;        // 8 stencil rows                       [rays][cap][2]
     double *sig;       // sigma (Cauchy term only)
     double *seg_sum;   // [segments][6] {sum w c+ (RGB), sum c+ (bn - bi) (RGB)}
+    double *rgb_add;   // 360 mode: [rays][3] background colour T_fg C_bg (replaces T bg)
+    double *bup;       // 360 mode: [rays] beta-regulariser upstream (K:827-833)
 };
+
+// The ray's colour total sum_w w c+ from its segment sums, in the order every
+// consumer of the sums uses (short rays: in segment order per lane; long
+// rays: lane-strided partial sums + a warp reduction), so all of them see
+// bit-identical totals.
+__device__ __forceinline__ void ray_colour_totals(const Scratch &S, int64_t s0, int64_t s1,
+                                                  int lane, double &C0, double &C1, double &C2) {
+    C0 = C1 = C2 = 0.0;
+    const bool few = s1 - s0 <= 4;
+    for (int64_t t = few ? s0 : s0 + lane; t < s1; t += few ? 1 : 32) {
+        const double *p = S.seg_sum + 6 * t;
+        C0 += p[0];
+        C1 += p[1];
+        C2 += p[2];
+    }
+    if (!few) {
+        C0 = warp_sum(C0);
+        C1 = warp_sum(C1);
+        C2 = warp_sum(C2);
+    }
+}
 
 // The q-th segment the colour / scatter kernels take (allocation order) and
 // its ray.  (A spatial order -- counting sort of the segments into 16^3
@@ -551,7 +576,7 @@ __global__ void __launch_bounds__(128, MINB)
             S.ray_d[3 * ray + 2] = (double)(rm.nsamp - 1);
             if (nseg) sbase = atomicAdd(S.nseg_total, nseg);
             S.seg_first[ray] = sbase;
-            if (ns == 0) {   // nothing composited: rgb = T bg (K:324-341), no gradient
+            if (ns == 0 && !out.bgmode) {   // nothing composited: rgb = T bg (K:324-341), no gradient
                 const double c0 = T * O.bg[0], c1 = T * O.bg[1], c2 = T * O.bg[2];
                 if (out.rgb) {
                     out.rgb[3 * ray] = c0;
@@ -1011,9 +1036,12 @@ __global__ void __launch_bounds__(128, MINB)
         double P0 = B0, P1 = B1, P2 = B2;
         const double Tfin = S.ray_d[3 * ray], dlt_last = S.ray_d[3 * ray + 1],
                      last_si = S.ray_d[3 * ray + 2];
-        const double rgb0 = C0 + Tfin * O.bg[0], rgb1 = C1 + Tfin * O.bg[1],
-                     rgb2 = C2 + Tfin * O.bg[2];
-        const bool first = sg == s0;
+        // rgb = C + T bg (K:234-238); 360: C + the background's T_fg C_bg
+        const double X0 = S.rgb_add ? S.rgb_add[3 * ray] : Tfin * O.bg[0];
+        const double X1 = S.rgb_add ? S.rgb_add[3 * ray + 1] : Tfin * O.bg[1];
+        const double X2 = S.rgb_add ? S.rgb_add[3 * ray + 2] : Tfin * O.bg[2];
+        const double rgb0 = C0 + X0, rgb1 = C1 + X1, rgb2 = C2 + X2;
+        const bool first = sg == s0 && !out.bgmode;
         if (first && lane == 0 && out.rgb) {
             out.rgb[3 * ray + 0] = rgb0;
             out.rgb[3 * ray + 1] = rgb1;
@@ -1074,6 +1102,10 @@ __global__ void __launch_bounds__(128, MINB)
         if (incl && cauchy) {   // K:384-386
             cau_part += log(1.0 + 2.0 * sig * sig);
             gsig += out.lam_cauchy * 4.0 * sig / (1.0 + 2.0 * sig * sig);
+        }
+        if (S.bup) {   // 360: the beta regulariser on the foreground transmittance (K:858-859)
+            const double bup = S.bup[ray];
+            if (bup != 0.0) gsig += bup * (-dl * Tfin);
         }
         // ---- lane-parallel staging of the scatter payload (K:387-410) ----
         const unsigned below = mask & lt_mask;
@@ -1140,6 +1172,235 @@ __global__ void __launch_bounds__(128, MINB)
     if (lane == 0) {
         if (mse_part != 0.0) atomicAdd(out.sums + 0, mse_part);
         if (cau_part != 0.0) atomicAdd(out.sums + 1, cau_part);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// msi_bg_kernel -- the background stage of the 360 backward (K:749-833 and
+// the background half of K:835-881).  The foreground runs through the
+// bounded kernels (march_bwd_kernel, colour_kernel, scatter_kernel in
+// bgmode); between colour and scatter this kernel, one warp per ray, takes
+// the ray's foreground colour total and T_fg, samples the sphere layers past
+// the grid's exit (lane = layer, compacted in layer order), composites them
+// from T_fg over black, writes rgb / T_fg / T and the mse and beta sums, and
+// leaves the scatter two per-ray scalars: the background colour (the
+// foreground samples' reverse-sweep suffix rgb - P_i then includes it) and
+// the beta upstream.  The background samples' own reverse sweep and texel
+// scatter (f64 atomics) follow here: they come after every foreground
+// sample, so their suffix sums are background-only.
+struct MsiBgArgs {
+    MsiDev B;
+    double lam_beta, beta_eps;
+    double *tfg, *trans;     // (N) outputs
+    double *bg_grad;         // [L*H*W][4]
+    uint8_t *bg_tmask;
+};
+
+// Per-warp shared records of the background samples (dynamic shared memory,
+// L-1 crossings per warp).
+struct BgRecs {
+    double *t, *sig, *dlt, *T, *w, *c0, *c1, *c2;
+    int *lay;   // layer, or -1: not composited (sigma < 0 or past the stop)
+};
+
+__global__ void __launch_bounds__(128) msi_bg_kernel(DGrid G, RayArgs R, KOpts O, Outs out,
+                                                     Scratch S, MsiBgArgs M) {
+    extern __shared__ double bg_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nc = M.B.L - 1;   // crossings per ray at most
+    BgRecs rec;
+    {
+        double *base = bg_smem + (int64_t)warp * nc * 9;
+        rec.t = base;
+        rec.sig = base + nc;
+        rec.dlt = base + 2 * nc;
+        rec.T = base + 3 * nc;
+        rec.w = base + 4 * nc;
+        rec.c0 = base + 5 * nc;
+        rec.c1 = base + 6 * nc;
+        rec.c2 = base + 7 * nc;
+        rec.lay = reinterpret_cast<int *>(base + 8 * nc);
+    }
+    const unsigned lt = (1u << lane) - 1u;
+    double mse_part = 0.0, beta_part = 0.0;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t ray = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; ray < R.n; ray += nwarps) {
+        double o[3], d[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            o[a] = __ldg(R.origins + 3 * ray + a);
+            d[a] = __ldg(R.dirs + 3 * ray + a);
+        }
+        double Cf0 = 0.0, Cf1 = 0.0, Cf2 = 0.0;
+        const int ns = S.ns[ray];
+        if (ns > 0) {
+            const int64_t s0 = S.seg_first[ray];
+            ray_colour_totals(S, s0, s0 + ((ns + 31) >> 5), lane, Cf0, Cf1, Cf2);
+        }
+        const double tfg = S.ray_d[3 * ray];
+        double T = tfg, A = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
+        int nx = 0;
+        if (T >= O.stop) {   // K:749-803
+            double t0a, t1a;
+            ray_aabb(o, d, G.lo, G.hi, t0a, t1a);
+            const double t_exit = t1a > 0.0 ? t1a : 0.0;
+            const double bdot = o[0] * d[0] + o[1] * d[1] + o[2] * d[2];
+            const double c0n = o[0] * o[0] + o[1] * o[1] + o[2] * o[2];
+            for (int l0 = 0; l0 < nc; l0 += 32) {
+                const int l = l0 + lane;
+                bool hit = false;
+                double tl = 0.0;
+                if (l < nc) {
+                    const double rad = __ldg(M.B.radii + l);
+                    const double disc = bdot * bdot - c0n + rad * rad;
+                    if (disc > 0.0) {
+                        tl = -bdot + sqrt(disc);
+                        hit = !(tl < t_exit);
+                    }
+                }
+                const unsigned hm = __ballot_sync(PLX_FULL_MASK, hit);
+                if (hit) {
+                    const int q = nx + __popc(hm & lt);
+                    rec.t[q] = tl;
+                    rec.lay[q] = l;
+                }
+                nx += __popc(hm);
+            }
+            __syncwarp();
+            bool stopped = false;
+            for (int q0 = 0; q0 < nx; q0 += 32) {
+                const int q = q0 + lane;
+                bool incl = false;
+                double att = 1.0, sig = 0.0, dlt = 0.0, o4[4] = {0.0, 0.0, 0.0, 0.0};
+                if (q < nx && !stopped) {
+                    if (q + 1 < nx) dlt = rec.t[q + 1] - rec.t[q];
+                    else if (q >= 1) dlt = rec.t[q] - rec.t[q - 1];
+                    else dlt = 1.0;
+                    const double t = rec.t[q];
+                    int idx4[4];
+                    double w4[4];
+                    bg_stencil(M.B.H, M.B.W, o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2],
+                               idx4, w4);
+                    bg_fetch(M.B, rec.lay[q], idx4, w4, o4);
+                    sig = o4[0];
+                    incl = sig >= 0.0;
+                    if (incl) att = exp(-sig * dlt);
+                }
+                double Ti = 0.0, wi = 0.0;
+                if (__any_sync(PLX_FULL_MASK, incl))
+                    composite_chunk<false>(incl, att, lane, O.stop, T, A, Ti, wi, stopped);
+                if (q < nx) {
+                    rec.sig[q] = sig;
+                    rec.dlt[q] = dlt;
+                    rec.T[q] = Ti;
+                    rec.w[q] = wi;
+                    rec.c0[q] = o4[1];
+                    rec.c1[q] = o4[2];
+                    rec.c2[q] = o4[3];
+                    if (!incl) rec.lay[q] = -1;
+                }
+                if (incl) {
+                    if (o4[1] > 0.0) b0 += wi * o4[1];
+                    if (o4[2] > 0.0) b1 += wi * o4[2];
+                    if (o4[3] > 0.0) b2 += wi * o4[3];
+                }
+            }
+            __syncwarp();
+        }
+        const double Cb0 = warp_sum(b0), Cb1 = warp_sum(b1), Cb2 = warp_sum(b2);
+        const double cr = Cf0 + Cb0, cg = Cf1 + Cb1, cb = Cf2 + Cb2;
+        if (lane == 0) {
+            if (out.rgb) {
+                out.rgb[3 * ray] = cr;
+                out.rgb[3 * ray + 1] = cg;
+                out.rgb[3 * ray + 2] = cb;
+            }
+            M.tfg[ray] = tfg;
+            M.trans[ray] = T;
+            S.rgb_add[3 * ray] = Cb0;
+            S.rgb_add[3 * ray + 1] = Cb1;
+            S.rgb_add[3 * ray + 2] = Cb2;
+        }
+        // upstream, beta regulariser (K:808-833)
+        double up0, up1, up2;
+        if (out.mse_mode) {
+            const double e0 = cr - ray_tgt(R, ray, 0), e1 = cg - ray_tgt(R, ray, 1),
+                         e2 = cb - ray_tgt(R, ray, 2);
+            if (lane == 0) mse_part += e0 * e0 + e1 * e1 + e2 * e2;
+            up0 = out.up_scale * e0;
+            up1 = out.up_scale * e1;
+            up2 = out.up_scale * e2;
+        } else {
+            up0 = ray_tgt(R, ray, 0);
+            up1 = ray_tgt(R, ray, 1);
+            up2 = ray_tgt(R, ray, 2);
+        }
+        double tc = tfg;
+        if (tc < M.beta_eps) tc = M.beta_eps;
+        if (tc > 1.0 - M.beta_eps) tc = 1.0 - M.beta_eps;
+        if (M.lam_beta > 0.0 && lane == 0) beta_part += log(tc) + log(1.0 - tc);
+        double bup = 0.0;
+        if (M.lam_beta > 0.0 && M.beta_eps < tfg && tfg < 1.0 - M.beta_eps)
+            bup = M.lam_beta * (1.0 / tc - 1.0 / (1.0 - tc));
+        if (lane == 0) S.bup[ray] = bup;
+        // background reverse sweep + texel scatter (K:835-881, lay >= 0)
+        double sf0 = 0.0, sf1 = 0.0, sf2 = 0.0;
+        for (int q0 = ((nx - 1) >> 5) << 5; q0 >= 0; q0 -= 32) {
+            const int q = q0 + lane;
+            const bool valid = q < nx && rec.lay[q] >= 0;
+            double sig = 0.0, dlt = 0.0, Ti = 0.0, w = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+            if (valid) {
+                sig = rec.sig[q];
+                dlt = rec.dlt[q];
+                Ti = rec.T[q];
+                w = rec.w[q];
+                c0 = rec.c0[q];
+                c1 = rec.c1[q];
+                c2 = rec.c2[q];
+            }
+            const double cc0 = c0 > 0.0 ? c0 : 0.0, cc1 = c1 > 0.0 ? c1 : 0.0,
+                         cc2 = c2 > 0.0 ? c2 : 0.0;
+            const double y0 = valid ? w * cc0 : 0.0, y1 = valid ? w * cc1 : 0.0,
+                         y2 = valid ? w * cc2 : 0.0;
+            const double i0 = warp_scan_add(y0, lane), i1 = warp_scan_add(y1, lane),
+                         i2 = warp_scan_add(y2, lane);
+            const double tot0 = __shfl_sync(PLX_FULL_MASK, i0, 31),
+                         tot1 = __shfl_sync(PLX_FULL_MASK, i1, 31),
+                         tot2 = __shfl_sync(PLX_FULL_MASK, i2, 31);
+            const double s0 = sf0 + (tot0 - i0), s1 = sf1 + (tot1 - i1), s2 = sf2 + (tot2 - i2);
+            sf0 += tot0;
+            sf1 += tot1;
+            sf2 += tot2;
+            if (valid) {
+                const double att = exp(-sig * dlt);
+                const double gsig = dlt * (up0 * (Ti * att * cc0 - s0) + up1 * (Ti * att * cc1 - s1) +
+                                           up2 * (Ti * att * cc2 - s2));
+                const double t = rec.t[q];
+                const int lay = rec.lay[q];
+                int idx4[4];
+                double w4[4];
+                bg_stencil(M.B.H, M.B.W, o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2], idx4,
+                           w4);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int64_t flat = (int64_t)lay * M.B.H * M.B.W + idx4[k];
+                    const double wq = w4[k];
+                    M.bg_tmask[flat] = 1;
+                    double *gb = M.bg_grad + 4 * flat;
+                    atomicAdd(gb, wq * gsig);
+                    if (c0 > 0.0) atomicAdd(gb + 1, wq * up0 * w);
+                    if (c1 > 0.0) atomicAdd(gb + 2, wq * up1 * w);
+                    if (c2 > 0.0) atomicAdd(gb + 3, wq * up2 * w);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    mse_part = warp_sum(mse_part);
+    beta_part = warp_sum(beta_part);
+    if (lane == 0) {
+        if (mse_part != 0.0) atomicAdd(out.sums + 0, mse_part);
+        if (beta_part != 0.0) atomicAdd(out.sums + 2, beta_part);
     }
 }
 }  // namespace plx
@@ -1250,7 +1511,7 @@ struct ScratchLayout {
     int64_t wave, cap, bytes;
     int nseg_max;
     int64_t off_ns, off_segfirst, off_segray, off_rayd, off_basis, off_att, off_T, off_w, off_c, off_cell, off_f, off_rows,
-        off_sig, off_segsum;
+        off_sig, off_segsum, off_rgbadd, off_bup;
 };
 
 ScratchLayout layout(const plx_grid *g, const plx_render_opts *o, int64_t n_rays) {
@@ -1289,6 +1550,8 @@ ScratchLayout layout(const plx_grid *g, const plx_render_opts *o, int64_t n_rays
     L.off_rows = take(n * 32);
     L.off_sig = take(n * 8);
     L.off_segsum = take(wave * L.nseg_max * 48);
+    L.off_rgbadd = take(wave * 24);
+    L.off_bup = take(wave * 8);
     L.bytes = off;
     return L;
 }
@@ -1361,7 +1624,8 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
                                const plx_render_opts *o, int32_t mse_mode, double up_scale,
                                double lam_cauchy, plx_grad *gb, double *out_rgb,
                                double *out_sums, void *scratch, int64_t scratch_bytes,
-                               void *stream, int counters_ready, void *after_march) {
+                               void *stream, int counters_ready, void *after_march,
+                               const MsiHook *msi) {
     if (!gb || !gb->grad || !gb->tmask || !out_sums) return PLX_EINVAL;
     const int rc = check_rays(g, rays, o, true);
     if (rc != PLX_OK) return rc;
@@ -1393,6 +1657,8 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
     S.rows = reinterpret_cast<int4 *>(base + L.off_rows);
     S.sig = lam_cauchy > 0.0 ? reinterpret_cast<double *>(base + L.off_sig) : nullptr;
     S.seg_sum = reinterpret_cast<double *>(base + L.off_segsum);
+    S.rgb_add = msi ? reinterpret_cast<double *>(base + L.off_rgbadd) : nullptr;
+    S.bup = msi ? reinterpret_cast<double *>(base + L.off_bup) : nullptr;
     cudaStream_t s = (cudaStream_t)stream;
     const int sms = num_sms();
     for (int64_t w0 = 0; w0 < rays->n; w0 += L.wave) {
@@ -1416,6 +1682,7 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
         out.mse_mode = mse_mode;
         out.up_scale = up_scale;
         out.lam_cauchy = lam_cauchy;
+        out.bgmode = msi != nullptr;
         // ray counter, segment counter, colour scheduler (zeroed by the
         // native step's prologue kernel for the first wave)
         if (!(counters_ready && w0 == 0) &&
@@ -1443,6 +1710,21 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
                              : resident_blocks(scatter_kernel<false, false, kScatterMinB>);
         }
         PLX_DISPATCH(o, colour_kernel, kColourMinB, dim3((unsigned)(sms * cb)), G, R, S);
+        if (msi) {   // 360: the background stage between colour and scatter
+            MsiBgArgs M{{msi->data, msi->radii, (int)msi->L, (int)msi->H, (int)msi->W},
+                        msi->lam_beta, msi->beta_eps, msi->out_tfg + w0, msi->out_trans + w0,
+                        msi->bg_grad, msi->bg_tmask};
+            const size_t smem = (size_t)kWarps * (msi->L - 1) * 9 * sizeof(double);
+            static bool smem_set = false;
+            if (!smem_set) {   // up to kMaxCross crossings per warp (74 KB per block)
+                cudaFuncSetAttribute(msi_bg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kWarps * kMaxCross * 9 * (int)sizeof(double));
+                smem_set = true;
+            }
+            int64_t nb = (nw + kWarps - 1) / kWarps;
+            if (nb > (int64_t)sms * 8) nb = (int64_t)sms * 8;
+            msi_bg_kernel<<<(unsigned)nb, kThreads, smem, s>>>(G, R, K, out, S, M);
+        }
         PLX_DISPATCH(o, scatter_kernel, kScatterMinB, dim3((unsigned)(sms * sb)), G, R, K, out, S);
     }
     return cudaPeekAtLastError() == cudaSuccess ? PLX_OK : PLX_ECUDA;

@@ -110,6 +110,21 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if os.environ.get("MSI_PROFILE"):   # per-kernel device times of the render (CUPTI)
+        from collections import defaultdict
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for _ in range(10):
+                render()
+                grads.clear()
+                bgg.clear()
+            torch.cuda.synchronize()
+        agg = defaultdict(float)
+        for ev_ in prof.events():
+            if ev_.device_type.name == "CUDA":
+                agg[ev_.name[:60]] += ev_.device_time / 10
+        for k_, v_ in sorted(agg.items(), key=lambda kv: -kv[1]):
+            print(f"{v_:9.1f} us/render  {k_}", file=sys.stderr)
     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     t_render = t_step = 0.0
     for _ in range(args.steps):

@@ -41,20 +41,18 @@ print(f"warps {len(a)}  kernel {T:.1f} us  starts within {start.max():.1f} us")
 for q in (0.5, 0.75, 0.9, 0.99):
     print(f"  {int(q * 100)}% of warps done at {ends[int(q * len(ends)) - 1]:.1f} us")
 
-# per-ray phase times vs march positions / samples
+# per-ray march times (start, end, positions)
 L.plx_debug_raylog.argtypes = [ctypes.c_void_p, ctypes.c_int]
-rb = (ctypes.c_ulonglong * (4 * 5000))()
+rb = (ctypes.c_ulonglong * (3 * 5000))()
 L.plx_debug_raylog(rb, 5000)
-r = np.array(rb, dtype=np.uint64).reshape(5000, 4)
-tA, tB, tC = r[:, 0] / 1e3, r[:, 1] / 1e3, r[:, 2] / 1e3
-pos, ns = (r[:, 3] >> np.uint64(32)).astype(np.int64), (r[:, 3] & np.uint64(0xffffffff)).astype(np.int64)
-tot = tA + tB + tC
-print(f"per ray (us): A {tA.mean():.1f}  B {tB.mean():.1f}  C {tC.mean():.1f}  total mean "
-      f"{tot.mean():.1f} p90 {np.percentile(tot, 90):.1f} max {tot.max():.1f}")
-print(f"  positions mean {pos.mean():.0f} max {pos.max()}  samples mean {ns.mean():.0f} max {ns.max()}")
-top = np.argsort(-tot)[:8]
-for i in top:
-    print(f"  ray {i:5d}: {tot[i]:6.1f} us  A {tA[i]:5.1f} B {tB[i]:5.1f} C {tC[i]:5.1f}  "
-          f"pos {pos[i]} samples {ns[i]}")
-print(f"  A us per 32 positions {np.sum(tA) / (np.sum(pos) / 32):.2f}; B+C us per 32 samples "
-      f"{np.sum(tB + tC) / max(np.sum(ns) / 32, 1):.2f}")
+r = np.array(rb, dtype=np.float64).reshape(5000, 3)
+rs, re, rp = (r[:, 0] - t0) / 1e3, (r[:, 1] - t0) / 1e3, r[:, 2]
+dur = re - rs
+print(f"rays: duration mean {dur.mean():.1f} us, p50 {np.median(dur):.1f}, max {dur.max():.1f}; "
+      f"positions mean {rp.mean():.0f}, max {rp.max():.0f}; ns/position {1e3 * dur.sum() / rp.sum():.2f}")
+late = rs > np.percentile(rs, 60)
+print(f"rays started after the first wave: {int((rs > 1.0).sum())}, their mean duration {dur[rs > 1.0].mean():.1f} us, "
+      f"first-wave rays {dur[rs <= 1.0].mean():.1f} us")
+for t in range(0, int(T) + 5, 5):
+    act = int(((start <= t) & (end > t)).sum())
+    print(f"  t={t:4d} us  active warps {act}")
