@@ -107,7 +107,10 @@ __device__ __forceinline__ double clamp_coord(double p, double lo, double scale,
     return g;
 }
 
-__device__ __forceinline__ int64_t flat(const DGrid &G, int64_t i, int64_t j, int64_t k) {
+// Flat C-order lattice index; 32-bit (plx_grid dims are checked to hold
+// fewer than 2^31 points), as are the coordinates and corner offsets below:
+// 64-bit index math was an eighth of the march's instructions.
+__device__ __forceinline__ int32_t flat(const DGrid &G, int32_t i, int32_t j, int32_t k) {
     return (i * G.Dy + j) * G.Dz + k;
 }
 
@@ -134,7 +137,7 @@ __device__ __forceinline__ void ray_march_setup(RayMarch &rm, const DGrid &G, do
 // Lattice coordinates of sample si (K:203-208): t, delta, g.
 __device__ __forceinline__ void sample_coords(const RayMarch &rm, const DGrid &G, double step,
                                               int64_t si, double &t, double &dlt, double *g) {
-    t = rm.t0 + (double)si * step;
+    t = rm.t0 + (double)(int32_t)si * step;   // si < nsamp <= the record capacity
     dlt = si < rm.nsamp - 1 ? step : rm.L - step * (double)(rm.nsamp - 1);
 #pragma unroll
     for (int a = 0; a < 3; ++a) g[a] = clamp_coord(rm.o[a] + t * rm.d[a], G.lo[a], G.scale[a], G.dmax[a]);
@@ -148,26 +151,26 @@ template <bool NEAREST>
 __device__ __forceinline__ int stencil(const DGrid &G, const double *g, int32_t *rows, double *f,
                                        bool &any_occ, int *ijk) {
     if (NEAREST) {
-        int64_t i = (int64_t)(g[0] + 0.5), j = (int64_t)(g[1] + 0.5), k = (int64_t)(g[2] + 0.5);
+        int32_t i = (int32_t)(g[0] + 0.5), j = (int32_t)(g[1] + 0.5), k = (int32_t)(g[2] + 0.5);
         if (i > G.Dx - 1) i = G.Dx - 1;
         if (j > G.Dy - 1) j = G.Dy - 1;
         if (k > G.Dz - 1) k = G.Dz - 1;
-        ijk[0] = (int)i;
-        ijk[1] = (int)j;
-        ijk[2] = (int)k;
+        ijk[0] = i;
+        ijk[1] = j;
+        ijk[2] = k;
         rows[0] = __ldg(G.links + flat(G, i, j, k));
         any_occ = rows[0] >= 0;
         return 1;
     }
-    int64_t i0 = (int64_t)g[0], j0 = (int64_t)g[1], k0 = (int64_t)g[2];
+    int32_t i0 = (int32_t)g[0], j0 = (int32_t)g[1], k0 = (int32_t)g[2];
     if (i0 > G.Dx - 2) i0 = G.Dx - 2;
     if (j0 > G.Dy - 2) j0 = G.Dy - 2;
     if (k0 > G.Dz - 2) k0 = G.Dz - 2;
-    ijk[0] = (int)i0;
-    ijk[1] = (int)j0;
-    ijk[2] = (int)k0;
+    ijk[0] = i0;
+    ijk[1] = j0;
+    ijk[2] = k0;
     if (G.cell_occ) {
-        int64_t c = flat(G, i0, j0, k0);
+        const int32_t c = flat(G, i0, j0, k0);
         if (!((__ldg(G.cell_occ + (c >> 5)) >> (c & 31)) & 1u)) {
             any_occ = false;
             return 8;
@@ -177,7 +180,7 @@ __device__ __forceinline__ int stencil(const DGrid &G, const double *g, int32_t 
     f[1] = g[1] - (double)j0;
     f[2] = g[2] - (double)k0;
     const int32_t *base = G.links + flat(G, i0, j0, k0);
-    const int64_t sy = G.Dz, sx = (int64_t)G.Dy * G.Dz;
+    const int32_t sy = G.Dz, sx = G.Dy * G.Dz;
     bool occ = false;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -192,9 +195,9 @@ __device__ __forceinline__ int stencil(const DGrid &G, const double *g, int32_t 
 // Stencil rows of a base cell / lattice point (K:84-123), -1 = empty.
 template <bool NEAREST>
 __device__ __forceinline__ void load_rows(const DGrid &G, const int *ijk, int32_t *rows) {
-    const int64_t c = flat(G, ijk[0], ijk[1], ijk[2]);
+    const int32_t c = flat(G, ijk[0], ijk[1], ijk[2]);
     if (G.identity) {   // dense identity-linked grid: row = lattice point
-        const int64_t sy = G.Dz, sx = (int64_t)G.Dy * G.Dz;
+        const int32_t sy = G.Dz, sx = G.Dy * G.Dz;
         rows[0] = (int32_t)c;
         if (!NEAREST) {
 #pragma unroll
@@ -208,7 +211,7 @@ __device__ __forceinline__ void load_rows(const DGrid &G, const int *ijk, int32_
         rows[0] = __ldg(base);
         return;
     }
-    const int64_t sy = G.Dz, sx = (int64_t)G.Dy * G.Dz;
+    const int32_t sy = G.Dz, sx = G.Dy * G.Dz;
 #pragma unroll
     for (int q = 0; q < 8; ++q) rows[q] = __ldg(base + ((q >> 2) & 1) * sx + ((q >> 1) & 1) * sy + (q & 1));
 }
@@ -378,32 +381,32 @@ __device__ __forceinline__ bool sigma_at(const DGrid &G, const double *g, double
         return true;
     }
     if (NEAREST) {
-        int64_t i = (int64_t)(g[0] + 0.5), j = (int64_t)(g[1] + 0.5), k = (int64_t)(g[2] + 0.5);
+        int32_t i = (int32_t)(g[0] + 0.5), j = (int32_t)(g[1] + 0.5), k = (int32_t)(g[2] + 0.5);
         if (i > G.Dx - 1) i = G.Dx - 1;
         if (j > G.Dy - 1) j = G.Dy - 1;
         if (k > G.Dz - 1) k = G.Dz - 1;
-        ijk[0] = (int)i;
-        ijk[1] = (int)j;
-        ijk[2] = (int)k;
+        ijk[0] = i;
+        ijk[1] = j;
+        ijk[2] = k;
         const float s = G.sigma_lat[flat(G, i, j, k)];
         if (s != s) return false;
         sig = stencil_w<NEAREST>(f, 0) * (double)s;
         return true;
     }
-    int64_t i0 = (int64_t)g[0], j0 = (int64_t)g[1], k0 = (int64_t)g[2];
+    int32_t i0 = (int32_t)g[0], j0 = (int32_t)g[1], k0 = (int32_t)g[2];
     if (i0 > G.Dx - 2) i0 = G.Dx - 2;
     if (j0 > G.Dy - 2) j0 = G.Dy - 2;
     if (k0 > G.Dz - 2) k0 = G.Dz - 2;
-    ijk[0] = (int)i0;
-    ijk[1] = (int)j0;
-    ijk[2] = (int)k0;
-    const int64_t c = flat(G, i0, j0, k0);
+    ijk[0] = i0;
+    ijk[1] = j0;
+    ijk[2] = k0;
+    const int32_t c = flat(G, i0, j0, k0);
     if (G.cell_occ && !((__ldg(G.cell_occ + (c >> 5)) >> (c & 31)) & 1u)) return false;
     f[0] = g[0] - (double)i0;
     f[1] = g[1] - (double)j0;
     f[2] = g[2] - (double)k0;
     const float *base = G.sigma_lat + c;
-    const int64_t sy = G.Dz, sx = (int64_t)G.Dy * G.Dz;
+    const int32_t sy = G.Dz, sx = G.Dy * G.Dz;
     float s[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) s[q] = base[((q >> 2) & 1) * sx + ((q >> 1) & 1) * sy + (q & 1)];
