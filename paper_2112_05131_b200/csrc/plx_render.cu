@@ -274,7 +274,9 @@ __device__ __forceinline__ int axis_bits(int mv) {
 // lanes 0..27 = 4 corners x 7 column quads, each lane expands its quad from
 // (at most two) components times the ray's basis into one
 // red.global.add.v4.f32.
-template <bool NEAREST>
+// DIAG (diagnostic builds, -DPLX_DIAG only; profiles/r2b_diag.md): 1 = no
+// reductions, 2 = reductions into an L2-resident 8 MB window.
+template <bool NEAREST, int DIAG = 0>
 struct LaneAcc {
     float acc;          // this lane's partial sum
     int32_t row;        // row of this lane's corner, -1 = empty / none
@@ -329,9 +331,16 @@ struct LaneAcc {
             const float v1 = ((hisel & 2u) ? ahi : alo) * cb[1];
             const float v2 = ((hisel & 4u) ? ahi : alo) * cb[2];
             const float v3 = ((hisel & 8u) ? ahi : alo) * cb[3];
-            if (quad == 0) tmask[r] = 1;
-            if (v0 != 0.f || v1 != 0.f || v2 != 0.f || v3 != 0.f)
-                red_add_v4(grad + (int64_t)r * PLX_STRIDE + 4 * quad, v0, v1, v2, v3);
+            if (DIAG == 1) {
+                if (v0 == 1.2345e-30f) red_add_v4(grad + 4 * quad, v0, v1, v2, v3);
+            } else if (DIAG == 2) {
+                if (v0 != 0.f || v1 != 0.f || v2 != 0.f || v3 != 0.f)
+                    red_add_v4(grad + (int64_t)(r & 0xffff) * PLX_STRIDE + 4 * quad, v0, v1, v2, v3);
+            } else {
+                if (quad == 0) tmask[r] = 1;
+                if (v0 != 0.f || v1 != 0.f || v2 != 0.f || v3 != 0.f)
+                    red_add_v4(grad + (int64_t)r * PLX_STRIDE + 4 * quad, v0, v1, v2, v3);
+            }
         }
         if (NEAREST || (((q ^ flip) & bit) != 0) == (side != 0)) {
             acc = 0.f;
@@ -661,7 +670,8 @@ __device__ __forceinline__ unsigned shared_corner_mask(int4 c, int4 p, int &ob) 
 // rows (that version ran at 70 % of the L1 throughput limit).  Each row's 3
 // dot products are reduced over its 8 lanes and staged in shared memory;
 // every lane then forms its sample's colour from 8 staged d's.
-template <bool ABS, bool NEAREST, int MINB>
+// DIAG 1 (diagnostic builds only): every row load from an L2-resident window.
+template <bool ABS, bool NEAREST, int MINB, int DIAG = 0>
 __global__ void __launch_bounds__(128, MINB)
     colour_kernel(DGrid G, RayArgs R, Scratch S) {
     R.idx = ray_index(R);
@@ -836,7 +846,8 @@ __global__ void __launch_bounds__(128, MINB)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int rr = r0 + 4 * u + sub;
-                const int32_t row = rr < nrow ? sm.urow[rr] : -1;
+                const int32_t row =
+                    rr < nrow ? (DIAG == 1 ? (sm.urow[rr] & 0xffff) : sm.urow[rr]) : -1;
                 v[u] = (row >= 0 && part < 7)
                            ? __ldg(reinterpret_cast<const float4 *>(G.table + (int64_t)row * PLX_STRIDE) + part)
                            : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -925,7 +936,7 @@ __global__ void __launch_bounds__(128, MINB)
     }
 }
 
-template <bool ABS, bool NEAREST, int MINB>
+template <bool ABS, bool NEAREST, int MINB, int DIAG = 0>
 __global__ void __launch_bounds__(128, MINB)
     scatter_kernel(DGrid G, RayArgs R, KOpts O, Outs out, Scratch S) {
     R.idx = ray_index(R);
@@ -1069,7 +1080,7 @@ __global__ void __launch_bounds__(128, MINB)
         const double bend = Tfin > 0.0 ? 1.0 : 0.0;
         float bf[9];
         ray_basis_rec(S, ray, bf);
-        LaneAcc<NEAREST> ra;
+        LaneAcc<NEAREST, DIAG> ra;
         ra.init(lane, bf);
         if (qn < nseg) fetch2(nx_ray);
         // delta of this sample (K:200-205): step, except at the last position
@@ -1709,6 +1720,34 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
             sb = o->absolute ? resident_blocks(scatter_kernel<true, false, kScatterMinB>)
                              : resident_blocks(scatter_kernel<false, false, kScatterMinB>);
         }
+#ifdef PLX_DIAG
+        // diagnostic builds (profiles/r2b_diag.md): PLX_DIAG_MODE bit 1 / 2 /
+        // 4 launches the colour (L2-resident rows) / scatter (no reductions)
+        // / scatter (L2-resident reductions) variant BEFORE the real kernel;
+        // its outputs are overwritten or go to a private buffer
+        if (!o->nearest && !o->absolute && !msi) {
+            static const int diag = getenv("PLX_DIAG_MODE") ? atoi(getenv("PLX_DIAG_MODE")) : 0;
+            static float *dgrad = nullptr;
+            static double *dsums = nullptr;
+            if (diag && !dgrad) {
+                cudaMalloc(&dgrad, (size_t)65536 * PLX_STRIDE * sizeof(float));
+                cudaMalloc(&dsums, 64);
+            }
+            Outs dout = out;
+            dout.rgb = nullptr;
+            dout.sums = dsums;
+            dout.grad = dgrad;
+            if (diag & 1) {
+                colour_kernel<false, false, kColourMinB, 1><<<sms * cb, kThreads, 0, s>>>(G, R, S);
+                cudaMemsetAsync(S.counter + 2, 0, sizeof(int), s);   // colour scheduler
+            }
+            PLX_DISPATCH(o, colour_kernel, kColourMinB, dim3((unsigned)(sms * cb)), G, R, S);
+            if (diag & 2)
+                scatter_kernel<false, false, kScatterMinB, 1><<<sms * sb, kThreads, 0, s>>>(G, R, K, dout, S);
+            if (diag & 4)
+                scatter_kernel<false, false, kScatterMinB, 2><<<sms * sb, kThreads, 0, s>>>(G, R, K, dout, S);
+        } else
+#endif
         PLX_DISPATCH(o, colour_kernel, kColourMinB, dim3((unsigned)(sms * cb)), G, R, S);
         if (msi) {   // 360: the background stage between colour and scatter
             MsiBgArgs M{{msi->data, msi->radii, (int)msi->L, (int)msi->H, (int)msi->W},
