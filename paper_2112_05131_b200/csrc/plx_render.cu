@@ -1515,7 +1515,12 @@ int64_t max_records(const plx_grid *g, double step) {
 
 // Records are kept for every march position of the longest chord of every
 // ray of a wave; a batch larger than the budget runs in waves.
-constexpr int64_t kRecordBudget = (int64_t)8 << 30;   // bytes of records per wave
+// Record budget per wave: 32 GiB of a 180 GB B200 (C5 sweep, 2^18..2^20
+// rays: 8 GiB waves 29.4 / 32.8 / 35.0 M rays/s, 32 GiB 30.4 / 33.7 / 36.0).
+#ifndef PLX_RECORD_GIB
+#define PLX_RECORD_GIB 32
+#endif
+constexpr int64_t kRecordBudget = (int64_t)PLX_RECORD_GIB << 30;   // bytes of records per wave
 constexpr int64_t kRecordBytes = 112;                 // att, T, w, c, cell, f, rows, sig
 
 struct ScratchLayout {
