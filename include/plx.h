@@ -364,8 +364,9 @@ typedef struct {
     int32_t *tids;         /* [L*H*W] compacted list (plx_msi_opt_step)      */
     int64_t *tcnt;         /* device int64                                    */
 } plx_msi_grad;
-/* Scratch for plx_msi_render (per-ray records; rays are processed in waves
- * that fit the scratch).  -1 on bad arguments. */
+/* Scratch for plx_msi_render: with gradients the foreground runs through the
+ * bounded backward (plx_render_fused_bwd's records, in waves) plus a
+ * background stage; forward only needs a ray counter.  -1 on bad arguments. */
 int64_t plx_msi_scratch_bytes(const plx_grid *g, const plx_msi *bg, const plx_render_opts *o,
                               int64_t n_rays);
 /* msi.render_rays_with_background (msi.py:130-183 -> K:661-881): rays.
