@@ -297,6 +297,19 @@ int64_t plx_scan_scratch_bytes(int64_t n);
 int plx_scan_ids(const uint8_t *flags, int64_t n, int32_t *ids, int64_t *count,
                  void *scratch, void *stream);
 
+/* SparseGrid.sample (G:182-200) at n world points pts (n,3) float64 inside
+ * the AABB (the caller checks, G:147-151): out (n,28) float64 = the
+ * interpolated (sigma, 27 SH) over occupied stencil corners, sigma clamped
+ * at 0.  nearest: the nearest lattice point (G:158-163). */
+int plx_grid_sample(const plx_grid *g, const double *pts, int64_t n, int32_t nearest,
+                    double *out, void *stream);
+/* SparseGrid.sample_backward (G:202-223): upstream (n,28) float64 dL/d(sigma,
+ * SH); w_q * upstream added to every occupied stencil row of each point
+ * (f32 atomics; the row is marked touched), the sigma entry dropped where the
+ * interpolated sigma is negative. */
+int plx_grid_sample_backward(const plx_grid *g, const double *pts, const double *upstream,
+                             int64_t n, int32_t nearest, plx_grad *gb, void *stream);
+
 /* Empty-space skipping helper: cell_occ bit (i,j,k) for every trilinear base
  * cell (i<Dx-1, j<Dy-1, k<Dz-1; stored over the full Dx*Dy*Dz index space)
  * = any of the 8 corner links >= 0.  Must be rebuilt after prune/upsample. */

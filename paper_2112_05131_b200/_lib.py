@@ -140,6 +140,9 @@ _SIGS = {
     "plx_build_cell_occ": [ctypes.POINTER(PlxGrid), _P, _P],
     "plx_build_sigma_lat": [ctypes.POINTER(PlxGrid), _P, _P],
     "plx_build_row_cell": [ctypes.POINTER(PlxGrid), _P, _P],
+    "plx_grid_sample": [ctypes.POINTER(PlxGrid), _P, _I64, _I32, _P, _P],
+    "plx_grid_sample_backward": [ctypes.POINTER(PlxGrid), _P, _P, _I64, _I32,
+                                 ctypes.POINTER(PlxGrad), _P],
     "plx_train_step": [ctypes.POINTER(PlxGrid), ctypes.POINTER(PlxGrad),
                        ctypes.POINTER(PlxStepArgs), _P],
     "plx_msi_scratch_bytes": [ctypes.POINTER(PlxGrid), ctypes.POINTER(PlxMsi),

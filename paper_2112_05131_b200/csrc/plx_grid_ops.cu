@@ -1158,6 +1158,134 @@ extern "C" int plx_build_row_cell(const plx_grid *g, int32_t *row_cell, void *st
     return status();
 }
 
+// ------------------------------------------------ point sampling ---------
+// SparseGrid.sample / sample_backward (G:154-223): the stencil of arbitrary
+// world points in the reference's numpy order (float64 lattice coordinates,
+// clipped, trilinear weights wx*wy*wz or the nearest point), one thread per
+// point.  sample: out[n][28] = sum_q w_q table[row_q] over occupied corners,
+// column 0 (sigma) clamped at zero.  backward: upstream * w_q added to every
+// occupied corner row (touching it), the sigma entry masked where the
+// interpolated sigma is negative.
+template <bool NEAREST>
+__device__ __forceinline__ int point_stencil(const DGrid &G, const double *p, int32_t *rows,
+                                             double *w) {
+    double g[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) g[a] = clamp_coord(p[a], G.lo[a], G.scale[a], G.dmax[a]);
+    int ijk[3];
+    if (NEAREST) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int D = a == 0 ? G.Dx : a == 1 ? G.Dy : G.Dz;
+            int i = (int)floor(g[a] + 0.5);
+            ijk[a] = i > D - 1 ? D - 1 : i;
+        }
+        rows[0] = __ldg(G.links + flat(G, ijk[0], ijk[1], ijk[2]));
+        w[0] = 1.0;
+        return 1;
+    }
+    double f[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const int D = a == 0 ? G.Dx : a == 1 ? G.Dy : G.Dz;
+        int i = (int)floor(g[a]);
+        ijk[a] = i > D - 2 ? D - 2 : i;
+        f[a] = g[a] - (double)ijk[a];
+    }
+    load_rows<false>(G, ijk, rows);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) w[q] = stencil_w<false>(f, q);
+    return 8;
+}
+
+template <bool NEAREST>
+__global__ void grid_sample_kernel(DGrid G, const double *pts, int64_t n, double *out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t rows[8];
+        double w[8];
+        const int nq = point_stencil<NEAREST>(G, pts + 3 * i, rows, w);
+        double acc[28];
+#pragma unroll
+        for (int c = 0; c < 28; ++c) acc[c] = 0.0;
+        for (int q = 0; q < nq; ++q) {
+            if (rows[q] < 0) continue;   // empty corner reads 0 (G:193-194)
+            const float *row = G.table + (int64_t)rows[q] * PLX_STRIDE;
+            acc[0] += w[q] * (double)__ldg(G.density + rows[q]);
+#pragma unroll
+            for (int c = 1; c < 28; ++c) acc[c] += w[q] * (double)__ldg(row + c);
+        }
+        double *o = out + 28 * i;
+        o[0] = acc[0] > 0.0 ? acc[0] : 0.0;   // G:196
+#pragma unroll
+        for (int c = 1; c < 28; ++c) o[c] = acc[c];
+    }
+}
+
+template <bool NEAREST>
+__global__ void grid_sample_bwd_kernel(DGrid G, const double *pts, const double *up, int64_t n,
+                                       float *grad, uint8_t *tmask) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t rows[8];
+        double w[8];
+        const int nq = point_stencil<NEAREST>(G, pts + 3 * i, rows, w);
+        double raw = 0.0;   // G:216-218: interpolated sigma before the clamp
+        for (int q = 0; q < nq; ++q)
+            if (rows[q] >= 0) raw += w[q] * (double)__ldg(G.density + rows[q]);
+        const double *u = up + 28 * i;
+        const double u0 = raw < 0.0 ? 0.0 : u[0];
+        for (int q = 0; q < nq; ++q) {
+            const int32_t r = rows[q];
+            if (r < 0) continue;
+            tmask[r] = 1;   // GradientBuffer.add touches the row (G:52-60)
+            float *gr = grad + (int64_t)r * PLX_STRIDE;
+            atomicAdd(gr, (float)(w[q] * u0));
+            for (int c = 1; c < 28; ++c) {
+                const float v = (float)(w[q] * u[c]);
+                if (v != 0.f) atomicAdd(gr + c, v);
+            }
+        }
+    }
+}
+
+extern "C" int plx_grid_sample(const plx_grid *g, const double *pts, int64_t n, int32_t nearest,
+                               double *out, void *stream) {
+    if (!grid_ok(g) || n < 0 || (n > 0 && (!pts || !out))) return PLX_EINVAL;
+    if (n == 0) return PLX_OK;
+    int64_t nb = (n + 255) / 256;
+    if (nb > (int64_t)num_sms() * 16) nb = (int64_t)num_sms() * 16;
+    plx_grid g2 = *g;
+    g2.sigma_lat = nullptr;   // rows through links (the lattice mirror is not used here)
+    g2.cell_occ = nullptr;
+    if (nearest)
+        grid_sample_kernel<true><<<(unsigned)nb, 256, 0, (cudaStream_t)stream>>>(make_dgrid(g2), pts, n, out);
+    else
+        grid_sample_kernel<false><<<(unsigned)nb, 256, 0, (cudaStream_t)stream>>>(make_dgrid(g2), pts, n, out);
+    return status();
+}
+
+extern "C" int plx_grid_sample_backward(const plx_grid *g, const double *pts,
+                                        const double *upstream, int64_t n, int32_t nearest,
+                                        plx_grad *gb, void *stream) {
+    if (!grid_ok(g) || n < 0 || !gb || !gb->grad || !gb->tmask ||
+        (n > 0 && (!pts || !upstream)))
+        return PLX_EINVAL;
+    if (n == 0) return PLX_OK;
+    int64_t nb = (n + 255) / 256;
+    if (nb > (int64_t)num_sms() * 16) nb = (int64_t)num_sms() * 16;
+    plx_grid g2 = *g;
+    g2.sigma_lat = nullptr;
+    g2.cell_occ = nullptr;
+    if (nearest)
+        grid_sample_bwd_kernel<true><<<(unsigned)nb, 256, 0, (cudaStream_t)stream>>>(
+            make_dgrid(g2), pts, upstream, n, gb->grad, gb->tmask);
+    else
+        grid_sample_bwd_kernel<false><<<(unsigned)nb, 256, 0, (cudaStream_t)stream>>>(
+            make_dgrid(g2), pts, upstream, n, gb->grad, gb->tmask);
+    return status();
+}
+
 extern "C" const char *plx_version(void) { return "plx-b200 0.1.0 (sm_100a)"; }
 
 extern "C" int plx_device_check(void) {

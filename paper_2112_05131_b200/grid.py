@@ -424,6 +424,69 @@ class SparseGrid:
                        "upsample_apply")
         return grid
 
+    # -- point sampling (G:141-223) -------------------------------------------
+    def _check_inside(self, pts: torch.Tensor) -> None:
+        """G:147-151."""
+        tol = 1e-9 * float(np.max(self.extent))
+        lo = torch.as_tensor(self.aabb_min, dtype=torch.float64, device=pts.device)
+        hi = torch.as_tensor(self.aabb_max, dtype=torch.float64, device=pts.device)
+        if bool(torch.any(pts < lo - tol)) or bool(torch.any(pts > hi + tol)):
+            raise ValueError("sample position outside the grid AABB")
+
+    def _points(self, pts):
+        as_np = not isinstance(pts, torch.Tensor)
+        t = torch.as_tensor(np.asarray(pts, dtype=np.float64) if as_np else pts,
+                            dtype=torch.float64).to(self.device)
+        single = t.dim() == 1
+        t = t.reshape(-1, 3).contiguous()
+        self._check_inside(t)
+        return t, as_np, single
+
+    def sample(self, pts, mode: str = "trilinear"):
+        """G:182-200: interpolated (sigma, coeffs) at world positions inside
+        the AABB (plx_grid_sample); sigma clamped at zero, empty corners read
+        zero.  A single (3,) point gives (float, (27,)); a batch (N, 3) gives
+        ((N,), (N, 27)) float64 -- numpy for numpy input."""
+        if mode not in ("trilinear", "nearest"):
+            raise ValueError(f"unknown interpolation mode {mode!r}")
+        t, as_np, single = self._points(pts)
+        out = torch.zeros((t.shape[0], ROW_SIZE), dtype=torch.float64, device=self.device)
+        if self.n_rows and t.shape[0]:
+            c = self._c(with_occ=False)
+            _lib.check(_lib.lib().plx_grid_sample(ctypes.byref(c), t.data_ptr(), t.shape[0],
+                                                  int(mode == "nearest"), out.data_ptr(),
+                                                  _lib.stream_ptr()), "grid_sample")
+        sigma, coeffs = out[:, 0], out[:, 1:]
+        if as_np:
+            sigma, coeffs = sigma.cpu().numpy(), coeffs.cpu().numpy()
+        if single:
+            return float(sigma[0]), coeffs[0]
+        return sigma, coeffs
+
+    def sample_backward(self, pts, upstream, grads: GradientBuffer,
+                        mode: str = "trilinear") -> None:
+        """G:202-223: adjoint of sample() -- upstream (N, 28) dL/d(sigma,
+        coeffs) times each stencil weight added to the occupied corner rows of
+        `grads` (plx_grid_sample_backward); the sigma entry is dropped where
+        the interpolated sigma was clamped (< 0)."""
+        if mode not in ("trilinear", "nearest"):
+            raise ValueError(f"unknown interpolation mode {mode!r}")
+        if grads.n_rows != self.n_rows:
+            raise ValueError("gradient buffer rows do not match the grid table")
+        t, _, _ = self._points(pts)
+        up = torch.as_tensor(np.asarray(upstream, dtype=np.float64)
+                             if not isinstance(upstream, torch.Tensor) else upstream,
+                             dtype=torch.float64).to(self.device).reshape(-1, ROW_SIZE)
+        if up.shape[0] != t.shape[0]:
+            raise ValueError("one upstream row of 28 values per point")
+        up = up.contiguous()
+        if self.n_rows and t.shape[0]:
+            c, gb = self._c(with_occ=False), grads._c(with_ids=False)
+            _lib.check(_lib.lib().plx_grid_sample_backward(
+                ctypes.byref(c), t.data_ptr(), up.data_ptr(), t.shape[0],
+                int(mode == "nearest"), ctypes.byref(gb), _lib.stream_ptr()),
+                "grid_sample_backward")
+
     def max_weight_accumulate(self, origins, dirs, step_frac: float = 0.5,
                               stop_thresh: float = 1e-4, interp: str = "trilinear",
                               chunk: int = 1 << 22):

@@ -110,6 +110,29 @@ def cauchy_sparsity_loss(sigmas, lam: float):
     return lam * float(np.sum(np.log1p(2.0 * s * s))), lam * 4.0 * s / (1.0 + 2.0 * s * s)
 
 
+BETA_EPS = 1e-6
+
+
+def beta_loss(trans_fg, lam: float, eps: float = BETA_EPS):
+    """L:91-102: lam * sum(log T + log(1 - T)) over the foreground
+    transmittances, T clamped to [eps, 1 - eps] -> (loss, dL/dT), the gradient
+    zero where the clamp is active.  A CUDA tensor stays on the device (the
+    360 training step computes the same terms inside msi_bg_kernel)."""
+    if isinstance(trans_fg, torch.Tensor):
+        t = trans_fg.to(torch.float64)
+        tc = t.clamp(eps, 1.0 - eps)
+        loss = lam * float(torch.sum(torch.log(tc) + torch.log1p(-tc)))
+        grad = lam * (1.0 / tc - 1.0 / (1.0 - tc))
+        grad = torch.where((t < eps) | (t > 1.0 - eps), torch.zeros_like(grad), grad)
+        return loss, grad
+    t = np.asarray(trans_fg, dtype=np.float64)
+    tc = np.clip(t, eps, 1.0 - eps)
+    loss = lam * float(np.sum(np.log(tc) + np.log1p(-tc)))
+    grad = lam * (1.0 / tc - 1.0 / (1.0 - tc))
+    grad = np.where((t < eps) | (t > 1.0 - eps), 0.0, grad)
+    return loss, grad
+
+
 def _gaussian_window(radius: int = 5, sigma: float = 1.5) -> np.ndarray:
     """L:124-128."""
     x = np.arange(-radius, radius + 1, dtype=np.float64)
