@@ -180,13 +180,41 @@ def config_from_dict(d: dict) -> TrainConfig:
     if "ladder" in kw:
         kw["ladder"] = [LadderRung(int(r["step"]), tuple(int(x) for x in r["dims"]))
                         for r in kw["ladder"]]
-    for key in ("lr_sigma", "lr_sh"):
+    sched_keys = {f.name for f in dataclasses.fields(optim.LrSchedule)}
+    for key in ("lr_sigma", "lr_sh", "bg_lr_sigma", "bg_lr_rgb"):
         if key in kw and isinstance(kw[key], dict):
+            bad = set(kw[key]) - sched_keys
+            if bad:
+                raise ValueError(f"unknown {key} schedule keys: {sorted(bad)}")
             kw[key] = optim.LrSchedule(**kw[key])
     for key in ("aabb", "background"):
         if key in kw:
             kw[key] = tuple(float(x) for x in kw[key])
     return TrainConfig(**kw)
+
+
+def apply_override(d: dict, dotted_key: str, value) -> None:
+    """T:209-218: set a (possibly nested, dotted) key of a config dict;
+    KeyError for a key the config does not have."""
+    node = d
+    parts = dotted_key.split(".")
+    for p in parts[:-1]:
+        if not isinstance(node.get(p), dict):
+            raise KeyError(f"unknown config key {dotted_key!r}")
+        node = node[p]
+    if parts[-1] not in node:
+        raise KeyError(f"unknown config key {dotted_key!r}")
+    node[parts[-1]] = value
+
+
+def train_split_scene_scale(data_dir, margin: float = 1.1) -> float:
+    """T:291-301: the 360 camera pre-scale from a NeRF-format dataset's
+    training split metadata (transforms_train.json camera positions)."""
+    import json
+    meta = json.loads((Path(data_dir) / "transforms_train.json").read_text())
+    pos = np.array([np.asarray(f["transform_matrix"], dtype=np.float64)[:3, 3]
+                    for f in meta["frames"]])
+    return _scale_from_positions(pos, margin)
 
 
 def load_config(path) -> TrainConfig:
