@@ -43,6 +43,18 @@ class RenderOptions:
 
 
 @dataclass
+class SamplePoint:
+    """R:45-52: one composited sample of render_ray(record=True)."""
+
+    position: np.ndarray
+    delta: float
+    sigma: float
+    rgb: np.ndarray
+    trans: float
+    weight: float
+
+
+@dataclass
 class RenderResult:
     rgb: np.ndarray
     trans: float
@@ -163,14 +175,55 @@ def render_rays(grid: SparseGrid, origins, dirs, opts: RenderOptions | None = No
 
 def render_ray(grid: SparseGrid, origin, direction, opts: RenderOptions | None = None,
                viewdir=None, record: bool = False) -> RenderResult:
-    """R:143-155 (the record=True numpy twin is a reference-side test aid and
-    is not provided on the device path)."""
+    """R:143-155.  record=True also returns the per-sample terms (R:158-202):
+    the march positions of `march`, their interpolated (sigma, SH) from ONE
+    SparseGrid.sample call on the device, and the compositing of R:171-201
+    done sample by sample in float64 on the host (a debugging / test path;
+    the fast path is the kernel)."""
+    opts = opts or RenderOptions()
     if record:
-        raise NotImplementedError("record=True is the reference's numpy twin (R:158-202)")
+        return _render_ray_record(grid, origin, direction, opts, viewdir)
     vd = None if viewdir is None else np.atleast_2d(viewdir)
     rgb, trans, wsum = render_rays(grid, np.atleast_2d(origin), np.atleast_2d(direction),
                                    opts, vd)
     return RenderResult(rgb=rgb[0], trans=float(trans[0]), weight_sum=float(wsum[0]))
+
+
+def _render_ray_record(grid, origin, direction, opts, viewdir) -> RenderResult:
+    """R:158-202 with the interpolation on the device."""
+    from .sh import eval_sh_basis, normalize_dirs
+    o = np.asarray(origin, dtype=np.float64).reshape(3)
+    d = np.asarray(direction, dtype=np.float64).reshape(3)
+    basis = eval_sh_basis(normalize_dirs(d if viewdir is None else
+                                         np.asarray(viewdir, dtype=np.float64).reshape(3)))
+    bg = np.asarray(opts.background, dtype=np.float64)
+    ts, deltas = march(grid, o, d, opts.step_frac)
+    rgb, T, asum, wsum, samples = np.zeros(3), 1.0, 0.0, 0.0, []
+    if len(ts) and grid.n_rows:
+        pos = o[None, :] + ts[:, None] * d[None, :]
+        # the stencil clamps to the lattice anyway; clipping keeps positions a
+        # rounding error outside a face inside sample()'s AABB check
+        sig, coeffs = grid.sample(np.clip(pos, grid.aabb_min, grid.aabb_max), opts.interp)
+        for i, dlt in enumerate(deltas):
+            s = float(sig[i])       # clamped at 0: skipped exactly when R:179 skips
+            if s <= 0.0:
+                continue
+            att = math.exp(-s * dlt)
+            if opts.formula == "absolute":
+                t_next = max(0.0, 1.0 - (asum + (1.0 - att)))
+                asum += 1.0 - att
+            else:
+                t_next = T * att
+            w = T - t_next
+            color = np.maximum(basis @ coeffs[i].reshape(3, 9).T, 0.0)
+            rgb += w * color
+            wsum += w
+            samples.append(SamplePoint(position=pos[i], delta=float(dlt), sigma=s, rgb=color,
+                                       trans=T, weight=w))
+            T = t_next
+            if T < opts.stop_thresh:
+                break
+    return RenderResult(rgb=rgb + T * bg, trans=T, weight_sum=wsum, samples=samples)
 
 
 def _launch_bwd(grid, r, opts, mse_mode, up_scale, lam_cauchy, grads, rgb, sums):
