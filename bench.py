@@ -222,7 +222,8 @@ def oracle_train(args, rays_for, n_pool, B, warmup, steps, budget_s):
                 break
     sample = (f"steps {warmup}..{warmup + len(times) - 1} timed ({warmup} untimed from the "
               f"dense init) of {B} rays, same pool and EpochBatcher draws, dense {args.dims}^3 "
-              f"f64 grid, TV 1% cells, RMSProp; sequential C port of K:173-600, 1 thread")
+              f"f64 grid, TV 1% cells, RMSProp; sequential C port of K:173-600, 1 thread "
+              f"(the reference's numba kernels are single-threaded @njit, no prange)")
     return B / float(np.mean(times)), len(times), sample
 
 
