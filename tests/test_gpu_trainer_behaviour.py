@@ -84,3 +84,25 @@ def test_eval_records_and_checkpoints(tiny, tmp_path):
     assert (out / "checkpoint_0000010.plnx").exists() and (out / "final.plnx").exists()
     grid, bg, state, bg_state, step = px.load_checkpoint(out / "final.plnx")
     assert step == 20 and state.v.shape[0] == grid.n_rows
+
+
+def test_trainer_accepts_any_dataset_with_the_reference_fields(tiny):
+    """Dataset loading stays host-side (the reference's camera.load_nerf_dataset,
+    camera.py:150-290): the trainer reads only `images`, `scene_type` and the
+    cameras' c2w / focal / width / height / near / position, so the
+    reference's own Dataset objects train as they are."""
+    import types
+    import paper_2112_05131_b200 as px
+    train = tiny[0]
+    cams = [types.SimpleNamespace(c2w=c.c2w.copy(), focal=c.focal, width=c.width,
+                                  height=c.height, near=c.near, far=np.inf,
+                                  position=c.c2w[:3, 3].copy()) for c in train.cameras]
+    ds = types.SimpleNamespace(images=np.asarray(train.images), cameras=cams,
+                               scene_type="bounded", background=np.ones(3), paths=[])
+    cfg = _cfg(steps=30, batch=128)
+    cfg.log_every = 10
+    a = px.train(ds, cfg)
+    b = px.train(train, cfg)
+    la = [m["loss"] for m in a.metrics if "loss" in m]
+    lb = [m["loss"] for m in b.metrics if "loss" in m]
+    np.testing.assert_allclose(la, lb, rtol=1e-3)
