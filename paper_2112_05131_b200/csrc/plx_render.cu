@@ -1530,11 +1530,22 @@ struct ScratchLayout {
         off_sig, off_segsum, off_rgbadd, off_bup;
 };
 
+// Record budget per wave; PLX_RECORD_MB overrides it (tests force
+// multi-wave batches at small sizes).
+int64_t record_budget() {
+    static int64_t v = -1;
+    if (v < 0) {
+        const char *e = getenv("PLX_RECORD_MB");
+        v = (e && atoll(e) > 0) ? atoll(e) << 20 : kRecordBudget;
+    }
+    return v;
+}
+
 ScratchLayout layout(const plx_grid *g, const plx_render_opts *o, int64_t n_rays) {
     ScratchLayout L;
     L.cap = max_records(g, o->step);
     L.nseg_max = (int)((L.cap + 31) / 32);
-    int64_t wave = kRecordBudget / (L.cap * kRecordBytes);
+    int64_t wave = record_budget() / (L.cap * kRecordBytes);
     if (wave < 1024) wave = 1024;
     if (n_rays > 0 && n_rays < wave) wave = n_rays;
     // equal waves: a fixed-size wave left a small last wave (2^18 rays at
