@@ -203,6 +203,12 @@ struct Scratch {
     double *seg_sum;   // [segments][6] {sum w c+ (RGB), sum c+ (bn - bi) (RGB)}
     double *rgb_add;   // 360 mode: [rays][3] background colour T_fg C_bg (replaces T bg)
     double *bup;       // 360 mode: [rays] beta-regulariser upstream (K:827-833)
+    // spatial processing order of the segments (seg_order_*): ord[q] =
+    // {segment, ray} of the q-th segment the colour / scatter kernels take;
+    // nullptr = allocation order
+    int2 *ord;
+    int *seg_key;      // [segments] spatial bucket of each segment
+    int *bucket;       // [kBuckets] counts, then (scan) cursors; zeroed by the march
 };
 
 // The ray's colour total sum_w w c+ from its segment sums, in the order every
@@ -226,13 +232,17 @@ __device__ __forceinline__ void ray_colour_totals(const Scratch &S, int64_t s0, 
     }
 }
 
-// The q-th segment the colour / scatter kernels take (allocation order) and
-// its ray.  (A spatial order -- counting sort of the segments into 16^3
-// Morton buckets of their first sample -- was measured: +12 us of sort
-// kernels, no gain in the colour or scatter kernel.)
+// The q-th segment of the processing order (allocation order, or the spatial
+// order of seg_place_kernel for large waves) and its ray.
 __device__ __forceinline__ void seg_at(const Scratch &S, int64_t q, int64_t &sg, int &ray) {
-    sg = q;
-    ray = S.seg_ray[q];
+    if (S.ord) {
+        const int2 e = S.ord[q];
+        sg = e.x;
+        ray = e.y;
+    } else {
+        sg = q;
+        ray = S.seg_ray[q];
+    }
 }
 
 // Per-warp shared staging of one chunk's scatter payload (pass 2).  The
@@ -487,6 +497,92 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
+// ---------------------------------------------------------------------------
+// Spatial order of the segments, for large waves.  A wave touches each SH /
+// gradient row from several rays at unrelated times; once the wave's row
+// working set exceeds L2, the colour kernel's row gathers and the scatter's
+// red.add row fills mostly miss L2 when segments are taken in allocation
+// (ray) order.  Processing segments bucketed by the 3-D location of their
+// first sample (a 16^3 Morton grid over the lattice) keeps the segments in
+// flight spatially compact, so rows shared by crossing rays are gathered /
+// reduced while still in L2.  Counting sort, three small kernels between the
+// march and the colour kernel; the order within a bucket is arbitrary
+// (results do not depend on it beyond f32 atomic order).  Measured (C5
+// 512^3, 32 GiB waves): 2^20 rays 36.6 -> 40.4 M rays/s, 2^18 30.9 -> 33.4,
+// 2^16 +2 %, equal at 2^15; at C2 (5000 rays, rays share few rows) the sort
+// costs 12 us for no kernel gain, so waves below kSegOrderMinRays skip it.
+// 8^3-cell buckets and keying on the middle sample measured the same.
+constexpr int kBucketBits = 4;
+constexpr int kBuckets = 1 << (3 * kBucketBits);
+constexpr int64_t kSegOrderMinRays = 49152;
+
+__device__ __forceinline__ int spread3(int v) {
+    int r = 0;
+#pragma unroll
+    for (int b = 0; b < kBucketBits; ++b) r |= ((v >> b) & 1) << (3 * b);
+    return r;
+}
+
+__global__ void seg_key_kernel(Scratch S, int shx, int shy, int shz) {
+    const int64_t nseg = *S.nseg_total;
+    for (int64_t sg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sg < nseg;
+         sg += (int64_t)gridDim.x * blockDim.x) {
+        const int ray = S.seg_ray[sg];
+        const int64_t j0 = (sg - S.seg_first[ray]) * 32;
+        const int4 c = S.cell[(int64_t)ray * S.cap + j0];
+        const int key =
+            (spread3(c.x >> shx) << 2) | (spread3(c.y >> shy) << 1) | spread3(c.z >> shz);
+        S.seg_key[sg] = key;
+        atomicAdd(S.bucket + key, 1);
+    }
+}
+
+// exclusive scan of the kBuckets counts in place (one block of 1024 threads)
+__global__ void __launch_bounds__(1024) seg_scan_kernel(Scratch S) {
+    constexpr int PER = kBuckets / 1024;
+    __shared__ int warp_tot[32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    int v[PER], sum = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        v[i] = S.bucket[PER * t + i];
+        sum += v[i];
+    }
+    int x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(PLX_FULL_MASK, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int y = warp_tot[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int z = __shfl_up_sync(PLX_FULL_MASK, y, o);
+            if (lane >= o) y += z;
+        }
+        warp_tot[lane] = y;
+    }
+    __syncthreads();
+    int excl = x - sum + (w ? warp_tot[w - 1] : 0);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        S.bucket[PER * t + i] = excl;
+        excl += v[i];
+    }
+}
+
+__global__ void seg_place_kernel(Scratch S) {
+    const int64_t nseg = *S.nseg_total;
+    for (int64_t sg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sg < nseg;
+         sg += (int64_t)gridDim.x * blockDim.x) {
+        const int pos = atomicAdd(S.bucket + S.seg_key[sg], 1);
+        S.ord[pos] = make_int2((int)sg, S.seg_ray[sg]);
+    }
+}
+
 template <bool ABS, bool NEAREST, int MINB>
 __global__ void __launch_bounds__(128, MINB)
     march_bwd_kernel(DGrid G, RayArgs R, KOpts O, Outs out, Scratch S) {
@@ -497,6 +593,8 @@ __global__ void __launch_bounds__(128, MINB)
     unsigned st_pos = 0, st_samp = 0, st_chunks = 0, st_rays = 0;   // warp-uniform
     const unsigned lt_mask = (1u << lane) - 1u;
     const bool cauchy = S.sig != nullptr;
+    if (S.bucket && blockIdx.x == 0)   // counts of seg_key_kernel (runs after this kernel)
+        for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) S.bucket[i] = 0;
 #ifdef PLX_TIMELINE
     const unsigned long long t_start = gtimer();
 #endif
@@ -1527,7 +1625,7 @@ struct ScratchLayout {
     int64_t wave, cap, bytes;
     int nseg_max;
     int64_t off_ns, off_segfirst, off_segray, off_rayd, off_basis, off_att, off_T, off_w, off_c, off_cell, off_f, off_rows,
-        off_sig, off_segsum, off_rgbadd, off_bup;
+        off_sig, off_segsum, off_rgbadd, off_bup, off_segkey, off_ord, off_bucket;
 };
 
 // Record budget per wave; PLX_RECORD_MB overrides it (tests force
@@ -1579,6 +1677,9 @@ ScratchLayout layout(const plx_grid *g, const plx_render_opts *o, int64_t n_rays
     L.off_segsum = take(wave * L.nseg_max * 48);
     L.off_rgbadd = take(wave * 24);
     L.off_bup = take(wave * 8);
+    L.off_segkey = take(wave * L.nseg_max * 4);
+    L.off_ord = take(wave * L.nseg_max * 8);
+    L.off_bucket = take(kBuckets * 4);
     L.bytes = off;
     return L;
 }
@@ -1686,6 +1787,19 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
     S.seg_sum = reinterpret_cast<double *>(base + L.off_segsum);
     S.rgb_add = msi ? reinterpret_cast<double *>(base + L.off_rgbadd) : nullptr;
     S.bup = msi ? reinterpret_cast<double *>(base + L.off_bup) : nullptr;
+    // PLX_SEG_ORDER=0 / 1 forces the spatial segment order off / on (tests,
+    // A/B); by default waves of at least kSegOrderMinRays rays use it
+    static const int order_env = [] {
+        const char *e = getenv("PLX_SEG_ORDER");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    S.seg_key = reinterpret_cast<int *>(base + L.off_segkey);
+    int shift[3];
+    for (int a = 0; a < 3; ++a) {   // 16 buckets per axis over the base cells
+        int bits = 0;
+        while (((g->dims[a] - 2) >> bits) > 0) ++bits;
+        shift[a] = bits > kBucketBits ? bits - kBucketBits : 0;
+    }
     cudaStream_t s = (cudaStream_t)stream;
     const int sms = num_sms();
     for (int64_t w0 = 0; w0 < rays->n; w0 += L.wave) {
@@ -1701,6 +1815,9 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
             R.viewdirs += 3 * w0;
             R.target += 3 * w0;
         }
+        const bool ordered = order_env >= 0 ? order_env == 1 : nw >= kSegOrderMinRays;
+        S.ord = ordered ? reinterpret_cast<int2 *>(base + L.off_ord) : nullptr;
+        S.bucket = ordered ? reinterpret_cast<int *>(base + L.off_bucket) : nullptr;
         Outs out{};
         out.rgb = out_rgb ? out_rgb + 3 * w0 : nullptr;
         out.sums = out_sums;
@@ -1735,6 +1852,11 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
                              : resident_blocks(colour_kernel<false, false, kColourMinB>);
             sb = o->absolute ? resident_blocks(scatter_kernel<true, false, kScatterMinB>)
                              : resident_blocks(scatter_kernel<false, false, kScatterMinB>);
+        }
+        if (S.ord) {
+            seg_key_kernel<<<sms * 2, 256, 0, s>>>(S, shift[0], shift[1], shift[2]);
+            seg_scan_kernel<<<1, 1024, 0, s>>>(S);
+            seg_place_kernel<<<sms * 2, 256, 0, s>>>(S);
         }
 #ifdef PLX_DIAG
         // diagnostic builds (profiles/r2b_diag.md): PLX_DIAG_MODE bit 1 / 2 /
