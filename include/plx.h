@@ -77,6 +77,17 @@ typedef struct {
     const int32_t *row_cell; /* [rows] lattice point of each row (inverse of
                               links, plx_build_row_cell); required with
                               sigma_lat by the optimisers                 */
+    uint32_t *brick_dead;  /* optional, with a sigma_lat that is not density:
+                              1 bit per brick of 8^3 base cells (bricks
+                              ((Dx-2)/8+1) x ((Dy-2)/8+1) x ((Dz-2)/8+1),
+                              z fastest), set iff every cell of the brick
+                              has no occupied corner or 8 occupied corners
+                              with sigma < 0 -- no position inside can be
+                              composited (K:211, K:293), so the march skips
+                              its sigma gathers.  plx_build_brick_dead
+                              sets it; the optimisers clear the bricks
+                              around every row whose sigma becomes >= 0;
+                              rebuild after editing density or links. */
 } plx_grid;
 
 /* GradientBuffer (G:25-68): data + touched mask, and optionally the
@@ -315,6 +326,10 @@ int plx_grid_sample_backward(const plx_grid *g, const double *pts, const double 
  * = any of the 8 corner links >= 0.  Must be rebuilt after prune/upsample. */
 int64_t plx_cell_occ_words(const int64_t dims[3]);
 int plx_build_cell_occ(const plx_grid *g, uint32_t *cell_occ, void *stream);
+/* Dead-brick bitmask (plx_grid.brick_dead) from sigma_lat: words needed,
+ * and the build (g->sigma_lat required). */
+int64_t plx_brick_words(const int64_t dims[3]);
+int plx_build_brick_dead(const plx_grid *g, uint32_t *brick_dead, void *stream);
 /* sigma_lat ([Dx*Dy*Dz] floats) and row_cell ([rows] int32). */
 int plx_build_sigma_lat(const plx_grid *g, float *sigma_lat, void *stream);
 int plx_build_row_cell(const plx_grid *g, int32_t *row_cell, void *stream);

@@ -32,7 +32,7 @@ class PlxGrid(ctypes.Structure):
                 ("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3),
                 ("scale", ctypes.c_double * 3), ("dmax", ctypes.c_double * 3),
                 ("cell_occ", ctypes.c_void_p), ("sigma_lat", ctypes.c_void_p),
-                ("row_cell", ctypes.c_void_p)]
+                ("row_cell", ctypes.c_void_p), ("brick_dead", ctypes.c_void_p)]
 
 
 class PlxGrad(ctypes.Structure):
@@ -140,6 +140,8 @@ _SIGS = {
     "plx_build_cell_occ": [ctypes.POINTER(PlxGrid), _P, _P],
     "plx_build_sigma_lat": [ctypes.POINTER(PlxGrid), _P, _P],
     "plx_build_row_cell": [ctypes.POINTER(PlxGrid), _P, _P],
+    "plx_brick_words": [ctypes.POINTER(_I64)],
+    "plx_build_brick_dead": [ctypes.POINTER(PlxGrid), _P, _P],
     "plx_grid_sample": [ctypes.POINTER(PlxGrid), _P, _I64, _I32, _P, _P],
     "plx_grid_sample_backward": [ctypes.POINTER(PlxGrid), _P, _P, _I64, _I32,
                                  ctypes.POINTER(PlxGrad), _P],
@@ -164,6 +166,7 @@ _SIGS = {
     "plx_device_check": [],
 }
 _RESTYPE = {"plx_scan_scratch_bytes": _I64, "plx_render_scratch_bytes": _I64, "plx_cell_occ_words": _I64,
+            "plx_brick_words": _I64,
             "plx_msi_scratch_bytes": _I64, "plx_image_metrics_scratch_bytes": _I64,
             "plx_version": ctypes.c_char_p}
 

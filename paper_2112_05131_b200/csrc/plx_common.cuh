@@ -18,6 +18,9 @@
 namespace plx {
 
 // Kernel-side copy of plx_grid (passed by value).
+// Empty-space bricks: kBrick^3 trilinear base cells.
+constexpr int kBrick = 8;
+
 struct DGrid {
     const int32_t *__restrict__ links;
     const float *__restrict__ table;     // SH rows (column 0 unused)
@@ -25,6 +28,10 @@ struct DGrid {
     const uint32_t *__restrict__ cell_occ;
     const float *sigma_lat;              // lattice-indexed sigma mirror, NaN = empty (mutable)
     bool identity;                       // links[c] == c for every point (dense grid)
+    // optional dead-brick bitmask over 8^3-cell bricks (plx_build_brick_dead):
+    // bit set = no position inside can be composited; Bx, By, Bz bricks per axis
+    const uint32_t *brick_dead;
+    int32_t Bx, By, Bz;
     int32_t Dx, Dy, Dz;
     double lo[3], hi[3], scale[3], dmax[3];
 };
@@ -39,6 +46,11 @@ inline DGrid make_dgrid(const plx_grid &g) {
     // the caller aliases the sigma mirror to density exactly when the grid is
     // identity-linked (SparseGrid.lattice_sigma)
     d.identity = g.sigma_lat != nullptr && g.sigma_lat == g.density;
+    // the mask is kept only beside a separate sigma mirror (sparse grids)
+    d.brick_dead = (g.sigma_lat && !d.identity) ? g.brick_dead : nullptr;
+    d.Bx = (int32_t)((g.dims[0] - 2) / kBrick + 1);
+    d.By = (int32_t)((g.dims[1] - 2) / kBrick + 1);
+    d.Bz = (int32_t)((g.dims[2] - 2) / kBrick + 1);
     d.Dx = (int32_t)g.dims[0];
     d.Dy = (int32_t)g.dims[1];
     d.Dz = (int32_t)g.dims[2];
@@ -400,6 +412,11 @@ __device__ __forceinline__ bool sigma_at(const DGrid &G, const double *g, double
     ijk[0] = i0;
     ijk[1] = j0;
     ijk[2] = k0;
+    if (G.brick_dead) {   // a dead brick: no position inside can be composited
+        const int32_t b = (((unsigned)i0 / kBrick) * G.By + (unsigned)j0 / kBrick) * G.Bz +
+                          (unsigned)k0 / kBrick;
+        if ((__ldg(G.brick_dead + (b >> 5)) >> (b & 31)) & 1u) return false;
+    }
     const int32_t c = flat(G, i0, j0, k0);
     if (G.cell_occ && !((__ldg(G.cell_occ + (c >> 5)) >> (c & 31)) & 1u)) return false;
     f[0] = g[0] - (double)i0;
@@ -426,6 +443,58 @@ __device__ __forceinline__ bool sigma_at(const DGrid &G, const double *g, double
         sig += stencil_w<NEAREST>(f, q) * (double)s[q];
     }
     return occ;
+}
+
+// Brick of the base cell at lattice coordinates g (sigma_at's clamped cell).
+__device__ __forceinline__ int32_t brick_of(const DGrid &G, const double *g) {
+    int32_t i0 = (int32_t)g[0], j0 = (int32_t)g[1], k0 = (int32_t)g[2];
+    if (i0 > G.Dx - 2) i0 = G.Dx - 2;
+    if (j0 > G.Dy - 2) j0 = G.Dy - 2;
+    if (k0 > G.Dz - 2) k0 = G.Dz - 2;
+    return (((unsigned)i0 / kBrick) * G.By + (unsigned)j0 / kBrick) * G.Bz + (unsigned)k0 / kBrick;
+}
+
+__device__ __forceinline__ void brick_xyz(const DGrid &G, const double *g, int &bx, int &by,
+                                          int &bz) {
+    int32_t i0 = (int32_t)g[0], j0 = (int32_t)g[1], k0 = (int32_t)g[2];
+    if (i0 > G.Dx - 2) i0 = G.Dx - 2;
+    if (j0 > G.Dy - 2) j0 = G.Dy - 2;
+    if (k0 > G.Dz - 2) k0 = G.Dz - 2;
+    bx = (int)((unsigned)i0 / kBrick);
+    by = (int)((unsigned)j0 / kBrick);
+    bz = (int)((unsigned)k0 / kBrick);
+}
+
+__device__ __forceinline__ bool brick_is_dead(const DGrid &G, int32_t b) {
+    return (__ldg(G.brick_dead + (b >> 5)) >> (b & 31)) & 1u;
+}
+
+// The sigma of lattice point c became >= 0: no brick whose cells have c as a
+// corner is dead any more (the mask stays a conservative under-approximation
+// between rebuilds).  Bits are tested before the atomic: most are clear.
+__device__ __forceinline__ void brick_revive(uint32_t *bits, int32_t c, int32_t Dx, int32_t Dy,
+                                             int32_t Dz) {
+    const int32_t x = c / (Dy * Dz), y = (c / Dz) % Dy, z = c % Dz;
+    const int32_t By = (Dy - 2) / kBrick + 1, Bz = (Dz - 2) / kBrick + 1;
+    int32_t bx[2], by[2], bz[2];
+    // cells x-1 and x (those that exist) have the point as a corner
+    bx[0] = (x > 0 ? x - 1 : 0) / kBrick;
+    bx[1] = (x < Dx - 1 ? x : Dx - 2) / kBrick;
+    by[0] = (y > 0 ? y - 1 : 0) / kBrick;
+    by[1] = (y < Dy - 1 ? y : Dy - 2) / kBrick;
+    bz[0] = (z > 0 ? z - 1 : 0) / kBrick;
+    bz[1] = (z < Dz - 1 ? z : Dz - 2) / kBrick;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                if ((a && bx[1] == bx[0]) || (b && by[1] == by[0]) || (e && bz[1] == bz[0])) continue;
+                const int32_t k = (bx[a] * By + by[b]) * Bz + bz[e];
+                const uint32_t m = 1u << (k & 31);
+                if (bits[k >> 5] & m) atomicAnd(bits + (k >> 5), ~m);
+            }
 }
 
 }  // namespace plx

@@ -42,6 +42,8 @@ struct ListArgs {
     uint8_t *tmask;
     float *sigma_lat;
     const int32_t *row_cell;
+    uint32_t *brick_dead;      // optional dead-brick mask beside sigma_lat
+    int32_t Dx, Dy, Dz;
     const int32_t *ids;
     const int64_t *count;
     double *guard;
@@ -83,6 +85,7 @@ __global__ void __launch_bounds__(256, 2) opt_list_kernel(ListArgs a) {
         if (quad == 0) {   // sigma lives in the density array (column 0 unused)
             a.density[r] = t4.x;
             if (a.sigma_lat) a.sigma_lat[cell] = t4.x;
+            if (a.brick_dead && t4.x >= 0.f) brick_revive(a.brick_dead, cell, a.Dx, a.Dy, a.Dz);
             t4.x = 0.f;
             if (a.clear) a.tmask[r] = 0;
         }
@@ -257,6 +260,10 @@ extern "C" int plx_opt_step_list(plx_grid *g, float *v, plx_grad *gb, const int3
     a.tmask = gb->tmask;
     a.sigma_lat = lat;
     a.row_cell = g->row_cell;
+    a.brick_dead = lat ? g->brick_dead : nullptr;
+    a.Dx = (int32_t)g->dims[0];
+    a.Dy = (int32_t)g->dims[1];
+    a.Dz = (int32_t)g->dims[2];
     a.ids = ids;
     a.count = count;
     a.guard = guard;

@@ -211,6 +211,8 @@ struct OptArgs {
     double lr_sigma, lr_sh, beta, eps;
     int rmsprop, clear, update;
     unsigned long long *count;
+    uint32_t *brick_dead;      // optional dead-brick mask (with sigma_lat): kept conservative
+    int32_t Dx, Dy, Dz;
 };
 
 __device__ __forceinline__ int nonzero_bytes(uint32_t m) {
@@ -223,6 +225,7 @@ __device__ __forceinline__ int nonzero_bytes(uint32_t m) {
 // sigma of a row at lattice point c changed: keep the lattice mirror current.
 __device__ __forceinline__ void lat_update(const OptArgs &a, int32_t c, float sigma) {
     if (a.sigma_lat) a.sigma_lat[c] = sigma;
+    if (a.brick_dead && sigma >= 0.f) brick_revive(a.brick_dead, c, a.Dx, a.Dy, a.Dz);
 }
 
 // The update of one float4 of one row (K:578-590), float64 arithmetic.
@@ -972,6 +975,10 @@ int plx::opt_step_impl(plx_grid *g, float *v, plx_grad *gb, double lr_sigma, dou
     if (lat && !g->row_cell) return PLX_EINVAL;
     OptArgs a{g->table, g->density, v, gb->grad, lr_dev, guard, lat, g->row_cell, gb->tmask, g->rows,
               lr_sigma, lr_sh, beta, eps, rmsprop, clear, 1, reinterpret_cast<unsigned long long *>(out_count)};
+    a.brick_dead = lat ? g->brick_dead : nullptr;
+    a.Dx = (int32_t)g->dims[0];
+    a.Dy = (int32_t)g->dims[1];
+    a.Dz = (int32_t)g->dims[2];
     constexpr int NT = 256;
     cudaStream_t s = (cudaStream_t)stream;
     if (gb->tids) {   // two-phase: compact the touched set, then update the list
@@ -1141,6 +1148,52 @@ extern "C" int plx_build_cell_occ(const plx_grid *g, uint32_t *cell_occ, void *s
     if (!grid_ok(g) || !cell_occ) return PLX_EINVAL;
     const int64_t n = ncell(g), nw = (n + 31) / 32;
     cell_occ_kernel<<<blocks(nw, 256), 256, 0, (cudaStream_t)stream>>>(make_dgrid(*g), cell_occ, nw, n);
+    return status();
+}
+
+// One block per brick, two cells per thread: a cell is skippable when its 8
+// corner sigmas are all empty (NaN) or all occupied and < 0 -- exactly the
+// two early exits of sigma_at -- and the brick is dead when all its cells
+// are.  The mask is zeroed first; dead bricks set their bit.
+__global__ void __launch_bounds__(256) brick_dead_kernel(DGrid G, uint32_t *bits) {
+    const int32_t b = blockIdx.x;
+    const int32_t bz = b % G.Bz, by = (b / G.Bz) % G.By, bx = b / (G.Bz * G.By);
+    const int32_t sy = G.Dz, sx = G.Dy * G.Dz;
+    bool dead = true;
+    for (int t = threadIdx.x; t < kBrick * kBrick * kBrick; t += blockDim.x) {
+        const int32_t i = bx * kBrick + t / (kBrick * kBrick), j = by * kBrick + (t / kBrick) % kBrick,
+                      k = bz * kBrick + t % kBrick;
+        if (i > G.Dx - 2 || j > G.Dy - 2 || k > G.Dz - 2) continue;
+        const float *base = G.sigma_lat + flat(G, i, j, k);
+        bool all_empty = true, all_neg = true;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const float v = base[((q >> 2) & 1) * sx + ((q >> 1) & 1) * sy + (q & 1)];
+            all_empty &= v != v;
+            all_neg &= v < 0.f;   // NaN compares false
+        }
+        dead &= all_empty || all_neg;
+    }
+    dead = __syncthreads_and(dead);
+    if (dead && threadIdx.x == 0) atomicOr(bits + (b >> 5), 1u << (b & 31));
+}
+
+extern "C" int64_t plx_brick_words(const int64_t dims[3]) {
+    int64_t n = 1;
+    for (int a = 0; a < 3; ++a) n *= (dims[a] - 2) / kBrick + 1;
+    return (n + 31) / 32;
+}
+
+extern "C" int plx_build_brick_dead(const plx_grid *g, uint32_t *brick_dead, void *stream) {
+    if (!grid_ok(g) || !brick_dead || !g->sigma_lat) return PLX_EINVAL;
+    plx_grid gg = *g;
+    gg.brick_dead = brick_dead;
+    const DGrid G = make_dgrid(gg);
+    const int64_t nb = (int64_t)G.Bx * G.By * G.Bz;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemsetAsync(brick_dead, 0, ((nb + 31) / 32) * sizeof(uint32_t), s) != cudaSuccess)
+        return PLX_ECUDA;
+    brick_dead_kernel<<<(unsigned)nb, 256, 0, s>>>(G, brick_dead);
     return status();
 }
 

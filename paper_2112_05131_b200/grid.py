@@ -15,6 +15,7 @@ through libplx.so; there is no CPU path.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -36,6 +37,10 @@ def row_array(n_rows: int, device, zero: bool = True) -> torch.Tensor:
 # Empty-space skipping through the per-cell occupancy bitmask (an exact
 # shortcut: a cell whose 8 corners are all empty has occ == False, K:126-135).
 USE_CELL_OCC = True
+# Dead-brick skipping (plx_grid.brick_dead, an exact shortcut: an 8^3-cell
+# brick none of whose positions can be composited is skipped by the march's
+# sigma gathers); sparse grids with a sigma mirror only.  PLX_BRICKS=0: off.
+USE_BRICKS = os.environ.get("PLX_BRICKS", "1") != "0"
 
 
 def _dev(device):
@@ -140,6 +145,7 @@ class SparseGrid:
         self._cell_occ = None
         self._lat = None
         self._row_cell = None
+        self._bricks = None
 
     # -- constructors -------------------------------------------------------
     @classmethod
@@ -155,6 +161,7 @@ class SparseGrid:
         g._cell_occ = None
         g._lat = None
         g._row_cell = None
+        g._bricks = None
         return g
 
     @classmethod
@@ -191,6 +198,7 @@ class SparseGrid:
         self._cell_occ = None
         self._lat = None
         self._row_cell = None
+        self._bricks = None
 
     @property
     def table(self) -> torch.Tensor:
@@ -219,6 +227,7 @@ class SparseGrid:
         self.sh[:, 0] = 0.0
         self._lat = None
         self._row_cell = None
+        self._bricks = None
 
     @property
     def device(self):
@@ -269,6 +278,7 @@ class SparseGrid:
             if aliased != identity:
                 self._lat = None
                 self._row_cell = None
+                self._bricks = None
                 self.lattice_sigma()
                 return
             if self._row_cell is not None and self.n_rows and not aliased:
@@ -277,6 +287,7 @@ class SparseGrid:
             if not aliased:
                 _lib.check(L.plx_build_sigma_lat(ctypes.byref(c), self._lat.data_ptr(), s),
                            "build_sigma_lat")
+                self.rebuild_bricks()
 
     def cell_occ(self) -> torch.Tensor:
         if self._cell_occ is None:
@@ -313,7 +324,28 @@ class SparseGrid:
             _lib.check(L.plx_build_sigma_lat(ctypes.byref(c), lat.data_ptr(), s),
                        "build_sigma_lat")
             self._row_cell, self._lat = rc, lat
+            if USE_BRICKS and getattr(self, "use_bricks", True):
+                self._bricks = torch.empty(int(L.plx_brick_words(_lib.dims_array(self.dims))),
+                                           dtype=torch.int32, device=self.device)
+                self.rebuild_bricks()
         return self._lat, self._row_cell
+
+    def rebuild_bricks(self) -> None:
+        """Recompute the dead-brick mask from the sigma mirror.  The
+        optimisers only clear bits (a brick revives when a corner's sigma
+        becomes >= 0), so the mask tightens only here: the trainer calls this
+        periodically."""
+        if getattr(self, "_bricks", None) is None:
+            return
+        c = self._c(with_occ=False, with_lat=False)
+        _lib.check(_lib.lib().plx_build_brick_dead(ctypes.byref(c), self._bricks.data_ptr(),
+                                                   _lib.stream_ptr()), "build_brick_dead")
+
+    def disable_bricks(self) -> None:
+        """No dead-brick mask on this grid (the N-GPU owner update keeps the
+        peers' sigma mirrors but not their masks)."""
+        self.use_bricks = False
+        self._bricks = None
 
     def _c(self, with_occ: bool = True, with_lat: bool | None = None) -> _lib.PlxGrid:
         """Kernel descriptor.  with_lat (default: with_occ) builds the
@@ -335,6 +367,8 @@ class SparseGrid:
             lat, rc = self.lattice_sigma()
             g.sigma_lat = lat.data_ptr()
             g.row_cell = rc.data_ptr()
+            bricks = getattr(self, "_bricks", None)
+            g.brick_dead = bricks.data_ptr() if bricks is not None else None
         # the cell-occupancy bitmask skips empty space; a fully occupied
         # (identity-linked) grid has none, and with the sigma mirror the test
         # would only add a dependent load to every march position

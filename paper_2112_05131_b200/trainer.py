@@ -227,6 +227,10 @@ def save_config(cfg: TrainConfig, path) -> None:
         yaml.safe_dump(config_to_dict(cfg), f, sort_keys=False)
 
 
+# steps between rebuilds of the grid's dead-brick mask (SparseGrid.rebuild_bricks)
+BRICK_REBUILD_EVERY = 100
+
+
 class EpochBatcher:
     """T:233-255 (identical RNG use) with a device mirror of the permutation:
     next_device() returns the same indices as next() as a CUDA int64 tensor,
@@ -410,6 +414,8 @@ class Trainer:
         self._refresh_cache()
 
     def _refresh_cache(self):
+        if self.world.active:   # the N-GPU owner update does not keep the peers' brick masks
+            self.grid.disable_bricks()
         self._cgrid = self.grid._c(with_occ=self.opts.interp == "trilinear")
         self._cgrid_plain = self.grid._c(with_occ=False)
         self._cgrad = self.grads._c()
@@ -512,6 +518,9 @@ class Trainer:
         never waits for the step it just enqueued and the GPU never idles
         between steps.  sync=True (logging steps) waits for this step's loss
         and returns it in the record."""
+        if step and step % BRICK_REBUILD_EVERY == 0:
+            # the optimisers only revive bricks; re-tighten the dead-brick mask
+            self.grid.rebuild_bricks()
         if self.is_360:
             return self._step_360(step)
         idx, off = self.batcher.next_slice()
