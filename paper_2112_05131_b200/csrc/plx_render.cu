@@ -523,17 +523,31 @@ __device__ __forceinline__ int spread3(int v) {
     return r;
 }
 
-__global__ void seg_key_kernel(Scratch S, int shx, int shy, int shz) {
+// Segments are keyed and counted in tiles of kSegTile per block: the counts
+// go through a shared histogram first, so a bucket that many segments share
+// (the occupied regions) takes one global atomic per tile instead of one per
+// segment (the per-segment atomics serialised on the hot buckets).
+constexpr int kSegTile = 2048;
+
+__global__ void __launch_bounds__(256) seg_key_kernel(Scratch S, int shx, int shy, int shz) {
+    __shared__ int hist[kBuckets];
     const int64_t nseg = *S.nseg_total;
-    for (int64_t sg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sg < nseg;
-         sg += (int64_t)gridDim.x * blockDim.x) {
-        const int ray = S.seg_ray[sg];
-        const int64_t j0 = (sg - S.seg_first[ray]) * 32;
-        const int4 c = S.cell[(int64_t)ray * S.cap + j0];
-        const int key =
-            (spread3(c.x >> shx) << 2) | (spread3(c.y >> shy) << 1) | spread3(c.z >> shz);
-        S.seg_key[sg] = key;
-        atomicAdd(S.bucket + key, 1);
+    for (int64_t t0 = (int64_t)blockIdx.x * kSegTile; t0 < nseg; t0 += (int64_t)gridDim.x * kSegTile) {
+        for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        for (int64_t sg = t0 + threadIdx.x; sg < nseg && sg < t0 + kSegTile; sg += blockDim.x) {
+            const int ray = S.seg_ray[sg];
+            const int64_t j0 = (sg - S.seg_first[ray]) * 32;
+            const int4 c = S.cell[(int64_t)ray * S.cap + j0];
+            const int key =
+                (spread3(c.x >> shx) << 2) | (spread3(c.y >> shy) << 1) | spread3(c.z >> shz);
+            S.seg_key[sg] = key;
+            atomicAdd(hist + key, 1);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kBuckets; i += blockDim.x)
+            if (hist[i]) atomicAdd(S.bucket + i, hist[i]);
+        __syncthreads();
     }
 }
 
@@ -574,12 +588,36 @@ __global__ void __launch_bounds__(1024) seg_scan_kernel(Scratch S) {
     }
 }
 
-__global__ void seg_place_kernel(Scratch S) {
+// Places the segments of a tile: ranks within the tile from a shared
+// histogram, one global atomic per (tile, bucket) reserves the tile's range
+// of the bucket, then every segment writes its slot.
+__global__ void __launch_bounds__(256) seg_place_kernel(Scratch S) {
+    __shared__ int hist[kBuckets];
+    constexpr int PER = kSegTile / 256;
     const int64_t nseg = *S.nseg_total;
-    for (int64_t sg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sg < nseg;
-         sg += (int64_t)gridDim.x * blockDim.x) {
-        const int pos = atomicAdd(S.bucket + S.seg_key[sg], 1);
-        S.ord[pos] = make_int2((int)sg, S.seg_ray[sg]);
+    for (int64_t t0 = (int64_t)blockIdx.x * kSegTile; t0 < nseg; t0 += (int64_t)gridDim.x * kSegTile) {
+        for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        int key[PER], rank[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int64_t sg = t0 + threadIdx.x + (int64_t)u * 256;
+            key[u] = -1;
+            if (sg < nseg) {
+                key[u] = S.seg_key[sg];
+                rank[u] = atomicAdd(hist + key[u], 1);
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kBuckets; i += blockDim.x)
+            if (hist[i]) hist[i] = atomicAdd(S.bucket + i, hist[i]);
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int64_t sg = t0 + threadIdx.x + (int64_t)u * 256;
+            if (key[u] >= 0) S.ord[hist[key[u]] + rank[u]] = make_int2((int)sg, S.seg_ray[sg]);
+        }
+        __syncthreads();
     }
 }
 
