@@ -137,6 +137,11 @@ class PeerMap:
 
     def __init__(self, world: World, grid, grads):
         L = _lib.lib()
+        if getattr(grid, "_bricks", None) is not None:
+            # plx_dp_owner_update keeps every rank's sigma mirror, not its
+            # dead-brick mask: the grid must be built without one
+            raise ValueError("p2p exchange: call grid.disable_bricks() before building "
+                             "descriptors (Trainer does this on N ranks)")
         mine = {}
         lat, _ = grid.lattice_sigma() if grid.n_rows else (None, None)
         if lat is not None and lat.data_ptr() == grid.density.data_ptr():

@@ -343,8 +343,13 @@ class SparseGrid:
 
     def disable_bricks(self) -> None:
         """No dead-brick mask on this grid (the N-GPU owner update keeps the
-        peers' sigma mirrors but not their masks)."""
+        peers' sigma mirrors but not their masks).  A mask already built is
+        cleared (no brick dead) and kept alive, so descriptors made before
+        this call stay valid; new descriptors carry none."""
         self.use_bricks = False
+        if getattr(self, "_bricks", None) is not None:
+            self._bricks.zero_()
+            self._bricks_retired = self._bricks
         self._bricks = None
 
     def _c(self, with_occ: bool = True, with_lat: bool | None = None) -> _lib.PlxGrid:

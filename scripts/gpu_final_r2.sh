@@ -13,12 +13,17 @@ timeout 900 python bench.py --impl reference > gpurun_out/bench_ref_$TAG.json 2>
 NB="python bench.py --steps 3 --warmup 5 --no-cpu-baseline --steady-step 0"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/launches_$TAG.csv $NB > /dev/null 2>&1
-timeout 900 ncu --cache-control none --clock-control none --kernel-name-base demangled -k 'regex:plx::' \
+# warm-cache traffic over the same 20-step window bench.py's algorithmic bytes average over
+timeout 1200 ncu --cache-control none --clock-control none --kernel-name-base demangled \
   --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv \
-  --log-file gpurun_out/warm_$TAG.csv $NB > /dev/null 2>&1
+  --log-file gpurun_out/warm_$TAG.csv python bench.py --steps 20 --warmup 5 --no-cpu-baseline \
+  --steady-step 0 > /dev/null 2>&1
 NCU="ncu --set full --clock-control none --import-source on --kernel-name-base demangled"
 timeout 900 $NCU -k "regex:march_bwd|colour_kernel|scatter_kernel|opt_rows|tv_kernel|touched_compact" -s 36 -c 6 \
   -o gpurun_out/prof_c2_$TAG $NB > /dev/null 2>&1
 STEPS=10 WARM=3 timeout 900 python scripts/sweep_c5.py > gpurun_out/sweep_c5_$TAG.log 2>&1
+# C5 2^20: the render kernels of one wave (dead-brick mask, spatial segment order)
+STEPS=1 WARM=2 LOGB0=20 LOGB1=21 timeout 1200 $NCU -k "regex:march_bwd|colour_kernel|scatter_kernel|seg_" \
+  -s 72 -c 6 -o gpurun_out/prof_c5_$TAG python scripts/sweep_c5.py > /dev/null 2>&1
 timeout 600 python scripts/bench_msi.py > gpurun_out/msi_$TAG.json 2>&1
 ls -la gpurun_out

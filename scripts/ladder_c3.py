@@ -60,7 +60,21 @@ def main():
     torch.cuda.synchronize()
     ms1 = e[0].elapsed_time(e[1]) / (S1 - 5)
     ms2 = e[4].elapsed_time(e[5]) / (S2 - 5)
+    st0 = tr.march_stats.clone()
+    for s in range(S1 + S2, S1 + S2 + 10):
+        tr.step(s)
+    torch.cuda.synchronize()
+    mst = ((tr.march_stats - st0).double() / 10 / A.batch).cpu().numpy()
+    e[0].record()
+    for _ in range(10):
+        tr.grid.rebuild_bricks()
+    e[1].record()
+    torch.cuda.synchronize()
+    brick_ms = e[0].elapsed_time(e[1]) / 10
     out = {"config": "C3 256^3 -> 512^3, density prune thr %.2f" % cfg.prune_threshold,
+           "march_per_ray_512": {"positions": float(mst[0]), "samples": float(mst[1]),
+                                 "chunks": float(mst[2])},
+           "brick_rebuild_ms": brick_ms if tr.grid._bricks is not None else None,
            "rows_256": rows_before, "rows_512": tr.grid.n_rows,
            "ms_per_step_256": ms1, "rays_per_s_256": A.batch / ms1 * 1e3,
            "ms_per_step_512": ms2, "rays_per_s_512": A.batch / ms2 * 1e3,
