@@ -384,6 +384,68 @@ struct LaneAcc {
     }
 };
 
+// Dead-brick probe stride of the march (positions between probes).
+#ifndef PLX_LOOK
+#define PLX_LOOK 8
+#endif
+constexpr int kLook = PLX_LOOK;
+
+// Empty-space skip of the march (sparse grids with a dead-brick mask),
+// called after a chunk that composited nothing: returns the next chunk
+// start (32-aligned with base).
+__device__ __forceinline__ int64_t skip_dead_chunks(const DGrid &G, const RayMarch &rm, double step,
+                                                    int64_t base, int lane) {
+    // Empty space: lane l probes position base + l*kLook.  Every
+    // lattice coordinate is monotone along the ray, so the
+    // positions between two consecutive probes lie in the box of
+    // the probes' bricks; when all bricks of that box are dead
+    // (same brick, a face neighbour, or an edge neighbour plus
+    // its two corner bricks) so is every position between: the
+    // leading run of such intervals is skipped without sample
+    // math or gathers (exact).
+    const int64_t sp = base + (int64_t)lane * kLook;
+    int bx = -1, by = 0, bz = 0;
+    bool dead = false;
+    if (sp < rm.nsamp) {
+        double tt, dd, gg[3];
+        sample_coords(rm, G, step, sp, tt, dd, gg);
+        brick_xyz(G, gg, bx, by, bz);
+        dead = brick_is_dead(G, (bx * G.By + by) * G.Bz + bz);
+    }
+    // the interval to the next probe is certainly dead when both
+    // ends are dead and the bricks between (per-axis monotone:
+    // inside the box of the two) are: same brick, a face
+    // neighbour, or an edge neighbour whose two corner bricks
+    // are dead too
+    const int nx = __shfl_down_sync(PLX_FULL_MASK, bx, 1);
+    const int ny = __shfl_down_sync(PLX_FULL_MASK, by, 1);
+    const int nz = __shfl_down_sync(PLX_FULL_MASK, bz, 1);
+    const unsigned dm = __ballot_sync(PLX_FULL_MASK, dead);
+    bool cert = lane < 31 && dead && ((dm >> (lane + 1)) & 1u);
+    if (cert) {
+        const int ax = nx - bx, ay = ny - by, az = nz - bz;
+        const int nd = (ax != 0) + (ay != 0) + (az != 0);
+        if (ax < -1 || ax > 1 || ay < -1 || ay > 1 || az < -1 || az > 1 || nd == 3) {
+            cert = false;
+        } else if (nd == 2) {
+            // the ray passes through one of the two other bricks
+            // of the 2x2 box: b with the first differing axis
+            // moved, or with the second one moved
+            const int f = ax ? 0 : 1, sc = az ? 2 : 1;
+            const int c1x = f == 0 ? nx : bx, c1y = f == 1 ? ny : by;
+            const int c2y = sc == 1 ? ny : by, c2z = sc == 2 ? nz : bz;
+            cert = brick_is_dead(G, (c1x * G.By + c1y) * G.Bz + bz) &&
+                   brick_is_dead(G, (bx * G.By + c2y) * G.Bz + c2z);
+        }
+    }
+    const unsigned cd = __ballot_sync(PLX_FULL_MASK, cert);
+    const int nskip = __ffs(~cd) - 1;   // leading certain-dead intervals
+    // whole chunks only: chunks keep their 32-aligned positions,
+    // so the compositing scans (and their rounding) are those of
+    // the march without skipping -- results are bit-identical
+    return base + (int64_t)(nskip * kLook / 32) * 32;
+}
+
 // Forward render / max-weight: one pass over the positions (K:173-238,
 // K:414-453).  Static grid-stride over rays.
 template <int MODE, bool ABS, bool NEAREST>
@@ -409,13 +471,15 @@ __global__ void __launch_bounds__(128, 6)
         const double jit = (MODE == FWD && R.jitter) ? R.jitter[ray] : 0.0;
         ray_march_setup(rm, G, O.step, jit);
         double T = 1.0, A = 0.0, C0 = 0.0, C1 = 0.0, C2 = 0.0, wsum = 0.0;
-        bool stopped = false;
+        bool stopped = false, idle = true;
         for (int64_t base = 0; base < rm.nsamp && !stopped; base += 32) {
+            if (!NEAREST && G.brick_dead && idle) base = skip_dead_chunks(G, rm, O.step, base, lane);
             Sample s;
             eval_sample<MODE, NEAREST>(G, rm, O.step, base + lane, bf, s);
             const int npos = (int)min((int64_t)32, rm.nsamp - base);
             st_chunks += 1;
-            if (!__any_sync(PLX_FULL_MASK, s.incl)) {
+            idle = !__any_sync(PLX_FULL_MASK, s.incl);
+            if (idle) {
                 st_pos += npos;
                 continue;
             }
@@ -621,12 +685,6 @@ __global__ void __launch_bounds__(256) seg_place_kernel(Scratch S) {
     }
 }
 
-// Dead-brick probe stride of the march (positions between probes).
-#ifndef PLX_LOOK
-#define PLX_LOOK 8
-#endif
-constexpr int kLook = PLX_LOOK;
-
 template <bool ABS, bool NEAREST, int MINB>
 __global__ void __launch_bounds__(128, MINB)
     march_bwd_kernel(DGrid G, RayArgs R, KOpts O, Outs out, Scratch S) {
@@ -672,57 +730,7 @@ __global__ void __launch_bounds__(128, MINB)
         bool stopped = false;
         bool idle = true;   // the previous chunk composited nothing
         for (int64_t base = 0; base < rm.nsamp && !stopped; base += 32) {
-            if (!NEAREST && G.brick_dead && idle) {
-                // Empty space: lane l probes position base + l*kLook.  Every
-                // lattice coordinate is monotone along the ray, so the
-                // positions between two consecutive probes lie in the box of
-                // the probes' bricks; when all bricks of that box are dead
-                // (same brick, a face neighbour, or an edge neighbour plus
-                // its two corner bricks) so is every position between: the
-                // leading run of such intervals is skipped without sample
-                // math or gathers (exact).
-                const int64_t sp = base + (int64_t)lane * kLook;
-                int bx = -1, by = 0, bz = 0;
-                bool dead = false;
-                if (sp < rm.nsamp) {
-                    double tt, dd, gg[3];
-                    sample_coords(rm, G, O.step, sp, tt, dd, gg);
-                    brick_xyz(G, gg, bx, by, bz);
-                    dead = brick_is_dead(G, (bx * G.By + by) * G.Bz + bz);
-                }
-                // the interval to the next probe is certainly dead when both
-                // ends are dead and the bricks between (per-axis monotone:
-                // inside the box of the two) are: same brick, a face
-                // neighbour, or an edge neighbour whose two corner bricks
-                // are dead too
-                const int nx = __shfl_down_sync(PLX_FULL_MASK, bx, 1);
-                const int ny = __shfl_down_sync(PLX_FULL_MASK, by, 1);
-                const int nz = __shfl_down_sync(PLX_FULL_MASK, bz, 1);
-                const unsigned dm = __ballot_sync(PLX_FULL_MASK, dead);
-                bool cert = lane < 31 && dead && ((dm >> (lane + 1)) & 1u);
-                if (cert) {
-                    const int ax = nx - bx, ay = ny - by, az = nz - bz;
-                    const int nd = (ax != 0) + (ay != 0) + (az != 0);
-                    if (ax < -1 || ax > 1 || ay < -1 || ay > 1 || az < -1 || az > 1 || nd == 3) {
-                        cert = false;
-                    } else if (nd == 2) {
-                        // the ray passes through one of the two other bricks
-                        // of the 2x2 box: b with the first differing axis
-                        // moved, or with the second one moved
-                        const int f = ax ? 0 : 1, sc = az ? 2 : 1;
-                        const int c1x = f == 0 ? nx : bx, c1y = f == 1 ? ny : by;
-                        const int c2y = sc == 1 ? ny : by, c2z = sc == 2 ? nz : bz;
-                        cert = brick_is_dead(G, (c1x * G.By + c1y) * G.Bz + bz) &&
-                               brick_is_dead(G, (bx * G.By + c2y) * G.Bz + c2z);
-                    }
-                }
-                const unsigned cd = __ballot_sync(PLX_FULL_MASK, cert);
-                const int nskip = __ffs(~cd) - 1;   // leading certain-dead intervals
-                // whole chunks only: chunks keep their 32-aligned positions,
-                // so the compositing scans (and their rounding) are those of
-                // the march without skipping -- results are bit-identical
-                base += (int64_t)(nskip * kLook / 32) * 32;
-            }
+            if (!NEAREST && G.brick_dead && idle) base = skip_dead_chunks(G, rm, O.step, base, lane);
             const int64_t si = base + lane;
             bool incl = false;
             double att = 1.0, sig = 0.0, t, dlt, g[3], fd[3];
