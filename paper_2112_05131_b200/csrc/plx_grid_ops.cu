@@ -58,8 +58,6 @@ __device__ __forceinline__ void root_and_rinv(double s, double &root, double &ri
 // (K:505-532) is column 0, owned by quad 0.
 template <int NT>
 __global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
-    using BR = cub::BlockReduce<double, NT>;
-    __shared__ typename BR::TempStorage tmp;
     const int lane = threadIdx.x & 31;
     const int sub = lane / 7, quad = lane % 7;
     const int64_t nw = (int64_t)gridDim.x * (NT / 32);
@@ -184,10 +182,28 @@ __global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
             }
         }
     }
-    double s1 = BR(tmp).Sum(sig_sum);
+    // both sums in one pass: warp shuffles, one shared-memory exchange, one
+    // barrier (short blocks run one iteration, so this reduction is a large
+    // share of a block's work)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        sig_sum += __shfl_down_sync(PLX_FULL_MASK, sig_sum, off);
+        sh_sum += __shfl_down_sync(PLX_FULL_MASK, sh_sum, off);
+    }
+    __shared__ double part[2][NT / 32];
+    const int wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        part[0][wid] = sig_sum;
+        part[1][wid] = sh_sum;
+    }
     __syncthreads();
-    double s2 = BR(tmp).Sum(sh_sum);
     if (threadIdx.x == 0) {
+        double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < NT / 32; ++k) {
+            s1 += part[0][k];
+            s2 += part[1][k];
+        }
         atomicAdd(a.sums + 0, s1);
         atomicAdd(a.sums + 1, s2);
     }
