@@ -418,7 +418,10 @@ __device__ __forceinline__ bool sigma_at(const DGrid &G, const double *g, double
         if ((__ldg(G.brick_dead + (b >> 5)) >> (b & 31)) & 1u) return false;
     }
     const int32_t c = flat(G, i0, j0, k0);
-    if (G.cell_occ && !((__ldg(G.cell_occ + (c >> 5)) >> (c & 31)) & 1u)) return false;
+    // with a brick mask the occupancy bit only adds a dependent load before
+    // the sigma gathers (an all-empty cell exits below just the same):
+    // C5 2^20 44.1 -> 44.9 M rays/s without it
+    if (G.cell_occ && !G.brick_dead && !((__ldg(G.cell_occ + (c >> 5)) >> (c & 31)) & 1u)) return false;
     f[0] = g[0] - (double)i0;
     f[1] = g[1] - (double)j0;
     f[2] = g[2] - (double)k0;
