@@ -1718,10 +1718,13 @@ int64_t max_records(const plx_grid *g, double step) {
 
 // Records are kept for every march position of the longest chord of every
 // ray of a wave; a batch larger than the budget runs in waves.
-// Record budget per wave: 32 GiB of a 180 GB B200 (C5 sweep, 2^18..2^20
-// rays: 8 GiB waves 29.4 / 32.8 / 35.0 M rays/s, 32 GiB 30.4 / 33.7 / 36.0).
+// Record budget per wave: 64 GiB of a 180 GB B200 (C5 sweep, 2^18..2^20
+// rays: 8 GiB waves 29.4 / 32.8 / 35.0 M rays/s, 32 GiB 30.4 / 33.7 / 36.0;
+// with the segment order and dead bricks 32 GiB 36.6 / 41.4 / 44.9, 64 GiB
+// 37.5 / 42.3 / 45.6, 96 GiB the same as 64).  Only batches that need it
+// allocate it (the scratch is sized for min(batch, wave)).
 #ifndef PLX_RECORD_GIB
-#define PLX_RECORD_GIB 32
+#define PLX_RECORD_GIB 64
 #endif
 constexpr int64_t kRecordBudget = (int64_t)PLX_RECORD_GIB << 30;   // bytes of records per wave
 constexpr int64_t kRecordBytes = 112;                 // att, T, w, c, cell, f, rows, sig

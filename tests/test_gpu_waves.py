@@ -1,4 +1,4 @@
-"""Batches larger than one wave of records (the record budget, 32 GiB, is
+"""Batches larger than one wave of records (the record budget, 64 GiB, is
 reached at C5-size batches) render in waves; every wave-sliced entry point
 (array rays, upstream mode with jitter, the 360 backward, the trainer's
 camera-pool / CUDA-graph step) must give the single-wave results.  A small
