@@ -50,14 +50,15 @@ __device__ __forceinline__ void root_and_rinv(double s, double &root, double &ri
     rinv = y;
 }
 
-// Warp-cooperative TV: 4 cells per warp iteration, lane = (cell, column
+// TV on identity-linked dense grids (every cell has an SH term): 4 cells per
+// warp iteration, lane = (cell, column
 // quad): the 7 lanes of a cell own its 7 float4 column groups, so the 4 rows
 // (self, +x, +y, +z) of a cell are read and reduced as 7 parallel float4s
 // instead of a 7-step loop per thread.  Per column the arithmetic is the
 // reference's (float64, one sqrt per coefficient, K:534-568); the sigma term
 // (K:505-532) is column 0, owned by quad 0.
 template <int NT>
-__global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
+__global__ void __launch_bounds__(NT) tv_dense_kernel(DGrid G, TvArgs a) {
     const int lane = threadIdx.x & 31;
     const int sub = lane / 7, quad = lane % 7;
     const int64_t nw = (int64_t)gridDim.x * (NT / 32);
@@ -195,6 +196,219 @@ __global__ void __launch_bounds__(NT) tv_kernel(DGrid G, TvArgs a) {
     if (lane == 0) {
         part[0][wid] = sig_sum;
         part[1][wid] = sh_sum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < NT / 32; ++k) {
+            s1 += part[0][k];
+            s2 += part[1][k];
+        }
+        atomicAdd(a.sums + 0, s1);
+        atomicAdd(a.sums + 1, s2);
+    }
+}
+
+// TV on sparse grids, in two phases per warp iteration of 32 cells.
+//   phase 1, lane = cell: the cell's 4 links (self, +x, +y, +z; none on an
+//     identity-linked grid), the sigma term (K:505-532; missing rows read as
+//     0) and its gradients.  A cell whose SH term is empty -- no self row or
+//     no neighbour row, K:534-568 then contributes 27 eps -- is finished here
+//     (scalar reductions into column 0).
+//   phase 2, the cells with an SH term, 4 at a time, lane = (cell, column
+//     quad): the 7 lanes of a cell own its 7 float4 column groups, so the 4
+//     rows of a cell are read and reduced as 7 parallel float4s; quad 0
+//     carries the cell's sigma gradients (column 0) from phase 1 into its
+//     reductions.
+// On sparse grids most cells of the run are empty (C3 at 512^3: ~86 %), so
+// they no longer occupy a 7-lane cell slot.  Per column the arithmetic is
+// the reference's (float64, one sqrt per coefficient).
+struct TvCell {
+    int32_t r0, rx, ry, rz;
+    float g0, gx, gy, gz;   // sigma gradients (column 0)
+    unsigned flags;         // bit 0..3: sigma touched self / x / y / z
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT) tv_sparse_kernel(DGrid G, TvArgs a) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int sub = lane / 7, quad = lane % 7;
+    __shared__ TvCell cells[NT / 32][32];
+    TvCell *wc = cells[wib];
+    const int64_t nw = (int64_t)gridDim.x * (NT / 32);
+    const double e2 = a.eps * a.eps;
+    const float *T = G.table;
+    double sig_sum = 0.0, sh_sum = 0.0;
+    for (int64_t w = (int64_t)blockIdx.x * (NT / 32) + wib; w * 32 < a.count; w += nw) {
+        // ---- phase 1: one cell per lane ----
+        const int64_t ci = w * 32 + lane;
+        const bool valid = ci < a.count;
+        int32_t r0 = -1, rx = -1, ry = -1, rz = -1;
+        bool sh_on = false;
+        if (valid) {
+            int64_t cid;   // L:41-47 (lattice < 2^31 cells: 32-bit index math)
+            if (a.cells) {
+                cid = a.cells[ci];
+            } else {
+                cid = (a.start_dev ? *a.start_dev : a.start) + ci;
+                if (cid >= a.ncell) cid %= a.ncell;   // wrapped run (rare branch)
+            }
+            const uint32_t c32 = (uint32_t)cid, dz = (uint32_t)G.Dz;
+            const uint32_t ij = c32 / dz, k = c32 - ij * dz;
+            const uint32_t i = ij / (uint32_t)G.Dy, j = ij - i * (uint32_t)G.Dy;
+            int64_t ii = i + 1, jj = j + 1, kk = k + 1;
+            bool hx = true, hy = true, hz = true;
+            if (ii >= G.Dx) { if (a.wrap[0]) ii = 0; else hx = false; }
+            if (jj >= G.Dy) { if (a.wrap[1]) jj = 0; else hy = false; }
+            if (kk >= G.Dz) { if (a.wrap[2]) kk = 0; else hz = false; }
+            if (G.identity) {   // dense identity-linked grid: no link gathers
+                r0 = (int32_t)cid;
+                rx = hx ? (int32_t)flat(G, ii, j, k) : -1;
+                ry = hy ? (int32_t)flat(G, i, jj, k) : -1;
+                rz = hz ? (int32_t)flat(G, i, j, kk) : -1;
+            } else {
+                r0 = __ldg(G.links + cid);
+                rx = hx ? __ldg(G.links + flat(G, ii, j, k)) : -1;
+                ry = hy ? __ldg(G.links + flat(G, i, jj, k)) : -1;
+                rz = hz ? __ldg(G.links + flat(G, i, j, kk)) : -1;
+            }
+            sh_on = r0 >= 0 && (rx >= 0 || ry >= 0 || rz >= 0);
+            // opacity term (K:505-532): missing neighbours read as 0
+            const double s0 = r0 >= 0 ? (double)__ldg(G.density + r0) : 0.0;
+            const double sx = rx >= 0 ? (double)__ldg(G.density + rx) : 0.0;
+            const double sy = ry >= 0 ? (double)__ldg(G.density + ry) : 0.0;
+            const double sz = rz >= 0 ? (double)__ldg(G.density + rz) : 0.0;
+            const double dxv = (sx - s0) * a.fac[0], dyv = (sy - s0) * a.fac[1],
+                         dzv = (sz - s0) * a.fac[2];
+            const double s2v = dxv * dxv + dyv * dyv + dzv * dzv + e2;
+            double val = 0.0, rinv = 0.0;
+            if (s2v > 0.0) root_and_rinv(s2v, val, rinv);
+            sig_sum += val;
+            if (!sh_on) sh_sum += 27.0 * a.eps;   // empty self / no neighbour
+            TvCell tc{r0, rx, ry, rz, 0.f, 0.f, 0.f, 0.f, 0u};
+            if (a.with_grad && val > 0.0) {
+                const double inv = a.f_sigma * rinv;
+                double g0 = 0.0;
+                if (rx >= 0) { tc.flags |= 2u; tc.gx = (float)(dxv * a.fac[0] * inv); }
+                g0 -= dxv * a.fac[0] * inv;
+                if (ry >= 0) { tc.flags |= 4u; tc.gy = (float)(dyv * a.fac[1] * inv); }
+                g0 -= dyv * a.fac[1] * inv;
+                if (rz >= 0) { tc.flags |= 8u; tc.gz = (float)(dzv * a.fac[2] * inv); }
+                g0 -= dzv * a.fac[2] * inv;
+                if (r0 >= 0 && g0 != 0.0) { tc.flags |= 1u; tc.g0 = (float)g0; }
+            }
+            if (sh_on) {
+                wc[lane] = tc;
+            } else if (a.with_grad) {   // sigma-only cell: finished here
+                if (tc.gx != 0.f) atomicAdd(a.grad + (int64_t)rx * PLX_STRIDE, tc.gx);
+                if (tc.gy != 0.f) atomicAdd(a.grad + (int64_t)ry * PLX_STRIDE, tc.gy);
+                if (tc.gz != 0.f) atomicAdd(a.grad + (int64_t)rz * PLX_STRIDE, tc.gz);
+                if (tc.g0 != 0.f) atomicAdd(a.grad + (int64_t)r0 * PLX_STRIDE, tc.g0);
+                if (tc.flags & 2u) a.tmask[rx] = 1;
+                if (tc.flags & 4u) a.tmask[ry] = 1;
+                if (tc.flags & 8u) a.tmask[rz] = 1;
+                if (tc.flags & 1u) a.tmask[r0] = 1;
+            }
+        }
+        // the cells with an SH term, compacted in lane order
+        const unsigned shm = __ballot_sync(PLX_FULL_MASK, sh_on);
+        const int nsh = __popc(shm);
+        __syncwarp();
+        // ---- phase 2: 4 SH cells per round, 7 lanes per cell ----
+        for (int g = 0; g < nsh; g += 4) {
+            const int idx = g + sub;
+            const bool ok = lane < 28 && idx < nsh;
+            // lane of the idx-th set bit of shm
+            int src = 0;
+            if (ok) {
+                unsigned m = shm;
+                for (int t = 0; t < idx; ++t) m &= m - 1;
+                src = __ffs(m) - 1;
+            }
+            TvCell tc{-1, -1, -1, -1, 0.f, 0.f, 0.f, 0.f, 0u};
+            if (ok) tc = wc[src];
+            bool tx = false, ty = false, tz = false, t0 = false;
+            float gx[4] = {0.f, 0.f, 0.f, 0.f}, gy[4] = {0.f, 0.f, 0.f, 0.f};
+            float gz[4] = {0.f, 0.f, 0.f, 0.f}, g0v[4] = {0.f, 0.f, 0.f, 0.f};
+            if (ok) {
+                const bool okx = tc.rx >= 0, oky = tc.ry >= 0, okz = tc.rz >= 0;
+                const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                const float4 v0 = __ldg(reinterpret_cast<const float4 *>(T + (int64_t)tc.r0 * PLX_STRIDE) + quad);
+                const float4 vx = okx ? __ldg(reinterpret_cast<const float4 *>(T + (int64_t)tc.rx * PLX_STRIDE) + quad) : z4;
+                const float4 vy = oky ? __ldg(reinterpret_cast<const float4 *>(T + (int64_t)tc.ry * PLX_STRIDE) + quad) : z4;
+                const float4 vz = okz ? __ldg(reinterpret_cast<const float4 *>(T + (int64_t)tc.rz * PLX_STRIDE) + quad) : z4;
+                if (quad == 0) {   // column 0: the sigma gradients of phase 1
+                    gx[0] = tc.gx;
+                    gy[0] = tc.gy;
+                    gz[0] = tc.gz;
+                    g0v[0] = tc.g0;
+                    tx = tc.flags & 2u;
+                    ty = tc.flags & 4u;
+                    tz = tc.flags & 8u;
+                    t0 = tc.flags & 1u;
+                }
+                // K:534-568, columns 4*quad .. 4*quad+3 (column 0 is sigma)
+                const float c0[4] = {v0.x, v0.y, v0.z, v0.w}, cx[4] = {vx.x, vx.y, vx.z, vx.w};
+                const float cy[4] = {vy.x, vy.y, vy.z, vy.w}, cz[4] = {vz.x, vz.y, vz.z, vz.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (quad == 0 && e == 0) continue;
+                    const double v0d = (double)c0[e];
+                    const double ax = okx ? ((double)cx[e] - v0d) * a.fac[0] : 0.0;
+                    const double ay = oky ? ((double)cy[e] - v0d) * a.fac[1] : 0.0;
+                    const double az = okz ? ((double)cz[e] - v0d) * a.fac[2] : 0.0;
+                    const double s2v = ax * ax + ay * ay + az * az + e2;
+                    double v = 0.0, rinv = 0.0;
+                    if (s2v > 0.0) root_and_rinv(s2v, v, rinv);
+                    sh_sum += v;
+                    if (a.with_grad && v > 0.0) {
+                        const double inv = a.f_sh * rinv;
+                        double g0 = 0.0;
+                        if (okx) { tx = true; gx[e] = (float)(ax * a.fac[0] * inv); g0 -= ax * a.fac[0] * inv; }
+                        if (oky) { ty = true; gy[e] = (float)(ay * a.fac[1] * inv); g0 -= ay * a.fac[1] * inv; }
+                        if (okz) { tz = true; gz[e] = (float)(az * a.fac[2] * inv); g0 -= az * a.fac[2] * inv; }
+                        if (g0 != 0.0) { t0 = true; g0v[e] = (float)g0; }
+                    }
+                }
+                if (a.with_grad) {
+                    if (okx && (gx[0] != 0.f || gx[1] != 0.f || gx[2] != 0.f || gx[3] != 0.f))
+                        red_add_v4(a.grad + (int64_t)tc.rx * PLX_STRIDE + 4 * quad, gx[0], gx[1], gx[2], gx[3]);
+                    if (oky && (gy[0] != 0.f || gy[1] != 0.f || gy[2] != 0.f || gy[3] != 0.f))
+                        red_add_v4(a.grad + (int64_t)tc.ry * PLX_STRIDE + 4 * quad, gy[0], gy[1], gy[2], gy[3]);
+                    if (okz && (gz[0] != 0.f || gz[1] != 0.f || gz[2] != 0.f || gz[3] != 0.f))
+                        red_add_v4(a.grad + (int64_t)tc.rz * PLX_STRIDE + 4 * quad, gz[0], gz[1], gz[2], gz[3]);
+                    if (g0v[0] != 0.f || g0v[1] != 0.f || g0v[2] != 0.f || g0v[3] != 0.f)
+                        red_add_v4(a.grad + (int64_t)tc.r0 * PLX_STRIDE + 4 * quad, g0v[0], g0v[1], g0v[2], g0v[3]);
+                }
+            }
+            if (a.with_grad) {   // _touch (K:155-160): a row is touched if any column got a value
+                const unsigned cell_lanes = 0x7fu << (7 * (sub & 3));
+                const bool bx = __ballot_sync(PLX_FULL_MASK, tx) & cell_lanes;
+                const bool by = __ballot_sync(PLX_FULL_MASK, ty) & cell_lanes;
+                const bool bz = __ballot_sync(PLX_FULL_MASK, tz) & cell_lanes;
+                const bool b0 = __ballot_sync(PLX_FULL_MASK, t0) & cell_lanes;
+                if (ok && quad == 0) {
+                    if (bx) a.tmask[tc.rx] = 1;
+                    if (by) a.tmask[tc.ry] = 1;
+                    if (bz) a.tmask[tc.rz] = 1;
+                    if (b0) a.tmask[tc.r0] = 1;
+                }
+            }
+        }
+        __syncwarp();   // wc reused by the next iteration
+    }
+    // both sums in one pass: warp shuffles, one shared-memory exchange, one
+    // barrier
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        sig_sum += __shfl_down_sync(PLX_FULL_MASK, sig_sum, off);
+        sh_sum += __shfl_down_sync(PLX_FULL_MASK, sh_sum, off);
+    }
+    __shared__ double part[2][NT / 32];
+    if (lane == 0) {
+        part[0][wib] = sig_sum;
+        part[1][wib] = sh_sum;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -920,17 +1134,29 @@ int plx::tv_impl(const plx_grid *g, const int64_t *cells, int64_t start, const i
     a.sums = out_sums;
     constexpr int NT = 256;
     // 8 warps x 4 cells per block iteration, at most one resident wave
-    static int tv_bps = 0;
-    if (!tv_bps) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tv_bps, tv_kernel<NT>, NT, 0);
-        if (tv_bps <= 0) tv_bps = 1;
+    // identity-linked dense grids: every cell has an SH term (C2: the
+    // two-phase kernel measured 54.9 vs 51.3 us there); sparse grids: the
+    // two-phase kernel (C3 at 512^3: 362 -> 226 us, the step 0.568 -> 0.437 ms)
+    const DGrid G = make_dgrid(*g);
+    static int bps_dense = 0, bps_sparse = 0;
+    if (!bps_dense) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_dense, tv_dense_kernel<NT>, NT, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_sparse, tv_sparse_kernel<NT>, NT, 0);
+        if (bps_dense <= 0) bps_dense = 1;
+        if (bps_sparse <= 0) bps_sparse = 1;
     }
-    int64_t nb = (count + 31) / 32;
-    // short_blocks: one 32-cell iteration per block, so the blocks of a
-    // background TV yield their SM slots quickly to a higher-priority
-    // stream's kernels; else one resident wave
-    if (!short_blocks && nb > (int64_t)num_sms() * tv_bps) nb = (int64_t)num_sms() * tv_bps;
-    tv_kernel<NT><<<(unsigned)nb, NT, 0, (cudaStream_t)stream>>>(make_dgrid(*g), a);
+    // cells per block iteration: 32 (dense: 8 warps x 4), NT (sparse: a cell per thread)
+    const int64_t per = G.identity ? 32 : NT;
+    const int bps = G.identity ? bps_dense : bps_sparse;
+    int64_t nb = (count + per - 1) / per;
+    // short_blocks: one iteration per block, so the blocks of a background
+    // TV yield their SM slots quickly to a higher-priority stream's kernels;
+    // else one resident wave
+    if (!short_blocks && nb > (int64_t)num_sms() * bps) nb = (int64_t)num_sms() * bps;
+    if (G.identity)
+        tv_dense_kernel<NT><<<(unsigned)nb, NT, 0, (cudaStream_t)stream>>>(G, a);
+    else
+        tv_sparse_kernel<NT><<<(unsigned)nb, NT, 0, (cudaStream_t)stream>>>(G, a);
     return status();
 }
 

@@ -19,7 +19,7 @@ timeout 1200 ncu --cache-control none --clock-control none --kernel-name-base de
   --log-file gpurun_out/warm_$TAG.csv python bench.py --steps 20 --warmup 5 --no-cpu-baseline \
   --steady-step 0 > /dev/null 2>&1
 NCU="ncu --set full --clock-control none --import-source on --kernel-name-base demangled"
-timeout 900 $NCU -k "regex:march_bwd|colour_kernel|scatter_kernel|opt_rows|tv_kernel|touched_compact" -s 36 -c 6 \
+timeout 900 $NCU -k "regex:march_bwd|colour_kernel|scatter_kernel|opt_rows|tv_dense_kernel|tv_sparse_kernel|touched_compact" -s 36 -c 6 \
   -o gpurun_out/prof_c2_$TAG $NB > /dev/null 2>&1
 STEPS=10 WARM=3 timeout 900 python scripts/sweep_c5.py > gpurun_out/sweep_c5_$TAG.log 2>&1
 # C5 2^20: the render kernels of one wave (dead-brick mask, spatial segment order)

@@ -6,7 +6,7 @@
 mkdir -p gpurun_out
 NCU="ncu --set full --clock-control none --import-source on --kernel-name-base demangled"
 # C2 headline: warm-up 5 steps, then kernels of step 5 (prologue, march, colour, scatter, tv, compact, opt)
-timeout 900 $NCU -k "regex:march_bwd|colour_kernel|scatter_kernel|opt_rows|tv_kernel" -s 30 -c 5 \
+timeout 900 $NCU -k "regex:march_bwd|colour_kernel|scatter_kernel|opt_rows|tv_dense_kernel|tv_sparse_kernel" -s 30 -c 5 \
   -o gpurun_out/prof_c2_r2 python bench.py --steps 3 --warmup 5 --no-cpu-baseline --steady-step 0 \
   > gpurun_out/prof_c2_r2.log 2>&1
 # C5 at 2^18 (6 waves/step) and 2^20: render kernels of the first wave after 3 warm-up steps

@@ -71,7 +71,21 @@ def main():
     e[1].record()
     torch.cuda.synchronize()
     brick_ms = e[0].elapsed_time(e[1]) / 10
+    kt = None
+    if os.environ.get("C3_PROFILE"):   # per-kernel device times at 512^3 (CUPTI)
+        from collections import defaultdict
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for s in range(S1 + S2 + 10, S1 + S2 + 20):
+                tr.step(s)
+            torch.cuda.synchronize()
+        agg = defaultdict(float)
+        for ev in prof.events():
+            if ev.device_type.name == "CUDA":
+                agg[ev.name[:50]] += ev.device_time / 10
+        kt = {k: round(v, 1) for k, v in sorted(agg.items(), key=lambda kv: -kv[1])[:10]}
     out = {"config": "C3 256^3 -> 512^3, density prune thr %.2f" % cfg.prune_threshold,
+           "kernel_us_per_step_512": kt,
            "march_per_ray_512": {"positions": float(mst[0]), "samples": float(mst[1]),
                                  "chunks": float(mst[2])},
            "brick_rebuild_ms": brick_ms if tr.grid._bricks is not None else None,

@@ -92,7 +92,7 @@ def main():
                                                   "scatter_kernel"))
                        else "opt_step" if any(k in name for k in
                                               ("opt_rows_kernel", "touched_compact"))
-                       else "tv" if "tv_kernel" in name else None)
+                       else "tv" if ("tv_dense_kernel" in name or "tv_sparse_kernel" in name or "plx::tv_kernel" in name) else None)
                 if key:
                     sums[key] = sums.get(key, 0.0) + rd + wr
             except (KeyError, ValueError):

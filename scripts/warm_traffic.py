@@ -29,7 +29,7 @@ for r in csv.DictReader(io.StringIO(body)):
              "usecond": 1e-6, "msecond": 1e-3}.get(u, 1)
     launches[i][r["Metric Name"]] = v * scale
 LEG = {"march_bwd": "render_fused_bwd", "colour_kernel": "render_fused_bwd",
-       "scatter_kernel": "render_fused_bwd", "seg_": "render_fused_bwd", "tv_kernel": "tv",
+       "scatter_kernel": "render_fused_bwd", "seg_": "render_fused_bwd", "tv_dense_kernel": "tv", "tv_sparse_kernel": "tv", "::tv_kernel": "tv",
        "touched_compact": "opt_step", "opt_rows": "opt_step"}
 steps, cur = [], None
 for i in sorted(launches):
