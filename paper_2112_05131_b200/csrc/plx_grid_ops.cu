@@ -234,15 +234,19 @@ template <int NT>
 __global__ void __launch_bounds__(NT) tv_sparse_kernel(DGrid G, TvArgs a) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int sub = lane / 7, quad = lane % 7;
-    __shared__ TvCell cells[NT / 32][32];
-    TvCell *wc = cells[wib];
-    const int64_t nw = (int64_t)gridDim.x * (NT / 32);
+    __shared__ TvCell cells[NT];           // phase-1 results, by thread
+    __shared__ uint16_t shl[NT];           // the block's SH cells, compacted
+    __shared__ int wcnt[NT / 32];
     const double e2 = a.eps * a.eps;
     const float *T = G.table;
     double sig_sum = 0.0, sh_sum = 0.0;
-    for (int64_t w = (int64_t)blockIdx.x * (NT / 32) + wib; w * 32 < a.count; w += nw) {
-        // ---- phase 1: one cell per lane ----
-        const int64_t ci = w * 32 + lane;
+    // block-wide iterations of NT cells (a cell per thread in phase 1); the
+    // SH cells of all NT are then shared out to the warps 4 at a time, so a
+    // warp whose 32 cells are empty does not leave the block waiting on one
+    // whose cells all carry SH terms
+    for (int64_t t0 = (int64_t)blockIdx.x * NT; t0 < a.count; t0 += (int64_t)gridDim.x * NT) {
+        // ---- phase 1: one cell per thread ----
+        const int64_t ci = t0 + threadIdx.x;
         const bool valid = ci < a.count;
         int32_t r0 = -1, rx = -1, ry = -1, rz = -1;
         bool sh_on = false;
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__(NT) tv_sparse_kernel(DGrid G, TvArgs a) {
                 if (r0 >= 0 && g0 != 0.0) { tc.flags |= 1u; tc.g0 = (float)g0; }
             }
             if (sh_on) {
-                wc[lane] = tc;
+                cells[threadIdx.x] = tc;
             } else if (a.with_grad) {   // sigma-only cell: finished here
                 if (tc.gx != 0.f) atomicAdd(a.grad + (int64_t)rx * PLX_STRIDE, tc.gx);
                 if (tc.gy != 0.f) atomicAdd(a.grad + (int64_t)ry * PLX_STRIDE, tc.gy);
@@ -311,23 +315,24 @@ __global__ void __launch_bounds__(NT) tv_sparse_kernel(DGrid G, TvArgs a) {
                 if (tc.flags & 1u) a.tmask[r0] = 1;
             }
         }
-        // the cells with an SH term, compacted in lane order
+        // the block's cells with an SH term, compacted in thread order
         const unsigned shm = __ballot_sync(PLX_FULL_MASK, sh_on);
-        const int nsh = __popc(shm);
-        __syncwarp();
-        // ---- phase 2: 4 SH cells per round, 7 lanes per cell ----
-        for (int g = 0; g < nsh; g += 4) {
+        if (lane == 0) wcnt[wib] = __popc(shm);
+        __syncthreads();
+        int before = 0, nsh = 0;
+#pragma unroll
+        for (int k = 0; k < NT / 32; ++k) {
+            before += k < wib ? wcnt[k] : 0;
+            nsh += wcnt[k];
+        }
+        if (sh_on) shl[before + __popc(shm & ((1u << lane) - 1u))] = (uint16_t)threadIdx.x;
+        __syncthreads();
+        // ---- phase 2: 4 SH cells per warp round, 7 lanes per cell ----
+        for (int g = wib * 4; g < nsh; g += 4 * (NT / 32)) {
             const int idx = g + sub;
             const bool ok = lane < 28 && idx < nsh;
-            // lane of the idx-th set bit of shm
-            int src = 0;
-            if (ok) {
-                unsigned m = shm;
-                for (int t = 0; t < idx; ++t) m &= m - 1;
-                src = __ffs(m) - 1;
-            }
             TvCell tc{-1, -1, -1, -1, 0.f, 0.f, 0.f, 0.f, 0u};
-            if (ok) tc = wc[src];
+            if (ok) tc = cells[shl[idx]];
             bool tx = false, ty = false, tz = false, t0 = false;
             float gx[4] = {0.f, 0.f, 0.f, 0.f}, gy[4] = {0.f, 0.f, 0.f, 0.f};
             float gz[4] = {0.f, 0.f, 0.f, 0.f}, g0v[4] = {0.f, 0.f, 0.f, 0.f};
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(NT) tv_sparse_kernel(DGrid G, TvArgs a) {
                 }
             }
         }
-        __syncwarp();   // wc reused by the next iteration
+        __syncthreads();   // cells / shl reused by the next iteration
     }
     // both sums in one pass: warp shuffles, one shared-memory exchange, one
     // barrier
