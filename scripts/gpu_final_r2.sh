@@ -24,7 +24,7 @@ timeout 900 $NCU -k "regex:march_bwd|colour_kernel|scatter_kernel|opt_rows|tv_de
 STEPS=10 WARM=3 timeout 900 python scripts/sweep_c5.py > gpurun_out/sweep_c5_$TAG.log 2>&1
 # C5 2^20: the render kernels of one wave (dead-brick mask, spatial segment order)
 STEPS=1 WARM=2 LOGB0=20 LOGB1=21 timeout 1200 $NCU -k "regex:march_bwd|colour_kernel|scatter_kernel|seg_" \
-  -s 72 -c 6 -o gpurun_out/prof_c5_$TAG python scripts/sweep_c5.py > /dev/null 2>&1
+  -s 36 -c 6 -o gpurun_out/prof_c5_$TAG python scripts/sweep_c5.py > /dev/null 2>&1
 timeout 600 python scripts/bench_msi.py > gpurun_out/msi_$TAG.json 2>&1
 timeout 900 python scripts/ladder_c3.py > gpurun_out/c3_$TAG.json 2>/dev/null
 timeout 900 python scripts/bench_c4.py > gpurun_out/c4_$TAG.json 2>/dev/null
