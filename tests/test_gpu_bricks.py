@@ -85,12 +85,12 @@ def test_brick_mask_matches_definition():
     np.testing.assert_array_equal(got, want)
 
 
-def _compare(a, b, rng, interp="trilinear"):
+def _compare(a, b, rng, interp="trilinear", formula="relative"):
     import paper_2112_05131_b200 as px
     o, d = ray_batch(rng, 3000)
     vd = d / np.linalg.norm(d, axis=1, keepdims=True)
     gt = rng.uniform(0, 1, (3000, 3))
-    opts = px.RenderOptions(interp=interp)
+    opts = px.RenderOptions(interp=interp, formula=formula)
     fa = px.render_rays(a, o, d, opts)
     fb = px.render_rays(b, o, d, opts)
     for x, y in zip(fa, fb):
@@ -109,10 +109,11 @@ def _compare(a, b, rng, interp="trilinear"):
     return ga
 
 
-@pytest.mark.parametrize("interp", ["trilinear", "nearest"])
-def test_brick_skipping_is_exact(interp):
+@pytest.mark.parametrize("interp,formula", [("trilinear", "relative"), ("nearest", "relative"),
+                                            ("trilinear", "absolute")])
+def test_brick_skipping_is_exact(interp, formula):
     a, b = _pair()
-    _compare(a, b, np.random.default_rng(1), interp)
+    _compare(a, b, np.random.default_rng(1), interp, formula)
 
 
 def test_revived_bricks_stay_exact():
