@@ -185,3 +185,17 @@ def test_trainer_steps_with_bricks_match(monkeypatch):
         out.append(np.array(losses))
         assert (tr.grid._bricks is not None) == use
     np.testing.assert_allclose(out[0], out[1], rtol=1e-3)
+
+
+def test_random_grids_bit_identical():
+    """scripts/stress_bricks.py on 6 random grids (odd dims, hole slabs,
+    negative regions, exact zeros, blobs; rays inside / outside / axis-aligned,
+    jitter): every result with the mask equals the result without it."""
+    import importlib.util
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts",
+                        "stress_bricks.py")
+    spec = importlib.util.spec_from_file_location("stress_bricks", path)
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    assert m.main(6) == 0
