@@ -209,7 +209,32 @@ struct Scratch {
     int2 *ord;
     int *seg_key;      // [segments] spatial bucket of each segment
     int *bucket;       // [kBuckets] counts, then (scan) cursors; zeroed by the march
+    // packed records (pack != 0): the sample's cell (i | j << pk_sy | k <<
+    // pk_sz) and its last-position flag (bit 31) ride in the unused 4th float
+    // of f, and the 16-byte cell array is neither written nor read
+    int pack, pk_sy, pk_sz;
 };
+
+// The record's cell {i, j, k, w} -- w = the position index (unpacked) or the
+// last-position flag (packed) -- and its fractional offsets.
+__device__ __forceinline__ void load_cell_f(const Scratch &S, int64_t k, bool with_f, int4 &cl,
+                                            float4 &f4) {
+    if (S.pack) {
+        f4 = S.f[k];
+        const uint32_t u = __float_as_uint(f4.w);
+        const uint32_t my = (1u << (S.pk_sz - S.pk_sy)) - 1u, mz = (1u << (31 - S.pk_sz)) - 1u;
+        cl = make_int4((int)(u & ((1u << S.pk_sy) - 1u)), (int)((u >> S.pk_sy) & my),
+                       (int)((u >> S.pk_sz) & mz), (int)(u >> 31));
+    } else {
+        cl = S.cell[k];
+        if (with_f) f4 = S.f[k];
+    }
+}
+
+// Whether a record is the ray's last march position (K:200-205 delta).
+__device__ __forceinline__ bool rec_is_last(const Scratch &S, const int4 &cl, double last_si) {
+    return S.pack ? cl.w != 0 : (double)cl.w == last_si;
+}
 
 // The ray's colour total sum_w w c+ from its segment sums, in the order every
 // consumer of the sums uses (short rays: in segment order per lane; long
@@ -602,7 +627,9 @@ __global__ void __launch_bounds__(256) seg_key_kernel(Scratch S, int shx, int sh
         for (int64_t sg = t0 + threadIdx.x; sg < nseg && sg < t0 + kSegTile; sg += blockDim.x) {
             const int ray = S.seg_ray[sg];
             const int64_t j0 = (sg - S.seg_first[ray]) * 32;
-            const int4 c = S.cell[(int64_t)ray * S.cap + j0];
+            int4 c;
+            float4 fd;
+            load_cell_f(S, (int64_t)ray * S.cap + j0, false, c, fd);
             const int key =
                 (spread3(c.x >> shx) << 2) | (spread3(c.y >> shy) << 1) | spread3(c.z >> shz);
             S.seg_key[sg] = key;
@@ -762,8 +789,17 @@ __global__ void __launch_bounds__(128, MINB)
                 S.att[k] = att;
                 S.T[k] = Ti;
                 S.w[k] = wi;
-                S.cell[k] = make_int4(ijk[0], ijk[1], ijk[2], (int)si);
-                if (!NEAREST) S.f[k] = make_float4((float)fd[0], (float)fd[1], (float)fd[2], 0.f);
+                if (S.pack) {
+                    const uint32_t u = (uint32_t)ijk[0] | ((uint32_t)ijk[1] << S.pk_sy) |
+                                       ((uint32_t)ijk[2] << S.pk_sz) |
+                                       (si == rm.nsamp - 1 ? 0x80000000u : 0u);
+                    S.f[k] = NEAREST ? make_float4(0.f, 0.f, 0.f, __uint_as_float(u))
+                                     : make_float4((float)fd[0], (float)fd[1], (float)fd[2],
+                                                   __uint_as_float(u));
+                } else {
+                    S.cell[k] = make_int4(ijk[0], ijk[1], ijk[2], (int)si);
+                    if (!NEAREST) S.f[k] = make_float4((float)fd[0], (float)fd[1], (float)fd[2], 0.f);
+                }
                 if (!G.identity) {   // identity grids: rows follow from the cell
                     if (!rows_ok) load_rows<NEAREST>(G, ijk, rows);
                     if (!NEAREST) {
@@ -946,8 +982,7 @@ __global__ void __launch_bounds__(128, MINB)
         float4 f4 = make_float4(0.f, 0.f, 0.f, 0.f);
         int32_t rows[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
         if (valid) {
-            cl = S.cell[k];
-            if (!NEAREST) f4 = S.f[k];
+            load_cell_f(S, k, !NEAREST, cl, f4);
             if (G.identity) {
                 identity_rows<NEAREST>(G, cl, rows);
             } else {
@@ -1190,8 +1225,7 @@ __global__ void __launch_bounds__(128, MINB)
             Ti = S.T[k];
             wi = S.w[k];
             c4 = S.c[k];
-            cl = S.cell[k];
-            if (!NEAREST) f4 = S.f[k];
+            load_cell_f(S, k, !NEAREST, cl, f4);
             if (G.identity) {
                 int32_t r8[8];
                 identity_rows<NEAREST>(G, cl, r8);
@@ -1287,7 +1321,7 @@ __global__ void __launch_bounds__(128, MINB)
         ra.init(lane, bf);
         if (qn < nseg) fetch2(nx_ray);
         // delta of this sample (K:200-205): step, except at the last position
-        const double dl = (double)cl.w == last_si ? dlt_last : O.step;
+        const double dl = rec_is_last(S, cl, last_si) ? dlt_last : O.step;
         const double cc0 = relu((double)c4.x), cc1 = relu((double)c4.y),
                      cc2 = relu((double)c4.z);
         double gsig;
@@ -1889,6 +1923,20 @@ int plx::render_fused_bwd_impl(const plx_grid *g, const plx_rays *rays, const in
     S.w = reinterpret_cast<double *>(base + L.off_w);
     S.c = reinterpret_cast<float4 *>(base + L.off_c);
     S.cell = reinterpret_cast<int4 *>(base + L.off_cell);
+    {   // packed cell records when i, j, k and a flag fit 32 bits (PLX_PACK=0: off)
+        static const bool pack_env = [] {
+            const char *e = getenv("PLX_PACK");
+            return !(e && e[0] == '0');
+        }();
+        int b[3];
+        for (int a = 0; a < 3; ++a) {
+            b[a] = 0;
+            while (((g->dims[a] - 1) >> b[a]) > 0) ++b[a];
+        }
+        S.pack = pack_env && b[0] + b[1] + b[2] <= 31;
+        S.pk_sy = b[0];
+        S.pk_sz = b[0] + b[1];
+    }
     S.f = reinterpret_cast<float4 *>(base + L.off_f);
     S.rows = reinterpret_cast<int4 *>(base + L.off_rows);
     S.sig = lam_cauchy > 0.0 ? reinterpret_cast<double *>(base + L.off_sig) : nullptr;

@@ -2,6 +2,8 @@
 """Dump the composited-sample records (ray, position, cell) of one C2 training
 step at the headline state (step 5) and at step 2000 -> gpurun_out/records_<step>.npz
 (for offline analysis of sample sort orders / row sharing)."""
+import os
+os.environ.setdefault("PLX_PACK", "0")   # reads the unpacked cell array
 import math
 import os
 import sys

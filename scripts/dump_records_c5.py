@@ -1,6 +1,8 @@
 #!/usr/bin/env python3
 """Dump one C5 step's composited-sample cells (512^3 toy-sparse grid, single
 wave: B = 2^15 and 40000 rays) -> gpurun_out/records_c5_<B>.npz."""
+import os
+os.environ.setdefault("PLX_PACK", "0")   # reads the unpacked cell array
 import math
 import os
 import sys
