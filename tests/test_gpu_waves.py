@@ -4,8 +4,8 @@ reached at C5-size batches) render in waves; every wave-sliced entry point
 camera-pool / CUDA-graph step) must give the single-wave results.  A small
 PLX_RECORD_MB forces 1024-ray waves on 3000-ray batches; each run is its own
 process (the budget is read once).  The spatial segment order of large
-waves (PLX_SEG_ORDER=1 forces it at these sizes) must not change results
-either."""
+waves (PLX_SEG_ORDER=1 forces it at these sizes) and the unpacked record
+layout of very large lattices (PLX_PACK=0) must not change results either."""
 import os
 import subprocess
 import sys
@@ -25,12 +25,13 @@ def _run(tmp_path, name, env_extra):
     return np.load(out)
 
 
-@pytest.mark.parametrize("variant", ["waves", "ordered", "ordered_waves"])
+@pytest.mark.parametrize("variant", ["waves", "ordered", "ordered_waves", "unpacked"])
 def test_multi_wave_batches_match_one_wave(tmp_path, variant):
     one = _run(tmp_path, "one", {"PLX_SEG_ORDER": "0"})
     env = {"waves": {"PLX_RECORD_MB": "1", "PLX_SEG_ORDER": "0"},
            "ordered": {"PLX_SEG_ORDER": "1"},
-           "ordered_waves": {"PLX_RECORD_MB": "1", "PLX_SEG_ORDER": "1"}}[variant]
+           "ordered_waves": {"PLX_RECORD_MB": "1", "PLX_SEG_ORDER": "1"},
+           "unpacked": {"PLX_SEG_ORDER": "0", "PLX_PACK": "0"}}[variant]
     many = _run(tmp_path, variant, env)
     for k in one.files:
         a, b = one[k], many[k]
